@@ -1,0 +1,180 @@
+/*
+ * mis2.h -- C ABI of libmis2.so, the B200 (sm_100a) implementation of the
+ * data-parallel hot path of Kelley & Rajamanickam, "Parallel, Portable
+ * Algorithms for Distance-2 Maximal Independent Set and Graph Coarsening"
+ * (arXiv 2204.02934).  "P:n" = PAPER.md line n.
+ *
+ * Conventions (all entry points)
+ * ------------------------------
+ *  - Graphs are CSR in DEVICE memory: rowptr int64[n+1] (rowptr[0] = 0,
+ *    nondecreasing), colinds int32[nnz].  The graph must be symmetric, in
+ *    range and duplicate free; a stored diagonal is allowed and ignored
+ *    ("CRS"; reading Q23).  Row order inside a row is free
+ *    except for mis2_validate_graph, which also requires sorted rows.
+ *    0 <= n <= 2^31 - 3.
+ *  - Every output array is a caller-owned device buffer; the library
+ *    allocates nothing per call.  Scratch comes from the caller's workspace
+ *    `ws` (device memory, >= mis2_workspace_size(...) bytes, 256-byte
+ *    aligned).  Workspace contents need not be initialised.
+ *  - All device work is enqueued on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream).  Functions returning host scalars synchronise that
+ *    stream before returning; device outputs are then complete.  The *_async
+ *    variants do not synchronise and write their scalars to device memory.
+ *  - Calls with disjoint workspaces and outputs may run concurrently.
+ *  - Return value: MIS2_OK (0) or a negative MIS2_E* code; no exception or
+ *    abort crosses the ABI.  mis2_strerror() names a code,
+ *    mis2_last_error() returns a thread-local detail string for the last
+ *    failing call on the calling thread.
+ */
+#ifndef MIS2_H
+#define MIS2_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ status codes */
+#define MIS2_OK 0
+#define MIS2_EINVAL (-1)         /* null pointer, n out of range, bad option      */
+#define MIS2_ENOMEM (-2)         /* workspace smaller than mis2_workspace_size()   */
+#define MIS2_ECUDA (-3)          /* CUDA runtime error (detail: mis2_last_error)   */
+#define MIS2_ENCCL (-4)          /* NCCL error (distributed entry points)          */
+#define MIS2_EGRAPH (-5)         /* VALIDATE failed: range / duplicate / asymmetry */
+#define MIS2_ENOTCONVERGED (-6)  /* max_iters reached with undecided vertices      */
+#define MIS2_ERANGE (-7)         /* output capacity too small; required size set   */
+#define MIS2_EINTERNAL (-9)      /* an invariant of the algorithm failed           */
+
+/* -------------------------------------------- priority schemes */
+#define MIS2_SCHEME_XORSTAR 0 /* h(i,v) = f(f(i ^ seed) ^ f(v)), f = xorshift64*   */
+#define MIS2_SCHEME_FIXED 1   /* Bell et al. fixed priorities: f(seed ^ f(v))     */
+#define MIS2_SCHEME_XOR 2     /* as XORSTAR with f = plain xorshift64     */
+
+/* -------------------------------------------------------------- op codes */
+#define MIS2_OP_MIS2 0      /* mis2 / mis2_async                            */
+#define MIS2_OP_AGGREGATE 1 /* mis2_aggregate                               */
+#define MIS2_OP_COARSEN 2   /* mis2_coarsen                                 */
+#define MIS2_OP_MIS2_HOST 3 /* mis2_host (graph staged through the workspace) */
+#define MIS2_OP_VALIDATE 4  /* mis2_validate_graph                          */
+
+/* ------------------------------------------------------------------- flags */
+#define MIS2_FLAG_VALIDATE 0x1u  /* run mis2_validate_graph first (EGRAPH on failure) */
+
+typedef struct {
+    int64_t n;              /* |V|                                         */
+    int64_t nnz;            /* stored entries = rowptr[n]                  */
+    const int64_t* rowptr;  /* device int64[n+1]                           */
+    const int32_t* colinds; /* device int32[nnz]                           */
+} mis2_graph;
+
+typedef struct {
+    uint64_t seed;      /* hash seed, mixed as f(iter ^ seed) (reading Q4); default 0 */
+    int32_t max_iters;  /* <= 0: 10*b + 20 with b = ceil(log2(n+2)) (reading Q12)     */
+    int32_t scheme;     /* MIS2_SCHEME_*                                              */
+    uint32_t flags;     /* MIS2_FLAG_*                                                */
+    int32_t group;      /* lanes per CSR row in the neighbour loops: 0 = auto, else
+                           1,2,4,8,16,32 (§V-D "SIMD"); never changes results */
+    /* TEST ONLY (Fig. 1 replay): when non-NULL, iteration i <
+       prio_iters uses T_v = (prio_override[i*n + v] << b) | (v + 1) instead
+       of the hash.  Device memory, uint64[prio_iters * n]. */
+    const uint64_t* prio_override;
+    int32_t prio_iters;
+    int32_t reserved;
+} mis2_opts;
+
+/* Fill *o with the defaults (seed 0, Xor*, auto everything). */
+void mis2_opts_default(mis2_opts* o);
+
+/* Workspace bytes needed for `op` (MIS2_OP_*) on a graph of n vertices and
+ * nnz stored entries on the CURRENT device.  MIS2_OK or MIS2_EINVAL. */
+int mis2_workspace_size(int64_t n, int64_t nnz, int32_t op, size_t* bytes);
+
+/*
+ * MIS-2 -- Alg. 1 "MIS-2: Kokkos Kernels Algorithm" (§III-A) with
+ * the §V optimisations: per-iteration xorshift* priorities, the two
+ * worklists, 64-bit compressed status words IN = 0 < (priority
+ * << b | id+1) < OUT = 2^64-1 (Eq. 1), closed neighbourhoods
+ * (reading Q1) and decide on the pre-update T_v (reading Q2).
+ *
+ *   in_set : device uint8[n]; 1 iff v is in the MIS-2 ({v : T_v = IN})
+ *   count  : host; |MIS-2|
+ *   iters  : host; loop bodies executed ("number of times the loop
+ *            ... is executed")
+ *   stats  : host int64[max_iters * 6] or NULL.  When non-NULL the call
+ *            also records, per iteration, |worklist1|, |worklist2|, E1, E2
+ *            (sums of stored row lengths over the lists) and |N[wl1]|,
+ *            |N[wl2]| (distinct closed-neighbourhood vertices) -- a slower
+ *            instrumented run used for the algorithmic-byte model.
+ * Returns MIS2_ENOTCONVERGED with in_set = vertices IN so far and
+ * *iters = max_iters when worklist1 is not empty after max_iters loops.
+ */
+int mis2(const mis2_graph* g, const mis2_opts* o, uint8_t* in_set, int64_t* count, int32_t* iters,
+         int64_t* stats, void* ws, size_t ws_bytes, void* stream);
+
+/* Same as mis2() without synchronisation: *d_count (int64), *d_iters
+ * (int32) and *d_status (int32, MIS2_OK / MIS2_ENOTCONVERGED) are DEVICE
+ * pointers written by the last kernel.  Argument errors are still returned. */
+int mis2_async(const mis2_graph* g, const mis2_opts* o, uint8_t* in_set, int64_t* d_count,
+               int32_t* d_iters, int32_t* d_status, void* ws, size_t ws_bytes, void* stream);
+
+/* End-to-end variant with HOST buffers: rowptr_h int64[n+1] and colinds_h
+ * int32[nnz] (pinned for full speed) are copied into the workspace, MIS-2
+ * runs, and in_set_h uint8[n] is copied back.  ws from MIS2_OP_MIS2_HOST. */
+int mis2_host(int64_t n, int64_t nnz, const int64_t* rowptr_h, const int32_t* colinds_h,
+              const mis2_opts* o, uint8_t* in_set_h, int64_t* count, int32_t* iters, void* ws,
+              size_t ws_bytes, void* stream);
+
+/*
+ * MIS-2 aggregation -- Alg. 3 (§III-B):
+ *   phase 1: roots = MIS2(G); each root and its neighbours form an aggregate,
+ *            numbered by ascending root id (reading Q18);
+ *   phase 2: MIS2 of the subgraph induced by unaggregated vertices (same
+ *            seed, original ids, iter from 0 -- reading Q15); a root with
+ *            >= 2 unaggregated neighbours aggregates them (Q16-Q17);
+ *   phase 3: frozen tentative labels; every leftover joins the adjacent
+ *            aggregate of max coupling, then min size, then min id
+ *            (reading Q19).
+ *   labels   : device int32[n], aggregate of each vertex, in [0, num_aggs)
+ *   num_aggs : host
+ *   roots    : device int32[n] or NULL; roots[a] = root vertex of aggregate a
+ *   stats    : host int64[8] or NULL: |M1|, iters1, |M2|, iters2, accepted
+ *              phase-2 roots, phase-3 leftovers, n1, num_aggs
+ */
+int mis2_aggregate(const mis2_graph* g, const mis2_opts* o, int32_t* labels, int64_t* num_aggs,
+                   int32_t* roots, int64_t* stats, void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * Coarse graph A_c <- coarsen(A) (Alg. 4 setup): vertices are the
+ * aggregates; (a,b), a != b, is an entry iff some stored fine entry (u,v)
+ * has labels[u] = a, labels[v] = b.  Rows sorted, deduplicated, no
+ * self-loops (reading Q21).
+ *   labels    : device int32[n], values in [0, num_aggs)
+ *   c_rowptr  : device int64[num_aggs + 1] -- always written
+ *   c_colinds : device int32[cap] -- written only when cap >= nnz_c
+ *   c_nnz     : host; stored coarse entries.  MIS2_ERANGE when cap < nnz_c
+ *               (two-call convention: query with cap = 0, allocate, repeat).
+ */
+int mis2_coarsen(const mis2_graph* g, const int32_t* labels, int64_t num_aggs, int64_t* c_rowptr,
+                 int32_t* c_colinds, int64_t cap, int64_t* c_nnz, void* ws, size_t ws_bytes,
+                 void* stream);
+
+/* Check the input contract on the device: rowptr monotone with rowptr[n] =
+ * nnz, colinds in range, rows sorted without duplicates, pattern symmetric.
+ * MIS2_OK or MIS2_EGRAPH (detail in mis2_last_error()). */
+int mis2_validate_graph(const mis2_graph* g, void* ws, size_t ws_bytes, void* stream);
+
+/* Number of kernel launches issued by the last call on this thread
+ * (measurement aid for bench.py's "gpu_launches"). */
+int64_t mis2_last_launch_count(void);
+
+const char* mis2_strerror(int status);
+const char* mis2_last_error(void);
+/* Library build string (arch, git-independent version). */
+const char* mis2_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MIS2_H */

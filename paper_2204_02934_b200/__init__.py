@@ -1,0 +1,279 @@
+"""B200-native MIS-2 / MIS-2 aggregation / coarsening (arXiv 2204.02934).
+
+Thin Python binding over the C ABI of ``libmis2.so`` (include/mis2.h):
+argument marshalling only -- torch CUDA tensors become device pointers and
+``torch.cuda.current_stream()`` becomes the cudaStream_t.  Every step of the
+hot path runs in the sm_100a kernels of ``csrc/``.  There is no CPU fallback:
+without the library or a CUDA device every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import build as _build
+
+__all__ = ["mis2", "mis2_async", "mis2_host", "aggregate", "coarsen", "validate_graph", "multilevel",
+           "Mis2Error", "lib", "SCHEMES", "EXPORTS", "workspace"]
+
+SCHEMES = {"xorstar": 0, "fixed": 1, "xor": 2}
+OP_MIS2, OP_AGGREGATE, OP_COARSEN, OP_MIS2_HOST, OP_VALIDATE = 0, 1, 2, 3, 4
+OK, EINVAL, ENOMEM, ECUDA, ENCCL, EGRAPH, ENOTCONVERGED, ERANGE, EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7, -9
+FLAG_VALIDATE = 1
+
+# every symbol include/mis2.h declares
+EXPORTS = ["mis2_opts_default", "mis2_workspace_size", "mis2", "mis2_async", "mis2_host", "mis2_aggregate",
+           "mis2_coarsen", "mis2_validate_graph", "mis2_last_launch_count", "mis2_strerror", "mis2_last_error",
+           "mis2_version"]
+
+
+class Mis2Error(RuntimeError):
+    def __init__(self, rc: int, where: str, detail: str = ""):
+        super().__init__(f"{where}: {rc} {detail}")
+        self.rc = rc
+
+
+class _Graph(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("nnz", ctypes.c_int64), ("rowptr", ctypes.c_void_p),
+                ("colinds", ctypes.c_void_p)]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("max_iters", ctypes.c_int32), ("scheme", ctypes.c_int32),
+                ("flags", ctypes.c_uint32), ("group", ctypes.c_int32), ("prio_override", ctypes.c_void_p),
+                ("prio_iters", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load (building in-tree first if sources are newer) libmis2.so."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if _build.stale() and os.path.exists(_build.NVCC):
+            path = _build.build()
+        if not os.path.exists(path):
+            raise ImportError(f"libmis2.so not built ({path}); run __graft_entry__.build()")
+        L = ctypes.CDLL(path)
+        P, I64, I32, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+        L.mis2_workspace_size.argtypes = [I64, I64, I32, ctypes.POINTER(SZ)]
+        L.mis2.argtypes = [P, P, P, P, P, P, P, SZ, P]
+        L.mis2_async.argtypes = [P, P, P, P, P, P, P, SZ, P]
+        L.mis2_host.argtypes = [I64, I64, P, P, P, P, P, P, P, SZ, P]
+        L.mis2_aggregate.argtypes = [P, P, P, P, P, P, P, SZ, P]
+        L.mis2_coarsen.argtypes = [P, P, I64, P, P, I64, P, P, SZ, P]
+        L.mis2_validate_graph.argtypes = [P, P, SZ, P]
+        L.mis2_last_launch_count.restype = I64
+        L.mis2_strerror.restype = ctypes.c_char_p
+        L.mis2_strerror.argtypes = [ctypes.c_int]
+        L.mis2_last_error.restype = ctypes.c_char_p
+        L.mis2_version.restype = ctypes.c_char_p
+        L.mis2_opts_default.argtypes = [P]
+        for name in ("mis2", "mis2_async", "mis2_host", "mis2_aggregate", "mis2_coarsen", "mis2_validate_graph",
+                     "mis2_workspace_size"):
+            getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, where: str, allow=()):
+    if rc != OK and rc not in allow:
+        L = lib()
+        raise Mis2Error(rc, where, f"{L.mis2_strerror(rc).decode()}: {L.mis2_last_error().decode()}")
+    return rc
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2204_02934_b200 needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def _stream():
+    return ctypes.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+_ws_cache: dict = {}
+
+
+def workspace(op: int, n: int, nnz: int):
+    """Device workspace tensor for `op` (cached per device and size)."""
+    torch = _torch()
+    sz = ctypes.c_size_t(0)
+    _check(lib().mis2_workspace_size(n, nnz, op, ctypes.byref(sz)), "mis2_workspace_size")
+    dev = torch.cuda.current_device()
+    key = (dev, op)
+    t = _ws_cache.get(key)
+    if t is None or t.numel() < sz.value:
+        t = torch.empty(max(sz.value, 256), dtype=torch.uint8, device=f"cuda:{dev}")
+        _ws_cache[key] = t
+    return t, sz.value
+
+
+def _graph(rowptr, colinds):
+    torch = _torch()
+    assert rowptr.is_cuda and colinds.is_cuda, "rowptr/colinds must be CUDA tensors"
+    assert rowptr.dtype == torch.int64 and colinds.dtype == torch.int32
+    assert rowptr.is_contiguous() and colinds.is_contiguous()
+    n = rowptr.numel() - 1
+    nnz = colinds.numel()
+    return _Graph(n, nnz, rowptr.data_ptr(), colinds.data_ptr() if nnz else None), n, nnz
+
+
+def _opts(seed=0, scheme="xorstar", max_iters=0, group=0, validate=False, prio_override=None):
+    o = _Opts()
+    lib().mis2_opts_default(ctypes.byref(o))
+    o.seed = seed & ((1 << 64) - 1)
+    o.scheme = SCHEMES[scheme]
+    o.max_iters = max_iters
+    o.group = group
+    o.flags = FLAG_VALIDATE if validate else 0
+    if prio_override is not None:
+        o.prio_override = prio_override.data_ptr()
+        o.prio_iters = prio_override.shape[0]
+    return o
+
+
+@dataclass
+class Mis2Result:
+    in_set: "object"          # torch.uint8 CUDA tensor [n]
+    count: int
+    iterations: int
+    rc: int = OK
+    stats: np.ndarray | None = None
+    launches: int = 0
+
+
+def mis2(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
+         validate: bool = False, prio_override=None, stats: bool = False, allow_partial: bool = False,
+         out=None) -> Mis2Result:
+    """Alg. 1 through ``mis2()`` of the C ABI."""
+    torch = _torch()
+    g, n, nnz = _graph(rowptr, colinds)
+    if prio_override is not None:
+        prio_override = prio_override.to(device=rowptr.device, dtype=torch.int64).contiguous()
+    o = _opts(seed, scheme, max_iters, group, validate, prio_override)
+    ws, wsb = workspace(OP_MIS2, n, nnz)
+    in_set = out if out is not None else torch.empty(max(n, 1), dtype=torch.uint8, device=rowptr.device)
+    cnt, its = ctypes.c_int64(0), ctypes.c_int32(0)
+    st = None
+    if stats:
+        b = (n + 1).bit_length()
+        mi = max_iters if max_iters > 0 else 10 * b + 20
+        st = np.zeros((mi, 6), dtype=np.int64)
+    rc = lib().mis2(ctypes.byref(g), ctypes.byref(o), in_set.data_ptr(), ctypes.byref(cnt), ctypes.byref(its),
+                    st.ctypes.data if st is not None else None, ws.data_ptr(), wsb, _stream())
+    launches = int(lib().mis2_last_launch_count())
+    _check(rc, "mis2", allow=(ENOTCONVERGED,) if allow_partial else ())
+    return Mis2Result(in_set[:n], int(cnt.value), int(its.value), rc,
+                      None if st is None else st[: its.value].copy(), launches)
+
+
+def mis2_async(rowptr, colinds, in_set, d_scalars, seed: int = 0, scheme: str = "xorstar", group: int = 0,
+               max_iters: int = 0):
+    """Enqueue MIS-2 without synchronising; d_scalars = int64 CUDA tensor [2]
+    receiving count and (iterations | status << 32)."""
+    g, n, nnz = _graph(rowptr, colinds)
+    o = _opts(seed, scheme, max_iters, group)
+    ws, wsb = workspace(OP_MIS2, n, nnz)
+    p = d_scalars.data_ptr()
+    rc = lib().mis2_async(ctypes.byref(g), ctypes.byref(o), in_set.data_ptr(), p, p + 8, p + 12, ws.data_ptr(),
+                          wsb, _stream())
+    _check(rc, "mis2_async")
+    return int(lib().mis2_last_launch_count())
+
+
+def mis2_host(rowptr_h: np.ndarray, colinds_h: np.ndarray, in_set_h: np.ndarray, seed: int = 0,
+              scheme: str = "xorstar", group: int = 0, ws=None):
+    """End-to-end MIS-2 from HOST arrays (copies inside the call)."""
+    n = rowptr_h.shape[0] - 1
+    nnz = colinds_h.shape[0]
+    o = _opts(seed, scheme, 0, group)
+    if ws is None:
+        ws, wsb = workspace(OP_MIS2_HOST, n, nnz)
+    else:
+        ws, wsb = ws
+    cnt, its = ctypes.c_int64(0), ctypes.c_int32(0)
+
+    def hp(a):
+        return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+
+    rc = lib().mis2_host(n, nnz, hp(rowptr_h), hp(colinds_h), ctypes.byref(o), hp(in_set_h), ctypes.byref(cnt),
+                         ctypes.byref(its), ws.data_ptr(), wsb, _stream())
+    _check(rc, "mis2_host")
+    return int(cnt.value), int(its.value)
+
+
+@dataclass
+class AggResult:
+    labels: "object"   # torch.int32 CUDA [n]
+    num_aggs: int
+    roots: "object"    # torch.int32 CUDA [num_aggs]
+    stats: dict
+
+
+def aggregate(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
+              validate: bool = False) -> AggResult:
+    """Alg. 3 through ``mis2_aggregate()``."""
+    torch = _torch()
+    g, n, nnz = _graph(rowptr, colinds)
+    o = _opts(seed, scheme, max_iters, group, validate)
+    ws, wsb = workspace(OP_AGGREGATE, n, nnz)
+    labels = torch.empty(max(n, 1), dtype=torch.int32, device=rowptr.device)
+    roots = torch.empty(max(n, 1), dtype=torch.int32, device=rowptr.device)
+    na = ctypes.c_int64(0)
+    st = np.zeros(8, dtype=np.int64)
+    rc = lib().mis2_aggregate(ctypes.byref(g), ctypes.byref(o), labels.data_ptr(), ctypes.byref(na),
+                              roots.data_ptr(), st.ctypes.data, ws.data_ptr(), wsb, _stream())
+    _check(rc, "mis2_aggregate")
+    keys = ["mis1", "iters1", "mis2", "iters2", "accepted2", "leftovers", "n1", "num_aggs"]
+    return AggResult(labels[:n], int(na.value), roots[: na.value], dict(zip(keys, map(int, st))))
+
+
+def coarsen(rowptr, colinds, labels, num_aggs: int):
+    """Coarse graph through ``mis2_coarsen()`` (two-call)."""
+    torch = _torch()
+    g, n, nnz = _graph(rowptr, colinds)
+    ws, wsb = workspace(OP_COARSEN, n, nnz)
+    crow = torch.empty(num_aggs + 1, dtype=torch.int64, device=rowptr.device)
+    cnnz = ctypes.c_int64(0)
+    L = lib()
+    rc = L.mis2_coarsen(ctypes.byref(g), labels.data_ptr(), num_aggs, crow.data_ptr(), None, 0, ctypes.byref(cnnz),
+                        ws.data_ptr(), wsb, _stream())
+    _check(rc, "mis2_coarsen(count)", allow=(ERANGE,))
+    ccol = torch.empty(max(cnnz.value, 1), dtype=torch.int32, device=rowptr.device)
+    rc = L.mis2_coarsen(ctypes.byref(g), labels.data_ptr(), num_aggs, crow.data_ptr(), ccol.data_ptr(),
+                        ccol.numel(), ctypes.byref(cnnz), ws.data_ptr(), wsb, _stream())
+    _check(rc, "mis2_coarsen")
+    return crow, ccol[: cnnz.value]
+
+
+def validate_graph(rowptr, colinds) -> None:
+    g, n, nnz = _graph(rowptr, colinds)
+    ws, wsb = workspace(OP_VALIDATE, n, nnz)
+    _check(lib().mis2_validate_graph(ctypes.byref(g), ws.data_ptr(), wsb, _stream()), "mis2_validate_graph")
+
+
+def multilevel(rowptr, colinds, threshold: int = 1000, max_levels: int = 32, seed: int = 0):
+    """Repeated aggregation + coarsening until n < threshold or no reduction
+    (reading Q22).  Returns [(n, nnz, num_aggs)], final CSR,
+    and the per-level label tensors."""
+    levels, labels_all = [], []
+    rp, ci = rowptr, colinds
+    for _ in range(max_levels):
+        n = rp.numel() - 1
+        if n < threshold:
+            break
+        agg = aggregate(rp, ci, seed=seed)
+        levels.append((n, ci.numel(), agg.num_aggs))
+        labels_all.append(agg.labels)
+        if agg.num_aggs == n:
+            break
+        rp, ci = coarsen(rp, ci, agg.labels, agg.num_aggs)
+    return levels, (rp, ci), labels_all

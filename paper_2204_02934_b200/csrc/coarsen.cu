@@ -1,0 +1,301 @@
+// coarsen.cu -- coarse graph A_c <- coarsen(A) (Alg. 4 setup): the
+// quotient graph over the aggregates, rows sorted and deduplicated, no
+// self-loops (reading Q21).
+//
+// Device pipeline (no global sort of all nnz keys):
+//   1. seglen[a] = sum of stored row lengths of a's members
+//   2. sptr = exclusive scan(seglen)
+//   3. every fine row u appends labels[adj(u)] (own label -> sentinel) into
+//      its aggregate's segment at an atomically reserved offset
+//   4. per segment: sort + unique in shared memory (warp-per-segment for
+//      <= 256 entries, block-per-segment for <= 8192); longer segments use an
+//      na-bit bitmap (set bits, then ordered compaction = sorted unique)
+//   5. c_rowptr = exclusive scan(unique counts); copy out.
+#include "common.cuh"
+#include "internal.h"
+
+namespace mis2k {
+
+constexpr int32_t kSent = 0x7fffffff;
+constexpr int kWarpSeg = 256;
+constexpr int kBlockSeg = 8192;
+
+__global__ void k_check_labels(int64_t n, const int32_t* __restrict__ labels, int64_t na, int* err) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t a = labels[v];
+        if (a < 0 || a >= na) atomicOr(err, 1);
+    }
+}
+
+__global__ void k_seglen(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ labels,
+                         unsigned long long* __restrict__ seglen) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t d = rowptr[v + 1] - rowptr[v];
+        if (d) atomicAdd(&seglen[labels[v]], (unsigned long long)d);
+    }
+}
+
+template <int G>
+__global__ void k_fill(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colinds,
+                       const int32_t* __restrict__ labels, unsigned long long* __restrict__ cursor,
+                       int32_t* __restrict__ buf) {
+    constexpr int RPW = 32 / G;
+    const int lane = threadIdx.x & 31, grp = lane / G, sub = lane % G;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (int64_t base = gwarp * RPW; base < n; base += nwarps * RPW) {
+        const int64_t v = base + grp;
+        const bool valid = v < n;
+        int64_t s = 0, e = 0;
+        int32_t a = 0;
+        unsigned long long pos = 0;
+        if (valid) {
+            s = rowptr[v];
+            e = rowptr[v + 1];
+            a = labels[v];
+            if (sub == 0 && e > s) pos = atomicAdd(&cursor[a], (unsigned long long)(e - s));
+        }
+        pos = __shfl_sync(kFull, pos, lane - sub);
+        if (valid)
+            for (int64_t j = s + sub; j < e; j += G) {
+                const int32_t b = labels[colinds[j]];
+                buf[pos + (j - s)] = (b == a) ? kSent : b;
+            }
+    }
+}
+
+// in-place bitonic sort of x[0..P) (P power of two) by `nthreads` threads
+__device__ __forceinline__ void bitonic(int32_t* x, int P, int tid, int nthreads, bool warp_only) {
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = tid; i < P / 2; i += nthreads) {
+                const int lo = 2 * i - (i & (j - 1));
+                const int hi = lo + j;
+                const bool up = (lo & k) == 0;
+                const int32_t a = x[lo], b = x[hi];
+                if ((a > b) == up) { x[lo] = b; x[hi] = a; }
+            }
+            if (warp_only) __syncwarp(); else __syncthreads();
+        }
+    }
+}
+
+// warp per segment, segments of <= kWarpSeg entries
+__global__ void k_sort_warp(int64_t na, const int64_t* __restrict__ sptr, int32_t* __restrict__ buf,
+                            int64_t* __restrict__ ucnt, int32_t* __restrict__ big, int* big_cnt) {
+    __shared__ int32_t sm[kWarpsPerBlock][kWarpSeg];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int32_t* x = sm[warp];
+    const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+    for (int64_t a = (int64_t)blockIdx.x * kWarpsPerBlock + warp; a < na; a += nwarps) {
+        const int64_t s = sptr[a], len = sptr[a + 1] - s;
+        if (len > kWarpSeg) {
+            if (lane == 0) ucnt[a] = -1;  // handled by the block / bitmap kernels
+            continue;
+        }
+        int P = 1;
+        while (P < len) P <<= 1;
+        for (int i = lane; i < P; i += 32) x[i] = i < len ? buf[s + i] : kSent;
+        __syncwarp();
+        bitonic(x, P, lane, 32, true);
+        int c = 0;
+        for (int base = 0; base < P; base += 32) {
+            const int i = base + lane;
+            const int32_t xi = x[i < P ? i : 0];
+            const bool first = i < P && xi != kSent && (i == 0 || x[i - 1] != xi);
+            const unsigned ball = __ballot_sync(kFull, first);
+            if (first) buf[s + c + __popc(ball & lanemask_lt())] = xi;
+            c += __popc(ball);
+        }
+        if (lane == 0) ucnt[a] = c;
+        __syncwarp();
+    }
+    (void)big; (void)big_cnt;
+}
+
+// block per segment, kWarpSeg < len <= kBlockSeg; longer ones go to `big`
+__global__ void k_sort_block(int64_t na, const int64_t* __restrict__ sptr, int32_t* __restrict__ buf,
+                             int64_t* __restrict__ ucnt, int32_t* __restrict__ big, int* big_cnt) {
+    __shared__ int32_t x[kBlockSeg];
+    __shared__ int s_w[kWarpsPerBlock];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t a = blockIdx.x; a < na; a += gridDim.x) {
+        const int64_t s = sptr[a], len = sptr[a + 1] - s;
+        if (len <= kWarpSeg) continue;
+        if (len > kBlockSeg) {
+            if (threadIdx.x == 0) big[atomicAdd(big_cnt, 1)] = (int32_t)a;
+            continue;
+        }
+        int P = 1;
+        while (P < len) P <<= 1;
+        for (int i = threadIdx.x; i < P; i += blockDim.x) x[i] = i < len ? buf[s + i] : kSent;
+        __syncthreads();
+        bitonic(x, P, threadIdx.x, blockDim.x, false);
+        int carry = 0;
+        for (int base = 0; base < P; base += blockDim.x) {
+            const int i = base + threadIdx.x;
+            const int32_t xi = i < P ? x[i] : kSent;
+            const bool first = i < P && xi != kSent && (i == 0 || x[i - 1] != xi);
+            const unsigned ball = __ballot_sync(kFull, first);
+            if (lane == 0) s_w[warp] = __popc(ball);
+            __syncthreads();
+            int off = carry;
+            for (int w = 0; w < warp; w++) off += s_w[w];
+            if (first) buf[s + off + __popc(ball & lanemask_lt())] = xi;
+            int tot = 0;
+            for (int w = 0; w < kWarpsPerBlock; w++) tot += s_w[w];
+            carry += tot;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) ucnt[a] = carry;
+        __syncthreads();
+    }
+}
+
+// one block handles one long segment via an na-bit bitmap
+__global__ void k_bitmap_segment(const int32_t* __restrict__ big, int idx, const int64_t* __restrict__ sptr,
+                                 int32_t* __restrict__ buf, int64_t* __restrict__ ucnt, unsigned* __restrict__ bm,
+                                 int64_t na) {
+    __shared__ int s_w[32 + 1];
+    const int64_t a = big[idx];
+    const int64_t s = sptr[a], e = sptr[a + 1];
+    const int64_t words = (na + 31) / 32;
+    for (int64_t i = threadIdx.x; i < words; i += blockDim.x) bm[i] = 0;
+    __syncthreads();
+    for (int64_t j = s + threadIdx.x; j < e; j += blockDim.x) {
+        const int32_t b = buf[j];
+        if (b != kSent) atomicOr(&bm[b >> 5], 1u << (b & 31));
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    int64_t carry = 0;
+    for (int64_t base = 0; base < words; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const unsigned wbits = i < words ? bm[i] : 0u;
+        int c = __popc(wbits);
+        int inc = c;
+        for (int off = 1; off < 32; off <<= 1) {
+            int y = __shfl_up_sync(kFull, inc, off);
+            if (lane >= off) inc += y;
+        }
+        if (lane == 31) s_w[warp] = inc;
+        __syncthreads();
+        int64_t off = carry;
+        for (int w = 0; w < warp; w++) off += s_w[w];
+        off += inc - c;
+        unsigned bits = wbits;
+        while (bits) {
+            const int t = __ffs(bits) - 1;
+            buf[s + off++] = (int32_t)(i * 32 + t);
+            bits &= bits - 1;
+        }
+        int tot = 0;
+        for (int w = 0; w < nw; w++) tot += s_w[w];
+        carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ucnt[a] = carry;
+}
+
+// warp per aggregate: copy uniques to the output CSR
+__global__ void k_copy_out(int64_t na, const int64_t* __restrict__ sptr, const int32_t* __restrict__ buf,
+                           const int64_t* __restrict__ crow, int32_t* __restrict__ ccol) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+    for (int64_t a = (int64_t)blockIdx.x * kWarpsPerBlock + warp; a < na; a += nwarps) {
+        const int64_t s = sptr[a], o = crow[a], len = crow[a + 1] - o;
+        for (int64_t i = lane; i < len; i += 32) ccol[o + i] = buf[s + i];
+    }
+}
+
+}  // namespace mis2k
+
+namespace mis2h {
+using namespace mis2k;
+
+int run_coarsen(const mis2_graph& g, const int32_t* labels, int64_t na, int64_t* c_rowptr, int32_t* c_colinds,
+                int64_t cap, int64_t* c_nnz, void* ws, size_t ws_bytes, cudaStream_t s, size_t* bytes_needed) {
+    DeviceInfo di;
+    MIS2_TRY(device_info(&di));
+    const int64_t n = g.n;
+    const int64_t nab = bytes_needed ? n : na;  // sizing uses the bound na <= n
+    Carve c(ws, ws_bytes);
+    unsigned long long* seglen = c.take<unsigned long long>((size_t)nab + 1);
+    int64_t* sptr = c.take<int64_t>((size_t)nab + 2);
+    unsigned long long* cursor = c.take<unsigned long long>((size_t)nab + 1);
+    int64_t* ucnt = c.take<int64_t>((size_t)nab + 1);
+    int32_t* big = c.take<int32_t>((size_t)nab + 1);
+    unsigned* bm = c.take<unsigned>((size_t)(nab + 31) / 32 + 1);
+    int32_t* buf = c.take<int32_t>((size_t)g.nnz + 1);
+    void* tmp = c.take<char>(scan64_ws_bytes(nab + 1));
+    int* scal = c.take<int>(16);
+    if (bytes_needed) { *bytes_needed = c.off; return MIS2_OK; }
+    if (!c.ok()) { set_error("workspace too small: need %zu bytes", c.off); return MIS2_ENOMEM; }
+    if (na < 0 || na > n || (n > 0 && na == 0)) { set_error("num_aggs out of range"); return MIS2_EINVAL; }
+
+    const int G = choose_group(g.n, g.nnz, 0);
+    int64_t blocks = (n + kBlock - 1) / kBlock;
+    if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
+    if (blocks < 1) blocks = 1;
+
+    MIS2_CUDA_TRY(cudaMemsetAsync(scal, 0, 16 * sizeof(int), s));
+    MIS2_CUDA_TRY(cudaMemsetAsync(seglen, 0, sizeof(unsigned long long) * ((size_t)na + 1), s));
+    count_launch(2);
+    k_check_labels<<<(unsigned)blocks, kBlock, 0, s>>>(n, labels, na, &scal[0]);
+    k_seglen<<<(unsigned)blocks, kBlock, 0, s>>>(n, g.rowptr, labels, seglen);
+    count_launch(2);
+    MIS2_TRY(scan_counts64((const int64_t*)seglen, na, sptr, tmp, s));
+    MIS2_CUDA_TRY(cudaMemcpyAsync(cursor, sptr, sizeof(int64_t) * (size_t)na, cudaMemcpyDeviceToDevice, s));
+    count_launch();
+    {
+        const int64_t rows_per_block = (int64_t)(kBlock / 32) * (32 / G);
+        int64_t fb = (n + rows_per_block - 1) / rows_per_block;
+        if (fb > (int64_t)di.sms * 16) fb = (int64_t)di.sms * 16;
+        if (fb < 1) fb = 1;
+        switch (G) {
+            case 1: k_fill<1><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, cursor, buf); break;
+            case 2: k_fill<2><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, cursor, buf); break;
+            case 4: k_fill<4><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, cursor, buf); break;
+            case 8: k_fill<8><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, cursor, buf); break;
+            case 16: k_fill<16><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, cursor, buf); break;
+            default: k_fill<32><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, cursor, buf); break;
+        }
+        count_launch();
+    }
+    {
+        int64_t wb = (na + kWarpsPerBlock - 1) / kWarpsPerBlock;
+        if (wb > (int64_t)di.sms * 32) wb = (int64_t)di.sms * 32;
+        if (wb < 1) wb = 1;
+        k_sort_warp<<<(unsigned)wb, kBlock, 0, s>>>(na, sptr, buf, ucnt, big, &scal[1]);
+        int64_t bb = na < (int64_t)di.sms * 8 ? na : (int64_t)di.sms * 8;
+        if (bb < 1) bb = 1;
+        k_sort_block<<<(unsigned)bb, kBlock, 0, s>>>(na, sptr, buf, ucnt, big, &scal[1]);
+        count_launch(2);
+    }
+    int hs[16];
+    MIS2_CUDA_TRY(cudaMemcpyAsync(hs, scal, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+    if (hs[0]) { set_error("labels out of [0, num_aggs)"); return MIS2_EINVAL; }
+    for (int i = 0; i < hs[1]; i++) {
+        k_bitmap_segment<<<1, 1024, 0, s>>>(big, i, sptr, buf, ucnt, bm, na);
+        count_launch();
+    }
+    MIS2_TRY(scan_counts64(ucnt, na, c_rowptr, tmp, s));
+    int64_t total = 0;
+    MIS2_CUDA_TRY(cudaMemcpyAsync(&total, c_rowptr + na, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+    *c_nnz = total;
+    if (c_colinds == nullptr || cap < total) return MIS2_ERANGE;
+    {
+        int64_t wb = (na + kWarpsPerBlock - 1) / kWarpsPerBlock;
+        if (wb > (int64_t)di.sms * 32) wb = (int64_t)di.sms * 32;
+        if (wb < 1) wb = 1;
+        k_copy_out<<<(unsigned)wb, kBlock, 0, s>>>(na, sptr, buf, c_rowptr, c_colinds);
+        count_launch();
+    }
+    MIS2_CUDA_TRY(cudaGetLastError());
+    MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+    return MIS2_OK;
+}
+
+}  // namespace mis2h

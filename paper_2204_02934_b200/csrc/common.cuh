@@ -1,0 +1,136 @@
+// common.cuh -- device helpers shared by the sm_100a kernels of libmis2.so.
+//
+// Product code (no oracle/ dependency).  "P:n" = PAPER.md line n; "Qk" =
+// DESIGN.md reading k.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/mis2.h"
+
+namespace mis2k {
+
+// §V-C compressed status words: IN = 0, OUT = UINT_MAX (64-bit, Q6).
+constexpr uint64_t kIN = 0ull;
+constexpr uint64_t kOUT = ~0ull;
+constexpr int kWarpsPerBlock = 8;
+constexpr int kBlock = 32 * kWarpsPerBlock;
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------- priorities
+// §V-A: h(iter, v) = f(f(iter) ^ f(v)); Xor*: f = xorshift64*
+// (xorshift (13,7,17) then * 0x2545F4914F6CDD1D, reading Q3); seed mixed
+// into the iteration term (Q4); the priority is the HIGH 64-b bits (Q5).
+__device__ __forceinline__ uint64_t xs64(uint64_t x) {
+    x ^= x << 13;
+    x ^= x >> 7;
+    x ^= x << 17;
+    return x;
+}
+__device__ __forceinline__ uint64_t xs64star(uint64_t x) { return xs64(x) * 0x2545F4914F6CDD1Dull; }
+
+struct Prio {
+    int scheme;
+    int b;
+    uint64_t seed;
+    uint64_t hi_mask;           // ~(2^b - 1)
+    int64_t n;
+    const uint64_t* override_;  // test-only (Fig. 1 replay)
+    int override_iters;
+
+    // per-iteration constant part of h
+    __device__ __forceinline__ uint64_t iter_term(int it) const {
+        if (scheme == MIS2_SCHEME_XOR) return xs64((uint64_t)it ^ seed);
+        return xs64star((uint64_t)it ^ seed);
+    }
+    // packed undecided word (priority << b) | (v + 1)
+    __device__ __forceinline__ uint64_t word(int it, uint64_t fi, int64_t v) const {
+        if (override_ != nullptr && it < override_iters)
+            return (override_[(int64_t)it * n + v] << b) | (uint64_t)(v + 1);
+        uint64_t h;
+        if (scheme == MIS2_SCHEME_FIXED) h = xs64star(seed ^ xs64star((uint64_t)v));
+        else if (scheme == MIS2_SCHEME_XOR) h = xs64(fi ^ xs64((uint64_t)v));
+        else h = xs64star(fi ^ xs64star((uint64_t)v));
+        return (h & hi_mask) | (uint64_t)(v + 1);
+    }
+};
+
+// ------------------------------------------------------------- warp helpers
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <int G>
+__device__ __forceinline__ uint64_t group_min(uint64_t x) {
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+        uint64_t y = __shfl_xor_sync(kFull, x, off);
+        x = y < x ? y : x;
+    }
+    return x;
+}
+template <int G>
+__device__ __forceinline__ int group_or(int x) {
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) x |= __shfl_xor_sync(kFull, x, off);
+    return x;
+}
+template <int G>
+__device__ __forceinline__ int group_and(int x) {
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) x &= __shfl_xor_sync(kFull, x, off);
+    return x;
+}
+template <int G>
+__device__ __forceinline__ int group_sum(int x) {
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) x += __shfl_xor_sync(kFull, x, off);
+    return x;
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long x) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(kFull, x, off);
+    return x;
+}
+
+// -------------------------------------------------------------- grid barrier
+// Sense-flip grid barrier for a cooperatively launched (co-resident) grid:
+// block 0 adds 0x80000000 - (nblocks - 1), every other block adds 1, so the
+// top bit flips exactly when all blocks have arrived.  Release on arrival,
+// acquire while polling (makes every block's prior global writes visible).
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int nb = (blockIdx.x == 0) ? (0x80000000u - (gridDim.x - 1)) : 1u;
+        unsigned int old;
+        asm volatile("atom.add.release.gpu.u32 %0,[%1],%2;" : "=r"(old) : "l"(bar), "r"(nb) : "memory");
+        unsigned int cur;
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0,[%1];" : "=r"(cur) : "l"(bar) : "memory");
+        } while (((old ^ cur) & 0x80000000u) == 0);
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.u64 %0,[%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// block-wide sum of one value per warp (lane 0 holds it); result in thread 0
+__device__ __forceinline__ long long block_sum_warps(long long warp_val, long long* s_tmp) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) s_tmp[warp] = warp_val;
+    __syncthreads();
+    long long s = 0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += s_tmp[w];
+    __syncthreads();
+    return s;
+}
+
+}  // namespace mis2k

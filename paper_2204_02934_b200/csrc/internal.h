@@ -1,0 +1,103 @@
+// internal.h -- host-side internals of libmis2.so (not part of the ABI).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/mis2.h"
+
+namespace mis2h {
+
+// thread-local error detail + launch counter (abi.cu)
+void set_error(const char* fmt, ...);
+void count_launch(int k = 1);
+void reset_launches();
+
+#define MIS2_CUDA_TRY(expr)                                                              \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess) {                                                         \
+            ::mis2h::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,               \
+                               cudaGetErrorString(_e));                                  \
+            return MIS2_ECUDA;                                                           \
+        }                                                                                \
+    } while (0)
+
+#define MIS2_TRY(expr)           \
+    do {                         \
+        int _rc = (expr);        \
+        if (_rc != MIS2_OK) return _rc; \
+    } while (0)
+
+// bump allocator over the caller's workspace (256-byte aligned pieces)
+struct Carve {
+    char* base;
+    size_t cap;
+    size_t off = 0;
+    bool dry;  // sizing pass: no base pointer
+    Carve(void* b, size_t c) : base((char*)b), cap(c), dry(b == nullptr) {}
+    template <class T>
+    T* take(size_t count) {
+        size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+        if (bytes == 0) bytes = 256;
+        T* p = dry ? nullptr : (T*)(base + off);
+        off += bytes;
+        return p;
+    }
+    bool ok() const { return dry || off <= cap; }
+};
+
+struct DeviceInfo {
+    int device;
+    int sms;
+    size_t smem_optin;
+};
+int device_info(DeviceInfo* out);
+
+constexpr int kStatsMaxIters = 400;
+
+// MIS-2 state carved from the workspace
+struct Mis2Ws {
+    uint64_t* T;
+    uint64_t* M;
+    int32_t* L1;
+    int32_t* L2;
+    int32_t* c1;
+    int32_t* c2;
+    unsigned int* mark;
+    unsigned long long* ctrl;  // [0]=barrier, [1..4]=ring of |wl1| sums, [5]=count, [6]=ticket
+    long long* dstats;         // [kStatsMaxIters * 6]
+    long long* scal;           // [8] host-visible scalars of mis2()/mis2_host()
+};
+void carve_mis2(Carve& c, int64_t n, int max_warps, Mis2Ws* w);
+int max_coop_warps(const DeviceInfo& d);
+
+// Runs Alg. 1 on the device.  labels != NULL restricts to {v : labels[v] < 0}
+// (phase 2 of Alg. 3, reading Q15).  Writes in_set, *d_count, *d_iters,
+// *d_status (device).  stats_host optional (synchronises).
+int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uint8_t* in_set,
+             int64_t* d_count, int32_t* d_iters, int32_t* d_status, int64_t* stats_host,
+             const Mis2Ws& w, cudaStream_t s);
+
+int choose_group(int64_t n, int64_t nnz, int requested);
+int max_iters_for(int64_t n, int requested);
+int bits_for(int64_t n);
+
+// aggregation / coarsening / validation (aggregate.cu, coarsen.cu)
+int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int64_t* num_aggs,
+                  int32_t* roots, int64_t* stats, void* ws, size_t ws_bytes, cudaStream_t s,
+                  size_t* bytes_needed);
+int run_coarsen(const mis2_graph& g, const int32_t* labels, int64_t na, int64_t* c_rowptr,
+                int32_t* c_colinds, int64_t cap, int64_t* c_nnz, void* ws, size_t ws_bytes,
+                cudaStream_t s, size_t* bytes_needed);
+int run_validate(const mis2_graph& g, void* ws, size_t ws_bytes, cudaStream_t s, size_t* bytes_needed);
+
+// device-wide exclusive scan of 0/1 (uint8) flags -> int32 prefix, total to *d_total
+size_t scan_ws_bytes(int64_t n);
+int scan_flags(const uint8_t* flags, int64_t n, int32_t* prefix, int32_t* d_total, void* tmp,
+               cudaStream_t s);
+// int64 exclusive scan of int64 counts (n entries) -> out[n+1]
+size_t scan64_ws_bytes(int64_t n);
+int scan_counts64(const int64_t* counts, int64_t n, int64_t* out, void* tmp, cudaStream_t s);
+
+}  // namespace mis2h

@@ -1,0 +1,269 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bit-exact: in-set masks, counts, iteration counts, per-iteration worklist
+statistics, aggregate labels/roots, coarse CSR -- all integer work.
+"""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import mis2gen as G
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def M():
+    import paper_2204_02934_b200 as m
+    return m
+
+
+def dev(g):
+    return (torch.from_numpy(g.rowptr).cuda(), torch.from_numpy(np.ascontiguousarray(g.colinds)).cuda())
+
+
+def small_graphs(count, seed, nmax=200):
+    rng = random.Random(seed)
+    out = []
+    for k in range(count):
+        kind = rng.random()
+        n = rng.randrange(0, nmax)
+        if kind < 0.6:
+            g = G.random_graph(n, rng.choice([0.0, 0.01, 0.03, 0.08, 0.2, 0.3]), seed * 7919 + k,
+                               diagonal=rng.random() < 0.5)
+        elif kind < 0.8:
+            g = G.random_powerlaw_graph(max(n, 2), rng.choice([2, 5, 12]), seed * 7919 + k)
+        else:
+            g = G.stencil(rng.randrange(1, 9), rng.randrange(1, 9), rng.randrange(1, 5), rng.choice([7, 27]),
+                          rng.choice([1, 1, 2, 3]))
+        out.append(g)
+    return out
+
+
+def check_mis2(g, seed=0, group=0, scheme="xorstar", stats=False):
+    rp, ci = dev(g)
+    r = M().mis2(rp, ci, seed=seed, group=group, scheme=scheme, stats=stats)
+    o = O.mis2(g.rowptr, g.colinds, seed=seed, scheme=scheme, stats=stats)
+    assert np.array_equal(r.in_set.cpu().numpy().astype(bool), o.in_set), g.name
+    assert (r.count, r.iterations) == (o.count, o.iterations), g.name
+    if stats:
+        assert np.array_equal(r.stats, o.stats), (g.name, r.stats, o.stats)
+    return r
+
+
+def test_fig1_replay_gpu():
+    """fig:example on the device with the figure's priorities."""
+    gold = json.load(open(os.path.join(GOLDEN, "fig1.json")))
+    g = G.fig1_graph()
+    rp, ci = dev(g)
+    prio = torch.tensor(gold["priorities"], dtype=torch.int64)
+    r = M().mis2(rp, ci, prio_override=prio)
+    assert sorted((np.nonzero(r.in_set.cpu().numpy())[0] + 1).tolist()) == gold["result_1based"]
+    assert r.iterations == gold["iterations"]
+    r1 = M().mis2(rp, ci, prio_override=prio, max_iters=1, allow_partial=True)
+    assert r1.rc == M().ENOTCONVERGED
+    assert sorted((np.nonzero(r1.in_set.cpu().numpy())[0] + 1).tolist()) == gold["in_after_iter0"]
+
+
+@pytest.mark.parametrize("chunk", range(6))
+def test_random_small_graphs(chunk):
+    for g in small_graphs(60, 1000 + chunk):
+        check_mis2(g, seed=chunk * 17)
+
+
+@pytest.mark.parametrize("group", [1, 2, 4, 8, 16, 32])
+def test_group_width_invariance(group):
+    """§V-D lane grouping never changes results."""
+    for g in small_graphs(25, 77, nmax=400) + [G.laplace3d_27pt(20), G.kronecker(11)]:
+        check_mis2(g, group=group)
+
+
+@pytest.mark.parametrize("scheme", ["xorstar", "fixed", "xor"])
+def test_schemes(scheme):
+    for g in [G.grid2d_5pt(10, 10), G.laplace3d_7pt(30), G.elasticity3d(8)]:
+        check_mis2(g, scheme=scheme)
+
+
+def test_stats_parity():
+    for g in [G.grid2d_5pt(10, 10), G.laplace3d_27pt(30), G.kronecker(12), G.random_graph(300, 0.02, 4)]:
+        check_mis2(g, stats=True)
+
+
+def test_edge_cases():
+    for g in [G.from_edges(0, []), G.from_edges(1, []), G.from_edges(37, []), G.from_edges(2, [(0, 1)]),
+              G.from_edges(64, [(0, j) for j in range(1, 64)])]:
+        check_mis2(g)
+
+
+def test_config1_full():
+    g = G.config_graph(0)
+    check_mis2(g, stats=True)
+    check_mis2(g, seed=12345)
+
+
+def test_config2_full():
+    """BASELINE.json configs[1]: 27-pt 100^3, the bench workload, default launch."""
+    g = G.config_graph(1)
+    r = check_mis2(g, stats=True)
+    assert (r.count, r.iterations) == (21587, 10)
+    check_mis2(g, seed=12345)
+
+
+@pytest.mark.slow
+def test_config3_full():
+    check_mis2(G.config_graph(2))
+
+
+@pytest.mark.slow
+def test_config4_full():
+    check_mis2(G.config_graph(3))
+
+
+@pytest.mark.slow
+def test_config5_mis2_full():
+    check_mis2(G.config_graph(4))
+
+
+def test_determinism_repeat():
+    g = G.laplace3d_27pt(60)
+    rp, ci = dev(g)
+    a = M().mis2(rp, ci).in_set.clone()
+    for _ in range(4):
+        assert torch.equal(M().mis2(rp, ci).in_set, a)
+
+
+def test_not_converged():
+    g = G.laplace3d_7pt(20)
+    rp, ci = dev(g)
+    r = M().mis2(rp, ci, max_iters=1, allow_partial=True)
+    o = O.mis2(g.rowptr, g.colinds, max_iters=1, allow_partial=True)
+    assert r.rc == M().ENOTCONVERGED and r.iterations == 1
+    assert np.array_equal(r.in_set.cpu().numpy().astype(bool), o.in_set)
+    with pytest.raises(M().Mis2Error):
+        M().mis2(rp, ci, max_iters=1)
+
+
+def test_validate_graph():
+    g = G.laplace3d_7pt(6)
+    rp, ci = dev(g)
+    M().validate_graph(rp, ci)
+    bad = ci.clone()
+    bad[5] = (bad[5] + 3) % g.n  # breaks symmetry / order
+    with pytest.raises(M().Mis2Error) as e:
+        M().validate_graph(rp, bad)
+    assert e.value.rc == M().EGRAPH
+    with pytest.raises(M().Mis2Error):
+        M().mis2(rp, bad, validate=True)
+
+
+def test_mis2_host_e2e():
+    g = G.laplace3d_27pt(40)
+    rph = torch.from_numpy(g.rowptr).pin_memory()
+    cih = torch.from_numpy(g.colinds).pin_memory()
+    out = torch.empty(g.n, dtype=torch.uint8).pin_memory()
+    cnt, its = M().mis2_host(rph, cih, out)
+    o = O.mis2(g.rowptr, g.colinds)
+    assert np.array_equal(out.numpy().astype(bool), o.in_set) and (cnt, its) == (o.count, o.iterations)
+
+
+# ----------------------------------------------------------------- aggregation
+def check_agg(g, seed=0):
+    rp, ci = dev(g)
+    a = M().aggregate(rp, ci, seed=seed)
+    o = O.aggregate(g.rowptr, g.colinds, seed=seed)
+    assert a.num_aggs == o.num_aggs, g.name
+    assert np.array_equal(a.labels.cpu().numpy(), o.labels), g.name
+    assert np.array_equal(a.roots.cpu().numpy(), o.roots), g.name
+    assert a.stats == o.stats, (a.stats, o.stats)
+    return a
+
+
+@pytest.mark.parametrize("chunk", range(3))
+def test_aggregate_small(chunk):
+    for g in small_graphs(40, 2000 + chunk):
+        check_agg(g, seed=chunk)
+
+
+def test_aggregate_heavy_leftovers():
+    # long rows exercise the block/hash phase-3 path (degree > 512)
+    for g in [G.random_powerlaw_graph(3000, 30, 5), G.kronecker(12), G.random_graph(1500, 0.5, 3)]:
+        check_agg(g)
+
+
+def test_aggregate_configs():
+    check_agg(G.config_graph(0))
+    a = check_agg(G.config_graph(1))
+    assert a.num_aggs == 42261
+
+
+@pytest.mark.slow
+def test_aggregate_config3():
+    check_agg(G.config_graph(2))
+
+
+# ----------------------------------------------------------------- coarsening
+def check_coarsen(g, labels=None, na=None):
+    rp, ci = dev(g)
+    if labels is None:
+        o = O.aggregate(g.rowptr, g.colinds)
+        labels, na = o.labels, o.num_aggs
+    crow, ccol = M().coarsen(rp, ci, torch.from_numpy(labels).cuda(), na)
+    orow, ocol = O.coarsen(g.rowptr, g.colinds, labels, na)
+    assert np.array_equal(crow.cpu().numpy(), orow) and np.array_equal(ccol.cpu().numpy(), ocol), g.name
+
+
+def test_coarsen_small():
+    for g in small_graphs(30, 3000):
+        if g.n:
+            check_coarsen(g)
+
+
+def test_coarsen_segments_all_paths():
+    g = G.random_graph(2000, 0.3, 9)  # big segments -> block + bitmap paths
+    rng = np.random.default_rng(0)
+    for na in (1, 3, 40, 700):
+        labels = rng.integers(0, na, g.n).astype(np.int32)
+        labels[:na] = np.arange(na)
+        check_coarsen(g, labels, na)
+    check_coarsen(G.config_graph(1))
+
+
+def test_coarsen_capacity_two_call():
+    g = G.laplace3d_7pt(10)
+    o = O.aggregate(g.rowptr, g.colinds)
+    rp, ci = dev(g)
+    import ctypes
+    m = M()
+    gg, n, nnz = m._graph(rp, ci)
+    ws, wsb = m.workspace(m.OP_COARSEN, n, nnz)
+    lab = torch.from_numpy(o.labels).cuda()
+    crow = torch.empty(o.num_aggs + 1, dtype=torch.int64, device="cuda")
+    c = ctypes.c_int64(0)
+    small = torch.empty(4, dtype=torch.int32, device="cuda")
+    rc = m.lib().mis2_coarsen(ctypes.byref(gg), lab.data_ptr(), o.num_aggs, crow.data_ptr(), small.data_ptr(), 4,
+                              ctypes.byref(c), ws.data_ptr(), wsb, m._stream())
+    assert rc == m.ERANGE and c.value == len(O.coarsen(g.rowptr, g.colinds, o.labels, o.num_aggs)[1])
+
+
+def test_multilevel_elasticity():
+    g = G.elasticity3d(30)
+    rp, ci = dev(g)
+    levels, (frp, fci), _ = M().multilevel(rp, ci, threshold=1000)
+    olevels, (orp, oci) = O.multilevel(g.rowptr, g.colinds, threshold=1000)
+    assert levels == olevels
+    assert np.array_equal(frp.cpu().numpy(), orp) and np.array_equal(fci.cpu().numpy(), oci)
+
+
+@pytest.mark.slow
+def test_multilevel_config5():
+    g = G.config_graph(4)
+    rp, ci = dev(g)
+    levels, _, _ = M().multilevel(rp, ci, threshold=1000)
+    olevels, _ = O.multilevel(g.rowptr, g.colinds, threshold=1000)
+    assert levels == olevels
