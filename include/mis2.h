@@ -61,6 +61,11 @@ extern "C" {
 
 /* ------------------------------------------------------------------- flags */
 #define MIS2_FLAG_VALIDATE 0x1u  /* run mis2_validate_graph first (EGRAPH on failure) */
+#define MIS2_FLAG_TIMELINE 0x2u  /* measurement aid: mis2()'s `stats` receives int64 device
+                                    timestamps (ns, %globaltimer) taken by block 0 after
+                                    the init phase and after every grid barrier:
+                                    [init, col0, dec0, col1, dec1, ...]; stats must hold
+                                    2 * max_iters + 2 entries */
 
 typedef struct {
     int64_t n;              /* |V|                                         */

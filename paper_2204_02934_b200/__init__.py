@@ -23,6 +23,7 @@ SCHEMES = {"xorstar": 0, "fixed": 1, "xor": 2}
 OP_MIS2, OP_AGGREGATE, OP_COARSEN, OP_MIS2_HOST, OP_VALIDATE = 0, 1, 2, 3, 4
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, EGRAPH, ENOTCONVERGED, ERANGE, EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7, -9
 FLAG_VALIDATE = 1
+FLAG_TIMELINE = 2
 
 # every symbol include/mis2.h declares
 EXPORTS = ["mis2_opts_default", "mis2_workspace_size", "mis2", "mis2_async", "mis2_host", "mis2_aggregate",
@@ -152,7 +153,7 @@ class Mis2Result:
 
 def mis2(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
          validate: bool = False, prio_override=None, stats: bool = False, allow_partial: bool = False,
-         out=None) -> Mis2Result:
+         out=None, timeline: bool = False) -> Mis2Result:
     """Alg. 1 through ``mis2()`` of the C ABI."""
     torch = _torch()
     g, n, nnz = _graph(rowptr, colinds)
@@ -163,16 +164,22 @@ def mis2(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int
     in_set = out if out is not None else torch.empty(max(n, 1), dtype=torch.uint8, device=rowptr.device)
     cnt, its = ctypes.c_int64(0), ctypes.c_int32(0)
     st = None
+    b = (n + 1).bit_length()
+    mi = max_iters if max_iters > 0 else 10 * b + 20
     if stats:
-        b = (n + 1).bit_length()
-        mi = max_iters if max_iters > 0 else 10 * b + 20
         st = np.zeros((mi, 6), dtype=np.int64)
+    elif timeline:
+        o.flags |= FLAG_TIMELINE
+        st = np.zeros(2 * mi + 2, dtype=np.int64)
     rc = lib().mis2(ctypes.byref(g), ctypes.byref(o), in_set.data_ptr(), ctypes.byref(cnt), ctypes.byref(its),
                     st.ctypes.data if st is not None else None, ws.data_ptr(), wsb, _stream())
     launches = int(lib().mis2_last_launch_count())
     _check(rc, "mis2", allow=(ENOTCONVERGED,) if allow_partial else ())
-    return Mis2Result(in_set[:n], int(cnt.value), int(its.value), rc,
-                      None if st is None else st[: its.value].copy(), launches)
+    if timeline:
+        st = np.diff(st[: 2 * its.value + 1]) / 1e3  # microseconds per phase
+    elif st is not None:
+        st = st[: its.value].copy()
+    return Mis2Result(in_set[:n], int(cnt.value), int(its.value), rc, st, launches)
 
 
 def mis2_async(rowptr, colinds, in_set, d_scalars, seed: int = 0, scheme: str = "xorstar", group: int = 0,

@@ -99,8 +99,11 @@ __device__ __forceinline__ long long warp_sum_ll(long long x) {
 // -------------------------------------------------------------- grid barrier
 // Sense-flip grid barrier for a cooperatively launched (co-resident) grid:
 // block 0 adds 0x80000000 - (nblocks - 1), every other block adds 1, so the
-// top bit flips exactly when all blocks have arrived.  Release on arrival,
-// acquire while polling (makes every block's prior global writes visible).
+// top bit flips exactly when all blocks have arrived.  Release on arrival;
+// the spin uses RELAXED loads with a short sleep (an acquire load compiles to
+// LD.STRONG + CCTL.IVALL, and invalidating L1 on every poll would wipe the
+// cache of co-resident blocks that are still gathering); one acquire fence
+// after the flip makes every block's prior writes visible.
 __device__ __forceinline__ void grid_barrier(unsigned int* bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -108,9 +111,12 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar) {
         unsigned int old;
         asm volatile("atom.add.release.gpu.u32 %0,[%1],%2;" : "=r"(old) : "l"(bar), "r"(nb) : "memory");
         unsigned int cur;
-        do {
-            asm volatile("ld.acquire.gpu.u32 %0,[%1];" : "=r"(cur) : "l"(bar) : "memory");
-        } while (((old ^ cur) & 0x80000000u) == 0);
+        for (;;) {
+            asm volatile("ld.relaxed.gpu.u32 %0,[%1];" : "=r"(cur) : "l"(bar) : "memory");
+            if ((old ^ cur) & 0x80000000u) break;
+            __nanosleep(32);
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
 }

@@ -60,10 +60,8 @@ constexpr int kStatsMaxIters = 400;
 struct Mis2Ws {
     uint64_t* T;
     uint64_t* M;
-    int32_t* L1;
-    int32_t* L2;
-    int32_t* c1;
-    int32_t* c2;
+    int32_t* L1[2];
+    int32_t* L2[2];
     unsigned int* mark;
     unsigned long long* ctrl;  // [0]=barrier, [1..4]=ring of |wl1| sums, [5]=count, [6]=ticket
     long long* dstats;         // [kStatsMaxIters * 6]

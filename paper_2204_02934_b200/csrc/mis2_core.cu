@@ -2,42 +2,58 @@
 // cooperatively launched sm_100a kernel.
 //
 // Design:
-//  * Every warp owns a fixed contiguous slice [lo, hi) of the vertex range.
-//    worklist_1 / worklist_2 (§V-B) are stored IN PLACE
-//    inside the owning warp's slice of two int32[n] arrays and compacted with
-//    __ballot_sync/__popc -- no global scan, no atomics, ascending order kept.
-//  * Each CSR row is processed by a group of G lanes (G = 1..32) -- §V-D
-//    "SIMD parallelism ... only if the average vertex degree is at least 16"
-//     generalised to a tunable group width; min / exists / forall
-//    are reduced with shuffles.
-//  * Phases are separated by a grid-wide barrier instead of kernel launches;
-//    the loop condition |worklist_1| == 0 is evaluated on the device, so one
-//    MIS-2 call is 1 memset + 1 kernel launch.
-//  * Refresh Row for iteration i+1 is fused into Decide of
+//  * Each thread block owns a contiguous vertex range [blo, bhi) and works
+//    through it in steps of RPB = 256/G rows, G lanes per CSR row
+//    (§V-D "SIMD parallelism", with a tunable group width).
+//  * worklist_1 / worklist_2 (§V-B) live in the block's slice of
+//    int32[n] arrays, double buffered (in -> out) and compacted with warp
+//    ballots + one shared-memory atomic per warp: no global scan, no global
+//    atomics, no block barrier per step.  The order inside a segment is
+//    free (reading Q11): every phase is a per-vertex function of the
+//    previous phase's arrays.
+//  * Dense phases (iteration 0, and any block whose worklist still covers
+//    >= 3/8 of its range) walk consecutive rows; the colinds of the next
+//    tile are streamed into shared memory by the Blackwell bulk-copy engine
+//    (cp.async.bulk + mbarrier complete_tx), double buffered, while the
+//    current tile gathers T / M.  Worklist membership is read from the
+//    status words (M_v != OUT for worklist_2, T_v undecided for worklist_1).
+//  * Sparse phases read the block's compacted worklist and process rows
+//    straight from global memory.  Rows longer than kHeavyDirect are
+//    deferred and reduced by the whole block.
+//  * Neighbour loops issue predicated batches of independent gathers.
+//  * Phases are separated by a grid-wide barrier; |worklist_1| == 0
+//    is tested on the device, so one call is 1 memset + 1 kernel launch.
+//  * Refresh Row of iteration i+1 is fused into Decide of
 //    iteration i; iteration 0's refresh is the init phase.
-//  * Status words are 64-bit (Eq. 1, reading Q6), so every min is
-//    one integer compare.
+//  * 64-bit status words (Eq. 1, reading Q6): a min is one compare.
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
 
 namespace mis2k {
 
+constexpr int kTileCap = 6912;      // int32 colinds per staging buffer (27 KB): 256 rows x 27
+constexpr int kHeavyDirect = 2048;  // rows longer than this are reduced by the whole block
+constexpr int kHeavyList = 64;
+constexpr int kDenseNum = 3, kDenseDen = 8;  // dense if |worklist segment| >= 3/8 of the range
+constexpr uint64_t kPending = 1ull;          // M of an active vertex before its first column pass
+
 struct MisParams {
     int64_t n;
+    int64_t nnz;
     const int64_t* __restrict__ rowptr;
     const int32_t* __restrict__ colinds;
     const int32_t* __restrict__ labels;  // phase-2 mask (active iff labels[v] < 0) or null
     uint64_t* T;                         // row status T_v
     uint64_t* M;                         // column status M_v
-    int32_t* L1;                         // worklist_1, per-warp in-place segments
-    int32_t* L2;                         // worklist_2
-    int32_t* c1;                         // per-warp |segment of worklist_1|
-    int32_t* c2;
+    int32_t* L1[2];                      // worklist_1, double buffered, per-block segments
+    int32_t* L2[2];                      // worklist_2
     unsigned long long* ctrl;
-    unsigned int* mark;    // stats only
-    long long* dstats;     // stats only
+    unsigned int* mark;   // stats only
+    long long* dstats;    // stats only
+    long long* timeline;  // MIS2_FLAG_TIMELINE only
     Prio prio;
     int max_iters;
     uint8_t* in_set;
@@ -46,220 +62,527 @@ struct MisParams {
     int32_t* d_status;
 };
 
-// ---------------------------------------------------------------- phases
-// Refresh Column: for v in worklist_2: M_v = min(T_w : w in N[v]);
-// IN -> OUT.  Inactive vertices (phase 2) carry T = OUT, neutral for min.
-// Survivors (M_v != OUT) are compacted in place into the warp's L2 segment.
-template <int G, bool STATS>
-__device__ __forceinline__ void column_phase(const MisParams& p, int it, int64_t lo, int64_t hi,
-                                             int gw, int lane) {
-    constexpr int RPW = 32 / G;
-    const int grp = lane / G, sub = lane % G;
-    const bool dense = (it == 0);
-    const int64_t total = dense ? (hi - lo) : (int64_t)p.c2[gw];
-    int32_t k = 0;
-    long long r_acc = 0, e_acc = 0, d_acc = 0;
-    const unsigned tag = 2u * (unsigned)it + 1u;  // column runs before decide
-    for (int64_t base = 0; base < total; base += RPW) {
-        const int64_t idx = base + grp;
-        const bool valid = idx < total;
-        int64_t v = 0;
-        bool act = false;
-        if (valid) {
-            v = dense ? lo + idx : (int64_t)p.L2[lo + idx];
-            act = dense && p.labels ? (p.labels[v] < 0) : true;
+struct __align__(16) TileSmem {
+    int32_t buf[2][kTileCap + 8];
+    unsigned long long mbar[2];   // dense tiles: one arrival (thread 0)
+    unsigned long long mbarS[2];  // sparse tiles: one arrival per row group
+    int64_t sal[2];  // 16-byte aligned colinds start of the staged span
+    int32_t fits[2];
+    int cnt;         // survivors written this phase
+    int hcount;
+    int32_t hlist[kHeavyList];
+    uint64_t red64[kWarpsPerBlock];
+    int wred[kWarpsPerBlock];
+};
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+// Blackwell bulk-copy engine: global -> shared, completion on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ------------------------------------------------------------ block helpers
+// Warp-aggregated append of the group leaders' survivors to out[base + ...]
+// (one shared atomic per warp; order inside the segment is free, Q11).
+__device__ __forceinline__ void append(TileSmem& sm, bool keep, int32_t v, int32_t* out, int64_t base) {
+    const unsigned ball = __ballot_sync(kFull, keep);
+    if (ball == 0) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(ball) - 1;
+    int pos = 0;
+    if (lane == leader) pos = atomicAdd(&sm.cnt, __popc(ball));
+    pos = __shfl_sync(kFull, pos, leader);
+    if (keep) out[base + pos + __popc(ball & lanemask_lt())] = v;
+}
+
+__device__ __forceinline__ uint64_t block_min_u64(TileSmem& sm, uint64_t x) {
+    x = group_min<32>(x);
+    const int warp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) sm.red64[warp] = x;
+    __syncthreads();
+    uint64_t r = sm.red64[0];
+#pragma unroll
+    for (int w = 1; w < kWarpsPerBlock; w++) r = sm.red64[w] < r ? sm.red64[w] : r;
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ long long block_sum_int(TileSmem& sm, int x) {
+    x = group_sum<32>(x);
+    if ((threadIdx.x & 31) == 0) sm.wred[threadIdx.x >> 5] = x;
+    __syncthreads();
+    long long s = 0;
+#pragma unroll
+    for (int w = 0; w < kWarpsPerBlock; w++) s += sm.wred[w];
+    __syncthreads();
+    return s;
+}
+
+// ------------------------------------------------------------ statistics
+struct Stat {
+    long long r = 0, e = 0, d = 0;
+};
+template <bool STATS>
+__device__ __forceinline__ void stat_row(const MisParams& p, unsigned tag, int64_t v, bool leader, int64_t deg,
+                                         Stat& st) {
+    if (STATS && leader) {
+        st.r++;
+        st.e += deg;
+        if (atomicMax(&p.mark[v], tag) < tag) st.d++;
+    }
+}
+template <bool STATS>
+__device__ __forceinline__ void stat_nbrs(const MisParams& p, unsigned tag, const int32_t* x, int64_t len, int sub,
+                                          int stride, Stat& st) {
+    if (STATS)
+        for (int64_t j = sub; j < len; j += stride)
+            if (atomicMax(&p.mark[x[j]], tag) < tag) st.d++;
+}
+template <bool STATS>
+__device__ __forceinline__ void stats_flush(const MisParams& p, int it, int slot0, Stat st) {
+    if (!STATS) return;
+    st.r = warp_sum_ll(st.r);
+    st.e = warp_sum_ll(st.e);
+    st.d = warp_sum_ll(st.d);
+    if ((threadIdx.x & 31) == 0) {
+        long long* o = p.dstats + 6 * it;
+        if (st.r) atomicAdd((unsigned long long*)&o[slot0], (unsigned long long)st.r);
+        if (st.e) atomicAdd((unsigned long long*)&o[slot0 + 2], (unsigned long long)st.e);
+        if (st.d) atomicAdd((unsigned long long*)&o[slot0 + 4], (unsigned long long)st.d);
+    }
+}
+
+// ------------------------------------------------------------ row kernels
+// Refresh Column of one row: min of T over the row's entries x[0..len)
+// (x is shared memory or global; generic addressing), lanes sub, sub+G, ...
+template <int G>
+__device__ __forceinline__ uint64_t row_min(const MisParams& p, const int32_t* x, int len, int sub, uint64_t m) {
+    constexpr int B = G == 1 ? 16 : (G == 2 ? 8 : 4);
+    for (int j = sub; j < len; j += B * G) {
+        uint64_t tt[B];
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            const int jj = j + q * G;
+            tt[q] = jj < len ? p.T[x[jj]] : kOUT;
         }
-        uint64_t m = kOUT;
-        if (act) {
-            const int64_t s = p.rowptr[v], e = p.rowptr[v + 1];
-            if (sub == 0) m = p.T[v];
-            int64_t j = s + sub;
-            // 4 independent gathers in flight per lane
-            for (; j + 3 * G < e; j += 4 * G) {
-                const int32_t w0 = p.colinds[j], w1 = p.colinds[j + G], w2 = p.colinds[j + 2 * G],
-                              w3 = p.colinds[j + 3 * G];
-                const uint64_t t0 = p.T[w0], t1 = p.T[w1], t2 = p.T[w2], t3 = p.T[w3];
-                const uint64_t a = t0 < t1 ? t0 : t1, b = t2 < t3 ? t2 : t3;
-                const uint64_t c = a < b ? a : b;
-                m = c < m ? c : m;
-            }
-            for (; j < e; j += G) {
-                const uint64_t t = p.T[p.colinds[j]];
-                m = t < m ? t : m;
-            }
-            if (STATS) {
-                if (sub == 0) {
-                    r_acc++;
-                    e_acc += e - s;
-                    if (atomicMax(&p.mark[v], tag) < tag) d_acc++;
-                }
-                for (int64_t jj = s + sub; jj < e; jj += G)
-                    if (atomicMax(&p.mark[p.colinds[jj]], tag) < tag) d_acc++;
-            }
+#pragma unroll
+        for (int q = 0; q < B; q++) m = tt[q] < m ? tt[q] : m;
+    }
+    return m;
+}
+
+// Decide of one row: exists M_w = OUT / forall M_w = T_v,
+// M_w = 0 (inactive, reading Q15) ignored.
+__device__ __forceinline__ void decide_acc(uint64_t m, uint64_t tv, int& any_out, int& all_eq) {
+    any_out |= (m == kOUT);
+    all_eq &= (m == tv) | (m == 0);
+}
+template <int G>
+__device__ __forceinline__ void row_decide(const MisParams& p, const int32_t* x, int len, int sub, uint64_t tv,
+                                           int& any_out, int& all_eq) {
+    constexpr int B = G == 1 ? 16 : (G == 2 ? 8 : 4);
+    for (int j = sub; j < len; j += B * G) {
+        uint64_t mm[B];
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            const int jj = j + q * G;
+            mm[q] = jj < len ? p.M[x[jj]] : tv;
         }
-        m = group_min<G>(m);
-        bool keep = false;
+#pragma unroll
+        for (int q = 0; q < B; q++) decide_acc(mm[q], tv, any_out, all_eq);
+    }
+}
+
+__device__ __forceinline__ bool decide_write(const MisParams& p, int64_t v, int any_out, int all_eq, int it,
+                                             uint64_t fi_next) {
+    if (any_out) {
+        p.T[v] = kOUT;
+        return false;
+    }
+    if (all_eq) {
+        p.T[v] = kIN;
+        return false;
+    }
+    p.T[v] = p.prio.word(it + 1, fi_next, v);  // fused Refresh Row
+    return true;
+}
+
+// issue the bulk copy of colinds[s, e) (16-byte aligned hull) into buffer `slot`
+__device__ __forceinline__ void stage_tile(TileSmem& sm, const MisParams& p, int slot, int64_t s, int64_t e) {
+    const int64_t sal = s & ~(int64_t)3;
+    const int64_t nnz4 = p.nnz & ~(int64_t)3;
+    const int64_t ecp = (e + 3) & ~(int64_t)3;
+    const bool fits = (ecp - sal) <= kTileCap && ecp <= nnz4;
+    sm.sal[slot] = sal;
+    sm.fits[slot] = fits;
+    fence_proxy_async();
+    if (fits && ecp > sal) {
+        mbar_expect_tx(&sm.mbar[slot], (uint32_t)((ecp - sal) * 4));
+        bulk_g2s(sm.buf[slot], p.colinds + sal, (uint32_t)((ecp - sal) * 4), &sm.mbar[slot]);
+    } else {
+        mbar_expect_tx(&sm.mbar[slot], 0u);
+    }
+}
+
+// One row, GG lanes: Refresh Column (PH 0) or Decide (PH 1).  Returns the
+// survivor flag in the group leader.  Must be called by all lanes.
+template <int GG, int PH>
+__device__ __forceinline__ bool process_row(const MisParams& p, bool act, int sub, int64_t v, const int32_t* x,
+                                            int len, uint64_t tv, int it, uint64_t fi_next) {
+    bool keep = false;
+    if (PH == 0) {
+        uint64_t m = (act && sub == 0) ? tv : kOUT;  // closed neighbourhood (Q1)
+        if (act) m = row_min<GG>(p, x, len, sub, m);
+        m = group_min<GG>(m);
         if (act && sub == 0) {
             if (m == kIN) m = kOUT;
             p.M[v] = m;
             keep = (m != kOUT);
         }
-        const unsigned ball = __ballot_sync(kFull, keep);
-        if (keep) p.L2[lo + k + __popc(ball & lanemask_lt())] = (int32_t)v;
-        k += __popc(ball);
-    }
-    if (lane == 0) p.c2[gw] = k;
-    if (STATS) {
-        long long r_tot = warp_sum_ll(r_acc), e_tot = warp_sum_ll(e_acc), d_tot = warp_sum_ll(d_acc);
-        if (lane == 0) {
-            long long* st = p.dstats + 6 * it;
-            atomicAdd((unsigned long long*)&st[1], (unsigned long long)r_tot);
-            atomicAdd((unsigned long long*)&st[3], (unsigned long long)e_tot);
-            atomicAdd((unsigned long long*)&st[5], (unsigned long long)d_tot);
+    } else {
+        int any_out = 0, all_eq = 1;
+        if (act) {
+            if (sub == 0) decide_acc(p.M[v], tv, any_out, all_eq);
+            row_decide<GG>(p, x, len, sub, tv, any_out, all_eq);
         }
+        any_out = group_or<GG>(any_out);
+        all_eq = group_and<GG>(all_eq);
+        if (act && sub == 0) keep = decide_write(p, v, any_out, all_eq, it, fi_next);
     }
+    return keep;
 }
 
-// Decide on the pre-update T_v (reading Q2):
-//   exists w in N[v]: M_w = OUT  -> OUT
-//   else forall w in N[v]: M_w = T_v -> IN
-//   else undecided: fused Refresh Row of iteration it+1.
-// M_w = 0 marks an inactive (phase-2) vertex and is ignored (reading Q15).
-template <int G, bool STATS>
-__device__ __forceinline__ int32_t decide_phase(const MisParams& p, int it, int64_t lo, int64_t hi,
-                                                int gw, int lane, uint64_t fi_next) {
-    constexpr int RPW = 32 / G;
-    const int grp = lane / G, sub = lane % G;
-    const bool dense = (it == 0);
-    const int64_t total = dense ? (hi - lo) : (int64_t)p.c1[gw];
-    int32_t k = 0;
-    long long r_acc = 0, e_acc = 0, d_acc = 0;
-    const unsigned tag = 2u * (unsigned)it + 2u;
-    for (int64_t base = 0; base < total; base += RPW) {
-        const int64_t idx = base + grp;
-        const bool valid = idx < total;
-        int64_t v = 0;
+// defer a long row to whole-block processing (group leader decides, group agrees)
+template <int GG>
+__device__ __forceinline__ bool defer_long(TileSmem& sm, bool act, int sub, int64_t v, int64_t len) {
+    bool defer = false;
+    if (act && sub == 0 && len > kHeavyDirect) {
+        const int h = atomicAdd(&sm.hcount, 1);
+        if (h < kHeavyList) {
+            sm.hlist[h] = (int32_t)v;
+            defer = true;
+        }
+    }
+    return __shfl_sync(kFull, defer, (threadIdx.x & 31) & ~(GG - 1));
+}
+
+// deferred long rows (whole block per row), stats flush, survivor count
+template <bool STATS, int PH>
+__device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, int32_t* lout, uint64_t fi_next,
+                            Stat& st) {
+    const int t = threadIdx.x;
+    const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
+    __syncthreads();
+    const int nh = min(sm.hcount, kHeavyList);
+    for (int h = 0; h < nh; h++) {
+        const int64_t v = sm.hlist[h];
+        const int64_t s = p.rowptr[v], e = p.rowptr[v + 1];
+        const uint64_t tv = p.T[v];
+        bool keep = false;
+        if (PH == 0) {
+            uint64_t m = (t == 0) ? tv : kOUT;
+            for (int64_t j = s + t; j < e; j += kBlock) {
+                const uint64_t tw = p.T[p.colinds[j]];
+                m = tw < m ? tw : m;
+            }
+            m = block_min_u64(sm, m);
+            if (t == 0) {
+                if (m == kIN) m = kOUT;
+                p.M[v] = m;
+                keep = (m != kOUT);
+            }
+        } else {
+            int any_out = 0, all_eq = 1;
+            if (t == 0) decide_acc(p.M[v], tv, any_out, all_eq);
+            for (int64_t j = s + t; j < e; j += kBlock) decide_acc(p.M[p.colinds[j]], tv, any_out, all_eq);
+            any_out = __syncthreads_or(any_out);
+            all_eq = __syncthreads_and(all_eq);
+            if (t == 0) keep = decide_write(p, v, any_out, all_eq, it, fi_next);
+        }
+        if (STATS) {
+            stat_row<STATS>(p, tag, v, t == 0, e - s, st);
+            stat_nbrs<STATS>(p, tag, p.colinds + s, e - s, t, kBlock, st);
+        }
+        append(sm, keep, (int32_t)v, lout, blo);
+    }
+    stats_flush<STATS>(p, it, PH == 0 ? 1 : 0, st);
+    __syncthreads();
+    const int out = sm.cnt;
+    __syncthreads();
+    return out;
+}
+
+// ------------------------------------------------------------ dense phase
+// Consecutive rows of the block range, RPB = kBlock/G per step; the step's
+// colinds span is bulk-copied into shared memory one step ahead.
+// PH = 0: Refresh Column over worklist_2 (M_v != OUT, active)
+// PH = 1: Decide over worklist_1 (T_v undecided)
+template <int G, bool STATS, int PH>
+__device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, int64_t bhi, int32_t* lout,
+                           uint32_t& ph, uint64_t fi_next) {
+    constexpr int RPB = kBlock / G;
+    const int t = threadIdx.x, g = t / G, sub = t % G;
+    const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
+    Stat st;
+    if (t == 0) {
+        sm.cnt = 0;
+        sm.hcount = 0;
+    }
+    const int64_t nsteps = (bhi - blo + RPB - 1) / RPB;
+    int64_t nx_s = 0, nx_e = 0;  // bounds of the next tile (thread 0), prefetched a step ahead
+    if (t == 0 && nsteps > 0) {
+        const int64_t r1 = blo + RPB < bhi ? blo + RPB : bhi;
+        const int64_t r2 = r1 + RPB < bhi ? r1 + RPB : bhi;
+        nx_s = p.rowptr[r1];
+        nx_e = p.rowptr[r2];
+        stage_tile(sm, p, 0, p.rowptr[blo], nx_s);
+    }
+    for (int64_t k = 0; k < nsteps; k++) {
+        const int slot = (int)(k & 1);
+        __syncthreads();  // tile k-1 consumed: its buffer may be refilled
+        if (t == 0 && k + 1 < nsteps) {
+            const int64_t s1 = nx_s, e1 = nx_e;
+            const int64_t r2 = blo + (k + 2) * RPB;
+            if (r2 < bhi) {
+                const int64_t r3 = r2 + RPB < bhi ? r2 + RPB : bhi;
+                nx_s = p.rowptr[r2];
+                nx_e = p.rowptr[r3];
+            }
+            stage_tile(sm, p, slot ^ 1, s1, e1);
+        }
+        const int64_t v = blo + k * RPB + g;
+        const bool valid = v < bhi;
+        int64_t s = 0, e = 0;
         uint64_t tv = kOUT;
         bool act = false;
         if (valid) {
-            v = dense ? lo + idx : (int64_t)p.L1[lo + idx];
+            s = p.rowptr[v];
+            e = p.rowptr[v + 1];
             tv = p.T[v];
-            act = (tv != kIN && tv != kOUT);
-        }
-        int any_out = 0, all_eq = 1;
-        if (act) {
-            const int64_t s = p.rowptr[v], e = p.rowptr[v + 1];
-            if (sub == 0) {
-                const uint64_t m = p.M[v];
-                any_out = (m == kOUT);
-                all_eq = (m == tv);
-            }
-            int64_t j = s + sub;
-            for (; j + 3 * G < e; j += 4 * G) {
-                const int32_t w0 = p.colinds[j], w1 = p.colinds[j + G], w2 = p.colinds[j + 2 * G],
-                              w3 = p.colinds[j + 3 * G];
-                const uint64_t m0 = p.M[w0], m1 = p.M[w1], m2 = p.M[w2], m3 = p.M[w3];
-                any_out |= (m0 == kOUT) | (m1 == kOUT) | (m2 == kOUT) | (m3 == kOUT);
-                all_eq &= (m0 == tv || m0 == 0) & (m1 == tv || m1 == 0) & (m2 == tv || m2 == 0) &
-                          (m3 == tv || m3 == 0);
-            }
-            for (; j < e; j += G) {
-                const uint64_t m = p.M[p.colinds[j]];
-                any_out |= (m == kOUT);
-                all_eq &= (m == tv || m == 0);
-            }
-            if (STATS) {
-                if (sub == 0) {
-                    r_acc++;
-                    e_acc += e - s;
-                    if (atomicMax(&p.mark[v], tag) < tag) d_acc++;
-                }
-                for (int64_t jj = s + sub; jj < e; jj += G)
-                    if (atomicMax(&p.mark[p.colinds[jj]], tag) < tag) d_acc++;
+            if (PH == 0) {
+                const uint64_t mv = p.M[v];
+                act = (mv != kOUT && mv != 0);
+            } else {
+                act = (tv != kIN && tv != kOUT);
             }
         }
-        any_out = group_or<G>(any_out);
-        all_eq = group_and<G>(all_eq);
-        bool keep = false;
-        if (act && sub == 0) {
-            if (any_out) p.T[v] = kOUT;
-            else if (all_eq) p.T[v] = kIN;
-            else {
-                p.T[v] = p.prio.word(it + 1, fi_next, v);
-                keep = true;
-            }
+        const int64_t len = e - s;
+        if (defer_long<G>(sm, act, sub, v, len)) act = false;
+        mbar_wait(&sm.mbar[slot], (ph >> slot) & 1u);
+        ph ^= 1u << slot;
+        const int32_t* x = sm.fits[slot] ? sm.buf[slot] + (s - sm.sal[slot]) : p.colinds + s;
+        const bool keep = process_row<G, PH>(p, act, sub, v, x, (int)len, tv, it, fi_next);
+        if (STATS && act) {
+            stat_row<STATS>(p, tag, v, sub == 0, len, st);
+            stat_nbrs<STATS>(p, tag, x, len, sub, G, st);
         }
-        const unsigned ball = __ballot_sync(kFull, keep);
-        if (keep) p.L1[lo + k + __popc(ball & lanemask_lt())] = (int32_t)v;
-        k += __popc(ball);
+        append(sm, keep, (int32_t)v, lout, blo);
     }
-    if (lane == 0) p.c1[gw] = k;
-    if (STATS) {
-        long long r_tot = warp_sum_ll(r_acc), e_tot = warp_sum_ll(e_acc), d_tot = warp_sum_ll(d_acc);
-        if (lane == 0) {
-            long long* st = p.dstats + 6 * it;
-            atomicAdd((unsigned long long*)&st[0], (unsigned long long)r_tot);
-            atomicAdd((unsigned long long*)&st[2], (unsigned long long)e_tot);
-            atomicAdd((unsigned long long*)&st[4], (unsigned long long)d_tot);
-        }
-    }
-    return k;
+    return finish_phase<STATS, PH>(sm, p, it, blo, lout, fi_next, st);
 }
 
+// ------------------------------------------------------------ sparse phase
+// Rows of the block's compacted worklist, RPBS = kBlock/GS per step with
+// GS = 2G lanes per row.  Each group leader bulk-copies its own row into a
+// fixed shared-memory slot (16-byte aligned hull, <= SLOT entries) one step
+// ahead; rows that do not fit are read from global memory.
+struct __align__(16) SMeta {
+    int64_t s;    // rowptr[v]
+    int32_t v;    // vertex (-1: no row)
+    int32_t len;  // row length; bit 30 set: staged in the slot
+};
+constexpr int kSlotRegion = 6144;  // entries of a buffer used for row slots; SMeta array after it
+
+template <int G, bool STATS, int PH>
+__device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, const int32_t* lin, int nin,
+                            int32_t* lout, uint32_t& ph, uint64_t fi_next) {
+    constexpr int GS = G * 2 <= 32 ? G * 2 : 32;
+    constexpr int RPBS = kBlock / GS;
+    constexpr int SLOT = (kSlotRegion / RPBS) & ~3;
+    static_assert(RPBS * sizeof(SMeta) <= (kTileCap - kSlotRegion) * 4, "SMeta region too small");
+    constexpr int kStaged = 1 << 30;
+    const int t = threadIdx.x, gs = t / GS, sub = t % GS;
+    const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
+    Stat st;
+    if (t == 0) {
+        sm.cnt = 0;
+        sm.hcount = 0;
+    }
+    const int nsteps = (nin + RPBS - 1) / RPBS;
+    const int64_t nnz4 = p.nnz & ~(int64_t)3;
+
+    // leaders: fetch the row of tile j, stage it, record its metadata
+    auto plan = [&](int j, int slot) {
+        if (sub != 0) return;
+        SMeta* meta = reinterpret_cast<SMeta*>(sm.buf[slot] + kSlotRegion);
+        const int idx = j * RPBS + gs;
+        SMeta m;
+        m.v = -1;
+        m.s = 0;
+        m.len = 0;
+        uint32_t bytes = 0;
+        int64_t sal = 0;
+        if (idx < nin) {
+            const int64_t v = lin[blo + idx];
+            const int64_t s = p.rowptr[v], e = p.rowptr[v + 1];
+            sal = s & ~(int64_t)3;
+            const int64_t ecp = (e + 3) & ~(int64_t)3;
+            const bool fits = (ecp - sal) <= SLOT && ecp <= nnz4;
+            m.v = (int32_t)v;
+            m.s = s;
+            m.len = (int32_t)(e - s) | (fits ? kStaged : 0);
+            if (fits && ecp > sal) bytes = (uint32_t)((ecp - sal) * 4);
+        }
+        meta[gs] = m;
+        mbar_expect_tx(&sm.mbarS[slot], bytes);
+        if (bytes) bulk_g2s(sm.buf[slot] + gs * SLOT, p.colinds + sal, bytes, &sm.mbarS[slot]);
+    };
+
+    if (nsteps > 0) {
+        fence_proxy_async();
+        plan(0, 0);
+    }
+    for (int k = 0; k < nsteps; k++) {
+        const int slot = k & 1;
+        __syncthreads();  // metadata of tile k visible; buffer of tile k-1 free
+        const SMeta m = reinterpret_cast<const SMeta*>(sm.buf[slot] + kSlotRegion)[gs];
+        const bool valid = m.v >= 0;
+        const int64_t v = valid ? m.v : 0;
+        const int len = m.len & ~kStaged;
+        uint64_t tv = kOUT;
+        if (valid) tv = p.T[v];  // status first: overlaps the planning chain below
+        if (k + 1 < nsteps) {
+            fence_proxy_async();
+            plan(k + 1, slot ^ 1);
+        }
+        bool act = valid;
+        if (defer_long<GS>(sm, act, sub, v, len)) act = false;
+        mbar_wait(&sm.mbarS[slot], (ph >> (2 + slot)) & 1u);
+        ph ^= 1u << (2 + slot);
+        const int32_t* x = (m.len & kStaged) ? sm.buf[slot] + gs * SLOT + (m.s - (m.s & ~(int64_t)3))
+                                             : p.colinds + m.s;
+        const bool keep = process_row<GS, PH>(p, act, sub, v, x, len, tv, it, fi_next);
+        if (STATS && act) {
+            stat_row<STATS>(p, tag, v, sub == 0, len, st);
+            stat_nbrs<STATS>(p, tag, x, len, sub, GS, st);
+        }
+        append(sm, keep, (int32_t)v, lout, blo);
+    }
+    return finish_phase<STATS, PH>(sm, p, it, blo, lout, fi_next, st);
+}
+
+__device__ __forceinline__ void stamp(const MisParams& p, int slot) {
+    if (p.timeline && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        p.timeline[slot] = (long long)ns;
+    }
+}
+
+// ------------------------------------------------------------ the kernel
 template <int G, bool STATS>
 __global__ void __launch_bounds__(kBlock) mis2_persistent(MisParams p) {
-    __shared__ long long s_tmp[kWarpsPerBlock];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int W = gridDim.x * kWarpsPerBlock;
-    const int gw = blockIdx.x * kWarpsPerBlock + warp;
-    const int64_t lo = p.n * gw / W, hi = p.n * (gw + 1) / W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+    const int t = threadIdx.x;
+    const int64_t B = gridDim.x;
+    const int64_t blo = p.n * blockIdx.x / B, bhi = p.n * (blockIdx.x + 1) / B;
     unsigned int* bar = (unsigned int*)&p.ctrl[0];
     unsigned long long* ring = &p.ctrl[1];
 
-    // worklists <- 0..|V| and Refresh Row of iteration 0
+    if (t == 0) {
+        mbar_init(&sm.mbar[0], 1);
+        mbar_init(&sm.mbar[1], 1);
+        constexpr int kRowGroups = kBlock / (G * 2 <= 32 ? G * 2 : 32);
+        mbar_init(&sm.mbarS[0], kRowGroups);
+        mbar_init(&sm.mbarS[1], kRowGroups);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    uint32_t ph = 0u;  // mbarrier phase bits: 0,1 dense buffers; 2,3 sparse buffers
+
+    // worklists <- 0..|V|; Refresh Row of iteration 0
     {
         const uint64_t fi0 = p.prio.iter_term(0);
-        for (int64_t v = lo + lane; v < hi; v += 32) {
+        int act_cnt = 0;
+        for (int64_t v = blo + t; v < bhi; v += kBlock) {
             const bool act = p.labels ? (p.labels[v] < 0) : true;
             p.T[v] = act ? p.prio.word(0, fi0, v) : kOUT;
-            if (!act) p.M[v] = 0;  // inactive sentinel (reading Q15)
+            p.M[v] = act ? kPending : 0;  // 0 = inactive sentinel (reading Q15)
+            act_cnt += act;
         }
+        const long long s = block_sum_int(sm, act_cnt);
+        if (t == 0 && s) atomicAdd(&p.ctrl[7], (unsigned long long)s);
     }
     grid_barrier(bar);
+    stamp(p, 0);
+    const unsigned long long n_active = ld_acquire_u64(&p.ctrl[7]);
 
     int it = 0;
     int status = MIS2_OK;
-    for (;;) {
-        column_phase<G, STATS>(p, it, lo, hi, gw, lane);
+    const int64_t range = bhi - blo;
+    int cnt1 = (int)range, cnt2 = (int)range;  // this block's worklist segment sizes
+    while (n_active > 0) {  // while worklist_1 != {}
+        const int cur = it & 1;
+        // ---- Refresh Column over worklist_2
+        const bool dense2 = (it == 0) || (int64_t)cnt2 * kDenseDen >= range * kDenseNum;
+        cnt2 = dense2 ? dense_phase<G, STATS, 0>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0)
+                      : sparse_phase<G, STATS, 0>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
         grid_barrier(bar);
+        stamp(p, 1 + 2 * it);
+        // ---- Decide over worklist_1 + fused refresh of iteration it+1
         const uint64_t fi_next = p.prio.iter_term(it + 1);
-        const int32_t k = decide_phase<G, STATS>(p, it, lo, hi, gw, lane, fi_next);
-        const long long bsum = block_sum_warps(lane == 0 ? k : 0, s_tmp);
-        if (threadIdx.x == 0) {
-            if (bsum) atomicAdd(&ring[it & 3], (unsigned long long)bsum);
-            if (blockIdx.x == 0) ring[(it + 2) & 3] = 0;  // slot read two barriers ago
+        const bool dense1 = (it == 0) || (int64_t)cnt1 * kDenseDen >= range * kDenseNum;
+        cnt1 = dense1 ? dense_phase<G, STATS, 1>(sm, p, it, blo, bhi, p.L1[cur ^ 1], ph, fi_next)
+                      : sparse_phase<G, STATS, 1>(sm, p, it, blo, p.L1[cur], cnt1, p.L1[cur ^ 1], ph, fi_next);
+        if (t == 0) {
+            if (cnt1) atomicAdd(&ring[it & 3], (unsigned long long)cnt1);
+            if (blockIdx.x == 0) ring[(it + 2) & 3] = 0;  // slot last read two barriers ago
         }
         grid_barrier(bar);
+        stamp(p, 2 + 2 * it);
         const unsigned long long remaining = ld_acquire_u64(&ring[it & 3]);
         it++;
-        if (remaining == 0) break;        // worklist_1 empty
-        if (it >= p.max_iters) {          // reading Q12
+        if (remaining == 0) break;
+        if (it >= p.max_iters) {  // reading Q12
             status = MIS2_ENOTCONVERGED;
             break;
         }
     }
 
     // return {v : T_v = IN}
-    long long cnt = 0;
-    for (int64_t v = lo + lane; v < hi; v += 32) {
+    int cnt = 0;
+    for (int64_t v = blo + t; v < bhi; v += kBlock) {
         const uint8_t in = (p.T[v] == kIN);
         p.in_set[v] = in;
         cnt += in;
     }
-    cnt = warp_sum_ll(cnt);
-    const long long bcnt = block_sum_warps(lane == 0 ? cnt : 0, s_tmp);
-    if (threadIdx.x == 0) {
-        atomicAdd(&p.ctrl[5], (unsigned long long)bcnt);
+    const long long bc = block_sum_int(sm, cnt);
+    if (t == 0) {
+        atomicAdd(&p.ctrl[5], (unsigned long long)bc);
         __threadfence();
         const unsigned long long ticket = atomicAdd(&p.ctrl[6], 1ull);
         if (ticket == gridDim.x - 1) {  // last block publishes the scalars
@@ -287,9 +610,9 @@ int max_iters_for(int64_t n, int requested) { return requested > 0 ? requested :
 int choose_group(int64_t n, int64_t nnz, int requested) {
     if (requested > 0) return requested;
     const double avg = n > 0 ? (double)nnz / (double)n : 0.0;
-    // about 4 entries per lane; a warp per row only for long rows
+    // a step of kBlock / G rows should fit one staging buffer
     int g = 1;
-    while (g < 32 && g * 4 < avg) g *= 2;
+    while (g < 32 && (double)(kBlock / g) * avg > (double)kTileCap) g *= 2;
     return g;
 }
 
@@ -310,34 +633,32 @@ static void* pick_kernel(int G, bool stats) {
     return nullptr;
 }
 
-int max_coop_warps(const DeviceInfo& d) {
-    // upper bound used for workspace sizing: 64 resident warps per SM
-    return d.sms * 64;
-}
+int max_coop_warps(const DeviceInfo& d) { return d.sms * 64; }
 
 void carve_mis2(Carve& c, int64_t n, int max_warps, Mis2Ws* w) {
+    (void)max_warps;
     w->ctrl = c.take<unsigned long long>(16);
     w->T = c.take<uint64_t>((size_t)n + 1);
     w->M = c.take<uint64_t>((size_t)n + 1);
-    w->L1 = c.take<int32_t>((size_t)n + 1);
-    w->L2 = c.take<int32_t>((size_t)n + 1);
-    w->c1 = c.take<int32_t>((size_t)max_warps);
-    w->c2 = c.take<int32_t>((size_t)max_warps);
+    for (int i = 0; i < 2; i++) {
+        w->L1[i] = c.take<int32_t>((size_t)n + 1);
+        w->L2[i] = c.take<int32_t>((size_t)n + 1);
+    }
     w->mark = c.take<unsigned int>((size_t)n + 1);
     w->dstats = c.take<long long>((size_t)kStatsMaxIters * 6);
     w->scal = c.take<long long>(8);
 }
 
-int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uint8_t* in_set,
-             int64_t* d_count, int32_t* d_iters, int32_t* d_status, int64_t* stats_host,
-             const Mis2Ws& w, cudaStream_t s) {
+int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uint8_t* in_set, int64_t* d_count,
+             int32_t* d_iters, int32_t* d_status, int64_t* stats_host, const Mis2Ws& w, cudaStream_t s) {
     DeviceInfo di;
     MIS2_TRY(device_info(&di));
     const int G = choose_group(g.n, g.nnz, o.group);
-    const bool stats = stats_host != nullptr;
+    const bool timeline = stats_host != nullptr && (o.flags & MIS2_FLAG_TIMELINE);
+    const bool stats = stats_host != nullptr && !timeline;
     const int max_iters = max_iters_for(g.n, o.max_iters);
-    if (stats && max_iters > kStatsMaxIters) {
-        set_error("stats mode supports max_iters <= %d", kStatsMaxIters);
+    if ((stats && max_iters > kStatsMaxIters) || (timeline && 2 * max_iters + 2 > kStatsMaxIters * 6)) {
+        set_error("stats/timeline mode supports max_iters <= %d", kStatsMaxIters);
         return MIS2_EINVAL;
     }
     void* fn = pick_kernel(G, stats);
@@ -345,14 +666,22 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
         set_error("group must be one of 1,2,4,8,16,32 (got %d)", G);
         return MIS2_EINVAL;
     }
+    const int smem = (int)sizeof(TileSmem);
+    MIS2_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0;
-    MIS2_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, 0));
+    MIS2_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, smem));
     if (per_sm < 1) {
         set_error("persistent kernel does not fit on an SM");
         return MIS2_EINTERNAL;
     }
+    if (const char* env = getenv("MIS2_BLOCKS_PER_SM")) {  // tuning knob (measurement only)
+        const int want_per_sm = atoi(env);
+        if (want_per_sm >= 1 && want_per_sm < per_sm) per_sm = want_per_sm;
+    }
     const int64_t max_grid = (int64_t)per_sm * di.sms;
-    int64_t want = (g.n + kBlock - 1) / kBlock;
+    // small graphs: about two steps of rows per block
+    const int64_t rpb = kBlock / G;
+    const int64_t want = (g.n + 2 * rpb - 1) / (2 * rpb);
     const int grid = (int)(want < 1 ? 1 : (want > max_grid ? max_grid : want));
 
     MIS2_CUDA_TRY(cudaMemsetAsync(w.ctrl, 0, 16 * sizeof(unsigned long long), s));
@@ -364,18 +693,20 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     }
     MisParams p;
     p.n = g.n;
+    p.nnz = g.nnz;
     p.rowptr = g.rowptr;
     p.colinds = g.colinds;
     p.labels = labels;
     p.T = w.T;
     p.M = w.M;
-    p.L1 = w.L1;
-    p.L2 = w.L2;
-    p.c1 = w.c1;
-    p.c2 = w.c2;
+    for (int i = 0; i < 2; i++) {
+        p.L1[i] = w.L1[i];
+        p.L2[i] = w.L2[i];
+    }
     p.ctrl = w.ctrl;
     p.mark = w.mark;
     p.dstats = w.dstats;
+    p.timeline = timeline ? w.dstats : nullptr;
     p.prio.scheme = o.scheme;
     p.prio.b = bits_for(g.n);
     p.prio.seed = o.seed;
@@ -389,11 +720,11 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     p.d_iters = d_iters;
     p.d_status = d_status;
     void* args[] = {&p};
-    MIS2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args, 0, s));
+    MIS2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args, smem, s));
     count_launch();
-    if (stats) {
-        MIS2_CUDA_TRY(cudaMemcpyAsync(stats_host, w.dstats, sizeof(long long) * 6 * (size_t)max_iters,
-                                      cudaMemcpyDeviceToHost, s));
+    if (stats || timeline) {
+        const size_t cnt = stats ? 6 * (size_t)max_iters : 2 * (size_t)max_iters + 2;
+        MIS2_CUDA_TRY(cudaMemcpyAsync(stats_host, w.dstats, sizeof(long long) * cnt, cudaMemcpyDeviceToHost, s));
         MIS2_CUDA_TRY(cudaStreamSynchronize(s));
     }
     return MIS2_OK;

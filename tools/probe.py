@@ -26,3 +26,9 @@ for grp in [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["
         s.record(); m.mis2_async(rp, ci, out, sc, group=grp); e.record(); torch.cuda.synchronize()
         warm.append(s.elapsed_time(e))
     print(f"cfg{cfg} n={g.n} nnz={g.nnz} G={grp} count={r.count} it={r.iterations} cold(L2 flushed) med {ts[len(ts)//2]:.4f} ms min {ts[0]:.4f}  warm med {sorted(warm)[5]:.4f} ms  GTEPS(cold) {g.nnz/ts[len(ts)//2]/1e6:.1f}", flush=True)
+
+if os.environ.get("TIMELINE"):
+    for grp in [1, 2]:
+        m.mis2(rp, ci, group=grp)
+        r = m.mis2(rp, ci, group=grp, timeline=True)
+        print(f"G={grp} phase us (col,dec per iteration):", np.round(r.stats, 1).tolist(), "sum", round(float(r.stats.sum()), 1))
