@@ -1,0 +1,315 @@
+#!/usr/bin/env python
+"""bench.py -- MIS-2 on the BASELINE.json headline workload (27-point
+Laplacian 100^3, BASELINE.json configs[1]) through the C ABI of libmis2.so.
+
+One "step" = one whole MIS-2 call (Alg. 1): init, every
+Refresh Column / Decide pass, worklist compaction, loop control, output.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  Timing rules: W untimed warm-up calls; K timed
+calls, each bracketed by CUDA events on the launching stream; the L2 is
+flushed (a 512 MiB memset) BETWEEN timed calls, outside the event pairs;
+barrier + synchronize around the timed region; max over ranks.  SM clocks and
+throttle reasons are sampled with NVML during the timed region.
+
+`--impl reference` times the CPU oracle (oracle/, serial C, 1 thread) on the
+same workload: this tier has no reference implementation, the oracle is the
+reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "MIS-2 ms & GTEPS on 27-pt 100^3 Laplacian, %HBM peak, at 1/2/4/8 B200"
+UNIT = "GTEPS"
+WORKLOAD = "MIS-2 (Alg. 1) on the 27-point Laplacian 100^3 graph (BASELINE.json configs[1])"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def alg_bytes(stats: np.ndarray, n: int) -> int:
+    """Compulsory HBM bytes of one MIS-2 call for this implementation's data
+    layout: T uint64, M uint32 (id field),
+    colinds int32, rowptr int64, worklists int32.  stats rows = iterations:
+    |wl1| |wl2| E1 E2 |N[wl1]| |N[wl2]|."""
+    total = 8 * n + 4 * n  # init: T, M
+    it = stats.shape[0]
+    for i in range(it):
+        w1, w2, e1, e2, d1, d2 = (int(x) for x in stats[i])
+        w1n = int(stats[i + 1, 0]) if i + 1 < it else 0
+        w2n = int(stats[i + 1, 1]) if i + 1 < it else 0
+        total += 4 * e2 + 8 * d2 + (8 + 4 + 4) * w2 + 4 * w2n          # Refresh Column
+        total += 4 * e1 + 4 * d1 + (8 + 4 + 8 + 8) * w1 + 4 * w1n      # Decide (+ refresh)
+    total += 8 * n + 1 * n  # output: read T, write in_set
+    return total
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + clock-event reasons during the timed region."""
+
+    NAMES = {
+        "nvmlClocksEventReasonHwSlowdown": "hw_slowdown",
+        "nvmlClocksEventReasonHwThermalSlowdown": "hw_thermal_slowdown",
+        "nvmlClocksEventReasonSwThermalSlowdown": "sw_thermal_slowdown",
+        "nvmlClocksEventReasonSwPowerCap": "sw_power_cap",
+        "nvmlClocksEventReasonHwPowerBrakeSlowdown": "hw_power_brake_slowdown",
+        "nvmlClocksEventReasonApplicationsClocksSetting": "applications_clocks_setting",
+        "nvmlClocksEventReasonSyncBoost": "sync_boost",
+    }
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons = [], set()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for attr, name in self.NAMES.items():
+                    if r & getattr(nv, attr, 0):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": float(self.max_mhz),
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+def cpu_oracle_rate(g, seconds: float):
+    """Serial C oracle (1 thread) on the same graph for about `seconds`."""
+    import oracle as O
+    runs, t0 = 0, time.perf_counter()
+    while True:
+        r = O.mis2(g.rowptr, g.colinds)
+        runs += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return g.nnz * runs / el / 1e9, runs, el, r
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import mis2gen as G
+    import oracle as O
+    g = G.config_graph(args.config)
+    for _ in range(args.warmup):
+        O.mis2(g.rowptr, g.colinds)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        r = O.mis2(g.rowptr, g.colinds)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = g.nnz / (ms / 1e3) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n": g.n, "nnz": g.nnz, "seed": 0, "mis2_size": r.count,
+                   "iterations": r.iterations},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} full serial MIS-2 calls (oracle/oracle.c, 1 thread) on the "
+                                   f"full workload"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    import mis2gen as G
+    import paper_2204_02934_b200 as m
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+
+    g = G.config_graph(args.config)
+    rp = torch.from_numpy(g.rowptr).cuda()
+    ci = torch.from_numpy(g.colinds).cuda()
+    out = torch.empty(g.n, dtype=torch.uint8, device="cuda")
+    sc = torch.zeros(2, dtype=torch.int64, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    # instrumented (untimed) call: worklist statistics for the byte model
+    st = m.mis2(rp, ci, stats=True)
+    check = m.mis2(rp, ci)
+    bytes_per_call = alg_bytes(st.stats, g.n)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        m.mis2_async(rp, ci, out, sc)
+    torch.cuda.synchronize()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches = 0
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(dev)
+    wall0 = time.perf_counter()
+    with sampler:
+        for k in range(args.steps):
+            flush.zero_()                          # L2 flush, outside the timed pair
+            evs[k][0].record(stream)
+            launches += m.mis2_async(rp, ci, out, sc)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        torch.distributed.barrier()
+    per = [a.elapsed_time(b) for a, b in evs]  # ms
+    ms = sum(per) / len(per)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * g.nnz / (ms / 1e3) / 1e9  # replicas: every rank solves the full graph
+    scal = sc.cpu().tolist()
+    assert scal[0] == check.count, "timed calls disagree with the checked call"
+
+    peak, peak_src = peaks()
+    achieved = bytes_per_call / (ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            td = json.load(fh)
+        if td.get("n") == g.n and td.get("nnz") == g.nnz:
+            traffic = td.get("dram_bytes_per_launch")
+
+    # end-to-end through mis2_host(): pinned host CSR in, in_set out
+    e2e = None
+    if not args.no_e2e:
+        rph = torch.from_numpy(g.rowptr).pin_memory()
+        cih = torch.from_numpy(g.colinds).pin_memory()
+        outh = torch.empty(g.n, dtype=torch.uint8).pin_memory()
+        ws = m.workspace(m.OP_MIS2_HOST, g.n, g.nnz)
+        for _ in range(2):
+            m.mis2_host(rph, cih, outh, ws=ws)
+        e_ms = []
+        for _ in range(max(3, min(args.steps, 20))):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            m.mis2_host(rph, cih, outh, ws=ws)
+            b.record(stream)
+            b.synchronize()
+            e_ms.append(a.elapsed_time(b))
+        ems = sum(e_ms) / len(e_ms)
+        assert int(outh.sum()) == check.count
+        e2e = {"value": world * g.nnz / (ems / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": int(g.rowptr.nbytes + g.colinds.nbytes), "d2h_bytes_per_step": int(g.n + 16)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, runs, el, _ = cpu_oracle_rate(g, args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{runs} full serial MIS-2 calls of the oracle (oracle/oracle.c, 1 thread) on the same "
+                         f"graph, {el:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n": g.n, "nnz": g.nnz, "seed": 0, "generator":
+                       "mis2gen.laplace3d_27pt(100)", "mis2_size": check.count, "iterations": check.iterations,
+                       "l2": "flushed between timed steps (512 MiB memset outside the event pairs)",
+                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                       "ms_min": min(per), "ms_median": statistics.median(per), "wall_s": wall},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "mis2k::mis2_persistent",
+                         "alg_bytes_per_launch": bytes_per_call, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": sampler.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1, help="BASELINE.json configs index (bench workload: 1)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

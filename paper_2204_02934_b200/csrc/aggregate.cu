@@ -343,7 +343,6 @@ int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int6
     const int G = choose_group(g.n, g.nnz, o.group);
     int32_t* s32 = (int32_t*)w.scal;
     MIS2_CUDA_TRY(cudaMemsetAsync(w.scal, 0, 32 * sizeof(long long), s));
-    count_launch();
 
     // ---- phase 1: M1 = MIS2(G)
     MIS2_TRY(run_mis2(g, o, nullptr, w.in1, (int64_t*)&w.scal[kCount1], &s32[2 * kIters1],
@@ -360,7 +359,6 @@ int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int6
 
     // ---- phase 3: frozen tentative labels, max coupling / min size / min id
     MIS2_CUDA_TRY(cudaMemsetAsync(w.size, 0, sizeof(int32_t) * ((size_t)n + 1), s));
-    count_launch();
     {
         int64_t blocks = (n + kBlock - 1) / kBlock;
         if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;

@@ -246,7 +246,6 @@ int run_coarsen(const mis2_graph& g, const int32_t* labels, int64_t na, int64_t*
     count_launch(2);
     MIS2_TRY(scan_counts64((const int64_t*)seglen, na, sptr, tmp, s));
     MIS2_CUDA_TRY(cudaMemcpyAsync(cursor, sptr, sizeof(int64_t) * (size_t)na, cudaMemcpyDeviceToDevice, s));
-    count_launch();
     {
         const int64_t rows_per_block = (int64_t)(kBlock / 32) * (32 / G);
         int64_t fb = (n + rows_per_block - 1) / rows_per_block;

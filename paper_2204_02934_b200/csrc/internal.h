@@ -59,7 +59,7 @@ constexpr int kStatsMaxIters = 400;
 // MIS-2 state carved from the workspace
 struct Mis2Ws {
     uint64_t* T;
-    uint64_t* M;
+    uint32_t* M;
     int32_t* L1[2];
     int32_t* L2[2];
     unsigned int* mark;

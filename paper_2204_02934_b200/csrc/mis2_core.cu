@@ -38,7 +38,17 @@ constexpr int kTileCap = 6912;      // int32 colinds per staging buffer (27 KB):
 constexpr int kHeavyDirect = 2048;  // rows longer than this are reduced by the whole block
 constexpr int kHeavyList = 64;
 constexpr int kDenseNum = 3, kDenseDen = 8;  // dense if |worklist segment| >= 3/8 of the range
-constexpr uint64_t kPending = 1ull;          // M of an active vertex before its first column pass
+// M_v is only ever compared against T_v (Decide: "M_w = T_v", "M_w = OUT").
+// By Eq. 1 the low b bits of an undecided word are id+1, unique per vertex,
+// never 0 and never all ones (2^b - 1 > |V|), and M_w is always a
+// word of the CURRENT iteration (worklist_2 vertices are recomputed every
+// iteration, the others hold OUT).  Hence M_w = T_v  <=>  id(M_w) = v + 1 and
+// M_w = OUT <=> id(M_w) = all ones, so M is stored as a uint32 id field:
+//   kM_OUT   : M_v = OUT
+//   0        : inactive vertex (phase 2, reading Q15) -- ignored by Decide
+//   a + 1    : M_v = T_a (a = argmin of T over N[v])
+constexpr uint32_t kM_OUT = 0xffffffffu;
+constexpr uint32_t kPending = 1u;  // M of an active vertex before its first column pass
 
 struct MisParams {
     int64_t n;
@@ -46,8 +56,9 @@ struct MisParams {
     const int64_t* __restrict__ rowptr;
     const int32_t* __restrict__ colinds;
     const int32_t* __restrict__ labels;  // phase-2 mask (active iff labels[v] < 0) or null
-    uint64_t* T;                         // row status T_v
-    uint64_t* M;                         // column status M_v
+    uint64_t* T;                         // row status T_v (64-bit packed word, Eq. 1)
+    uint32_t* M;                         // column status M_v, stored as its id field (see below)
+    uint32_t id_mask;                    // 2^b - 1
     int32_t* L1[2];                      // worklist_1, double buffered, per-block segments
     int32_t* L2[2];                      // worklist_2
     unsigned long long* ctrl;
@@ -179,42 +190,47 @@ __device__ __forceinline__ void stats_flush(const MisParams& p, int it, int slot
 // ------------------------------------------------------------ row kernels
 // Refresh Column of one row: min of T over the row's entries x[0..len)
 // (x is shared memory or global; generic addressing), lanes sub, sub+G, ...
+// Indices past the row end are clamped to its last entry: min / exists /
+// forall are idempotent, so a repeated entry never changes the result and the
+// loads need no predicate.
 template <int G>
-__device__ __forceinline__ uint64_t row_min(const MisParams& p, const int32_t* x, int len, int sub, uint64_t m) {
+__device__ __forceinline__ uint64_t row_min(const uint64_t* __restrict__ T, const int32_t* x, int len, int sub,
+                                            uint64_t m) {
     constexpr int B = G == 1 ? 16 : (G == 2 ? 8 : 4);
+    const int last = len - 1;
     for (int j = sub; j < len; j += B * G) {
         uint64_t tt[B];
 #pragma unroll
-        for (int q = 0; q < B; q++) {
-            const int jj = j + q * G;
-            tt[q] = jj < len ? p.T[x[jj]] : kOUT;
-        }
+        for (int q = 0; q < B; q++) tt[q] = T[x[min(j + q * G, last)]];
 #pragma unroll
         for (int q = 0; q < B; q++) m = tt[q] < m ? tt[q] : m;
     }
     return m;
 }
 
-// Decide of one row: exists M_w = OUT / forall M_w = T_v,
-// M_w = 0 (inactive, reading Q15) ignored.
-__device__ __forceinline__ void decide_acc(uint64_t m, uint64_t tv, int& any_out, int& all_eq) {
-    any_out |= (m == kOUT);
-    all_eq &= (m == tv) | (m == 0);
+// Decide of one row on id fields: exists M_w = OUT / forall
+// M_w = T_v (id v+1); M_w = 0 (inactive, reading Q15) is ignored.
+__device__ __forceinline__ void decide_acc(uint32_t m, uint32_t vid1, int& any_out, int& all_eq) {
+    any_out |= (m == kM_OUT);
+    all_eq &= (m == vid1) | (m == 0u);
 }
 template <int G>
-__device__ __forceinline__ void row_decide(const MisParams& p, const int32_t* x, int len, int sub, uint64_t tv,
-                                           int& any_out, int& all_eq) {
+__device__ __forceinline__ void row_decide(const uint32_t* __restrict__ M, const int32_t* x, int len, int sub,
+                                           uint32_t vid1, int& any_out, int& all_eq) {
     constexpr int B = G == 1 ? 16 : (G == 2 ? 8 : 4);
+    const int last = len - 1;
     for (int j = sub; j < len; j += B * G) {
-        uint64_t mm[B];
+        uint32_t mm[B];
 #pragma unroll
-        for (int q = 0; q < B; q++) {
-            const int jj = j + q * G;
-            mm[q] = jj < len ? p.M[x[jj]] : tv;
-        }
+        for (int q = 0; q < B; q++) mm[q] = M[x[min(j + q * G, last)]];
 #pragma unroll
-        for (int q = 0; q < B; q++) decide_acc(mm[q], tv, any_out, all_eq);
+        for (int q = 0; q < B; q++) decide_acc(mm[q], vid1, any_out, all_eq);
     }
+}
+
+// M_v from the column minimum m (IN -> OUT)
+__device__ __forceinline__ uint32_t m_field(uint64_t m, uint32_t id_mask) {
+    return (m == kIN || m == kOUT) ? kM_OUT : (uint32_t)m & id_mask;
 }
 
 __device__ __forceinline__ bool decide_write(const MisParams& p, int64_t v, int any_out, int all_eq, int it,
@@ -256,18 +272,19 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
     bool keep = false;
     if (PH == 0) {
         uint64_t m = (act && sub == 0) ? tv : kOUT;  // closed neighbourhood (Q1)
-        if (act) m = row_min<GG>(p, x, len, sub, m);
+        if (act && len > 0) m = row_min<GG>(p.T, x, len, sub, m);
         m = group_min<GG>(m);
         if (act && sub == 0) {
-            if (m == kIN) m = kOUT;
-            p.M[v] = m;
-            keep = (m != kOUT);
+            const uint32_t mf = m_field(m, p.id_mask);
+            p.M[v] = mf;
+            keep = (mf != kM_OUT);
         }
     } else {
         int any_out = 0, all_eq = 1;
+        const uint32_t vid1 = (uint32_t)v + 1u;
         if (act) {
-            if (sub == 0) decide_acc(p.M[v], tv, any_out, all_eq);
-            row_decide<GG>(p, x, len, sub, tv, any_out, all_eq);
+            if (sub == 0) decide_acc(p.M[v], vid1, any_out, all_eq);
+            if (len > 0) row_decide<GG>(p.M, x, len, sub, vid1, any_out, all_eq);
         }
         any_out = group_or<GG>(any_out);
         all_eq = group_and<GG>(all_eq);
@@ -311,14 +328,15 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
             }
             m = block_min_u64(sm, m);
             if (t == 0) {
-                if (m == kIN) m = kOUT;
-                p.M[v] = m;
-                keep = (m != kOUT);
+                const uint32_t mf = m_field(m, p.id_mask);
+                p.M[v] = mf;
+                keep = (mf != kM_OUT);
             }
         } else {
             int any_out = 0, all_eq = 1;
-            if (t == 0) decide_acc(p.M[v], tv, any_out, all_eq);
-            for (int64_t j = s + t; j < e; j += kBlock) decide_acc(p.M[p.colinds[j]], tv, any_out, all_eq);
+            const uint32_t vid1 = (uint32_t)v + 1u;
+            if (t == 0) decide_acc(p.M[v], vid1, any_out, all_eq);
+            for (int64_t j = s + t; j < e; j += kBlock) decide_acc(p.M[p.colinds[j]], vid1, any_out, all_eq);
             any_out = __syncthreads_or(any_out);
             all_eq = __syncthreads_and(all_eq);
             if (t == 0) keep = decide_write(p, v, any_out, all_eq, it, fi_next);
@@ -384,8 +402,8 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
             e = p.rowptr[v + 1];
             tv = p.T[v];
             if (PH == 0) {
-                const uint64_t mv = p.M[v];
-                act = (mv != kOUT && mv != 0);
+                const uint32_t mv = p.M[v];
+                act = (mv != kM_OUT && mv != 0u);
             } else {
                 act = (tv != kIN && tv != kOUT);
             }
@@ -505,7 +523,7 @@ __device__ __forceinline__ void stamp(const MisParams& p, int slot) {
 
 // ------------------------------------------------------------ the kernel
 template <int G, bool STATS>
-__global__ void __launch_bounds__(kBlock) mis2_persistent(MisParams p) {
+__global__ void __launch_bounds__(kBlock, 4) mis2_persistent(MisParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
     const int t = threadIdx.x;
@@ -531,7 +549,7 @@ __global__ void __launch_bounds__(kBlock) mis2_persistent(MisParams p) {
         for (int64_t v = blo + t; v < bhi; v += kBlock) {
             const bool act = p.labels ? (p.labels[v] < 0) : true;
             p.T[v] = act ? p.prio.word(0, fi0, v) : kOUT;
-            p.M[v] = act ? kPending : 0;  // 0 = inactive sentinel (reading Q15)
+            p.M[v] = act ? kPending : 0u;  // 0 = inactive sentinel (reading Q15)
             act_cnt += act;
         }
         const long long s = block_sum_int(sm, act_cnt);
@@ -639,7 +657,7 @@ void carve_mis2(Carve& c, int64_t n, int max_warps, Mis2Ws* w) {
     (void)max_warps;
     w->ctrl = c.take<unsigned long long>(16);
     w->T = c.take<uint64_t>((size_t)n + 1);
-    w->M = c.take<uint64_t>((size_t)n + 1);
+    w->M = c.take<uint32_t>((size_t)n + 1);
     for (int i = 0; i < 2; i++) {
         w->L1[i] = c.take<int32_t>((size_t)n + 1);
         w->L2[i] = c.take<int32_t>((size_t)n + 1);
@@ -685,11 +703,9 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     const int grid = (int)(want < 1 ? 1 : (want > max_grid ? max_grid : want));
 
     MIS2_CUDA_TRY(cudaMemsetAsync(w.ctrl, 0, 16 * sizeof(unsigned long long), s));
-    count_launch();
     if (stats) {
         MIS2_CUDA_TRY(cudaMemsetAsync(w.mark, 0, sizeof(unsigned int) * ((size_t)g.n + 1), s));
         MIS2_CUDA_TRY(cudaMemsetAsync(w.dstats, 0, sizeof(long long) * kStatsMaxIters * 6, s));
-        count_launch(2);
     }
     MisParams p;
     p.n = g.n;
@@ -711,6 +727,7 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     p.prio.b = bits_for(g.n);
     p.prio.seed = o.seed;
     p.prio.hi_mask = ~((1ull << p.prio.b) - 1ull);
+    p.id_mask = (uint32_t)((1ull << p.prio.b) - 1ull);
     p.prio.n = g.n;
     p.prio.override_ = o.prio_override;
     p.prio.override_iters = o.prio_override ? o.prio_iters : 0;

@@ -173,7 +173,6 @@ int scan_counts64(const int64_t* counts, int64_t n, int64_t* out, void* tmp, cud
         count_launch();
     } else {
         MIS2_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(int64_t), s));
-        count_launch();
     }
     MIS2_CUDA_TRY(cudaGetLastError());
     return MIS2_OK;
