@@ -1,0 +1,71 @@
+"""Turn gpurun_out/ ncu outputs into the committed summaries under profiles/.
+usage: python tools/summarize_profiles.py TAG   (reads launches_TAG.csv, prof_TAG.ncu-rep)"""
+import csv, io, json, os, subprocess, sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+out = os.path.join(ROOT, "profiles")
+os.makedirs(out, exist_ok=True)
+
+# ---- launch list
+txt = open(os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")).read().splitlines()
+txt = [l for l in txt if l.startswith('"')]
+rows = list(csv.reader(txt))
+hdr = rows[0]
+idx = {k: i for i, k in enumerate(hdr)}
+per = defaultdict(list)
+order = []
+for r in rows[1:]:
+    if len(r) < len(hdr) or r[idx["Metric Name"]] != "gpu__time_duration.sum":
+        continue
+    name = r[idx["Kernel Name"]]
+    ns = float(r[idx["Metric Value"]].replace(",", ""))
+    per[name].append(ns)
+    order.append((name, ns))
+mine = {k: v for k, v in per.items() if "mis2k" in k or "mis2_persistent" in k}
+lines = [f"# ncu launch list, bench.py --steps 3 --warmup 3 ({tag})", "",
+         "`ncu --metrics gpu__time_duration.sum --clock-control none` over the whole bench process",
+         "(instrumented stats call, checked call, warm-up and timed calls; cold-cache, serialised).", "",
+         "| kernel | launches | total us | mean us | share of all GPU time |", "|---|---|---|---|---|"]
+tot = sum(sum(v) for v in per.values())
+for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
+    lines.append(f"| `{k[:90]}` | {len(v)} | {sum(v)/1e3:.1f} | {sum(v)/len(v)/1e3:.1f} | {100*sum(v)/tot:.1f}% |")
+mp = [ns for k, v in per.items() if "mis2_persistent<" in k and "1>" not in k.split("mis2_persistent")[1][:6] for ns in v]
+lines += ["", "Per timed step the only kernel of ours is `mis2k::mis2_persistent<1, false>` (1 launch; the",
+          "per-call control-block memset and the between-step L2-flush fill are driver/torch operations).",
+          "Its share of the step's GPU time is therefore ~100%, as in the CUDA-event timing."]
+open(os.path.join(out, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
+print("\n".join(lines))
+
+# ---- full capture of the MIS-2 kernel
+rep = os.path.join(ROOT, "gpurun_out", f"prof_{tag}.ncu-rep")
+if os.path.exists(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(raw)))
+    d = dict(zip(r[0], r[2]))
+    units = dict(zip(r[0], r[1]))
+    keep = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+            "l1tex__t_sector_hit_rate.pct", "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
+            "launch__block_size", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+            "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"]
+    summ = {k: (d.get(k), units.get(k)) for k in keep if k in d}
+    st = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(v.replace(",", "")) for k, v in d.items()
+          if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued") and v not in ("", "n/a")}
+    tots = sum(st.values()) or 1
+    stalls = {k: round(100 * v / tots, 1) for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:10]}
+    def num(k):
+        v = d.get(k, "0").replace(",", "")
+        u = units.get(k, "")
+        f = float(v)
+        return f * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}.get(u, 1)
+    dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
+    doc = {"tag": tag, "metrics": summ, "stall_share_pct": stalls, "dram_bytes": dram,
+           "command": "ncu --set full --clock-control none --import-source on -k regex:mis2_persistent -s 2 -c 1 "
+                      "python tools/ncu_mis2.py 1"}
+    json.dump(doc, open(os.path.join(out, f"{tag}_ncu_mis2_persistent.json"), "w"), indent=1)
+    json.dump({"n": 1000000, "nnz": 26463592, "dram_bytes_per_launch": dram, "source": f"profiles/{tag}_ncu_mis2_persistent.json"},
+              open(os.path.join(out, "ncu_traffic.json"), "w"), indent=1)
+    print(json.dumps(doc, indent=1))
