@@ -61,6 +61,9 @@ extern "C" {
 
 /* ------------------------------------------------------------------- flags */
 #define MIS2_FLAG_VALIDATE 0x1u  /* run mis2_validate_graph first (EGRAPH on failure) */
+#define MIS2_FLAG_BASIC 0x4u     /* mis2_aggregate: Alg. 2 "Basic MIS-2 Coarsening"
+                                    instead of Alg. 3; leftovers join the aggregate of their
+                                    smallest-id aggregated neighbour (reading Q28) */
 #define MIS2_FLAG_TIMELINE 0x2u  /* measurement aid: mis2()'s `stats` receives int64 device
                                     timestamps (ns, %globaltimer) taken by block 0 after
                                     the init phase and after every grid barrier:

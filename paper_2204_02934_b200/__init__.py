@@ -24,6 +24,7 @@ OP_MIS2, OP_AGGREGATE, OP_COARSEN, OP_MIS2_HOST, OP_VALIDATE = 0, 1, 2, 3, 4
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, EGRAPH, ENOTCONVERGED, ERANGE, EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7, -9
 FLAG_VALIDATE = 1
 FLAG_TIMELINE = 2
+FLAG_BASIC = 4
 
 # every symbol include/mis2.h declares
 EXPORTS = ["mis2_opts_default", "mis2_workspace_size", "mis2", "mis2_async", "mis2_host", "mis2_aggregate",
@@ -226,11 +227,14 @@ class AggResult:
 
 
 def aggregate(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
-              validate: bool = False) -> AggResult:
-    """Alg. 3 through ``mis2_aggregate()``."""
+              validate: bool = False, basic: bool = False) -> AggResult:
+    """Alg. 3, or Alg. 2 with basic=True,
+    through ``mis2_aggregate()``."""
     torch = _torch()
     g, n, nnz = _graph(rowptr, colinds)
     o = _opts(seed, scheme, max_iters, group, validate)
+    if basic:
+        o.flags |= FLAG_BASIC
     ws, wsb = workspace(OP_AGGREGATE, n, nnz)
     labels = torch.empty(max(n, 1), dtype=torch.int32, device=rowptr.device)
     roots = torch.empty(max(n, 1), dtype=torch.int32, device=rowptr.device)

@@ -254,6 +254,29 @@ __global__ void k_phase3_heavy(const int64_t* __restrict__ rowptr, const int32_t
     }
 }
 
+// Alg. 2 join: a vertex left unaggregated by phase 1 joins the
+// aggregate of its smallest-id aggregated neighbour ("any neighbor", made
+// deterministic -- reading Q28).
+template <int G>
+__global__ void k_basic_join(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colinds,
+                             const int32_t* __restrict__ tent, int32_t* __restrict__ labels, int* err) {
+    ROWS_BEGIN(G, n)
+    const bool left = valid && tent[v] < 0;
+    int best = 0x7fffffff;
+    if (left)
+        for (int64_t j = rowptr[v] + sub; j < rowptr[v + 1]; j += G) {
+            const int32_t u = colinds[j];
+            if (u != v && tent[u] >= 0 && u < best) best = u;
+        }
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) best = min(best, __shfl_xor_sync(kFull, best, off));
+    if (left && sub == 0) {
+        if (best == 0x7fffffff) atomicOr(err, kErrNoCandidate);  // impossible by maximality
+        else labels[v] = tent[best];
+    }
+    ROWS_END
+}
+
 __global__ void k_finish(const int32_t* d_n1, const int32_t* d_n2, int64_t* out_na) {
     *out_na = (int64_t)*d_n1 + (int64_t)*d_n2;
 }
@@ -314,6 +337,9 @@ static void launch_rows(int64_t n, int sms, cudaStream_t s, int which, const mis
             k_phase3<G><<<(unsigned)blocks, kBlock, 0, s>>>(n, g.rowptr, g.colinds, w.tent, w.size, labels, w.heavy,
                                                           &s32[2 * kHeavyCnt], &s32[2 * kErr]);
             break;
+        case 5:
+            k_basic_join<G><<<(unsigned)blocks, kBlock, 0, s>>>(n, g.rowptr, g.colinds, w.tent, labels, &s32[2 * kErr]);
+            break;
     }
     count_launch();
 }
@@ -350,6 +376,21 @@ int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int6
     MIS2_TRY(scan_flags(w.in1, n, w.rid, &s32[2 * kN1], w.scan_tmp, s));
     rows(G, n, di.sms, s, 1, g, w, labels, roots);
 
+    const bool basic = (o.flags & MIS2_FLAG_BASIC) != 0;
+    if (basic) {
+        // ---- Alg. 2: every leftover joins an adjacent phase-1 aggregate
+        MIS2_CUDA_TRY(cudaMemsetAsync(w.size, 0, sizeof(int32_t) * ((size_t)n + 1), s));
+        int64_t blocks = (n + kBlock - 1) / kBlock;
+        if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
+        if (blocks < 1) blocks = 1;
+        k_tent_size<<<(unsigned)blocks, kBlock, 0, s>>>(n, labels, w.tent, w.size,
+                                                        (unsigned long long*)&w.scal[kLeft]);
+        count_launch();
+        rows(G, n, di.sms, s, 5, g, w, labels, roots);
+        k_finish<<<1, 1, 0, s>>>(&s32[2 * kN1], &s32[2 * kN2], (int64_t*)&w.scal[kNa]);
+        count_launch();
+    } else {
+
     // ---- phase 2: M2 = MIS2(G \ aggregated) on the same ids / seed (Q15)
     MIS2_TRY(run_mis2(g, o, labels, w.in2, (int64_t*)&w.scal[kCount2], &s32[2 * kIters2],
                       &s32[2 * kStatus2], nullptr, w.mis, s));
@@ -373,6 +414,7 @@ int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int6
     count_launch();
     k_finish<<<1, 1, 0, s>>>(&s32[2 * kN1], &s32[2 * kN2], (int64_t*)&w.scal[kNa]);
     count_launch();
+    }  // Alg. 3
     MIS2_CUDA_TRY(cudaGetLastError());
 
     long long h[32];

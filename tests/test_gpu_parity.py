@@ -267,3 +267,14 @@ def test_multilevel_config5():
     levels, _, _ = M().multilevel(rp, ci, threshold=1000)
     olevels, _ = O.multilevel(g.rowptr, g.colinds, threshold=1000)
     assert levels == olevels
+
+
+# ----------------------------------------------------------------- Alg. 2 (NEXT-1)
+@pytest.mark.parametrize("chunk", range(2))
+def test_basic_coarsening_alg2(chunk):
+    gs = small_graphs(30, 4000 + chunk) + [G.config_graph(0), G.laplace3d_27pt(30), G.kronecker(11)]
+    for g in gs:
+        rp, ci = dev(g)
+        a = M().aggregate(rp, ci, basic=True, seed=chunk)
+        labels, na = O.coarsen_basic(g.rowptr, g.colinds, seed=chunk)
+        assert a.num_aggs == na and np.array_equal(a.labels.cpu().numpy(), labels), g.name
