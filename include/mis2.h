@@ -173,6 +173,48 @@ int mis2_coarsen(const mis2_graph* g, const int32_t* labels, int64_t num_aggs, i
  * MIS2_OK or MIS2_EGRAPH (detail in mis2_last_error()). */
 int mis2_validate_graph(const mis2_graph* g, void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Partitioned MIS-2 (1-D row partition).  Part q of P owns
+ * rows [n*q/P, n*(q+1)/P).  Before every Refresh Column the ghost T values
+ * are exchanged, before every Decide the ghost M values, after every Decide
+ * |worklist_1| is summed over the parts; hashes use global ids and b
+ * uses the global n, so the result is bit-identical to mis2() on one GPU
+ * (each phase reads only the previous phase's arrays).
+ *
+ * A mis2_comm owns its communicator and the device copies of its parts
+ * (allocated by mis2_comm_set_graph, freed by mis2_comm_destroy).
+ *   NCCL : one process per GPU; rank 0 gets the id from mis2_comm_unique_id,
+ *          broadcasts it (e.g. torch.distributed), every rank calls
+ *          mis2_comm_init_nccl on its current device.  set_graph takes this
+ *          rank's rows: rowptr_h[n_own + 1], colinds_h[rowptr_h[0] ..
+ *          rowptr_h[n_own]) with GLOBAL column ids (collective call).
+ *          mis2_dist_mis2's in_set is the rank's n_own-entry device mask.
+ *   LOCAL: all P parts in this process on the current device (halos copied
+ *          device to device): set_graph takes the whole host CSR; in_set is
+ *          the global n-entry mask.  Same algorithm, for testing and for
+ *          graphs partitioned on one GPU.
+ * ---------------------------------------------------------------------- */
+typedef struct mis2_comm mis2_comm;
+int mis2_comm_unique_id(uint8_t* id128);
+int mis2_comm_init_nccl(const uint8_t* id128, int nranks, int rank, mis2_comm** out);
+int mis2_comm_init_local(int nparts, mis2_comm** out);
+int mis2_comm_set_graph(mis2_comm* c, int64_t n_global, const int64_t* rowptr_h, const int32_t* colinds_h,
+                        void* stream);
+int mis2_dist_mis2(mis2_comm* c, const mis2_opts* o, uint8_t* in_set, int64_t* count, int32_t* iters,
+                   void* stream);
+/* rows [lo, hi) and ghost count of local part `part` (NCCL: part 0) */
+int mis2_comm_part_info(mis2_comm* c, int part, int64_t* lo, int64_t* hi, int64_t* n_ghost);
+int mis2_comm_destroy(mis2_comm* c);
+
+/* Host-only partition planner (no device, no communicator): part `part` of
+ * `nparts` with rows rowptr_local[n_own+1] and GLOBAL column ids.  Returns the
+ * number of ghosts, their sorted global ids (ghost_ids may be NULL), the
+ * number requested from each owner (req_counts[nparts]) and the columns in
+ * the local index space [owned | ghosts] (colinds_local may be NULL). */
+int mis2_plan_part(int64_t n_global, int nparts, int part, const int64_t* rowptr_local,
+                   const int32_t* colinds_global, int64_t* n_ghost, int64_t* ghost_ids, int64_t* req_counts,
+                   int32_t* colinds_local);
+
 /* Number of kernel launches issued by the last call on this thread
  * (measurement aid for bench.py's "gpu_launches"). */
 int64_t mis2_last_launch_count(void);

@@ -29,7 +29,8 @@ FLAG_BASIC = 4
 # every symbol include/mis2.h declares
 EXPORTS = ["mis2_opts_default", "mis2_workspace_size", "mis2", "mis2_async", "mis2_host", "mis2_aggregate",
            "mis2_coarsen", "mis2_validate_graph", "mis2_last_launch_count", "mis2_strerror", "mis2_last_error",
-           "mis2_version"]
+           "mis2_version", "mis2_comm_unique_id", "mis2_comm_init_nccl", "mis2_comm_init_local",
+           "mis2_comm_set_graph", "mis2_dist_mis2", "mis2_comm_part_info", "mis2_comm_destroy", "mis2_plan_part"]
 
 
 class Mis2Error(RuntimeError):
@@ -76,8 +77,18 @@ def lib():
         L.mis2_last_error.restype = ctypes.c_char_p
         L.mis2_version.restype = ctypes.c_char_p
         L.mis2_opts_default.argtypes = [P]
+        L.mis2_comm_unique_id.argtypes = [P]
+        L.mis2_comm_init_nccl.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(P)]
+        L.mis2_comm_init_local.argtypes = [ctypes.c_int, ctypes.POINTER(P)]
+        L.mis2_comm_set_graph.argtypes = [P, I64, P, P, P]
+        L.mis2_dist_mis2.argtypes = [P, P, P, P, P, P]
+        L.mis2_comm_part_info.argtypes = [P, ctypes.c_int, P, P, P]
+        L.mis2_comm_destroy.argtypes = [P]
+        L.mis2_plan_part.argtypes = [I64, ctypes.c_int, ctypes.c_int, P, P, P, P, P, P]
         for name in ("mis2", "mis2_async", "mis2_host", "mis2_aggregate", "mis2_coarsen", "mis2_validate_graph",
-                     "mis2_workspace_size"):
+                     "mis2_workspace_size", "mis2_comm_unique_id", "mis2_comm_init_nccl", "mis2_comm_init_local",
+                     "mis2_comm_set_graph", "mis2_dist_mis2", "mis2_comm_part_info", "mis2_comm_destroy",
+                     "mis2_plan_part"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -288,3 +299,86 @@ def multilevel(rowptr, colinds, threshold: int = 1000, max_levels: int = 32, see
             break
         rp, ci = coarsen(rp, ci, agg.labels, agg.num_aggs)
     return levels, (rp, ci), labels_all
+
+
+# ---------------------------------------------------------------- partitioned
+def plan_part(n_global: int, nparts: int, part: int, rowptr_local: np.ndarray, colinds_global: np.ndarray):
+    """Host-only partition planner (C ABI ``mis2_plan_part``): returns
+    (ghost global ids, requests per owner, colinds in the local index space)."""
+    L = lib()
+    rowptr_local = np.ascontiguousarray(rowptr_local, dtype=np.int64)
+    colinds_global = np.ascontiguousarray(colinds_global, dtype=np.int32)
+    ng = ctypes.c_int64(0)
+    req = np.zeros(nparts, dtype=np.int64)
+    _check(L.mis2_plan_part(n_global, nparts, part, rowptr_local.ctypes.data, colinds_global.ctypes.data,
+                            ctypes.byref(ng), None, req.ctypes.data, None), "mis2_plan_part")
+    ghosts = np.zeros(max(ng.value, 1), dtype=np.int64)
+    nnz = int(rowptr_local[-1] - rowptr_local[0])
+    loc = np.zeros(max(nnz, 1), dtype=np.int32)
+    _check(L.mis2_plan_part(n_global, nparts, part, rowptr_local.ctypes.data, colinds_global.ctypes.data,
+                            ctypes.byref(ng), ghosts.ctypes.data, req.ctypes.data, loc.ctypes.data), "mis2_plan_part")
+    return ghosts[: ng.value], req, loc[:nnz]
+
+
+def comm_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().mis2_comm_unique_id(buf), "mis2_comm_unique_id")
+    return bytes(buf)
+
+
+class Comm:
+    """Partitioned MIS-2 driver (C ABI ``mis2_comm_*`` / ``mis2_dist_mis2``).
+
+    ``Comm.local(P)``: P partitions in this process on the current device.
+    ``Comm.nccl(uid, world, rank)``: one partition per process/GPU over NCCL."""
+
+    def __init__(self, handle, local: bool, nparts: int):
+        self.h, self.local, self.nparts = handle, local, nparts
+        self.n_global = 0
+
+    @classmethod
+    def local_parts(cls, nparts: int):
+        h = ctypes.c_void_p()
+        _check(lib().mis2_comm_init_local(nparts, ctypes.byref(h)), "mis2_comm_init_local")
+        return cls(h, True, nparts)
+
+    @classmethod
+    def nccl(cls, uid: bytes, world: int, rank: int):
+        h = ctypes.c_void_p()
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().mis2_comm_init_nccl(buf, world, rank, ctypes.byref(h)), "mis2_comm_init_nccl")
+        return cls(h, False, world)
+
+    def set_graph(self, n_global: int, rowptr_h: np.ndarray, colinds_h: np.ndarray):
+        rowptr_h = np.ascontiguousarray(rowptr_h, dtype=np.int64)
+        colinds_h = np.ascontiguousarray(colinds_h, dtype=np.int32)
+        if colinds_h.shape[0] == 0:
+            colinds_h = np.zeros(1, dtype=np.int32)
+        _check(lib().mis2_comm_set_graph(self.h, n_global, rowptr_h.ctypes.data, colinds_h.ctypes.data, _stream()),
+               "mis2_comm_set_graph")
+        self.n_global = n_global
+        return self
+
+    def part_info(self, part: int = 0):
+        lo, hi, ng = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+        _check(lib().mis2_comm_part_info(self.h, part, ctypes.byref(lo), ctypes.byref(hi), ctypes.byref(ng)),
+               "mis2_comm_part_info")
+        return lo.value, hi.value, ng.value
+
+    def mis2(self, in_set, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0):
+        o = _opts(seed, scheme, max_iters, group)
+        cnt, its = ctypes.c_int64(0), ctypes.c_int32(0)
+        _check(lib().mis2_dist_mis2(self.h, ctypes.byref(o), in_set.data_ptr(), ctypes.byref(cnt), ctypes.byref(its),
+                                    _stream()), "mis2_dist_mis2")
+        return int(cnt.value), int(its.value)
+
+    def close(self):
+        if self.h:
+            lib().mis2_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -15,6 +15,16 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=def
          "--expt-relaxed-constexpr", "-Xptxas", "-O3"]
 
 
+def nccl_include():
+    """nccl.h of the pip NCCL that torch loads (the library dlopens libnccl.so.2)."""
+    import sysconfig
+    for base in (sysconfig.get_paths()["purelib"], sysconfig.get_paths()["platlib"]):
+        inc = os.path.join(base, "nvidia", "nccl", "include")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc
+    raise RuntimeError("nccl.h not found (pip nvidia-nccl)")
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -35,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", tmp, *sources()]
+    cmd = [NVCC, *ARCH, *FLAGS, "-I", nccl_include(), "-o", tmp, *sources(), "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

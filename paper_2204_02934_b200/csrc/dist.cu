@@ -1,0 +1,523 @@
+// dist.cu -- MIS-2 over a 1-D row partition.
+//
+// Every phase of Alg. 1 is a pure per-vertex function of the previous
+// phase's arrays, the hash uses global ids and the packing uses the
+// global n (Eq. 1), so any row partition reproduces the single-GPU result
+// bit for bit provided each partition sees, before each phase, the current
+// values of the vertices its rows reference:
+//   before Refresh Column : T of the ghosts (owned by other partitions)
+//   before Decide         : M of the ghosts
+//   after Decide          : sum of |worklist_1| over all partitions
+// Partition q owns rows [n*q/P, n*(q+1)/P); its local index space is
+// [owned | ghosts], ghosts sorted by global id (hence grouped by owner), so a
+// received halo lands directly in T / M without an unpack step.
+//
+// Transports: NCCL (one process per GPU; grouped ncclSend/ncclRecv for the
+// halos, ncclAllReduce for the count; libnccl is dlopen'ed so the library
+// loads without it), and LOCAL (all partitions in one process on the current
+// device; halos copied device to device) -- the local transport runs the
+// complete partitioned algorithm on one GPU, which is how it is tested.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+#include "nccl.h"
+
+using namespace mis2h;
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
+        nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+int nccl_api(NcclApi** out) {
+    static NcclApi api;
+    if (!api.h) {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            set_error("cannot dlopen libnccl.so.2: %s", dlerror());
+            return MIS2_ENCCL;
+        }
+#define SYM(f)                                                              \
+    api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, "nccl" #f));         \
+    if (!api.f) {                                                           \
+        set_error("libnccl lacks nccl" #f);                                 \
+        return MIS2_ENCCL;                                                  \
+    }
+        SYM(GetUniqueId) SYM(CommInitRank) SYM(CommDestroy) SYM(Send) SYM(Recv) SYM(GroupStart) SYM(GroupEnd)
+        SYM(AllReduce) SYM(AllGather) SYM(GetErrorString)
+#undef SYM
+        api.h = h;
+    }
+    *out = &api;
+    return MIS2_OK;
+}
+
+#define NCCL_TRY(api, expr)                                                               \
+    do {                                                                                  \
+        ncclResult_t _r = (expr);                                                         \
+        if (_r != ncclSuccess) {                                                          \
+            set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, (api)->GetErrorString(_r)); \
+            return MIS2_ENCCL;                                                            \
+        }                                                                                 \
+    } while (0)
+
+// ------------------------------------------------------------------ plan
+inline int64_t part_lo(int64_t n, int P, int q) { return n * q / P; }
+
+struct HostPart {
+    int64_t lo = 0, hi = 0, n_own = 0, nnz = 0;
+    std::vector<int64_t> rowptr;     // local rows, rebased
+    std::vector<int32_t> colinds;    // local indices
+    std::vector<int64_t> ghosts;     // global ids, sorted
+    std::vector<int64_t> recv_cnt;   // per owner
+    std::vector<int64_t> recv_off;   // [P+1] into the ghost slots
+    std::vector<int32_t> send_idx;   // owned local indices, grouped by destination
+    std::vector<int64_t> send_cnt;   // per destination
+    std::vector<int64_t> send_off;   // [P+1]
+};
+
+// ghost discovery + local colinds (pure host)
+int plan_local(int64_t n, int P, int q, const int64_t* rowptr, const int32_t* colinds, HostPart& hp) {
+    hp.lo = part_lo(n, P, q);
+    hp.hi = part_lo(n, P, q + 1);
+    hp.n_own = hp.hi - hp.lo;
+    hp.nnz = rowptr[hp.n_own] - rowptr[0];
+    hp.rowptr.resize(hp.n_own + 1);
+    for (int64_t i = 0; i <= hp.n_own; i++) hp.rowptr[i] = rowptr[i] - rowptr[0];
+    std::vector<int64_t> g;
+    for (int64_t j = 0; j < hp.nnz; j++) {
+        const int64_t c = colinds[rowptr[0] + j];
+        if (c < 0 || c >= n) {
+            set_error("column index %lld out of range", (long long)c);
+            return MIS2_EGRAPH;
+        }
+        if (c < hp.lo || c >= hp.hi) g.push_back(c);
+    }
+    std::sort(g.begin(), g.end());
+    g.erase(std::unique(g.begin(), g.end()), g.end());
+    hp.ghosts = g;
+    hp.recv_cnt.assign(P, 0);
+    for (int64_t c : g) {
+        int o = (int)((c * P) / n);  // owner: largest q with n*q/P <= c
+        while (o + 1 <= P - 1 && part_lo(n, P, o + 1) <= c) o++;
+        while (o > 0 && part_lo(n, P, o) > c) o--;
+        hp.recv_cnt[o]++;
+    }
+    hp.recv_off.assign(P + 1, 0);
+    for (int o = 0; o < P; o++) hp.recv_off[o + 1] = hp.recv_off[o] + hp.recv_cnt[o];
+    hp.colinds.resize(hp.nnz);
+    for (int64_t j = 0; j < hp.nnz; j++) {
+        const int64_t c = colinds[rowptr[0] + j];
+        if (c >= hp.lo && c < hp.hi) hp.colinds[j] = (int32_t)(c - hp.lo);
+        else hp.colinds[j] = (int32_t)(hp.n_own + (std::lower_bound(g.begin(), g.end(), c) - g.begin()));
+    }
+    return MIS2_OK;
+}
+
+// requests[o] = ghost ids this part wants from owner o -> send lists of the owner
+void finish_sends(HostPart& owner, const std::vector<std::vector<int64_t>>& wanted_by, int P) {
+    owner.send_cnt.assign(P, 0);
+    owner.send_off.assign(P + 1, 0);
+    owner.send_idx.clear();
+    for (int d = 0; d < P; d++) {
+        owner.send_cnt[d] = (int64_t)wanted_by[d].size();
+        owner.send_off[d + 1] = owner.send_off[d] + owner.send_cnt[d];
+        for (int64_t id : wanted_by[d]) owner.send_idx.push_back((int32_t)(id - owner.lo));
+    }
+}
+
+__global__ void k_pack_u64(const uint64_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t cnt,
+                           uint64_t* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+__global__ void k_pack_u32(const uint32_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t cnt,
+                           uint32_t* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ handles
+struct mis2_comm {
+    bool local = false;
+    int nparts = 1;  // P
+    int rank = 0;    // NCCL rank (local: unused)
+    NcclApi* api = nullptr;
+    ncclComm_t nccl = nullptr;
+    int64_t n_global = 0;
+    std::vector<HostPart> hp;   // local: P parts; NCCL: 1 (this rank)
+    std::vector<PartDev> dev;   // same
+    std::vector<void*> allocs;
+    std::vector<uint64_t*> sendT;
+    std::vector<uint32_t*> sendM;
+    std::vector<int32_t*> send_idx_d;
+    unsigned long long* d_sum = nullptr;  // NCCL allreduce buffer
+};
+
+static int dev_alloc(mis2_comm* c, void** p, size_t bytes) {
+    MIS2_CUDA_TRY(cudaMalloc(p, bytes < 256 ? 256 : bytes));
+    c->allocs.push_back(*p);
+    return MIS2_OK;
+}
+
+static void free_parts(mis2_comm* c) {
+    for (void* p : c->allocs) cudaFree(p);
+    c->allocs.clear();
+    c->hp.clear();
+    c->dev.clear();
+    c->sendT.clear();
+    c->sendM.clear();
+    c->send_idx_d.clear();
+    c->d_sum = nullptr;
+}
+
+// upload one planned part
+static int upload_part(mis2_comm* c, const HostPart& h, PartDev& d, cudaStream_t s) {
+    memset(&d, 0, sizeof(d));
+    d.n_global = c->n_global;
+    d.n_own = h.n_own;
+    d.n_ghost = (int64_t)h.ghosts.size();
+    d.gbase = h.lo;
+    d.nnz = h.nnz;
+    d.G = choose_group(h.n_own, h.nnz, 0);
+    d.grid = part_grid(h.n_own, d.G);
+    const int64_t nt = d.n_own + d.n_ghost + 1;
+    void* p;
+    MIS2_TRY(dev_alloc(c, &p, sizeof(int64_t) * (d.n_own + 1)));
+    d.rowptr = (const int64_t*)p;
+    MIS2_CUDA_TRY(cudaMemcpyAsync(p, h.rowptr.data(), sizeof(int64_t) * (d.n_own + 1), cudaMemcpyHostToDevice, s));
+    MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * (h.nnz + 1)));
+    d.colinds = (const int32_t*)p;
+    if (h.nnz) MIS2_CUDA_TRY(cudaMemcpyAsync(p, h.colinds.data(), sizeof(int32_t) * h.nnz, cudaMemcpyHostToDevice, s));
+    MIS2_TRY(dev_alloc(c, &p, sizeof(uint64_t) * nt));
+    d.T = (uint64_t*)p;
+    MIS2_TRY(dev_alloc(c, &p, sizeof(uint32_t) * nt));
+    d.M = (uint32_t*)p;
+    for (int i = 0; i < 2; i++) {
+        MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * (d.n_own + 1)));
+        d.L1[i] = (int32_t*)p;
+        MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * (d.n_own + 1)));
+        d.L2[i] = (int32_t*)p;
+    }
+    MIS2_TRY(dev_alloc(c, &p, sizeof(int) * 2 * (d.grid + 1)));
+    d.cnts = (int*)p;
+    MIS2_TRY(dev_alloc(c, &p, sizeof(unsigned long long) * 8));
+    d.ctr = (unsigned long long*)p;
+    const int64_t ns = (int64_t)h.send_idx.size();
+    MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * (ns + 1)));
+    c->send_idx_d.push_back((int32_t*)p);
+    if (ns) MIS2_CUDA_TRY(cudaMemcpyAsync(p, h.send_idx.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, s));
+    MIS2_TRY(dev_alloc(c, &p, sizeof(uint64_t) * (ns + 1)));
+    c->sendT.push_back((uint64_t*)p);
+    MIS2_TRY(dev_alloc(c, &p, sizeof(uint32_t) * (ns + 1)));
+    c->sendM.push_back((uint32_t*)p);
+    return MIS2_OK;
+}
+
+// ------------------------------------------------------------------ halo exchange
+// which = 0: T (uint64), 1: M (uint32)
+static int exchange(mis2_comm* c, int which, cudaStream_t s) {
+    const int P = c->nparts;
+    const int L = (int)c->dev.size();
+    for (int i = 0; i < L; i++) {  // pack
+        const int64_t ns = (int64_t)c->hp[i].send_idx.size();
+        if (!ns) continue;
+        const int blocks = (int)std::min<int64_t>((ns + 255) / 256, 1024);
+        if (which == 0) k_pack_u64<<<blocks, 256, 0, s>>>(c->dev[i].T, c->send_idx_d[i], ns, c->sendT[i]);
+        else k_pack_u32<<<blocks, 256, 0, s>>>(c->dev[i].M, c->send_idx_d[i], ns, c->sendM[i]);
+        count_launch();
+    }
+    MIS2_CUDA_TRY(cudaGetLastError());
+    const size_t es = which == 0 ? sizeof(uint64_t) : sizeof(uint32_t);
+    if (c->local) {
+        for (int p = 0; p < P; p++) {
+            char* dst = which == 0 ? (char*)c->dev[p].T : (char*)c->dev[p].M;
+            for (int q = 0; q < P; q++) {
+                const int64_t cnt = c->hp[p].recv_cnt[q];
+                if (!cnt || q == p) continue;
+                const char* src = (which == 0 ? (const char*)c->sendT[q] : (const char*)c->sendM[q]) +
+                                  es * c->hp[q].send_off[p];
+                MIS2_CUDA_TRY(cudaMemcpyAsync(dst + es * (c->dev[p].n_own + c->hp[p].recv_off[q]), src, es * cnt,
+                                              cudaMemcpyDeviceToDevice, s));
+            }
+        }
+        return MIS2_OK;
+    }
+    const HostPart& h = c->hp[0];
+    const PartDev& d = c->dev[0];
+    const ncclDataType_t ty = which == 0 ? ncclUint64 : ncclUint32;
+    char* dst = which == 0 ? (char*)d.T : (char*)d.M;
+    const char* sb = which == 0 ? (const char*)c->sendT[0] : (const char*)c->sendM[0];
+    NCCL_TRY(c->api, c->api->GroupStart());
+    for (int q = 0; q < P; q++) {
+        if (q == c->rank) continue;
+        if (h.send_cnt[q]) NCCL_TRY(c->api, c->api->Send(sb + es * h.send_off[q], h.send_cnt[q], ty, q, c->nccl, s));
+        if (h.recv_cnt[q])
+            NCCL_TRY(c->api, c->api->Recv(dst + es * (d.n_own + h.recv_off[q]), h.recv_cnt[q], ty, q, c->nccl, s));
+    }
+    NCCL_TRY(c->api, c->api->GroupEnd());
+    return MIS2_OK;
+}
+
+// sum of ctr[slot] over all partitions -> host
+static int global_sum(mis2_comm* c, int slot, unsigned long long* out, cudaStream_t s) {
+    if (c->local) {
+        unsigned long long tot = 0;
+        for (auto& d : c->dev) {
+            unsigned long long v = 0;
+            MIS2_CUDA_TRY(cudaMemcpyAsync(&v, d.ctr + slot, sizeof(v), cudaMemcpyDeviceToHost, s));
+            MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+            tot += v;
+        }
+        *out = tot;
+        return MIS2_OK;
+    }
+    NCCL_TRY(c->api, c->api->AllReduce(c->dev[0].ctr + slot, c->d_sum, 1, ncclUint64, ncclSum, c->nccl, s));
+    MIS2_CUDA_TRY(cudaMemcpyAsync(out, c->d_sum, sizeof(*out), cudaMemcpyDeviceToHost, s));
+    MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+    return MIS2_OK;
+}
+
+extern "C" {
+
+int mis2_plan_part(int64_t n_global, int nparts, int part, const int64_t* rowptr_local, const int32_t* colinds_global,
+                   int64_t* n_ghost, int64_t* ghost_ids, int64_t* req_counts, int32_t* colinds_local) {
+    reset_launches();
+    if (n_global < 0 || nparts < 1 || part < 0 || part >= nparts || !rowptr_local || !n_ghost || !req_counts) {
+        set_error("bad arguments");
+        return MIS2_EINVAL;
+    }
+    HostPart hp;
+    MIS2_TRY(plan_local(n_global, nparts, part, rowptr_local, colinds_global, hp));
+    *n_ghost = (int64_t)hp.ghosts.size();
+    for (int q = 0; q < nparts; q++) req_counts[q] = hp.recv_cnt[q];
+    if (ghost_ids) memcpy(ghost_ids, hp.ghosts.data(), sizeof(int64_t) * hp.ghosts.size());
+    if (colinds_local) memcpy(colinds_local, hp.colinds.data(), sizeof(int32_t) * hp.colinds.size());
+    return MIS2_OK;
+}
+
+int mis2_comm_unique_id(uint8_t* id128) {
+    reset_launches();
+    NcclApi* api;
+    MIS2_TRY(nccl_api(&api));
+    ncclUniqueId u;
+    NCCL_TRY(api, api->GetUniqueId(&u));
+    static_assert(sizeof(u) == 128, "ncclUniqueId size");
+    memcpy(id128, &u, 128);
+    return MIS2_OK;
+}
+
+int mis2_comm_init_nccl(const uint8_t* id128, int nranks, int rank, mis2_comm** out) {
+    reset_launches();
+    if (!id128 || !out || nranks < 1 || rank < 0 || rank >= nranks) {
+        set_error("bad arguments");
+        return MIS2_EINVAL;
+    }
+    NcclApi* api;
+    MIS2_TRY(nccl_api(&api));
+    mis2_comm* c = new mis2_comm();
+    c->api = api;
+    c->nparts = nranks;
+    c->rank = rank;
+    ncclUniqueId u;
+    memcpy(&u, id128, 128);
+    ncclResult_t r = api->CommInitRank(&c->nccl, nranks, u, rank);
+    if (r != ncclSuccess) {
+        set_error("ncclCommInitRank: %s", api->GetErrorString(r));
+        delete c;
+        return MIS2_ENCCL;
+    }
+    *out = c;
+    return MIS2_OK;
+}
+
+int mis2_comm_init_local(int nparts, mis2_comm** out) {
+    reset_launches();
+    if (nparts < 1 || !out) {
+        set_error("bad arguments");
+        return MIS2_EINVAL;
+    }
+    mis2_comm* c = new mis2_comm();
+    c->local = true;
+    c->nparts = nparts;
+    *out = c;
+    return MIS2_OK;
+}
+
+int mis2_comm_destroy(mis2_comm* c) {
+    if (!c) return MIS2_OK;
+    free_parts(c);
+    if (c->nccl && c->api) c->api->CommDestroy(c->nccl);
+    delete c;
+    return MIS2_OK;
+}
+
+int mis2_comm_set_graph(mis2_comm* c, int64_t n_global, const int64_t* rowptr_h, const int32_t* colinds_h,
+                        void* stream) {
+    reset_launches();
+    if (!c || n_global < 0 || !rowptr_h || n_global > 2147483645LL) {
+        set_error("bad arguments");
+        return MIS2_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    free_parts(c);
+    c->n_global = n_global;
+    const int P = c->nparts;
+    if (c->local) {
+        c->hp.resize(P);
+        for (int q = 0; q < P; q++) {
+            const int64_t lo = part_lo(n_global, P, q);
+            MIS2_TRY(plan_local(n_global, P, q, rowptr_h + lo, colinds_h, c->hp[q]));
+        }
+        // owner q sends to p the ghosts p requests from q (ascending ids)
+        for (int q = 0; q < P; q++) {
+            std::vector<std::vector<int64_t>> wanted(P);
+            for (int p = 0; p < P; p++) {
+                if (p == q) continue;
+                const HostPart& hpp = c->hp[p];
+                wanted[p].assign(hpp.ghosts.begin() + hpp.recv_off[q], hpp.ghosts.begin() + hpp.recv_off[q + 1]);
+            }
+            finish_sends(c->hp[q], wanted, P);
+        }
+    } else {
+        c->hp.resize(1);
+        HostPart& h = c->hp[0];
+        MIS2_TRY(plan_local(n_global, P, c->rank, rowptr_h, colinds_h, h));
+        // all-to-all of the request lists: counts (allgather), then ids
+        std::vector<int64_t> cnt_all((size_t)P * P, 0);
+        int64_t *d_cnt, *d_all;
+        MIS2_CUDA_TRY(cudaMalloc(&d_cnt, sizeof(int64_t) * P));
+        MIS2_CUDA_TRY(cudaMalloc(&d_all, sizeof(int64_t) * P * P));
+        MIS2_CUDA_TRY(cudaMemcpyAsync(d_cnt, h.recv_cnt.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, s));
+        NCCL_TRY(c->api, c->api->AllGather(d_cnt, d_all, P, ncclInt64, c->nccl, s));
+        MIS2_CUDA_TRY(cudaMemcpyAsync(cnt_all.data(), d_all, sizeof(int64_t) * P * P, cudaMemcpyDeviceToHost, s));
+        MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+        cudaFree(d_cnt);
+        cudaFree(d_all);
+        int64_t tot_in = 0;
+        for (int p = 0; p < P; p++) tot_in += (p == c->rank) ? 0 : cnt_all[(size_t)p * P + c->rank];
+        int64_t *d_req, *d_in;
+        MIS2_CUDA_TRY(cudaMalloc(&d_req, sizeof(int64_t) * (h.ghosts.size() + 1)));
+        MIS2_CUDA_TRY(cudaMalloc(&d_in, sizeof(int64_t) * (tot_in + 1)));
+        if (!h.ghosts.empty())
+            MIS2_CUDA_TRY(cudaMemcpyAsync(d_req, h.ghosts.data(), sizeof(int64_t) * h.ghosts.size(),
+                                          cudaMemcpyHostToDevice, s));
+        std::vector<int64_t> in_off(P + 1, 0);
+        for (int p = 0; p < P; p++) in_off[p + 1] = in_off[p] + ((p == c->rank) ? 0 : cnt_all[(size_t)p * P + c->rank]);
+        NCCL_TRY(c->api, c->api->GroupStart());
+        for (int q = 0; q < P; q++) {
+            if (q == c->rank) continue;
+            if (h.recv_cnt[q]) NCCL_TRY(c->api, c->api->Send(d_req + h.recv_off[q], h.recv_cnt[q], ncclInt64, q, c->nccl, s));
+            const int64_t k = in_off[q + 1] - in_off[q];
+            if (k) NCCL_TRY(c->api, c->api->Recv(d_in + in_off[q], k, ncclInt64, q, c->nccl, s));
+        }
+        NCCL_TRY(c->api, c->api->GroupEnd());
+        std::vector<int64_t> in(tot_in);
+        if (tot_in) MIS2_CUDA_TRY(cudaMemcpyAsync(in.data(), d_in, sizeof(int64_t) * tot_in, cudaMemcpyDeviceToHost, s));
+        MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+        cudaFree(d_req);
+        cudaFree(d_in);
+        std::vector<std::vector<int64_t>> wanted(P);
+        for (int p = 0; p < P; p++) wanted[p].assign(in.begin() + in_off[p], in.begin() + in_off[p + 1]);
+        finish_sends(h, wanted, P);
+        void* p;
+        MIS2_TRY(dev_alloc(c, &p, sizeof(unsigned long long) * 2));
+        c->d_sum = (unsigned long long*)p;
+    }
+    c->dev.resize(c->hp.size());
+    for (size_t i = 0; i < c->hp.size(); i++) MIS2_TRY(upload_part(c, c->hp[i], c->dev[i], s));
+    MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+    return MIS2_OK;
+}
+
+int mis2_dist_mis2(mis2_comm* c, const mis2_opts* o, uint8_t* in_set, int64_t* count, int32_t* iters, void* stream) {
+    reset_launches();
+    if (!c || !count || !iters || c->dev.empty()) {
+        set_error("bad arguments (graph not set?)");
+        return MIS2_EINVAL;
+    }
+    if (c->n_global > 0 && !in_set) {
+        set_error("null in_set");
+        return MIS2_EINVAL;
+    }
+    mis2_opts def;
+    mis2_opts_default(&def);
+    const mis2_opts& opt = o ? *o : def;
+    if (opt.prio_override) {
+        set_error("prio_override is not supported by the partitioned driver");
+        return MIS2_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const int max_iters = max_iters_for(c->n_global, opt.max_iters);
+    const int L = (int)c->dev.size();
+    for (int i = 0; i < L; i++) {
+        PartDev& d = c->dev[i];
+        d.seed = opt.seed;
+        d.scheme = opt.scheme;
+        if (opt.group) d.G = opt.group;
+        d.in_set = c->local ? in_set + c->hp[i].lo : in_set;
+        MIS2_CUDA_TRY(cudaMemsetAsync(d.ctr, 0, sizeof(unsigned long long) * 8, s));
+        MIS2_TRY(part_step(d, kPartInit, 0, s));
+    }
+    unsigned long long active = 0;
+    MIS2_TRY(global_sum(c, 0, &active, s));
+    int it = 0, status = MIS2_OK;
+    while (active > 0) {  // while worklist_1 != {}
+        MIS2_TRY(exchange(c, 0, s));  // ghost T before Refresh Column
+        for (int i = 0; i < L; i++) MIS2_TRY(part_step(c->dev[i], kPartColumn, it, s));
+        MIS2_TRY(exchange(c, 1, s));  // ghost M before Decide
+        for (int i = 0; i < L; i++) {
+            MIS2_CUDA_TRY(cudaMemsetAsync(c->dev[i].ctr + 1, 0, sizeof(unsigned long long), s));
+            MIS2_TRY(part_step(c->dev[i], kPartDecide, it, s));
+        }
+        unsigned long long rem = 0;
+        MIS2_TRY(global_sum(c, 1, &rem, s));
+        it++;
+        if (rem == 0) break;
+        if (it >= max_iters) {
+            status = MIS2_ENOTCONVERGED;
+            break;
+        }
+    }
+    for (int i = 0; i < L; i++) MIS2_TRY(part_step(c->dev[i], kPartFinal, it, s));
+    unsigned long long cnt = 0;
+    MIS2_TRY(global_sum(c, 2, &cnt, s));
+    *count = (int64_t)cnt;
+    *iters = it;
+    if (status != MIS2_OK) set_error("MIS-2 did not converge within max_iters");
+    return status;
+}
+
+int mis2_comm_part_info(mis2_comm* c, int part, int64_t* lo, int64_t* hi, int64_t* n_ghost) {
+    if (!c || part < 0 || part >= (int)c->hp.size()) {
+        set_error("bad arguments");
+        return MIS2_EINVAL;
+    }
+    if (lo) *lo = c->hp[part].lo;
+    if (hi) *hi = c->hp[part].hi;
+    if (n_ghost) *n_ghost = (int64_t)c->hp[part].ghosts.size();
+    return MIS2_OK;
+}
+
+}  // extern "C"

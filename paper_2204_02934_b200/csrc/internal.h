@@ -81,6 +81,26 @@ int choose_group(int64_t n, int64_t nnz, int requested);
 int max_iters_for(int64_t n, int requested);
 int bits_for(int64_t n);
 
+// ---- partitioned (multi-GPU) MIS-2: device state of one partition
+struct PartDev {
+    int64_t n_global, n_own, n_ghost, gbase, nnz;
+    const int64_t* rowptr;   // device, local rows, n_own + 1
+    const int32_t* colinds;  // device, LOCAL indices: owned [0, n_own), ghosts [n_own, n_own + n_ghost)
+    const int32_t* labels;   // phase-2 mask or null
+    uint64_t* T;             // n_own + n_ghost
+    uint32_t* M;             // n_own + n_ghost
+    int32_t* L1[2];
+    int32_t* L2[2];
+    int* cnts;               // [2 * grid]
+    unsigned long long* ctr; // [0] active, [1] |wl1| this iteration, [2] count
+    uint8_t* in_set;         // n_own
+    int grid, G, scheme;
+    uint64_t seed;
+};
+enum { kPartInit = 0, kPartColumn = 1, kPartDecide = 2, kPartFinal = 3 };
+int part_step(const PartDev& d, int op, int it, cudaStream_t s);
+int part_grid(int64_t n_own, int G);
+
 // aggregation / coarsening / validation (aggregate.cu, coarsen.cu)
 int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int64_t* num_aggs,
                   int32_t* roots, int64_t* stats, void* ws, size_t ws_bytes, cudaStream_t s,

@@ -28,6 +28,7 @@
 //  * 64-bit status words (Eq. 1, reading Q6): a min is one compare.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "internal.h"
@@ -51,7 +52,8 @@ constexpr uint32_t kM_OUT = 0xffffffffu;
 constexpr uint32_t kPending = 1u;  // M of an active vertex before its first column pass
 
 struct MisParams {
-    int64_t n;
+    int64_t n;       // rows processed (all of them, or the owned rows of a partition)
+    int64_t gbase;   // global id of local row 0 (0 on one GPU): hashes and ids use gbase + v
     int64_t nnz;
     const int64_t* __restrict__ rowptr;
     const int32_t* __restrict__ colinds;
@@ -243,7 +245,7 @@ __device__ __forceinline__ bool decide_write(const MisParams& p, int64_t v, int 
         p.T[v] = kIN;
         return false;
     }
-    p.T[v] = p.prio.word(it + 1, fi_next, v);  // fused Refresh Row
+    p.T[v] = p.prio.word(it + 1, fi_next, p.gbase + v);  // fused Refresh Row
     return true;
 }
 
@@ -281,7 +283,7 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
         }
     } else {
         int any_out = 0, all_eq = 1;
-        const uint32_t vid1 = (uint32_t)v + 1u;
+        const uint32_t vid1 = (uint32_t)(p.gbase + v) + 1u;
         if (act) {
             if (sub == 0) decide_acc(p.M[v], vid1, any_out, all_eq);
             if (len > 0) row_decide<GG>(p.M, x, len, sub, vid1, any_out, all_eq);
@@ -334,7 +336,7 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
             }
         } else {
             int any_out = 0, all_eq = 1;
-            const uint32_t vid1 = (uint32_t)v + 1u;
+            const uint32_t vid1 = (uint32_t)(p.gbase + v) + 1u;
             if (t == 0) decide_acc(p.M[v], vid1, any_out, all_eq);
             for (int64_t j = s + t; j < e; j += kBlock) decide_acc(p.M[p.colinds[j]], vid1, any_out, all_eq);
             any_out = __syncthreads_or(any_out);
@@ -548,7 +550,7 @@ __global__ void __launch_bounds__(kBlock, 4) mis2_persistent(MisParams p) {
         int act_cnt = 0;
         for (int64_t v = blo + t; v < bhi; v += kBlock) {
             const bool act = p.labels ? (p.labels[v] < 0) : true;
-            p.T[v] = act ? p.prio.word(0, fi0, v) : kOUT;
+            p.T[v] = act ? p.prio.word(0, fi0, p.gbase + v) : kOUT;
             p.M[v] = act ? kPending : 0u;  // 0 = inactive sentinel (reading Q15)
             act_cnt += act;
         }
@@ -612,6 +614,82 @@ __global__ void __launch_bounds__(kBlock, 4) mis2_persistent(MisParams p) {
     }
 }
 
+// ------------------------------------------------------------ per-phase kernels
+// The same phases as one launch each, for the partitioned driver (dist.cu),
+// which exchanges ghost T / M between them.  Block worklist segment sizes
+// live in cnts[0..B) (worklist_1) and cnts[B..2B) (worklist_2).
+__device__ __forceinline__ void init_mbars(TileSmem& sm, int G2) {
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.mbar[0], 1);
+        mbar_init(&sm.mbar[1], 1);
+        mbar_init(&sm.mbarS[0], kBlock / G2);
+        mbar_init(&sm.mbarS[1], kBlock / G2);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBlock) mis2_part_init(MisParams p, int* cnts, unsigned long long* n_active) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+    const int64_t B = gridDim.x;
+    const int64_t blo = p.n * blockIdx.x / B, bhi = p.n * (blockIdx.x + 1) / B;
+    const uint64_t fi0 = p.prio.iter_term(0);
+    int act_cnt = 0;
+    for (int64_t v = blo + threadIdx.x; v < bhi; v += kBlock) {
+        const bool act = p.labels ? (p.labels[v] < 0) : true;
+        p.T[v] = act ? p.prio.word(0, fi0, p.gbase + v) : kOUT;
+        p.M[v] = act ? kPending : 0u;
+        act_cnt += act;
+    }
+    const long long s = block_sum_int(sm, act_cnt);
+    if (threadIdx.x == 0) {
+        cnts[blockIdx.x] = (int)(bhi - blo);
+        cnts[B + blockIdx.x] = (int)(bhi - blo);
+        if (s) atomicAdd(n_active, (unsigned long long)s);
+    }
+}
+
+template <int G, int PH>
+__global__ void __launch_bounds__(kBlock, 4) mis2_part_phase(MisParams p, int it, int* cnts,
+                                                              unsigned long long* wl1_total) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+    init_mbars(sm, G * 2 <= 32 ? G * 2 : 32);
+    uint32_t ph = 0u;
+    const int64_t B = gridDim.x;
+    const int64_t blo = p.n * blockIdx.x / B, bhi = p.n * (blockIdx.x + 1) / B;
+    const int64_t range = bhi - blo;
+    const int cur = it & 1;
+    int* cnt = &cnts[(PH == 0 ? B : 0) + blockIdx.x];
+    const int c = *cnt;
+    const bool dense = (it == 0) || (int64_t)c * kDenseDen >= range * kDenseNum;
+    int out;
+    if (PH == 0) {
+        out = dense ? dense_phase<G, false, 0>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0)
+                    : sparse_phase<G, false, 0>(sm, p, it, blo, p.L2[cur], c, p.L2[cur ^ 1], ph, 0);
+    } else {
+        const uint64_t fi_next = p.prio.iter_term(it + 1);
+        out = dense ? dense_phase<G, false, 1>(sm, p, it, blo, bhi, p.L1[cur ^ 1], ph, fi_next)
+                    : sparse_phase<G, false, 1>(sm, p, it, blo, p.L1[cur], c, p.L1[cur ^ 1], ph, fi_next);
+    }
+    if (threadIdx.x == 0) {
+        *cnt = out;
+        if (PH == 1 && out) atomicAdd(wl1_total, (unsigned long long)out);
+    }
+}
+
+__global__ void mis2_part_final(MisParams p, unsigned long long* count) {
+    int c = 0;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < p.n; v += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t in = (p.T[v] == kIN);
+        p.in_set[v] = in;
+        c += in;
+    }
+    c = group_sum<32>(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
+}
+
 }  // namespace mis2k
 
 namespace mis2h {
@@ -667,6 +745,90 @@ void carve_mis2(Carve& c, int64_t n, int max_warps, Mis2Ws* w) {
     w->scal = c.take<long long>(8);
 }
 
+template <int G>
+static cudaError_t launch_part_phase(int ph, const MisParams& p, int it, int grid, int smem, int* cnts,
+                                     unsigned long long* wl1, cudaStream_t s) {
+    if (ph == 0) {
+        cudaFuncSetAttribute((const void*)mis2_part_phase<G, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        mis2_part_phase<G, 0><<<grid, kBlock, smem, s>>>(p, it, cnts, wl1);
+    } else {
+        cudaFuncSetAttribute((const void*)mis2_part_phase<G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        mis2_part_phase<G, 1><<<grid, kBlock, smem, s>>>(p, it, cnts, wl1);
+    }
+    return cudaGetLastError();
+}
+
+static MisParams part_params(const PartDev& d) {
+    MisParams p;
+    memset(&p, 0, sizeof(p));
+    p.n = d.n_own;
+    p.gbase = d.gbase;
+    p.nnz = d.nnz;
+    p.rowptr = d.rowptr;
+    p.colinds = d.colinds;
+    p.labels = d.labels;
+    p.T = d.T;
+    p.M = d.M;
+    for (int i = 0; i < 2; i++) {
+        p.L1[i] = d.L1[i];
+        p.L2[i] = d.L2[i];
+    }
+    p.prio.scheme = d.scheme;
+    p.prio.b = bits_for(d.n_global);
+    p.prio.seed = d.seed;
+    p.prio.hi_mask = ~((1ull << p.prio.b) - 1ull);
+    p.id_mask = (uint32_t)((1ull << p.prio.b) - 1ull);
+    p.prio.n = d.n_global;
+    p.in_set = d.in_set;
+    return p;
+}
+
+int part_step(const PartDev& d, int op, int it, cudaStream_t s) {
+    const MisParams p = part_params(d);
+    const int smem = (int)sizeof(TileSmem);
+    const int grid = d.grid;
+    if (op == kPartInit) {
+        cudaFuncSetAttribute((const void*)mis2_part_init, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        mis2_part_init<<<grid, kBlock, smem, s>>>(p, d.cnts, d.ctr + 0);
+        count_launch();
+        MIS2_CUDA_TRY(cudaGetLastError());
+        return MIS2_OK;
+    }
+    if (op == kPartFinal) {
+        mis2_part_final<<<grid, kBlock, 0, s>>>(p, d.ctr + 2);
+        count_launch();
+        MIS2_CUDA_TRY(cudaGetLastError());
+        return MIS2_OK;
+    }
+    const int ph = op == kPartColumn ? 0 : 1;
+    cudaError_t e;
+    switch (d.G) {
+        case 1: e = launch_part_phase<1>(ph, p, it, grid, smem, d.cnts, d.ctr + 1, s); break;
+        case 2: e = launch_part_phase<2>(ph, p, it, grid, smem, d.cnts, d.ctr + 1, s); break;
+        case 4: e = launch_part_phase<4>(ph, p, it, grid, smem, d.cnts, d.ctr + 1, s); break;
+        case 8: e = launch_part_phase<8>(ph, p, it, grid, smem, d.cnts, d.ctr + 1, s); break;
+        case 16: e = launch_part_phase<16>(ph, p, it, grid, smem, d.cnts, d.ctr + 1, s); break;
+        default: e = launch_part_phase<32>(ph, p, it, grid, smem, d.cnts, d.ctr + 1, s); break;
+    }
+    count_launch();
+    if (e != cudaSuccess) {
+        set_error("part phase launch: %s", cudaGetErrorString(e));
+        return MIS2_ECUDA;
+    }
+    return MIS2_OK;
+}
+
+int part_grid(int64_t n_own, int G) {
+    DeviceInfo di;
+    if (device_info(&di) != MIS2_OK) return 1;
+    const int64_t rpb = kBlock / G;
+    int64_t want = (n_own + 2 * rpb - 1) / (2 * rpb);
+    const int64_t cap = (int64_t)4 * di.sms;
+    if (want > cap) want = cap;
+    if (want < 1) want = 1;
+    return (int)want;
+}
+
 int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uint8_t* in_set, int64_t* d_count,
              int32_t* d_iters, int32_t* d_status, int64_t* stats_host, const Mis2Ws& w, cudaStream_t s) {
     DeviceInfo di;
@@ -708,7 +870,9 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
         MIS2_CUDA_TRY(cudaMemsetAsync(w.dstats, 0, sizeof(long long) * kStatsMaxIters * 6, s));
     }
     MisParams p;
+    memset(&p, 0, sizeof(p));
     p.n = g.n;
+    p.gbase = 0;
     p.nnz = g.nnz;
     p.rowptr = g.rowptr;
     p.colinds = g.colinds;

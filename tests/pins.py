@@ -249,3 +249,22 @@ def coarse_ptap(rowptr, colinds, labels, num_aggs):
     C = (C > 0).tocsr()
     C.sort_indices()
     return C.indptr.astype(np.int64), C.indices.astype(np.int32)
+
+
+def np_words(it: int, gids: np.ndarray, n: int, seed: int = 0) -> np.ndarray:
+    """Vectorised word(it, v) for global ids (same reading Q3-Q5 as py_word)."""
+    b = py_bits(n)
+    mask_hi = np.uint64(~((1 << b) - 1) & MASK64)
+    g = np.asarray(gids, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        x = g.copy()
+        x ^= x << np.uint64(13)
+        x ^= x >> np.uint64(7)
+        x ^= x << np.uint64(17)
+        fv = x * np.uint64(0x2545F4914F6CDD1D)
+        y = fv ^ np.uint64(py_f(it ^ seed))
+        y ^= y << np.uint64(13)
+        y ^= y >> np.uint64(7)
+        y ^= y << np.uint64(17)
+        h = y * np.uint64(0x2545F4914F6CDD1D)
+    return (h & mask_hi) | (g + np.uint64(1))

@@ -278,3 +278,41 @@ def test_basic_coarsening_alg2(chunk):
         a = M().aggregate(rp, ci, basic=True, seed=chunk)
         labels, na = O.coarsen_basic(g.rowptr, g.colinds, seed=chunk)
         assert a.num_aggs == na and np.array_equal(a.labels.cpu().numpy(), labels), g.name
+
+
+# ----------------------------------------------------------------- partitioned (§8(e))
+@pytest.mark.parametrize("nparts", [1, 2, 3, 4, 8])
+def test_partitioned_local_transport(nparts):
+    """The multi-GPU driver with P partitions on this GPU (halo copies in
+    device memory): bit-identical to one GPU and to the oracle."""
+    gs = [G.config_graph(0), G.laplace3d_27pt(30), G.kronecker(11), G.random_graph(500, 0.02, 8),
+          G.elasticity3d(6), G.random_powerlaw_graph(2000, 6, 4), G.from_edges(5, [])]
+    for g in gs:
+        for seed in (0, 99):
+            c = M().Comm.local_parts(nparts).set_graph(g.n, g.rowptr, g.colinds)
+            out = torch.empty(max(g.n, 1), dtype=torch.uint8, device="cuda")
+            cnt, its = c.mis2(out, seed=seed)
+            c.close()
+            o = O.mis2(g.rowptr, g.colinds, seed=seed)
+            assert np.array_equal(out[: g.n].cpu().numpy().astype(bool), o.in_set), (g.name, nparts)
+            assert (cnt, its) == (o.count, o.iterations), (g.name, nparts)
+
+
+def test_partitioned_config2_8parts():
+    g = G.config_graph(1)
+    c = M().Comm.local_parts(8).set_graph(g.n, g.rowptr, g.colinds)
+    out = torch.empty(g.n, dtype=torch.uint8, device="cuda")
+    cnt, its = c.mis2(out)
+    rp, ci = dev(g)
+    r = M().mis2(rp, ci)
+    assert torch.equal(out, r.in_set) and (cnt, its) == (r.count, r.iterations)
+
+
+@pytest.mark.slow
+def test_partitioned_config3_4parts():
+    g = G.config_graph(2)
+    c = M().Comm.local_parts(4).set_graph(g.n, g.rowptr, g.colinds)
+    out = torch.empty(g.n, dtype=torch.uint8, device="cuda")
+    cnt, its = c.mis2(out)
+    o = O.mis2(g.rowptr, g.colinds)
+    assert np.array_equal(out.cpu().numpy().astype(bool), o.in_set) and (cnt, its) == (o.count, o.iterations)
