@@ -233,6 +233,12 @@ int mis2_coarsen(const mis2_graph* g, const int32_t* labels, int64_t num_aggs, i
 
 int64_t mis2_last_launch_count(void) { return g_launches; }
 
+// measurement aid (not in mis2.h): copies the instrumentation words a
+// MIS2_FLAG_TIMELINE run with MIS2_DBG_IT set left in the workspace
+int mis2_debug_read(void* ws, size_t ws_bytes, int64_t n, long long* out, int64_t count) {
+    return debug_read(ws, ws_bytes, n, out, count);
+}
+
 const char* mis2_strerror(int status) {
     switch (status) {
         case MIS2_OK: return "ok";

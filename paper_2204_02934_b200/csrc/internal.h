@@ -100,6 +100,7 @@ struct PartDev {
 enum { kPartInit = 0, kPartColumn = 1, kPartDecide = 2, kPartFinal = 3 };
 int part_step(const PartDev& d, int op, int it, cudaStream_t s);
 int part_grid(int64_t n_own, int G);
+int debug_read(void* ws, size_t ws_bytes, int64_t n, long long* out, int64_t count);
 
 // aggregation / coarsening / validation (aggregate.cu, coarsen.cu)
 int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int64_t* num_aggs,

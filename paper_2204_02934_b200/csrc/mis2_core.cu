@@ -67,6 +67,7 @@ struct MisParams {
     unsigned int* mark;   // stats only
     long long* dstats;    // stats only
     long long* timeline;  // MIS2_FLAG_TIMELINE only
+    int dbg_it, dbg_ph;   // MIS2_FLAG_TIMELINE: sparse phase instrumented into `mark`
     Prio prio;
     int max_iters;
     uint8_t* in_set;
@@ -198,7 +199,7 @@ __device__ __forceinline__ void stats_flush(const MisParams& p, int it, int slot
 template <int G>
 __device__ __forceinline__ uint64_t row_min(const uint64_t* __restrict__ T, const int32_t* x, int len, int sub,
                                             uint64_t m) {
-    constexpr int B = G == 1 ? 16 : (G == 2 ? 8 : 4);
+    constexpr int B = G <= 2 ? 16 : (G == 4 ? 8 : 4);
     const int last = len - 1;
     for (int j = sub; j < len; j += B * G) {
         uint64_t tt[B];
@@ -219,7 +220,7 @@ __device__ __forceinline__ void decide_acc(uint32_t m, uint32_t vid1, int& any_o
 template <int G>
 __device__ __forceinline__ void row_decide(const uint32_t* __restrict__ M, const int32_t* x, int len, int sub,
                                            uint32_t vid1, int& any_out, int& all_eq) {
-    constexpr int B = G == 1 ? 16 : (G == 2 ? 8 : 4);
+    constexpr int B = G <= 2 ? 16 : (G == 4 ? 8 : 4);
     const int last = len - 1;
     for (int j = sub; j < len; j += B * G) {
         uint32_t mm[B];
@@ -257,7 +258,9 @@ __device__ __forceinline__ void stage_tile(TileSmem& sm, const MisParams& p, int
     const bool fits = (ecp - sal) <= kTileCap && ecp <= nnz4;
     sm.sal[slot] = sal;
     sm.fits[slot] = fits;
-    fence_proxy_async();
+    // no proxy fence: the buffer was only READ by the generic proxy before the
+    // __syncthreads that precedes this call (write-after-read needs no
+    // fence.proxy.async, which would also drain this thread's global stores)
     if (fits && ecp > sal) {
         mbar_expect_tx(&sm.mbar[slot], (uint32_t)((ecp - sal) * 4));
         bulk_g2s(sm.buf[slot], p.colinds + sal, (uint32_t)((ecp - sal) * 4), &sm.mbar[slot]);
@@ -381,9 +384,23 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
         nx_e = p.rowptr[r2];
         stage_tile(sm, p, 0, p.rowptr[blo], nx_s);
     }
+    const bool dbg = p.timeline && it == p.dbg_it && PH == p.dbg_ph && threadIdx.x == 0;
+    long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
+    auto gt = []() {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        return (long long)ns;
+    };
+    if (dbg) {
+        dbuf[0] = gt();
+        dbuf[1] = nsteps;
+        dbuf[2] = bhi - blo;
+    }
     for (int64_t k = 0; k < nsteps; k++) {
         const int slot = (int)(k & 1);
+        if (dbg && k < 12) dbuf[4 + 5 * k] = gt();
         __syncthreads();  // tile k-1 consumed: its buffer may be refilled
+        if (dbg && k < 12) dbuf[4 + 5 * k + 1] = gt();
         if (t == 0 && k + 1 < nsteps) {
             const int64_t s1 = nx_s, e1 = nx_e;
             const int64_t r2 = blo + (k + 2) * RPB;
@@ -412,16 +429,20 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
         }
         const int64_t len = e - s;
         if (defer_long<G>(sm, act, sub, v, len)) act = false;
+        if (dbg && k < 12) dbuf[4 + 5 * k + 2] = gt();
         mbar_wait(&sm.mbar[slot], (ph >> slot) & 1u);
         ph ^= 1u << slot;
+        if (dbg && k < 12) dbuf[4 + 5 * k + 3] = gt();
         const int32_t* x = sm.fits[slot] ? sm.buf[slot] + (s - sm.sal[slot]) : p.colinds + s;
         const bool keep = process_row<G, PH>(p, act, sub, v, x, (int)len, tv, it, fi_next);
+        if (dbg && k < 12) dbuf[4 + 5 * k + 4] = gt();
         if (STATS && act) {
             stat_row<STATS>(p, tag, v, sub == 0, len, st);
             stat_nbrs<STATS>(p, tag, x, len, sub, G, st);
         }
         append(sm, keep, (int32_t)v, lout, blo);
     }
+    if (dbg) dbuf[3] = gt();
     return finish_phase<STATS, PH>(sm, p, it, blo, lout, fi_next, st);
 }
 
@@ -435,7 +456,10 @@ struct __align__(16) SMeta {
     int32_t v;    // vertex (-1: no row)
     int32_t len;  // row length; bit 30 set: staged in the slot
 };
+constexpr int kMaxDbgBlocks = 1184;
 constexpr int kSlotRegion = 6144;  // entries of a buffer used for row slots; SMeta array after it
+constexpr int kTvOff = 6656;       // then the T_v of each row (uint64, <= 128 rows)
+static_assert(kTvOff + 2 * 128 <= kTileCap + 8, "T_v region does not fit");
 
 template <int G, bool STATS, int PH>
 __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, const int32_t* lin, int nin,
@@ -455,20 +479,23 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
     const int nsteps = (nin + RPBS - 1) / RPBS;
     const int64_t nnz4 = p.nnz & ~(int64_t)3;
 
-    // leaders: fetch the row of tile j, stage it, record its metadata
-    auto plan = [&](int j, int slot) {
+    // Leaders pipeline the row metadata: worklist entry of tile j+3, row
+    // bounds of tile j+2 and T_v of tile j+1 are loaded while tile j is
+    // processed, so the copy of tile j+1 is issued without waiting on loads.
+    auto row_of = [&](int j) -> int64_t {
+        const int idx = j * RPBS + gs;
+        return (sub == 0 && j < nsteps && idx < nin) ? (int64_t)lin[blo + idx] : -1;
+    };
+    auto issue = [&](int slot, int64_t v, int64_t s, int64_t e, uint64_t tv) {
         if (sub != 0) return;
         SMeta* meta = reinterpret_cast<SMeta*>(sm.buf[slot] + kSlotRegion);
-        const int idx = j * RPBS + gs;
         SMeta m;
         m.v = -1;
         m.s = 0;
         m.len = 0;
         uint32_t bytes = 0;
         int64_t sal = 0;
-        if (idx < nin) {
-            const int64_t v = lin[blo + idx];
-            const int64_t s = p.rowptr[v], e = p.rowptr[v + 1];
+        if (v >= 0) {
             sal = s & ~(int64_t)3;
             const int64_t ecp = (e + 3) & ~(int64_t)3;
             const bool fits = (ecp - sal) <= SLOT && ecp <= nnz4;
@@ -478,40 +505,81 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
             if (fits && ecp > sal) bytes = (uint32_t)((ecp - sal) * 4);
         }
         meta[gs] = m;
+        reinterpret_cast<uint64_t*>(sm.buf[slot] + kTvOff)[gs] = tv;
         mbar_expect_tx(&sm.mbarS[slot], bytes);
         if (bytes) bulk_g2s(sm.buf[slot] + gs * SLOT, p.colinds + sal, bytes, &sm.mbarS[slot]);
     };
+    auto bounds = [&](int64_t v, int64_t& s, int64_t& e) {
+        s = 0;
+        e = 0;
+        if (v >= 0) {
+            s = p.rowptr[v];
+            e = p.rowptr[v + 1];
+        }
+    };
 
+    // prologue
+    int64_t v1 = -1, s1 = 0, e1 = 0, v2 = -1, s2 = 0, e2 = 0, v3 = -1;
+    uint64_t tv1 = kOUT, tv2 = kOUT;
     if (nsteps > 0) {
-        fence_proxy_async();
-        plan(0, 0);
+        const int64_t v0 = row_of(0);
+        v1 = row_of(1);
+        v2 = row_of(2);
+        int64_t s0, e0;
+        bounds(v0, s0, e0);
+        bounds(v1, s1, e1);
+        const uint64_t tv0 = v0 >= 0 ? p.T[v0] : kOUT;
+        tv1 = v1 >= 0 ? p.T[v1] : kOUT;
+        issue(0, v0, s0, e0, tv0);
+    }
+    const bool dbg = p.timeline && it == p.dbg_it && PH == p.dbg_ph && threadIdx.x == 0;
+    long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
+    auto gt = []() {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        return (long long)ns;
+    };
+    if (dbg) {
+        dbuf[0] = gt();
+        dbuf[1] = nsteps;
+        dbuf[2] = nin;
     }
     for (int k = 0; k < nsteps; k++) {
         const int slot = k & 1;
+        if (dbg && k < 12) dbuf[4 + 5 * k] = gt();
         __syncthreads();  // metadata of tile k visible; buffer of tile k-1 free
+        if (dbg && k < 12) dbuf[4 + 5 * k + 1] = gt();
+        if (k + 1 < nsteps) issue(slot ^ 1, v1, s1, e1, tv1);  // no proxy fence needed (see stage_tile)
+        bounds(v2, s2, e2);     // prefetch for tile k+2
+        tv2 = v2 >= 0 ? p.T[v2] : kOUT;
+        v3 = row_of(k + 3);     // prefetch for tile k+3
         const SMeta m = reinterpret_cast<const SMeta*>(sm.buf[slot] + kSlotRegion)[gs];
         const bool valid = m.v >= 0;
         const int64_t v = valid ? m.v : 0;
         const int len = m.len & ~kStaged;
-        uint64_t tv = kOUT;
-        if (valid) tv = p.T[v];  // status first: overlaps the planning chain below
-        if (k + 1 < nsteps) {
-            fence_proxy_async();
-            plan(k + 1, slot ^ 1);
-        }
+        const uint64_t tv = reinterpret_cast<const uint64_t*>(sm.buf[slot] + kTvOff)[gs];
         bool act = valid;
         if (defer_long<GS>(sm, act, sub, v, len)) act = false;
+        if (dbg && k < 12) dbuf[4 + 5 * k + 2] = gt();
         mbar_wait(&sm.mbarS[slot], (ph >> (2 + slot)) & 1u);
         ph ^= 1u << (2 + slot);
+        if (dbg && k < 12) dbuf[4 + 5 * k + 3] = gt();
         const int32_t* x = (m.len & kStaged) ? sm.buf[slot] + gs * SLOT + (m.s - (m.s & ~(int64_t)3))
                                              : p.colinds + m.s;
         const bool keep = process_row<GS, PH>(p, act, sub, v, x, len, tv, it, fi_next);
+        if (dbg && k < 12) dbuf[4 + 5 * k + 4] = gt();
         if (STATS && act) {
             stat_row<STATS>(p, tag, v, sub == 0, len, st);
             stat_nbrs<STATS>(p, tag, x, len, sub, GS, st);
         }
         append(sm, keep, (int32_t)v, lout, blo);
+        v1 = v2;
+        s1 = s2;
+        e1 = e2;
+        tv1 = tv2;
+        v2 = v3;
     }
+    if (dbg) dbuf[3] = gt();
     return finish_phase<STATS, PH>(sm, p, it, blo, lout, fi_next, st);
 }
 
@@ -818,6 +886,18 @@ int part_step(const PartDev& d, int op, int it, cudaStream_t s) {
     return MIS2_OK;
 }
 
+int debug_read(void* ws, size_t ws_bytes, int64_t n, long long* out, int64_t count) {
+    Carve c(ws, ws_bytes);
+    Mis2Ws w;
+    DeviceInfo di;
+    MIS2_TRY(device_info(&di));
+    carve_mis2(c, n, max_coop_warps(di), &w);
+    const int64_t cap = ((int64_t)n + 1) / 2;
+    if (count > cap) count = cap;
+    MIS2_CUDA_TRY(cudaMemcpy(out, w.mark, sizeof(long long) * count, cudaMemcpyDeviceToHost));
+    return MIS2_OK;
+}
+
 int part_grid(int64_t n_own, int G) {
     DeviceInfo di;
     if (device_info(&di) != MIS2_OK) return 1;
@@ -887,6 +967,13 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     p.mark = w.mark;
     p.dstats = w.dstats;
     p.timeline = timeline ? w.dstats : nullptr;
+    p.dbg_it = -1;
+    p.dbg_ph = 0;
+    if (timeline) {
+        if (const char* e = getenv("MIS2_DBG_IT")) p.dbg_it = atoi(e);
+        if (const char* e = getenv("MIS2_DBG_PH")) p.dbg_ph = atoi(e);
+        if (p.dbg_it >= 0) MIS2_CUDA_TRY(cudaMemsetAsync(w.mark, 0, sizeof(long long) * 64 * kMaxDbgBlocks, s));
+    }
     p.prio.scheme = o.scheme;
     p.prio.b = bits_for(g.n);
     p.prio.seed = o.seed;
