@@ -8,8 +8,9 @@
 //   3. every fine row u appends labels[adj(u)] (own label -> sentinel) into
 //      its aggregate's segment at an atomically reserved offset
 //   4. per segment: sort + unique in shared memory (warp-per-segment for
-//      <= 256 entries, block-per-segment for <= 8192); longer segments use an
-//      na-bit bitmap (set bits, then ordered compaction = sorted unique)
+//      <= 256 entries); longer segments: block-level shared-memory hash set of
+//      the distinct labels, then sort of the uniques; segments with more than
+//      2048 distinct labels use an na-bit bitmap (ordered compaction = sorted unique)
 //   5. c_rowptr = exclusive scan(unique counts); copy out.
 #include "common.cuh"
 #include "internal.h"
@@ -18,7 +19,6 @@ namespace mis2k {
 
 constexpr int32_t kSent = 0x7fffffff;
 constexpr int kWarpSeg = 256;
-constexpr int kBlockSeg = 8192;
 
 __global__ void k_check_labels(int64_t n, const int32_t* __restrict__ labels, int64_t na, int* err) {
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
@@ -113,41 +113,54 @@ __global__ void k_sort_warp(int64_t na, const int64_t* __restrict__ sptr, int32_
     (void)big; (void)big_cnt;
 }
 
-// block per segment, kWarpSeg < len <= kBlockSeg; longer ones go to `big`
-__global__ void k_sort_block(int64_t na, const int64_t* __restrict__ sptr, int32_t* __restrict__ buf,
-                             int64_t* __restrict__ ucnt, int32_t* __restrict__ big, int* big_cnt) {
-    __shared__ int32_t x[kBlockSeg];
-    __shared__ int s_w[kWarpsPerBlock];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// block per segment longer than kWarpSeg: the distinct labels are collected
+// in a shared-memory hash set (coarse rows have few distinct neighbours, e.g.
+// ~17 per aggregate on the elasticity graph against ~5.7K entries), then only
+// the uniques are sorted.  Segments with more than kMaxUniq distinct labels go
+// to `big` (bitmap path).
+constexpr int kHashCap = 4096;
+constexpr int kMaxUniq = 2048;
+__global__ void k_dedupe_block(int64_t na, const int64_t* __restrict__ sptr, int32_t* __restrict__ buf,
+                               int64_t* __restrict__ ucnt, int32_t* __restrict__ big, int* big_cnt) {
+    __shared__ int32_t keys[kHashCap];
+    __shared__ int32_t uq[kMaxUniq];
+    __shared__ int s_cnt;
     for (int64_t a = blockIdx.x; a < na; a += gridDim.x) {
         const int64_t s = sptr[a], len = sptr[a + 1] - s;
         if (len <= kWarpSeg) continue;
-        if (len > kBlockSeg) {
+        for (int i = threadIdx.x; i < kHashCap; i += blockDim.x) keys[i] = -1;
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+        for (int64_t j = s + threadIdx.x; j < s + len; j += blockDim.x) {
+            const int32_t b = buf[j];
+            if (b == kSent) continue;
+            if (*(volatile int*)&s_cnt >= kMaxUniq) break;  // overflow: bitmap path below
+            uint32_t slot = ((uint32_t)b * 2654435761u) >> 20;  // 12-bit hash
+            for (;;) {
+                const int32_t prev = atomicCAS(&keys[slot], -1, b);
+                if (prev == -1) {
+                    const int k = atomicAdd(&s_cnt, 1);
+                    if (k < kMaxUniq) uq[k] = b;
+                    break;
+                }
+                if (prev == b) break;
+                slot = (slot + 1) & (kHashCap - 1);
+            }
+        }
+        __syncthreads();
+        const int cnt = s_cnt;
+        if (cnt > kMaxUniq || (cnt == kMaxUniq)) {
             if (threadIdx.x == 0) big[atomicAdd(big_cnt, 1)] = (int32_t)a;
+            __syncthreads();
             continue;
         }
         int P = 1;
-        while (P < len) P <<= 1;
-        for (int i = threadIdx.x; i < P; i += blockDim.x) x[i] = i < len ? buf[s + i] : kSent;
+        while (P < cnt) P <<= 1;
+        for (int i = cnt + threadIdx.x; i < P; i += blockDim.x) uq[i] = kSent;
         __syncthreads();
-        bitonic(x, P, threadIdx.x, blockDim.x, false);
-        int carry = 0;
-        for (int base = 0; base < P; base += blockDim.x) {
-            const int i = base + threadIdx.x;
-            const int32_t xi = i < P ? x[i] : kSent;
-            const bool first = i < P && xi != kSent && (i == 0 || x[i - 1] != xi);
-            const unsigned ball = __ballot_sync(kFull, first);
-            if (lane == 0) s_w[warp] = __popc(ball);
-            __syncthreads();
-            int off = carry;
-            for (int w = 0; w < warp; w++) off += s_w[w];
-            if (first) buf[s + off + __popc(ball & lanemask_lt())] = xi;
-            int tot = 0;
-            for (int w = 0; w < kWarpsPerBlock; w++) tot += s_w[w];
-            carry += tot;
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) ucnt[a] = carry;
+        bitonic(uq, P, threadIdx.x, blockDim.x, false);
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) buf[s + i] = uq[i];
+        if (threadIdx.x == 0) ucnt[a] = cnt;
         __syncthreads();
     }
 }
@@ -268,7 +281,7 @@ int run_coarsen(const mis2_graph& g, const int32_t* labels, int64_t na, int64_t*
         k_sort_warp<<<(unsigned)wb, kBlock, 0, s>>>(na, sptr, buf, ucnt, big, &scal[1]);
         int64_t bb = na < (int64_t)di.sms * 8 ? na : (int64_t)di.sms * 8;
         if (bb < 1) bb = 1;
-        k_sort_block<<<(unsigned)bb, kBlock, 0, s>>>(na, sptr, buf, ucnt, big, &scal[1]);
+        k_dedupe_block<<<(unsigned)bb, kBlock, 0, s>>>(na, sptr, buf, ucnt, big, &scal[1]);
         count_launch(2);
     }
     int hs[16];

@@ -224,6 +224,8 @@ static int upload_part(mis2_comm* c, const HostPart& h, PartDev& d, cudaStream_t
     d.cnts = (int*)p;
     MIS2_TRY(dev_alloc(c, &p, sizeof(unsigned long long) * 8));
     d.ctr = (unsigned long long*)p;
+    MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * (d.n_own + 1)));
+    d.heavy = (int32_t*)p;
     const int64_t ns = (int64_t)h.send_idx.size();
     MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * (ns + 1)));
     c->send_idx_d.push_back((int32_t*)p);

@@ -62,6 +62,7 @@ struct Mis2Ws {
     uint32_t* M;
     int32_t* L1[2];
     int32_t* L2[2];
+    int32_t* heavy;
     unsigned int* mark;
     unsigned long long* ctrl;  // [0]=barrier, [1..4]=ring of |wl1| sums, [5]=count, [6]=ticket
     long long* dstats;         // [kStatsMaxIters * 6]
@@ -93,6 +94,7 @@ struct PartDev {
     int32_t* L2[2];
     int* cnts;               // [2 * grid]
     unsigned long long* ctr; // [0] active, [1] |wl1| this iteration, [2] count
+    int32_t* heavy;          // n_own deferred long rows
     uint8_t* in_set;         // n_own
     int grid, G, scheme;
     uint64_t seed;

@@ -36,8 +36,12 @@
 namespace mis2k {
 
 constexpr int kTileCap = 6912;      // int32 colinds per staging buffer (27 KB): 256 rows x 27
-constexpr int kHeavyDirect = 2048;  // rows longer than this are reduced by the whole block
-constexpr int kHeavyList = 64;
+// rows longer than 8 gather batches of their lane group are deferred and
+// reduced by the whole block (flattened over all deferred rows of the block)
+template <int G>
+__host__ __device__ constexpr int heavy_len() {
+    return 8 * G * (G <= 2 ? 16 : (G == 4 ? 8 : 4));
+}
 constexpr int kDenseNum = 3, kDenseDen = 8;  // dense if |worklist segment| >= 3/8 of the range
 // M_v is only ever compared against T_v (Decide: "M_w = T_v", "M_w = OUT").
 // By Eq. 1 the low b bits of an undecided word are id+1, unique per vertex,
@@ -64,6 +68,7 @@ struct MisParams {
     int32_t* L1[2];                      // worklist_1, double buffered, per-block segments
     int32_t* L2[2];                      // worklist_2
     unsigned long long* ctrl;
+    int32_t* heavy;       // [n] deferred long rows, per-block segments at blo
     unsigned int* mark;   // stats only
     long long* dstats;    // stats only
     long long* timeline;  // MIS2_FLAG_TIMELINE only
@@ -84,7 +89,6 @@ struct __align__(16) TileSmem {
     int32_t fits[2];
     int cnt;         // survivors written this phase
     int hcount;
-    int32_t hlist[kHeavyList];
     uint64_t red64[kWarpsPerBlock];
     int wred[kWarpsPerBlock];
 };
@@ -300,57 +304,133 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
 
 // defer a long row to whole-block processing (group leader decides, group agrees)
 template <int GG>
-__device__ __forceinline__ bool defer_long(TileSmem& sm, bool act, int sub, int64_t v, int64_t len) {
+__device__ __forceinline__ bool defer_long(TileSmem& sm, const MisParams& p, int64_t blo, bool act, int sub,
+                                           int64_t v, int64_t len) {
     bool defer = false;
-    if (act && sub == 0 && len > kHeavyDirect) {
+    if (act && sub == 0 && len > heavy_len<GG>()) {
         const int h = atomicAdd(&sm.hcount, 1);
-        if (h < kHeavyList) {
-            sm.hlist[h] = (int32_t)v;
-            defer = true;
-        }
+        p.heavy[blo + h] = (int32_t)v;  // at most one entry per row of the block's range
+        defer = true;
     }
     return __shfl_sync(kFull, defer, (threadIdx.x & 31) & ~(GG - 1));
 }
 
-// deferred long rows (whole block per row), stats flush, survivor count
+// Deferred long rows, stats flush, survivor count.  The block reduces all its
+// deferred rows together: up to 256 rows per round, their entries flattened
+// (prefix of the row lengths), 8 independent gathers per thread per pass,
+// combined per row with shared-memory atomics (min is exact in any order;
+// exists / forall likewise).
 template <bool STATS, int PH>
 __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, int32_t* lout, uint64_t fi_next,
                             Stat& st) {
     const int t = threadIdx.x;
     const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
     __syncthreads();
-    const int nh = min(sm.hcount, kHeavyList);
-    for (int h = 0; h < nh; h++) {
-        const int64_t v = sm.hlist[h];
-        const int64_t s = p.rowptr[v], e = p.rowptr[v + 1];
-        const uint64_t tv = p.T[v];
-        bool keep = false;
-        if (PH == 0) {
-            uint64_t m = (t == 0) ? tv : kOUT;
-            for (int64_t j = s + t; j < e; j += kBlock) {
-                const uint64_t tw = p.T[p.colinds[j]];
-                m = tw < m ? tw : m;
+    const int nh = sm.hcount;
+    char* base_ptr = reinterpret_cast<char*>(sm.buf[0]);
+    int64_t* pref = reinterpret_cast<int64_t*>(base_ptr);              // [kBlock + 1]
+    int64_t* rs = pref + (kBlock + 1);                                  // [kBlock] row starts
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(rs + kBlock);  // [kBlock] PH 0 min
+    int32_t* rv = reinterpret_cast<int32_t*>(acc + kBlock);             // [kBlock] rows
+    int32_t* anyo = rv + kBlock;                                        // [kBlock] PH 1 exists OUT
+    int32_t* alle = anyo + kBlock;                                      // [kBlock] PH 1 forall equal
+    for (int hb = 0; hb < nh; hb += kBlock) {
+        const int cnt = min(kBlock, nh - hb);
+        int64_t v = 0, s = 0, len = 0;
+        if (t < cnt) {
+            v = p.heavy[blo + hb + t];
+            s = p.rowptr[v];
+            len = p.rowptr[v + 1] - s;
+            rv[t] = (int32_t)v;
+            rs[t] = s;
+            if (PH == 0) {
+                acc[t] = p.T[v];  // closed neighbourhood (Q1)
+            } else {
+                const uint32_t mv = p.M[v];
+                const uint32_t vid1 = (uint32_t)(p.gbase + v) + 1u;
+                anyo[t] = (mv == kM_OUT);
+                alle[t] = (mv == vid1) | (mv == 0u);
             }
-            m = block_min_u64(sm, m);
-            if (t == 0) {
-                const uint32_t mf = m_field(m, p.id_mask);
+            if (STATS) stat_row<STATS>(p, tag, v, true, len, st);
+        }
+        // exclusive prefix of the lengths (int64)
+        {
+            const int lane = t & 31, warp = t >> 5;
+            long long inc = len;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const long long y = __shfl_up_sync(kFull, inc, off);
+                if (lane >= off) inc += y;
+            }
+            if (lane == 31) sm.red64[warp] = (uint64_t)inc;
+            __syncthreads();
+            long long wb = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < kWarpsPerBlock; w++) {
+                wb += (w < warp) ? (long long)sm.red64[w] : 0;
+                tot += (long long)sm.red64[w];
+            }
+            pref[t] = wb + inc - len;
+            if (t == 0) pref[kBlock] = tot;
+            __syncthreads();
+        }
+        const int64_t total = pref[kBlock];
+        for (int64_t c = 0; c < total; c += (int64_t)kBlock * 8) {
+            int32_t rr[8];
+            int32_t ww[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int64_t idx = c + t + (int64_t)kBlock * u;
+                rr[u] = -1;
+                ww[u] = 0;
+                if (idx < total) {
+                    int lo = 0, hi = cnt;  // last row with pref[row] <= idx
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (pref[mid] <= idx) lo = mid; else hi = mid;
+                    }
+                    rr[u] = lo;
+                    ww[u] = p.colinds[rs[lo] + (idx - pref[lo])];
+                }
+            }
+            if (PH == 0) {
+                uint64_t tv[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) tv[u] = rr[u] >= 0 ? p.T[ww[u]] : kOUT;
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+                    if (rr[u] >= 0 && tv[u] < acc[rr[u]]) atomicMin(&acc[rr[u]], (unsigned long long)tv[u]);
+            } else {
+                uint32_t mm[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) mm[u] = rr[u] >= 0 ? p.M[ww[u]] : 0u;
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    if (rr[u] < 0) continue;
+                    const uint32_t vid1 = (uint32_t)(p.gbase + rv[rr[u]]) + 1u;
+                    if (mm[u] == kM_OUT) anyo[rr[u]] = 1;
+                    if (mm[u] != vid1 && mm[u] != 0u) alle[rr[u]] = 0;
+                }
+            }
+            if (STATS) {
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+                    if (rr[u] >= 0 && atomicMax(&p.mark[ww[u]], tag) < tag) st.d++;
+            }
+        }
+        __syncthreads();
+        bool keep = false;
+        if (t < cnt) {
+            if (PH == 0) {
+                const uint32_t mf = m_field(acc[t], p.id_mask);
                 p.M[v] = mf;
                 keep = (mf != kM_OUT);
+            } else {
+                keep = decide_write(p, v, anyo[t], alle[t], it, fi_next);
             }
-        } else {
-            int any_out = 0, all_eq = 1;
-            const uint32_t vid1 = (uint32_t)(p.gbase + v) + 1u;
-            if (t == 0) decide_acc(p.M[v], vid1, any_out, all_eq);
-            for (int64_t j = s + t; j < e; j += kBlock) decide_acc(p.M[p.colinds[j]], vid1, any_out, all_eq);
-            any_out = __syncthreads_or(any_out);
-            all_eq = __syncthreads_and(all_eq);
-            if (t == 0) keep = decide_write(p, v, any_out, all_eq, it, fi_next);
-        }
-        if (STATS) {
-            stat_row<STATS>(p, tag, v, t == 0, e - s, st);
-            stat_nbrs<STATS>(p, tag, p.colinds + s, e - s, t, kBlock, st);
         }
         append(sm, keep, (int32_t)v, lout, blo);
+        __syncthreads();
     }
     stats_flush<STATS>(p, it, PH == 0 ? 1 : 0, st);
     __syncthreads();
@@ -428,7 +508,7 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
             }
         }
         const int64_t len = e - s;
-        if (defer_long<G>(sm, act, sub, v, len)) act = false;
+        if (defer_long<G>(sm, p, blo, act, sub, v, len)) act = false;
         if (dbg && k < 12) dbuf[4 + 5 * k + 2] = gt();
         mbar_wait(&sm.mbar[slot], (ph >> slot) & 1u);
         ph ^= 1u << slot;
@@ -559,7 +639,7 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         const int len = m.len & ~kStaged;
         const uint64_t tv = reinterpret_cast<const uint64_t*>(sm.buf[slot] + kTvOff)[gs];
         bool act = valid;
-        if (defer_long<GS>(sm, act, sub, v, len)) act = false;
+        if (defer_long<GS>(sm, p, blo, act, sub, v, len)) act = false;
         if (dbg && k < 12) dbuf[4 + 5 * k + 2] = gt();
         mbar_wait(&sm.mbarS[slot], (ph >> (2 + slot)) & 1u);
         ph ^= 1u << (2 + slot);
@@ -808,6 +888,7 @@ void carve_mis2(Carve& c, int64_t n, int max_warps, Mis2Ws* w) {
         w->L1[i] = c.take<int32_t>((size_t)n + 1);
         w->L2[i] = c.take<int32_t>((size_t)n + 1);
     }
+    w->heavy = c.take<int32_t>((size_t)n + 1);
     w->mark = c.take<unsigned int>((size_t)n + 1);
     w->dstats = c.take<long long>((size_t)kStatsMaxIters * 6);
     w->scal = c.take<long long>(8);
@@ -848,6 +929,7 @@ static MisParams part_params(const PartDev& d) {
     p.id_mask = (uint32_t)((1ull << p.prio.b) - 1ull);
     p.prio.n = d.n_global;
     p.in_set = d.in_set;
+    p.heavy = d.heavy;
     return p;
 }
 
@@ -964,6 +1046,7 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
         p.L2[i] = w.L2[i];
     }
     p.ctrl = w.ctrl;
+    p.heavy = w.heavy;
     p.mark = w.mark;
     p.dstats = w.dstats;
     p.timeline = timeline ? w.dstats : nullptr;

@@ -316,3 +316,14 @@ def test_partitioned_config3_4parts():
     cnt, its = c.mis2(out)
     o = O.mis2(g.rowptr, g.colinds)
     assert np.array_equal(out.cpu().numpy().astype(bool), o.in_set) and (cnt, its) == (o.count, o.iterations)
+
+
+def test_coarsen_bitmap_path():
+    # one aggregate with > 2048 distinct neighbour labels forces the bitmap path
+    g = G.random_graph(6000, 0.01, 21)
+    rng = np.random.default_rng(1)
+    na = 3000
+    labels = rng.integers(0, na, g.n).astype(np.int32)
+    labels[:na] = np.arange(na)
+    labels[na: na + 2500] = 7  # aggregate 7 gets ~2500 members x ~60 neighbours
+    check_coarsen(g, labels, na)
