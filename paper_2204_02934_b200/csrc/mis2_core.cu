@@ -327,6 +327,14 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
     const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
     __syncthreads();
     const int nh = sm.hcount;
+    const bool dbg = p.timeline && it == p.dbg_it && PH == p.dbg_ph && t == 0;
+    long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
+    if (dbg) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        dbuf[60] = (long long)ns;
+        dbuf[61] = nh;
+    }
     char* base_ptr = reinterpret_cast<char*>(sm.buf[0]);
     int64_t* pref = reinterpret_cast<int64_t*>(base_ptr);              // [kBlock + 1]
     int64_t* rs = pref + (kBlock + 1);                                  // [kBlock] row starts
@@ -375,22 +383,41 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
             __syncthreads();
         }
         const int64_t total = pref[kBlock];
-        for (int64_t c = 0; c < total; c += (int64_t)kBlock * 8) {
-            int32_t rr[8];
-            int32_t ww[8];
+        // each thread takes 8 consecutive entries per round and keeps a
+        // running accumulator for its current row; one shared atomic per row
+        // change (a hub row is reduced almost entirely in registers)
+        int cur = -1;
+        uint64_t cmin = kOUT;
+        int cany = 0, call = 1;
+        auto flush = [&]() {
+            if (cur < 0) return;
+            if (PH == 0) {
+                if (cmin < acc[cur]) atomicMin(&acc[cur], (unsigned long long)cmin);
+            } else {
+                if (cany) anyo[cur] = 1;
+                if (!call) alle[cur] = 0;
+            }
+        };
+        for (int64_t c = (int64_t)t * 8; c < total; c += (int64_t)kBlock * 8) {
+            int r = 0;
+            {
+                int lo = 0, hi = cnt;  // last row with pref[row] <= c
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (pref[mid] <= c) lo = mid; else hi = mid;
+                }
+                r = lo;
+            }
+            int32_t rr[8], ww[8];
 #pragma unroll
             for (int u = 0; u < 8; u++) {
-                const int64_t idx = c + t + (int64_t)kBlock * u;
+                const int64_t idx = c + u;
                 rr[u] = -1;
                 ww[u] = 0;
                 if (idx < total) {
-                    int lo = 0, hi = cnt;  // last row with pref[row] <= idx
-                    while (hi - lo > 1) {
-                        const int mid = (lo + hi) >> 1;
-                        if (pref[mid] <= idx) lo = mid; else hi = mid;
-                    }
-                    rr[u] = lo;
-                    ww[u] = p.colinds[rs[lo] + (idx - pref[lo])];
+                    while (pref[r + 1] <= idx) r++;
+                    rr[u] = r;
+                    ww[u] = p.colinds[rs[r] + (idx - pref[r])];
                 }
             }
             if (PH == 0) {
@@ -398,8 +425,15 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
 #pragma unroll
                 for (int u = 0; u < 8; u++) tv[u] = rr[u] >= 0 ? p.T[ww[u]] : kOUT;
 #pragma unroll
-                for (int u = 0; u < 8; u++)
-                    if (rr[u] >= 0 && tv[u] < acc[rr[u]]) atomicMin(&acc[rr[u]], (unsigned long long)tv[u]);
+                for (int u = 0; u < 8; u++) {
+                    if (rr[u] < 0) continue;
+                    if (rr[u] != cur) {
+                        flush();
+                        cur = rr[u];
+                        cmin = kOUT;
+                    }
+                    cmin = tv[u] < cmin ? tv[u] : cmin;
+                }
             } else {
                 uint32_t mm[8];
 #pragma unroll
@@ -407,9 +441,15 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
 #pragma unroll
                 for (int u = 0; u < 8; u++) {
                     if (rr[u] < 0) continue;
-                    const uint32_t vid1 = (uint32_t)(p.gbase + rv[rr[u]]) + 1u;
-                    if (mm[u] == kM_OUT) anyo[rr[u]] = 1;
-                    if (mm[u] != vid1 && mm[u] != 0u) alle[rr[u]] = 0;
+                    if (rr[u] != cur) {
+                        flush();
+                        cur = rr[u];
+                        cany = 0;
+                        call = 1;
+                    }
+                    const uint32_t vid1 = (uint32_t)(p.gbase + rv[cur]) + 1u;
+                    cany |= (mm[u] == kM_OUT);
+                    call &= (mm[u] == vid1) | (mm[u] == 0u);
                 }
             }
             if (STATS) {
@@ -418,6 +458,7 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
                     if (rr[u] >= 0 && atomicMax(&p.mark[ww[u]], tag) < tag) st.d++;
             }
         }
+        flush();
         __syncthreads();
         bool keep = false;
         if (t < cnt) {
@@ -433,6 +474,17 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         __syncthreads();
     }
     stats_flush<STATS>(p, it, PH == 0 ? 1 : 0, st);
+    if (dbg) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        dbuf[62] = (long long)ns;
+        long long e = 0;
+        for (int i = 0; i < nh; i++) {
+            const int64_t v = p.heavy[blo + i];
+            e += p.rowptr[v + 1] - p.rowptr[v];
+        }
+        dbuf[63] = e;
+    }
     __syncthreads();
     const int out = sm.cnt;
     __syncthreads();
@@ -475,6 +527,19 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
         dbuf[0] = gt();
         dbuf[1] = nsteps;
         dbuf[2] = bhi - blo;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        dbuf[59] = smid;
+    }
+    // prefetched row bounds / status of the next tile (this thread's row)
+    int64_t ns0 = 0, ne0 = 0;
+    uint64_t ntv = kOUT;
+    uint32_t nmv = kM_OUT;
+    if (blo + g < bhi) {
+        ns0 = p.rowptr[blo + g];
+        ne0 = p.rowptr[blo + g + 1];
+        ntv = p.T[blo + g];
+        if (PH == 0) nmv = p.M[blo + g];
     }
     for (int64_t k = 0; k < nsteps; k++) {
         const int slot = (int)(k & 1);
@@ -491,20 +556,22 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
             }
             stage_tile(sm, p, slot ^ 1, s1, e1);
         }
+        // this tile's row bounds and status were loaded one step ahead; load
+        // the next tile's now (a phase writes only rows of the tile it is
+        // processing, so the prefetched words are current)
         const int64_t v = blo + k * RPB + g;
         const bool valid = v < bhi;
-        int64_t s = 0, e = 0;
-        uint64_t tv = kOUT;
+        const int64_t s = ns0, e = ne0;
+        const uint64_t tv = ntv;
         bool act = false;
-        if (valid) {
-            s = p.rowptr[v];
-            e = p.rowptr[v + 1];
-            tv = p.T[v];
-            if (PH == 0) {
-                const uint32_t mv = p.M[v];
-                act = (mv != kM_OUT && mv != 0u);
-            } else {
-                act = (tv != kIN && tv != kOUT);
+        if (valid) act = PH == 0 ? (nmv != kM_OUT && nmv != 0u) : (tv != kIN && tv != kOUT);
+        {
+            const int64_t vn = v + RPB;
+            if (vn < bhi) {
+                ns0 = p.rowptr[vn];
+                ne0 = p.rowptr[vn + 1];
+                ntv = p.T[vn];
+                if (PH == 0) nmv = p.M[vn];
             }
         }
         const int64_t len = e - s;
