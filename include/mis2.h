@@ -64,6 +64,11 @@ extern "C" {
 #define MIS2_FLAG_BASIC 0x4u     /* mis2_aggregate: Alg. 2 "Basic MIS-2 Coarsening"
                                     instead of Alg. 3; leftovers join the aggregate of their
                                     smallest-id aggregated neighbour (reading Q28) */
+#define MIS2_FLAG_PUSH_DECIDE 0x8u  /* force the push form of Decide (P:96-104 restated: the column
+                                       pass marks N[w] of every w whose M_w becomes OUT and counts
+                                       w for its argmin; Decide then reads no neighbour).  Default:
+                                       push iff nnz/n >= 32.  Never changes results. */
+#define MIS2_FLAG_PULL_DECIDE 0x10u /* force the pull form (Alg. 1 as written).  Never changes results. */
 #define MIS2_FLAG_TIMELINE 0x2u  /* measurement aid: mis2()'s `stats` receives int64 device
                                     timestamps (ns, %globaltimer) taken by block 0 after
                                     the init phase and after every grid barrier:

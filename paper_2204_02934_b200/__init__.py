@@ -25,6 +25,9 @@ OK, EINVAL, ENOMEM, ECUDA, ENCCL, EGRAPH, ENOTCONVERGED, ERANGE, EINTERNAL = 0, 
 FLAG_VALIDATE = 1
 FLAG_TIMELINE = 2
 FLAG_BASIC = 4
+FLAG_PUSH_DECIDE = 8
+FLAG_PULL_DECIDE = 16
+DECIDE = {"auto": 0, "push": FLAG_PUSH_DECIDE, "pull": FLAG_PULL_DECIDE}
 
 # every symbol include/mis2.h declares
 EXPORTS = ["mis2_opts_default", "mis2_workspace_size", "mis2", "mis2_async", "mis2_host", "mis2_aggregate",
@@ -58,7 +61,9 @@ def lib():
     global _lib
     if _lib is None:
         path = _build.LIB
-        if _build.stale() and os.path.exists(_build.NVCC):
+        if os.environ.get("MIS2_LIB_PATH"):  # measurement only: A/B another build of the same ABI
+            path = os.environ["MIS2_LIB_PATH"]
+        elif _build.stale() and os.path.exists(_build.NVCC):
             path = _build.build()
         if not os.path.exists(path):
             raise ImportError(f"libmis2.so not built ({path}); run __graft_entry__.build()")
@@ -139,14 +144,14 @@ def _graph(rowptr, colinds):
     return _Graph(n, nnz, rowptr.data_ptr(), colinds.data_ptr() if nnz else None), n, nnz
 
 
-def _opts(seed=0, scheme="xorstar", max_iters=0, group=0, validate=False, prio_override=None):
+def _opts(seed=0, scheme="xorstar", max_iters=0, group=0, validate=False, prio_override=None, decide="auto"):
     o = _Opts()
     lib().mis2_opts_default(ctypes.byref(o))
     o.seed = seed & ((1 << 64) - 1)
     o.scheme = SCHEMES[scheme]
     o.max_iters = max_iters
     o.group = group
-    o.flags = FLAG_VALIDATE if validate else 0
+    o.flags = (FLAG_VALIDATE if validate else 0) | DECIDE[decide]
     if prio_override is not None:
         o.prio_override = prio_override.data_ptr()
         o.prio_iters = prio_override.shape[0]
@@ -165,13 +170,13 @@ class Mis2Result:
 
 def mis2(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
          validate: bool = False, prio_override=None, stats: bool = False, allow_partial: bool = False,
-         out=None, timeline: bool = False) -> Mis2Result:
+         out=None, timeline: bool = False, decide: str = "auto") -> Mis2Result:
     """Alg. 1 through ``mis2()`` of the C ABI."""
     torch = _torch()
     g, n, nnz = _graph(rowptr, colinds)
     if prio_override is not None:
         prio_override = prio_override.to(device=rowptr.device, dtype=torch.int64).contiguous()
-    o = _opts(seed, scheme, max_iters, group, validate, prio_override)
+    o = _opts(seed, scheme, max_iters, group, validate, prio_override, decide)
     ws, wsb = workspace(OP_MIS2, n, nnz)
     in_set = out if out is not None else torch.empty(max(n, 1), dtype=torch.uint8, device=rowptr.device)
     cnt, its = ctypes.c_int64(0), ctypes.c_int32(0)
@@ -195,11 +200,11 @@ def mis2(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int
 
 
 def mis2_async(rowptr, colinds, in_set, d_scalars, seed: int = 0, scheme: str = "xorstar", group: int = 0,
-               max_iters: int = 0):
+               max_iters: int = 0, decide: str = "auto"):
     """Enqueue MIS-2 without synchronising; d_scalars = int64 CUDA tensor [2]
     receiving count and (iterations | status << 32)."""
     g, n, nnz = _graph(rowptr, colinds)
-    o = _opts(seed, scheme, max_iters, group)
+    o = _opts(seed, scheme, max_iters, group, decide=decide)
     ws, wsb = workspace(OP_MIS2, n, nnz)
     p = d_scalars.data_ptr()
     rc = lib().mis2_async(ctypes.byref(g), ctypes.byref(o), in_set.data_ptr(), p, p + 8, p + 12, ws.data_ptr(),
@@ -238,12 +243,12 @@ class AggResult:
 
 
 def aggregate(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
-              validate: bool = False, basic: bool = False) -> AggResult:
+              validate: bool = False, basic: bool = False, decide: str = "auto") -> AggResult:
     """Alg. 3, or Alg. 2 with basic=True,
     through ``mis2_aggregate()``."""
     torch = _torch()
     g, n, nnz = _graph(rowptr, colinds)
-    o = _opts(seed, scheme, max_iters, group, validate)
+    o = _opts(seed, scheme, max_iters, group, validate, decide=decide)
     if basic:
         o.flags |= FLAG_BASIC
     ws, wsb = workspace(OP_AGGREGATE, n, nnz)

@@ -60,12 +60,12 @@ static int check_opts(const mis2_opts* o, int64_t n) {
     return MIS2_OK;
 }
 
-static size_t mis2_bytes(int64_t n) {
+static size_t mis2_bytes(int64_t n, int64_t nnz) {
     DeviceInfo di;
     if (device_info(&di) != MIS2_OK) di.sms = 148;
     Carve c(nullptr, 0);
     Mis2Ws w;
-    carve_mis2(c, n, max_coop_warps(di), &w);
+    carve_mis2(c, n, nnz, max_coop_warps(di), &w);
     return c.off;
 }
 
@@ -86,13 +86,13 @@ int mis2_workspace_size(int64_t n, int64_t nnz, int32_t op, size_t* bytes) {
     reset_launches();
     mis2_graph g{n, nnz, nullptr, nullptr};
     switch (op) {
-        case MIS2_OP_MIS2: *bytes = mis2_bytes(n); return MIS2_OK;
+        case MIS2_OP_MIS2: *bytes = mis2_bytes(n, nnz); return MIS2_OK;
         case MIS2_OP_MIS2_HOST: {
             DeviceInfo di;
             MIS2_TRY(device_info(&di));
             Carve c(nullptr, 0);
             Mis2Ws w;
-            carve_mis2(c, n, max_coop_warps(di), &w);
+            carve_mis2(c, n, nnz, max_coop_warps(di), &w);
             c.take<int64_t>((size_t)n + 1);
             c.take<int32_t>((size_t)nnz);
             c.take<uint8_t>((size_t)n + 1);
@@ -132,7 +132,7 @@ int mis2_async(const mis2_graph* g, const mis2_opts* o, uint8_t* in_set, int64_t
     Mis2Ws w;
     DeviceInfo di;
     MIS2_TRY(device_info(&di));
-    carve_mis2(c, g->n, max_coop_warps(di), &w);
+    carve_mis2(c, g->n, g->nnz, max_coop_warps(di), &w);
     if (!c.ok()) { set_error("workspace too small: need %zu bytes, got %zu", c.off, ws_bytes); return MIS2_ENOMEM; }
     return run_mis2(*g, opt, nullptr, in_set, d_count, d_iters, d_status, nullptr, w, s);
 }
@@ -152,7 +152,7 @@ int mis2(const mis2_graph* g, const mis2_opts* o, uint8_t* in_set, int64_t* coun
     Mis2Ws w;
     DeviceInfo di;
     MIS2_TRY(device_info(&di));
-    carve_mis2(c, g->n, max_coop_warps(di), &w);
+    carve_mis2(c, g->n, g->nnz, max_coop_warps(di), &w);
     int64_t* scal = (int64_t*)w.scal;
     if (!c.ok()) { set_error("workspace too small: need %zu bytes, got %zu", c.off, ws_bytes); return MIS2_ENOMEM; }
     int32_t* s32 = (int32_t*)(scal + 1);
@@ -183,7 +183,7 @@ int mis2_host(int64_t n, int64_t nnz, const int64_t* rowptr_h, const int32_t* co
     Mis2Ws w;
     DeviceInfo di;
     MIS2_TRY(device_info(&di));
-    carve_mis2(c, n, max_coop_warps(di), &w);
+    carve_mis2(c, n, nnz, max_coop_warps(di), &w);
     int64_t* d_rowptr = c.take<int64_t>((size_t)n + 1);
     int32_t* d_col = c.take<int32_t>((size_t)nnz);
     uint8_t* d_in = c.take<uint8_t>((size_t)n + 1);

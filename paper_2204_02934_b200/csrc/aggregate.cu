@@ -294,8 +294,8 @@ struct AggWs {
     long long* scal;  // device scalars
 };
 
-static void carve_agg(Carve& c, int64_t n, int max_warps, AggWs* w) {
-    carve_mis2(c, n, max_warps, &w->mis);
+static void carve_agg(Carve& c, int64_t n, int64_t nnz, int max_warps, AggWs* w) {
+    carve_mis2(c, n, nnz, max_warps, &w->mis);
     w->in1 = c.take<uint8_t>((size_t)n + 1);
     w->in2 = c.take<uint8_t>((size_t)n + 1);
     w->acc = c.take<uint8_t>((size_t)n + 1);
@@ -362,7 +362,7 @@ int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int6
     MIS2_TRY(device_info(&di));
     Carve c(ws, ws_bytes);
     AggWs w;
-    carve_agg(c, g.n, max_coop_warps(di), &w);
+    carve_agg(c, g.n, g.nnz, max_coop_warps(di), &w);
     if (bytes_needed) { *bytes_needed = c.off; return MIS2_OK; }
     if (!c.ok()) { set_error("workspace too small: need %zu bytes", c.off); return MIS2_ENOMEM; }
     const int64_t n = g.n;

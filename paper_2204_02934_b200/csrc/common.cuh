@@ -104,19 +104,26 @@ __device__ __forceinline__ long long warp_sum_ll(long long x) {
 // LD.STRONG + CCTL.IVALL, and invalidating L1 on every poll would wipe the
 // cache of co-resident blocks that are still gathering); one acquire fence
 // after the flip makes every block's prior writes visible.
-__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, int mode = 0) {
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned int nb = (blockIdx.x == 0) ? (0x80000000u - (gridDim.x - 1)) : 1u;
         unsigned int old;
         asm volatile("atom.add.release.gpu.u32 %0,[%1],%2;" : "=r"(old) : "l"(bar), "r"(nb) : "memory");
         unsigned int cur;
-        for (;;) {
-            asm volatile("ld.relaxed.gpu.u32 %0,[%1];" : "=r"(cur) : "l"(bar) : "memory");
-            if ((old ^ cur) & 0x80000000u) break;
-            __nanosleep(32);
+        if (mode == 2) {  // acquire polling (as cooperative_groups)
+            for (;;) {
+                asm volatile("ld.acquire.gpu.u32 %0,[%1];" : "=r"(cur) : "l"(bar) : "memory");
+                if ((old ^ cur) & 0x80000000u) break;
+            }
+        } else {
+            for (;;) {
+                asm volatile("ld.relaxed.gpu.u32 %0,[%1];" : "=r"(cur) : "l"(bar) : "memory");
+                if ((old ^ cur) & 0x80000000u) break;
+                if (mode == 0) __nanosleep(32);
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
         }
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
 }

@@ -64,11 +64,16 @@ struct Mis2Ws {
     int32_t* L2[2];
     int32_t* heavy;
     unsigned int* mark;
+    uint8_t* oflag;     // push-form Decide state (mis2_core.cu)
+    uint32_t* cnt;
+    uint32_t* degc;
+    int32_t* len2;      // pruned row lengths
+    int32_t* ci2;       // pruned adjacency (nnz entries; carved by carve_mis2_adj)
     unsigned long long* ctrl;  // [0]=barrier, [1..4]=ring of |wl1| sums, [5]=count, [6]=ticket
     long long* dstats;         // [kStatsMaxIters * 6]
     long long* scal;           // [8] host-visible scalars of mis2()/mis2_host()
 };
-void carve_mis2(Carve& c, int64_t n, int max_warps, Mis2Ws* w);
+void carve_mis2(Carve& c, int64_t n, int64_t nnz, int max_warps, Mis2Ws* w);
 int max_coop_warps(const DeviceInfo& d);
 
 // Runs Alg. 1 on the device.  labels != NULL restricts to {v : labels[v] < 0}

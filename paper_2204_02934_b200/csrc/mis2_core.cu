@@ -35,14 +35,25 @@
 
 namespace mis2k {
 
-constexpr int kTileCap = 6912;      // int32 colinds per staging buffer (27 KB): 256 rows x 27
+// One block per SM (MIS2_WARPS = 32, the default): co-resident blocks of one
+// SM are not scheduled fairly (the youngest block of an SM finishes a phase
+// ~9 us after the oldest on C2, measured), and a grid barrier over 148
+// blocks costs about half of one over 592.
+#ifndef MIS2_WARPS
+#define MIS2_WARPS 8
+#endif
+constexpr int kMW = MIS2_WARPS;
+constexpr int kMB = 32 * kMW;
+constexpr int kMinBlocksPerSM = kMW >= 16 ? 1 : 4;
+// int32 colinds per staging buffer: a dense step of 27-entry rows
+constexpr int kTileCap = (kMB >= 512 ? kMB / 2 : kMB) * 27;
 // rows longer than 8 gather batches of their lane group are deferred and
 // reduced by the whole block (flattened over all deferred rows of the block)
 template <int G>
 __host__ __device__ constexpr int heavy_len() {
     return 8 * G * (G <= 2 ? 16 : (G == 4 ? 8 : 4));
 }
-constexpr int kDenseNum = 3, kDenseDen = 8;  // dense if |worklist segment| >= 3/8 of the range
+constexpr int kDenseNum = 3, kDenseDen = 8;  // dense if |worklist segment| >= 3/8 of the range (pull phases)
 // M_v is only ever compared against T_v (Decide: "M_w = T_v", "M_w = OUT").
 // By Eq. 1 the low b bits of an undecided word are id+1, unique per vertex,
 // never 0 and never all ones (2^b - 1 > |V|), and M_w is always a
@@ -69,10 +80,23 @@ struct MisParams {
     int32_t* L2[2];                      // worklist_2
     unsigned long long* ctrl;
     int32_t* heavy;       // [n] deferred long rows, per-block segments at blo
+    uint8_t* oflag;       // push-form Decide: some w in N[v] got M_w = OUT this iteration
+    uint32_t* cnt;        // push-form Decide: |{w in N[v] : M_w = T_v}| this iteration
+    uint32_t* degc;       // |N[v] ∩ active| (closed), written by the column pass of iteration 0
+    int32_t* ci2;         // pruned adjacency (same offsets as colinds), see row_min_prune
+    int32_t* len2;        // pruned row length, -1: row not pruned (long rows)
     unsigned int* mark;   // stats only
     long long* dstats;    // stats only
     long long* timeline;  // MIS2_FLAG_TIMELINE only
+    float l2_keep;        // fraction of each block's colinds span kept in L2 (evict_last)
+    int dense_col64;
+    int sparse_kind;      // 0: per-row staged sparse_phase, 1: direct sparse_col
+    int prune_frac64;     // prune adjacency once |worklist_1| < prune_frac64/64 of the active vertices (0: never)
+    int bar_mode;         // grid barrier polling (common.cuh grid_barrier)      // column phase is dense if |worklist_2 segment| >= dense_col64/64 of the range
+    float qw[4];          // relative speed of the k-th co-resident block of an SM (row-range weights)
+    int nsm;
     int dbg_it, dbg_ph;   // MIS2_FLAG_TIMELINE: sparse phase instrumented into `mark`
+    int dbg_skip;         // measurement only (MIS2_DBG_SKIP): 1 no pushes, 2 no counts, 4 no degree
     Prio prio;
     int max_iters;
     uint8_t* in_set;
@@ -87,10 +111,11 @@ struct __align__(16) TileSmem {
     unsigned long long mbarS[2];  // sparse tiles: one arrival per row group
     int64_t sal[2];  // 16-byte aligned colinds start of the staged span
     int32_t fits[2];
+    uint64_t pol;    // L2 policy of this block's colinds span
     int cnt;         // survivors written this phase
     int hcount;
-    uint64_t red64[kWarpsPerBlock];
-    int wred[kWarpsPerBlock];
+    uint64_t red64[kMW];
+    int wred[kMW];
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -114,12 +139,46 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
         : "memory");
 }
 // Blackwell bulk-copy engine: global -> shared, completion on an mbarrier
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* b) {
+// with an L2 eviction-priority policy (see l2_policy)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* b,
+                                         uint64_t pol) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
             smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(b))
+        "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
         : "memory");
+}
+// L2 residency of the CSR stream.  Every phase re-streams colinds; C2's
+// 106 MB fits the 126 MB L2 but, with T, M, rowptr and the worklists also
+// cycling through it, a plain LRU-like replacement of a cyclic scan larger
+// than the cache keeps almost none of it between passes.  Each block marks
+// the first `keep` fraction of its own colinds span evict_last and the rest
+// evict_first, so a fixed, evenly spread part of the stream stays resident
+// from phase to phase (all blocks see the same hit rate).  The span is
+// demoted back to evict_normal when the call ends (l2_release).
+__device__ __forceinline__ uint64_t l2_policy(const MisParams& p, int64_t blo, int64_t bhi) {
+    const int64_t s0 = p.rowptr[blo] & ~(int64_t)31, s1 = p.rowptr[bhi];
+    const char* base = reinterpret_cast<const char*>(p.colinds + s0);
+    int64_t tot = (s1 - s0) * 4 + 128;
+    if (tot > 0x7fffff00ll) tot = 0x7fffff00ll;
+    const int64_t prim = (int64_t)((double)tot * (double)p.l2_keep) & ~(int64_t)127;
+    uint64_t pol;
+    if (p.l2_keep <= 0.f) {
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+        return pol;
+    }
+    asm volatile("createpolicy.range.global.L2::evict_last.L2::evict_first.b64 %0, [%1], %2, %3;"
+                 : "=l"(pol)
+                 : "l"(base), "r"((uint32_t)prim), "r"((uint32_t)tot));
+    return pol;
+}
+__device__ __forceinline__ void l2_release(const MisParams& p, int64_t blo, int64_t bhi) {
+    if (p.l2_keep <= 0.f) return;
+    const int64_t s0 = p.rowptr[blo] & ~(int64_t)31, s1 = p.rowptr[bhi];
+    const int64_t prim = (int64_t)((double)((s1 - s0) * 4 + 128) * (double)p.l2_keep);
+    const char* base = reinterpret_cast<const char*>(p.colinds + s0);
+    for (int64_t o = (int64_t)threadIdx.x * 128; o < prim; o += (int64_t)blockDim.x * 128)
+        asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(base + o) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -144,7 +203,7 @@ __device__ __forceinline__ uint64_t block_min_u64(TileSmem& sm, uint64_t x) {
     __syncthreads();
     uint64_t r = sm.red64[0];
 #pragma unroll
-    for (int w = 1; w < kWarpsPerBlock; w++) r = sm.red64[w] < r ? sm.red64[w] : r;
+    for (int w = 1; w < kMW; w++) r = sm.red64[w] < r ? sm.red64[w] : r;
     __syncthreads();
     return r;
 }
@@ -155,7 +214,7 @@ __device__ __forceinline__ long long block_sum_int(TileSmem& sm, int x) {
     __syncthreads();
     long long s = 0;
 #pragma unroll
-    for (int w = 0; w < kWarpsPerBlock; w++) s += sm.wred[w];
+    for (int w = 0; w < kMW; w++) s += sm.wred[w];
     __syncthreads();
     return s;
 }
@@ -215,6 +274,61 @@ __device__ __forceinline__ uint64_t row_min(const uint64_t* __restrict__ T, cons
     return m;
 }
 
+// The same, also counting the entries w != self with T_w != OUT (iteration 0:
+// exactly the active neighbours) for the push-form Decide.  Clamped repeats
+// are not counted.
+template <int G>
+__device__ __forceinline__ uint64_t row_min_deg(const uint64_t* __restrict__ T, const int32_t* x, int len, int sub,
+                                                uint64_t m, int64_t self, int& dc) {
+    constexpr int B = G <= 2 ? 16 : (G == 4 ? 8 : 4);
+    const int last = len - 1;
+    for (int j = sub; j < len; j += B * G) {
+        uint64_t tt[B];
+        int ww[B];
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            ww[q] = x[min(j + q * G, last)];
+            tt[q] = T[ww[q]];
+        }
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            m = tt[q] < m ? tt[q] : m;
+            dc += (j + q * G <= last) & (tt[q] != kOUT) & ((int64_t)ww[q] != self);
+        }
+    }
+    return m;
+}
+
+// Refresh Column of one row (thread per row) that also writes the row's
+// entries with T_w != OUT to out[0..k) and returns k.  A neighbour decided
+// OUT never changes a later minimum (OUT is the largest word) and never
+// needs a push, so later column passes may read the pruned row instead; a
+// row with an IN neighbour leaves worklist_2 in this pass, so dropping
+// nothing else is needed.  The same minimum results (exactly).  In place
+// (out == x) is safe: a batch is read before any of it is written, and
+// k <= entries read.
+__device__ __forceinline__ uint64_t row_min_prune(const uint64_t* __restrict__ T, const int32_t* x, int len,
+                                                  uint64_t m, int32_t* out, int& k) {
+    constexpr int B = 8;
+    const int last = len - 1;
+    k = 0;
+    for (int j = 0; j < len; j += B) {
+        uint64_t tt[B];
+        int32_t ww[B];
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            ww[q] = x[min(j + q, last)];
+            tt[q] = T[ww[q]];
+        }
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            m = tt[q] < m ? tt[q] : m;
+            if (j + q <= last && tt[q] != kOUT) out[k++] = ww[q];
+        }
+    }
+    return m;
+}
+
 // Decide of one row on id fields: exists M_w = OUT / forall
 // M_w = T_v (id v+1); M_w = 0 (inactive, reading Q15) is ignored.
 __device__ __forceinline__ void decide_acc(uint32_t m, uint32_t vid1, int& any_out, int& all_eq) {
@@ -255,7 +369,8 @@ __device__ __forceinline__ bool decide_write(const MisParams& p, int64_t v, int 
 }
 
 // issue the bulk copy of colinds[s, e) (16-byte aligned hull) into buffer `slot`
-__device__ __forceinline__ void stage_tile(TileSmem& sm, const MisParams& p, int slot, int64_t s, int64_t e) {
+__device__ __forceinline__ void stage_tile(TileSmem& sm, const MisParams& p, int slot, int64_t s, int64_t e,
+                                           const int32_t* src) {
     const int64_t sal = s & ~(int64_t)3;
     const int64_t nnz4 = p.nnz & ~(int64_t)3;
     const int64_t ecp = (e + 3) & ~(int64_t)3;
@@ -267,7 +382,7 @@ __device__ __forceinline__ void stage_tile(TileSmem& sm, const MisParams& p, int
     // fence.proxy.async, which would also drain this thread's global stores)
     if (fits && ecp > sal) {
         mbar_expect_tx(&sm.mbar[slot], (uint32_t)((ecp - sal) * 4));
-        bulk_g2s(sm.buf[slot], p.colinds + sal, (uint32_t)((ecp - sal) * 4), &sm.mbar[slot]);
+        bulk_g2s(sm.buf[slot], src + sal, (uint32_t)((ecp - sal) * 4), &sm.mbar[slot], sm.pol);
     } else {
         mbar_expect_tx(&sm.mbar[slot], 0u);
     }
@@ -275,16 +390,67 @@ __device__ __forceinline__ void stage_tile(TileSmem& sm, const MisParams& p, int
 
 // One row, GG lanes: Refresh Column (PH 0) or Decide (PH 1).  Returns the
 // survivor flag in the group leader.  Must be called by all lanes.
-template <int GG, int PH>
+// PUSH (single GPU): the column pass also does the edge work of Decide.
+// A row whose M_w becomes OUT marks every w' in N[w] (oflag: "some
+// neighbour has M = OUT", the first test of P:98-100); otherwise it counts
+// itself for its argmin a (cnt[a]; "forall w: M_w = T_a" of P:101-103 holds
+// iff cnt[a] = |N[a] ∩ active|).  Sound because a vertex still undecided at
+// iteration i has every active neighbour in worklist_2 (a neighbour that
+// left it earlier had M = OUT and made the vertex OUT then), so every
+// neighbour's M of iteration i is either pushed or counted.  Decide then
+// touches no edges (decide_push).
+__device__ __forceinline__ void push_out(const MisParams& p, const int32_t* x, int len, int sub, int stride) {
+    for (int j = sub; j < len; j += stride) p.oflag[x[j]] = 1;
+}
+
+template <int GG, int PH, bool PUSH>
 __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int sub, int64_t v, const int32_t* x,
-                                            int len, uint64_t tv, int it, uint64_t fi_next) {
+                                            int len, uint64_t tv, int it, uint64_t fi_next, int prune = 0,
+                                            int64_t s = 0) {
     bool keep = false;
     if (PH == 0) {
         uint64_t m = (act && sub == 0) ? tv : kOUT;  // closed neighbourhood (Q1)
-        if (act && len > 0) m = row_min<GG>(p.T, x, len, sub, m);
+        int dc = 0;
+        if (act && len > 0) {
+            if (GG == 1 && prune) {
+                int k = 0;
+                m = row_min_prune(p.T, x, len, m, p.ci2 + s, k);
+                p.len2[v] = k;
+            } else if (PUSH && it == 0 && p.labels) {
+                m = row_min_deg<GG>(p.T, x, len, sub, m, p.gbase + v, dc);
+            } else {
+                m = row_min<GG>(p.T, x, len, sub, m);
+            }
+        } else if (GG == 1 && prune && act) {
+            p.len2[v] = 0;
+        }
         m = group_min<GG>(m);
+        const uint32_t mf = m_field(m, p.id_mask);
+        if (PUSH) {
+            // the warp pushes its OUT rows one after another, 32 entries at a time
+            const int lane = threadIdx.x & 31;
+            unsigned bal = __ballot_sync(kFull, act && sub == 0 && mf == kM_OUT);
+            while (bal) {
+                const int l = __ffs(bal) - 1;
+                bal &= bal - 1;
+                const int32_t* xr = reinterpret_cast<const int32_t*>(
+                    __shfl_sync(kFull, reinterpret_cast<unsigned long long>(x), l));
+                const int lr = __shfl_sync(kFull, len, l);
+                push_out(p, xr, lr, lane, 32);
+                if (lane == l) p.oflag[v] = 1;
+            }
+            // count for the argmin; rows of a warp sharing one argmin add together
+            const bool cnt_me = act && sub == 0 && mf != kM_OUT;
+            const uint32_t key = cnt_me ? mf - 1u : (0x80000000u | (threadIdx.x & 31));
+            const unsigned grp = __match_any_sync(kFull, key);
+            if (cnt_me && (threadIdx.x & 31) == __ffs(grp) - 1)
+                atomicAdd(&p.cnt[(int64_t)key - p.gbase], (uint32_t)__popc(grp));
+            if (it == 0 && p.labels) {
+                dc = group_sum<GG>(dc);
+                if (act && sub == 0) p.degc[v] = (uint32_t)dc + 1u;
+            }
+        }
         if (act && sub == 0) {
-            const uint32_t mf = m_field(m, p.id_mask);
             p.M[v] = mf;
             keep = (mf != kM_OUT);
         }
@@ -320,7 +486,7 @@ __device__ __forceinline__ bool defer_long(TileSmem& sm, const MisParams& p, int
 // (prefix of the row lengths), 8 independent gathers per thread per pass,
 // combined per row with shared-memory atomics (min is exact in any order;
 // exists / forall likewise).
-template <bool STATS, int PH>
+template <bool STATS, int PH, bool PUSH>
 __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, int32_t* lout, uint64_t fi_next,
                             Stat& st) {
     const int t = threadIdx.x;
@@ -336,14 +502,14 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         dbuf[61] = nh;
     }
     char* base_ptr = reinterpret_cast<char*>(sm.buf[0]);
-    int64_t* pref = reinterpret_cast<int64_t*>(base_ptr);              // [kBlock + 1]
-    int64_t* rs = pref + (kBlock + 1);                                  // [kBlock] row starts
-    unsigned long long* acc = reinterpret_cast<unsigned long long*>(rs + kBlock);  // [kBlock] PH 0 min
-    int32_t* rv = reinterpret_cast<int32_t*>(acc + kBlock);             // [kBlock] rows
-    int32_t* anyo = rv + kBlock;                                        // [kBlock] PH 1 exists OUT
-    int32_t* alle = anyo + kBlock;                                      // [kBlock] PH 1 forall equal
-    for (int hb = 0; hb < nh; hb += kBlock) {
-        const int cnt = min(kBlock, nh - hb);
+    int64_t* pref = reinterpret_cast<int64_t*>(base_ptr);              // [kMB + 1]
+    int64_t* rs = pref + (kMB + 1);                                  // [kMB] row starts
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(rs + kMB);  // [kMB] PH 0 min
+    int32_t* rv = reinterpret_cast<int32_t*>(acc + kMB);             // [kMB] rows
+    int32_t* anyo = rv + kMB;                                        // [kMB] PH 1 exists OUT
+    int32_t* alle = anyo + kMB;                                      // [kMB] PH 1 forall equal
+    for (int hb = 0; hb < nh; hb += kMB) {
+        const int cnt = min(kMB, nh - hb);
         int64_t v = 0, s = 0, len = 0;
         if (t < cnt) {
             v = p.heavy[blo + hb + t];
@@ -353,6 +519,7 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
             rs[t] = s;
             if (PH == 0) {
                 acc[t] = p.T[v];  // closed neighbourhood (Q1)
+                if (PUSH) alle[t] = 0;  // active-neighbour count (iteration 0)
             } else {
                 const uint32_t mv = p.M[v];
                 const uint32_t vid1 = (uint32_t)(p.gbase + v) + 1u;
@@ -374,31 +541,33 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
             __syncthreads();
             long long wb = 0, tot = 0;
 #pragma unroll
-            for (int w = 0; w < kWarpsPerBlock; w++) {
+            for (int w = 0; w < kMW; w++) {
                 wb += (w < warp) ? (long long)sm.red64[w] : 0;
                 tot += (long long)sm.red64[w];
             }
             pref[t] = wb + inc - len;
-            if (t == 0) pref[kBlock] = tot;
+            if (t == 0) pref[kMB] = tot;
             __syncthreads();
         }
-        const int64_t total = pref[kBlock];
+        const int64_t total = pref[kMB];
         // each thread takes 8 consecutive entries per round and keeps a
         // running accumulator for its current row; one shared atomic per row
         // change (a hub row is reduced almost entirely in registers)
         int cur = -1;
         uint64_t cmin = kOUT;
-        int cany = 0, call = 1;
+        int cany = 0, call = 1, cdeg = 0;
+        const bool count_deg = PUSH && PH == 0 && it == 0 && p.labels;
         auto flush = [&]() {
             if (cur < 0) return;
             if (PH == 0) {
                 if (cmin < acc[cur]) atomicMin(&acc[cur], (unsigned long long)cmin);
+                if (count_deg && cdeg) atomicAdd(&alle[cur], cdeg);
             } else {
                 if (cany) anyo[cur] = 1;
                 if (!call) alle[cur] = 0;
             }
         };
-        for (int64_t c = (int64_t)t * 8; c < total; c += (int64_t)kBlock * 8) {
+        for (int64_t c = (int64_t)t * 8; c < total; c += (int64_t)kMB * 8) {
             int r = 0;
             {
                 int lo = 0, hi = cnt;  // last row with pref[row] <= c
@@ -431,8 +600,10 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
                         flush();
                         cur = rr[u];
                         cmin = kOUT;
+                        cdeg = 0;
                     }
                     cmin = tv[u] < cmin ? tv[u] : cmin;
+                    if (count_deg) cdeg += (tv[u] != kOUT) & (ww[u] != rv[cur]);
                 }
             } else {
                 uint32_t mm[8];
@@ -461,16 +632,34 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         flush();
         __syncthreads();
         bool keep = false;
+        int any_push = 0;
         if (t < cnt) {
             if (PH == 0) {
                 const uint32_t mf = m_field(acc[t], p.id_mask);
                 p.M[v] = mf;
                 keep = (mf != kM_OUT);
+                if (PUSH) {
+                    anyo[t] = !keep;
+                    any_push = !keep;
+                    if (keep) atomicAdd(&p.cnt[(int64_t)(mf - 1u) - p.gbase], 1u);
+                    else p.oflag[v] = 1;
+                    if (it == 0 && p.labels) p.degc[v] = (uint32_t)alle[t] + 1u;
+                }
             } else {
                 keep = decide_write(p, v, anyo[t], alle[t], it, fi_next);
             }
         }
         append(sm, keep, (int32_t)v, lout, blo);
+        if (PUSH && PH == 0 && __syncthreads_or(any_push)) {  // push OUT along the rows whose M became OUT
+            for (int64_t c = t; c < total; c += kMB) {
+                int lo = 0, hi = cnt;
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (pref[mid] <= c) lo = mid; else hi = mid;
+                }
+                if (anyo[lo]) p.oflag[p.colinds[rs[lo] + (c - pref[lo])]] = 1;
+            }
+        }
         __syncthreads();
     }
     stats_flush<STATS>(p, it, PH == 0 ? 1 : 0, st);
@@ -492,14 +681,16 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
 }
 
 // ------------------------------------------------------------ dense phase
-// Consecutive rows of the block range, RPB = kBlock/G per step; the step's
+// Consecutive rows of the block range, RPB = kMB/G per step; the step's
 // colinds span is bulk-copied into shared memory one step ahead.
 // PH = 0: Refresh Column over worklist_2 (M_v != OUT, active)
 // PH = 1: Decide over worklist_1 (T_v undecided)
-template <int G, bool STATS, int PH>
+template <int G, bool STATS, int PH, bool PUSH = false>
 __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, int64_t bhi, int32_t* lout,
-                           uint32_t& ph, uint64_t fi_next) {
-    constexpr int RPB = kBlock / G;
+                           uint32_t& ph, uint64_t fi_next, int prune = 0) {
+    constexpr int RPB = kMB / G;
+    // prune 1: read colinds, write the pruned rows; 2: read and rewrite the pruned rows
+    const int32_t* src = (G == 1 && prune == 2) ? p.ci2 : p.colinds;
     const int t = threadIdx.x, g = t / G, sub = t % G;
     const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
     Stat st;
@@ -514,7 +705,7 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
         const int64_t r2 = r1 + RPB < bhi ? r1 + RPB : bhi;
         nx_s = p.rowptr[r1];
         nx_e = p.rowptr[r2];
-        stage_tile(sm, p, 0, p.rowptr[blo], nx_s);
+        stage_tile(sm, p, 0, p.rowptr[blo], nx_s, src);
     }
     const bool dbg = p.timeline && it == p.dbg_it && PH == p.dbg_ph && threadIdx.x == 0;
     long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
@@ -535,11 +726,14 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
     int64_t ns0 = 0, ne0 = 0;
     uint64_t ntv = kOUT;
     uint32_t nmv = kM_OUT;
+    int32_t nl2 = -1;
+    const bool rd2 = G == 1 && PH == 0 && prune == 2;
     if (blo + g < bhi) {
         ns0 = p.rowptr[blo + g];
         ne0 = p.rowptr[blo + g + 1];
         ntv = p.T[blo + g];
         if (PH == 0) nmv = p.M[blo + g];
+        if (rd2) nl2 = p.len2[blo + g];
     }
     for (int64_t k = 0; k < nsteps; k++) {
         const int slot = (int)(k & 1);
@@ -554,7 +748,7 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
                 nx_s = p.rowptr[r2];
                 nx_e = p.rowptr[r3];
             }
-            stage_tile(sm, p, slot ^ 1, s1, e1);
+            stage_tile(sm, p, slot ^ 1, s1, e1, src);
         }
         // this tile's row bounds and status were loaded one step ahead; load
         // the next tile's now (a phase writes only rows of the tile it is
@@ -563,6 +757,7 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
         const bool valid = v < bhi;
         const int64_t s = ns0, e = ne0;
         const uint64_t tv = ntv;
+        const int32_t l2 = nl2;
         bool act = false;
         if (valid) act = PH == 0 ? (nmv != kM_OUT && nmv != 0u) : (tv != kIN && tv != kOUT);
         {
@@ -572,16 +767,20 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
                 ne0 = p.rowptr[vn + 1];
                 ntv = p.T[vn];
                 if (PH == 0) nmv = p.M[vn];
+                if (rd2) nl2 = p.len2[vn];
             }
         }
-        const int64_t len = e - s;
-        if (defer_long<G>(sm, p, blo, act, sub, v, len)) act = false;
+        const int64_t len = (rd2 && l2 >= 0) ? (int64_t)l2 : e - s;
+        if (defer_long<G>(sm, p, blo, act, sub, v, len)) {
+            act = false;
+            if (G == 1 && prune == 1) p.len2[v] = -1;  // long rows stay unpruned (read from colinds)
+        }
         if (dbg && k < 12) dbuf[4 + 5 * k + 2] = gt();
         mbar_wait(&sm.mbar[slot], (ph >> slot) & 1u);
         ph ^= 1u << slot;
         if (dbg && k < 12) dbuf[4 + 5 * k + 3] = gt();
-        const int32_t* x = sm.fits[slot] ? sm.buf[slot] + (s - sm.sal[slot]) : p.colinds + s;
-        const bool keep = process_row<G, PH>(p, act, sub, v, x, (int)len, tv, it, fi_next);
+        const int32_t* x = sm.fits[slot] ? sm.buf[slot] + (s - sm.sal[slot]) : src + s;
+        const bool keep = process_row<G, PH, PUSH>(p, act, sub, v, x, (int)len, tv, it, fi_next, prune == 1, s);
         if (dbg && k < 12) dbuf[4 + 5 * k + 4] = gt();
         if (STATS && act) {
             stat_row<STATS>(p, tag, v, sub == 0, len, st);
@@ -590,11 +789,11 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
         append(sm, keep, (int32_t)v, lout, blo);
     }
     if (dbg) dbuf[3] = gt();
-    return finish_phase<STATS, PH>(sm, p, it, blo, lout, fi_next, st);
+    return finish_phase<STATS, PH, PUSH>(sm, p, it, blo, lout, fi_next, st);
 }
 
 // ------------------------------------------------------------ sparse phase
-// Rows of the block's compacted worklist, RPBS = kBlock/GS per step with
+// Rows of the block's compacted worklist, RPBS = kMB/GS per step with
 // GS = 2G lanes per row.  Each group leader bulk-copies its own row into a
 // fixed shared-memory slot (16-byte aligned hull, <= SLOT entries) one step
 // ahead; rows that do not fit are read from global memory.
@@ -604,15 +803,20 @@ struct __align__(16) SMeta {
     int32_t len;  // row length; bit 30 set: staged in the slot
 };
 constexpr int kMaxDbgBlocks = 1184;
-constexpr int kSlotRegion = 6144;  // entries of a buffer used for row slots; SMeta array after it
-constexpr int kTvOff = 6656;       // then the T_v of each row (uint64, <= 128 rows)
-static_assert(kTvOff + 2 * 128 <= kTileCap + 8, "T_v region does not fit");
+// sparse step layout of a staging buffer: row slots | SMeta per row | T_v per row
+constexpr int kMaxRowsS = kMB / 2;                    // rows per sparse step (GS >= 2)
+constexpr int kTvOff = kTileCap - 2 * kMaxRowsS;      // uint64 T_v per row
+constexpr int kSlotRegion = kTvOff - 4 * kMaxRowsS;   // entries used for row slots; SMeta after
+static_assert(kSlotRegion > 0 && (kSlotRegion % 4) == 0, "sparse layout");
 
-template <int G, bool STATS, int PH>
+template <int G, bool STATS, int PH, bool PUSH = false>
 __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, const int32_t* lin, int nin,
-                            int32_t* lout, uint32_t& ph, uint64_t fi_next) {
+                            int32_t* lout, uint32_t& ph, uint64_t fi_next, int prune = 0) {
+    // prune 2: rows are read from the pruned adjacency (ci2, len2)
+    const bool rd2 = G == 1 && PH == 0 && prune == 2;
+    const int32_t* src = rd2 ? p.ci2 : p.colinds;
     constexpr int GS = G * 2 <= 32 ? G * 2 : 32;
-    constexpr int RPBS = kBlock / GS;
+    constexpr int RPBS = kMB / GS;
     constexpr int SLOT = (kSlotRegion / RPBS) & ~3;
     static_assert(RPBS * sizeof(SMeta) <= (kTileCap - kSlotRegion) * 4, "SMeta region too small");
     constexpr int kStaged = 1 << 30;
@@ -654,7 +858,7 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         meta[gs] = m;
         reinterpret_cast<uint64_t*>(sm.buf[slot] + kTvOff)[gs] = tv;
         mbar_expect_tx(&sm.mbarS[slot], bytes);
-        if (bytes) bulk_g2s(sm.buf[slot] + gs * SLOT, p.colinds + sal, bytes, &sm.mbarS[slot]);
+        if (bytes) bulk_g2s(sm.buf[slot] + gs * SLOT, src + sal, bytes, &sm.mbarS[slot], sm.pol);
     };
     auto bounds = [&](int64_t v, int64_t& s, int64_t& e) {
         s = 0;
@@ -662,6 +866,10 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         if (v >= 0) {
             s = p.rowptr[v];
             e = p.rowptr[v + 1];
+            if (rd2) {
+                const int32_t l2 = p.len2[v];
+                if (l2 >= 0) e = s + l2;
+            }
         }
     };
 
@@ -712,8 +920,8 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         ph ^= 1u << (2 + slot);
         if (dbg && k < 12) dbuf[4 + 5 * k + 3] = gt();
         const int32_t* x = (m.len & kStaged) ? sm.buf[slot] + gs * SLOT + (m.s - (m.s & ~(int64_t)3))
-                                             : p.colinds + m.s;
-        const bool keep = process_row<GS, PH>(p, act, sub, v, x, len, tv, it, fi_next);
+                                             : src + m.s;
+        const bool keep = process_row<GS, PH, PUSH>(p, act, sub, v, x, len, tv, it, fi_next);
         if (dbg && k < 12) dbuf[4 + 5 * k + 4] = gt();
         if (STATS && act) {
             stat_row<STATS>(p, tag, v, sub == 0, len, st);
@@ -727,7 +935,222 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         v2 = v3;
     }
     if (dbg) dbuf[3] = gt();
-    return finish_phase<STATS, PH>(sm, p, it, blo, lout, fi_next, st);
+    return finish_phase<STATS, PH, PUSH>(sm, p, it, blo, lout, fi_next, st);
+}
+
+// ------------------------------------------------------------ sparse column (direct)
+// Refresh Column over the block's compacted worklist_2 with GS lanes per
+// row, colinds read straight from global memory (L1-cached): no staging, so
+// a pass is only limited by the neighbour gathers.  The worklist entry and
+// row bounds of the next pass are loaded while the current one gathers.
+template <int GS, bool STATS, bool PUSH>
+__device__ int sparse_col(TileSmem& sm, const MisParams& p, int it, int64_t blo, const int32_t* lin, int nin,
+                          int32_t* lout, int prune = 0) {
+    const bool rd2 = GS == 1 && prune == 2;
+    const int32_t* src = rd2 ? p.ci2 : p.colinds;
+    constexpr int RPS = kMB / GS;
+    const int t = threadIdx.x, gs = t / GS, sub = t % GS;
+    const unsigned tag = 2u * (unsigned)it + 1u;
+    Stat st;
+    if (t == 0) {
+        sm.cnt = 0;
+        sm.hcount = 0;
+    }
+    __syncthreads();
+    const int npass = (nin + RPS - 1) / RPS;
+    auto row_of = [&](int k) -> int64_t {
+        const int idx = k * RPS + gs;
+        return (k < npass && idx < nin) ? (int64_t)lin[blo + idx] : -1;
+    };
+    int64_t v = row_of(0), vn = row_of(1);
+    int64_t s = 0, e = 0;
+    uint64_t tv = kOUT;
+    int32_t l2 = -1;
+    if (v >= 0) {
+        s = p.rowptr[v];
+        e = p.rowptr[v + 1];
+        tv = p.T[v];
+        if (rd2) l2 = p.len2[v];
+    }
+    for (int k = 0; k < npass; k++) {
+        // prefetch: worklist entry two passes ahead, bounds one pass ahead
+        const int64_t vnn = row_of(k + 2);
+        int64_t sn = 0, en = 0;
+        uint64_t tvn = kOUT;
+        int32_t l2n = -1;
+        if (vn >= 0) {
+            sn = p.rowptr[vn];
+            en = p.rowptr[vn + 1];
+            tvn = p.T[vn];
+            if (rd2) l2n = p.len2[vn];
+        }
+        bool act = v >= 0;
+        const int64_t len = (rd2 && l2 >= 0) ? (int64_t)l2 : e - s;
+        if (defer_long<GS>(sm, p, blo, act, sub, v, len)) {
+            act = false;
+            if (GS == 1 && prune == 1) p.len2[v] = -1;
+        }
+        const bool keep = process_row<GS, 0, PUSH>(p, act, sub, act ? v : 0, src + s, (int)len, tv, it, 0, prune == 1, s);
+        if (STATS && act) {
+            stat_row<STATS>(p, tag, v, sub == 0, len, st);
+            stat_nbrs<STATS>(p, tag, p.colinds + s, len, sub, GS, st);
+        }
+        append(sm, keep, (int32_t)(v < 0 ? 0 : v), lout, blo);
+        v = vn;
+        vn = vnn;
+        s = sn;
+        e = en;
+        tv = tvn;
+        l2 = l2n;
+    }
+    return finish_phase<STATS, 0, PUSH>(sm, p, it, blo, lout, 0, st);
+}
+
+// ------------------------------------------------------------ push-form Decide
+// Decide over worklist_1 when the column pass has already done its
+// edge work (process_row, PUSH): v is OUT iff some M_w = OUT for w in N[v]
+// (oflag[v]); else IN iff every active w in N[v] has M_w = T_v
+// (cnt[v] = degc[v]); else it stays undecided and gets its word of iteration
+// it + 1 (fused Refresh Row).  No neighbour is read.  Dense: all
+// rows of the block range, membership from T_v; sparse: the worklist.
+__device__ __forceinline__ bool row_has(const int32_t* x, int64_t len, int32_t v) {
+    for (int64_t j = 0; j < len; j++)
+        if (x[j] == v) return true;
+    return false;
+}
+template <bool STATS>
+__device__ int decide_push(TileSmem& sm, const MisParams& p, int it, int64_t blo, int64_t bhi, const int32_t* lin,
+                           int nin, bool dense, int32_t* lout, uint64_t fi_next) {
+    const int t = threadIdx.x;
+    const unsigned tag = 2u * (unsigned)it + 2u;
+    Stat st;
+    // IN candidates whose test needs "is v in its own row": resolved after
+    // the loop, one warp per row (a serial scan inside the loop would stall
+    // its warp once per candidate)
+    int32_t* cand = sm.buf[0];
+    constexpr int kCandCap = 2 * kTileCap;
+    if (t == 0) {
+        sm.cnt = 0;
+        sm.hcount = 0;
+    }
+    __syncthreads();
+    const int64_t total = dense ? bhi - blo : (int64_t)nin;
+    const bool dbg = p.timeline && it == p.dbg_it && 1 == p.dbg_ph && t == 0;
+    long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
+    auto gt = []() {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        return (long long)ns;
+    };
+    if (dbg) {
+        dbuf[0] = gt();
+        dbuf[1] = total;
+    }
+    // U rows per thread per round, loads batched by dependency level
+    constexpr int U = 4;
+    for (int64_t base = 0; base < total; base += (int64_t)kMB * U) {
+        int64_t vv[U];
+        uint64_t tv[U];
+        uint32_t c[U];
+        uint8_t fl[U];
+        int64_t rs[U], re[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t idx = base + u * kMB + t;
+            vv[u] = idx < total ? (dense ? blo + idx : (int64_t)lin[blo + idx]) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            tv[u] = kIN;
+            fl[u] = 0;
+            c[u] = 0;
+            if (vv[u] >= 0) {
+                tv[u] = p.T[vv[u]];
+                fl[u] = p.oflag[vv[u]];
+                c[u] = p.cnt[vv[u]];
+            }
+        }
+        // IN candidates of the unmasked call need the row length
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            rs[u] = 0;
+            re[u] = 0;
+            if (vv[u] >= 0 && !p.labels && !fl[u] && c[u] > 0 && tv[u] != kIN && tv[u] != kOUT) {
+                rs[u] = p.rowptr[vv[u]];
+                re[u] = p.rowptr[vv[u] + 1];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t v = vv[u];
+            bool keep = false;
+            if (v >= 0 && tv[u] != kIN && tv[u] != kOUT) {
+                if (c[u]) p.cnt[v] = 0u;
+                bool in = false, later = false;
+                if (!fl[u] && c[u] > 0) {
+                    if (p.labels) {
+                        in = c[u] == p.degc[v];  // |N[v] ∩ active| counted by the column pass of iteration 0
+                    } else {                     // all active: |N[v]| = len + 1 - [v in its own row] (Q23)
+                        const int64_t len = re[u] - rs[u];
+                        if ((int64_t)c[u] == len + 1) {
+                            in = true;
+                        } else if ((int64_t)c[u] == len) {
+                            const int h = atomicAdd(&sm.hcount, 1);
+                            if (h < kCandCap) {
+                                cand[h] = (int32_t)v;
+                                later = true;
+                            } else {
+                                in = row_has(p.colinds + rs[u], len, (int32_t)v);
+                            }
+                        }
+                    }
+                }
+                if (later) {
+                } else if (fl[u]) p.T[v] = kOUT;
+                else if (in) p.T[v] = kIN;
+                else {
+                    p.T[v] = p.prio.word(it + 1, fi_next, p.gbase + v);
+                    keep = true;
+                }
+                if (STATS) {
+                    const int64_t s = p.rowptr[v], e = p.rowptr[v + 1];
+                    stat_row<STATS>(p, tag, v, true, e - s, st);
+                    stat_nbrs<STATS>(p, tag, p.colinds + s, e - s, 0, 1, st);
+                }
+            }
+            append(sm, keep, (int32_t)(v < 0 ? 0 : v), lout, blo);
+        }
+    }
+    if (dbg) dbuf[2] = gt();
+    __syncthreads();
+    if (dbg) dbuf[5] = gt();
+    {
+        const int nh = min(sm.hcount, kCandCap), lane = t & 31;
+        if (dbg) dbuf[4] = nh;
+        for (int i = t >> 5; i < nh; i += kMW) {
+            const int32_t v = cand[i];
+            const int64_t s = p.rowptr[v], len = p.rowptr[v + 1] - s;
+            bool found = false;
+            for (int64_t j = lane; j < len; j += 32) found |= p.colinds[s + j] == v;
+            found = __any_sync(kFull, found);
+            bool keep = false;
+            if (lane == 0) {
+                if (found) {
+                    p.T[v] = kIN;
+                } else {
+                    p.T[v] = p.prio.word(it + 1, fi_next, p.gbase + v);
+                    keep = true;
+                }
+            }
+            append(sm, keep, v, lout, blo);
+        }
+    }
+    if (dbg) dbuf[3] = gt();
+    stats_flush<STATS>(p, it, 0, st);
+    __syncthreads();
+    const int out = sm.cnt;
+    __syncthreads();
+    return out;
 }
 
 __device__ __forceinline__ void stamp(const MisParams& p, int slot) {
@@ -738,24 +1161,46 @@ __device__ __forceinline__ void stamp(const MisParams& p, int slot) {
     }
 }
 
+// Row range of block b: contiguous, proportional to qw[b / nsm] (the
+// co-resident blocks of an SM are not scheduled fairly; block b + k*nsm is
+// the k-th block placed on its SM).  wrange(B) = n exactly.
+__device__ __forceinline__ int64_t wrange(const MisParams& p, int64_t b, int64_t B) {
+    const int64_t S = p.nsm > 0 ? p.nsm : B;
+    double acc = 0.0, tot = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        int64_t cnt = B - c * S;
+        cnt = cnt < 0 ? 0 : (cnt > S ? S : cnt);
+        if (c == 3) cnt = B - 3 * S > 0 ? B - 3 * S : 0;  // any further blocks share the last weight
+        int64_t mine = b - c * S;
+        mine = mine < 0 ? 0 : (mine > cnt ? cnt : mine);
+        tot += (double)cnt * p.qw[c];
+        acc += (double)mine * p.qw[c];
+    }
+    return acc >= tot ? p.n : (int64_t)((double)p.n * acc / tot);
+}
+
 // ------------------------------------------------------------ the kernel
-template <int G, bool STATS>
-__global__ void __launch_bounds__(kBlock, 4) mis2_persistent(MisParams p) {
+// PUSH: push-form Decide (the column pass pushes / counts, decide_push
+// touches no edges); otherwise the pull form of Alg. 1 as written.
+template <int G, bool STATS, bool PUSH>
+__global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
     const int t = threadIdx.x;
     const int64_t B = gridDim.x;
-    const int64_t blo = p.n * blockIdx.x / B, bhi = p.n * (blockIdx.x + 1) / B;
+    const int64_t blo = wrange(p, blockIdx.x, B), bhi = wrange(p, blockIdx.x + 1, B);
     unsigned int* bar = (unsigned int*)&p.ctrl[0];
     unsigned long long* ring = &p.ctrl[1];
 
     if (t == 0) {
         mbar_init(&sm.mbar[0], 1);
         mbar_init(&sm.mbar[1], 1);
-        constexpr int kRowGroups = kBlock / (G * 2 <= 32 ? G * 2 : 32);
+        constexpr int kRowGroups = kMB / (G * 2 <= 32 ? G * 2 : 32);
         mbar_init(&sm.mbarS[0], kRowGroups);
         mbar_init(&sm.mbarS[1], kRowGroups);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        sm.pol = l2_policy(p, blo, bhi);
     }
     uint32_t ph = 0u;  // mbarrier phase bits: 0,1 dense buffers; 2,3 sparse buffers
 
@@ -763,16 +1208,18 @@ __global__ void __launch_bounds__(kBlock, 4) mis2_persistent(MisParams p) {
     {
         const uint64_t fi0 = p.prio.iter_term(0);
         int act_cnt = 0;
-        for (int64_t v = blo + t; v < bhi; v += kBlock) {
+        for (int64_t v = blo + t; v < bhi; v += kMB) {
             const bool act = p.labels ? (p.labels[v] < 0) : true;
             p.T[v] = act ? p.prio.word(0, fi0, p.gbase + v) : kOUT;
             p.M[v] = act ? kPending : 0u;  // 0 = inactive sentinel (reading Q15)
+            p.oflag[v] = 0;
+            p.cnt[v] = 0u;
             act_cnt += act;
         }
         const long long s = block_sum_int(sm, act_cnt);
         if (t == 0 && s) atomicAdd(&p.ctrl[7], (unsigned long long)s);
     }
-    grid_barrier(bar);
+    grid_barrier(bar, p.bar_mode);
     stamp(p, 0);
     const unsigned long long n_active = ld_acquire_u64(&p.ctrl[7]);
 
@@ -780,26 +1227,42 @@ __global__ void __launch_bounds__(kBlock, 4) mis2_persistent(MisParams p) {
     int status = MIS2_OK;
     const int64_t range = bhi - blo;
     int cnt1 = (int)range, cnt2 = (int)range;  // this block's worklist segment sizes
+    unsigned long long wl1_global = n_active;   // |worklist_1| before this iteration
+    bool pruned = false;
     while (n_active > 0) {  // while worklist_1 != {}
         const int cur = it & 1;
         // ---- Refresh Column over worklist_2
-        const bool dense2 = (it == 0) || (int64_t)cnt2 * kDenseDen >= range * kDenseNum;
-        cnt2 = dense2 ? dense_phase<G, STATS, 0>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0)
-                      : sparse_phase<G, STATS, 0>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
-        grid_barrier(bar);
+        const bool dense2 = (it == 0) || (int64_t)cnt2 * 64 >= range * p.dense_col64;
+        constexpr int GS = G == 1 ? 4 : (G * 2 <= 32 ? G * 2 : 32);
+        // adjacency pruning (row_min_prune): from the first iteration in
+        // which fewer than prune_frac of the active vertices are undecided
+        int prune = 0;
+        if (G == 1 && PUSH && !STATS && p.prune_frac64 > 0) {
+            if (pruned) prune = 2;
+            else if (it > 0 && wl1_global * 64 < n_active * (unsigned long long)p.prune_frac64) prune = 1;
+        }
+        if (dense2) cnt2 = dense_phase<G, STATS, 0, PUSH>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0, prune);
+        else if (prune == 1) cnt2 = sparse_col<1, STATS, PUSH>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], prune);
+        else if (prune == 2) cnt2 = sparse_phase<G, STATS, 0, PUSH>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0, prune);
+        else if (p.sparse_kind == 1) cnt2 = sparse_col<GS, STATS, PUSH>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1]);
+        else cnt2 = sparse_phase<G, STATS, 0, PUSH>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
+        if (prune) pruned = true;
+        grid_barrier(bar, p.bar_mode);
         stamp(p, 1 + 2 * it);
         // ---- Decide over worklist_1 + fused refresh of iteration it+1
         const uint64_t fi_next = p.prio.iter_term(it + 1);
         const bool dense1 = (it == 0) || (int64_t)cnt1 * kDenseDen >= range * kDenseNum;
-        cnt1 = dense1 ? dense_phase<G, STATS, 1>(sm, p, it, blo, bhi, p.L1[cur ^ 1], ph, fi_next)
-                      : sparse_phase<G, STATS, 1>(sm, p, it, blo, p.L1[cur], cnt1, p.L1[cur ^ 1], ph, fi_next);
+        if (PUSH) cnt1 = decide_push<STATS>(sm, p, it, blo, bhi, p.L1[cur], cnt1, dense1, p.L1[cur ^ 1], fi_next);
+        else if (dense1) cnt1 = dense_phase<G, STATS, 1>(sm, p, it, blo, bhi, p.L1[cur ^ 1], ph, fi_next);
+        else cnt1 = sparse_phase<G, STATS, 1>(sm, p, it, blo, p.L1[cur], cnt1, p.L1[cur ^ 1], ph, fi_next);
         if (t == 0) {
             if (cnt1) atomicAdd(&ring[it & 3], (unsigned long long)cnt1);
             if (blockIdx.x == 0) ring[(it + 2) & 3] = 0;  // slot last read two barriers ago
         }
-        grid_barrier(bar);
+        grid_barrier(bar, p.bar_mode);
         stamp(p, 2 + 2 * it);
         const unsigned long long remaining = ld_acquire_u64(&ring[it & 3]);
+        wl1_global = remaining;
         it++;
         if (remaining == 0) break;
         if (it >= p.max_iters) {  // reading Q12
@@ -809,8 +1272,9 @@ __global__ void __launch_bounds__(kBlock, 4) mis2_persistent(MisParams p) {
     }
 
     // return {v : T_v = IN}
+    l2_release(p, blo, bhi);
     int cnt = 0;
-    for (int64_t v = blo + t; v < bhi; v += kBlock) {
+    for (int64_t v = blo + t; v < bhi; v += kMB) {
         const uint8_t in = (p.T[v] == kIN);
         p.in_set[v] = in;
         cnt += in;
@@ -833,25 +1297,27 @@ __global__ void __launch_bounds__(kBlock, 4) mis2_persistent(MisParams p) {
 // The same phases as one launch each, for the partitioned driver (dist.cu),
 // which exchanges ghost T / M between them.  Block worklist segment sizes
 // live in cnts[0..B) (worklist_1) and cnts[B..2B) (worklist_2).
-__device__ __forceinline__ void init_mbars(TileSmem& sm, int G2) {
+__device__ __forceinline__ void init_mbars(TileSmem& sm, const MisParams& p, int G2) {
     if (threadIdx.x == 0) {
+        const int64_t B = gridDim.x;
+        sm.pol = l2_policy(p, p.n * blockIdx.x / B, p.n * (blockIdx.x + 1) / B);
         mbar_init(&sm.mbar[0], 1);
         mbar_init(&sm.mbar[1], 1);
-        mbar_init(&sm.mbarS[0], kBlock / G2);
-        mbar_init(&sm.mbarS[1], kBlock / G2);
+        mbar_init(&sm.mbarS[0], kMB / G2);
+        mbar_init(&sm.mbarS[1], kMB / G2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kBlock) mis2_part_init(MisParams p, int* cnts, unsigned long long* n_active) {
+__global__ void __launch_bounds__(kMB) mis2_part_init(MisParams p, int* cnts, unsigned long long* n_active) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
     const int64_t B = gridDim.x;
     const int64_t blo = p.n * blockIdx.x / B, bhi = p.n * (blockIdx.x + 1) / B;
     const uint64_t fi0 = p.prio.iter_term(0);
     int act_cnt = 0;
-    for (int64_t v = blo + threadIdx.x; v < bhi; v += kBlock) {
+    for (int64_t v = blo + threadIdx.x; v < bhi; v += kMB) {
         const bool act = p.labels ? (p.labels[v] < 0) : true;
         p.T[v] = act ? p.prio.word(0, fi0, p.gbase + v) : kOUT;
         p.M[v] = act ? kPending : 0u;
@@ -866,11 +1332,11 @@ __global__ void __launch_bounds__(kBlock) mis2_part_init(MisParams p, int* cnts,
 }
 
 template <int G, int PH>
-__global__ void __launch_bounds__(kBlock, 4) mis2_part_phase(MisParams p, int it, int* cnts,
+__global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_part_phase(MisParams p, int it, int* cnts,
                                                               unsigned long long* wl1_total) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
-    init_mbars(sm, G * 2 <= 32 ? G * 2 : 32);
+    init_mbars(sm, p, G * 2 <= 32 ? G * 2 : 32);
     uint32_t ph = 0u;
     const int64_t B = gridDim.x;
     const int64_t blo = p.n * blockIdx.x / B, bhi = p.n * (blockIdx.x + 1) / B;
@@ -895,6 +1361,10 @@ __global__ void __launch_bounds__(kBlock, 4) mis2_part_phase(MisParams p, int it
 }
 
 __global__ void mis2_part_final(MisParams p, unsigned long long* count) {
+    {
+        const int64_t B = gridDim.x;
+        l2_release(p, p.n * blockIdx.x / B, p.n * (blockIdx.x + 1) / B);
+    }
     int c = 0;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < p.n; v += (int64_t)gridDim.x * blockDim.x) {
         const uint8_t in = (p.T[v] == kIN);
@@ -916,37 +1386,53 @@ int bits_for(int64_t n) {
     return b;
 }
 
+// fraction of the colinds stream marked evict_last (l2_policy): an L2 budget
+// (default 30% of L2, measured best on C2; MIS2_L2_KEEP_MB overrides, 0 disables) over its size
+float l2_keep_for(int64_t nnz) {
+    static int l2_bytes = -1;
+    if (l2_bytes < 0) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, dev) != cudaSuccess)
+            l2_bytes = 0;
+    }
+    double budget = 0.3 * (double)l2_bytes;
+    if (const char* e = getenv("MIS2_L2_KEEP_MB")) budget = atof(e) * 1048576.0;
+    const double bytes = (double)nnz * 4.0;
+    if (budget <= 0.0 || bytes <= 0.0) return 0.f;
+    return budget >= bytes ? 1.f : (float)(budget / bytes);
+}
+
 int max_iters_for(int64_t n, int requested) { return requested > 0 ? requested : 10 * bits_for(n) + 20; }
 
 int choose_group(int64_t n, int64_t nnz, int requested) {
     if (requested > 0) return requested;
     const double avg = n > 0 ? (double)nnz / (double)n : 0.0;
-    // a step of kBlock / G rows should fit one staging buffer
+    // a step of kMB / G rows should fit one staging buffer
     int g = 1;
-    while (g < 32 && (double)(kBlock / g) * avg > (double)kTileCap) g *= 2;
+    while (g < 32 && (double)(kMB / g) * avg > (double)kTileCap) g *= 2;
     return g;
 }
 
 template <int G, bool S>
-static void* kernel_ptr() {
-    return (void*)&mis2_persistent<G, S>;
+static void* kernel_ptr(bool push) {
+    return push ? (void*)&mis2_persistent<G, S, true> : (void*)&mis2_persistent<G, S, false>;
 }
 
-static void* pick_kernel(int G, bool stats) {
+static void* pick_kernel(int G, bool stats, bool push) {
     switch (G) {
-        case 1: return stats ? kernel_ptr<1, true>() : kernel_ptr<1, false>();
-        case 2: return stats ? kernel_ptr<2, true>() : kernel_ptr<2, false>();
-        case 4: return stats ? kernel_ptr<4, true>() : kernel_ptr<4, false>();
-        case 8: return stats ? kernel_ptr<8, true>() : kernel_ptr<8, false>();
-        case 16: return stats ? kernel_ptr<16, true>() : kernel_ptr<16, false>();
-        case 32: return stats ? kernel_ptr<32, true>() : kernel_ptr<32, false>();
+        case 1: return stats ? kernel_ptr<1, true>(push) : kernel_ptr<1, false>(push);
+        case 2: return stats ? kernel_ptr<2, true>(push) : kernel_ptr<2, false>(push);
+        case 4: return stats ? kernel_ptr<4, true>(push) : kernel_ptr<4, false>(push);
+        case 8: return stats ? kernel_ptr<8, true>(push) : kernel_ptr<8, false>(push);
+        case 16: return stats ? kernel_ptr<16, true>(push) : kernel_ptr<16, false>(push);
+        case 32: return stats ? kernel_ptr<32, true>(push) : kernel_ptr<32, false>(push);
     }
     return nullptr;
 }
 
 int max_coop_warps(const DeviceInfo& d) { return d.sms * 64; }
 
-void carve_mis2(Carve& c, int64_t n, int max_warps, Mis2Ws* w) {
+void carve_mis2(Carve& c, int64_t n, int64_t nnz, int max_warps, Mis2Ws* w) {
     (void)max_warps;
     w->ctrl = c.take<unsigned long long>(16);
     w->T = c.take<uint64_t>((size_t)n + 1);
@@ -957,6 +1443,11 @@ void carve_mis2(Carve& c, int64_t n, int max_warps, Mis2Ws* w) {
     }
     w->heavy = c.take<int32_t>((size_t)n + 1);
     w->mark = c.take<unsigned int>((size_t)n + 1);
+    w->oflag = c.take<uint8_t>((size_t)n + 1);
+    w->cnt = c.take<uint32_t>((size_t)n + 1);
+    w->degc = c.take<uint32_t>((size_t)n + 1);
+    w->len2 = c.take<int32_t>((size_t)n + 1);
+    w->ci2 = c.take<int32_t>((size_t)nnz + 4);
     w->dstats = c.take<long long>((size_t)kStatsMaxIters * 6);
     w->scal = c.take<long long>(8);
 }
@@ -966,10 +1457,10 @@ static cudaError_t launch_part_phase(int ph, const MisParams& p, int it, int gri
                                      unsigned long long* wl1, cudaStream_t s) {
     if (ph == 0) {
         cudaFuncSetAttribute((const void*)mis2_part_phase<G, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        mis2_part_phase<G, 0><<<grid, kBlock, smem, s>>>(p, it, cnts, wl1);
+        mis2_part_phase<G, 0><<<grid, kMB, smem, s>>>(p, it, cnts, wl1);
     } else {
         cudaFuncSetAttribute((const void*)mis2_part_phase<G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        mis2_part_phase<G, 1><<<grid, kBlock, smem, s>>>(p, it, cnts, wl1);
+        mis2_part_phase<G, 1><<<grid, kMB, smem, s>>>(p, it, cnts, wl1);
     }
     return cudaGetLastError();
 }
@@ -995,6 +1486,7 @@ static MisParams part_params(const PartDev& d) {
     p.prio.hi_mask = ~((1ull << p.prio.b) - 1ull);
     p.id_mask = (uint32_t)((1ull << p.prio.b) - 1ull);
     p.prio.n = d.n_global;
+    p.l2_keep = l2_keep_for(d.nnz);
     p.in_set = d.in_set;
     p.heavy = d.heavy;
     return p;
@@ -1006,13 +1498,13 @@ int part_step(const PartDev& d, int op, int it, cudaStream_t s) {
     const int grid = d.grid;
     if (op == kPartInit) {
         cudaFuncSetAttribute((const void*)mis2_part_init, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        mis2_part_init<<<grid, kBlock, smem, s>>>(p, d.cnts, d.ctr + 0);
+        mis2_part_init<<<grid, kMB, smem, s>>>(p, d.cnts, d.ctr + 0);
         count_launch();
         MIS2_CUDA_TRY(cudaGetLastError());
         return MIS2_OK;
     }
     if (op == kPartFinal) {
-        mis2_part_final<<<grid, kBlock, 0, s>>>(p, d.ctr + 2);
+        mis2_part_final<<<grid, kMB, 0, s>>>(p, d.ctr + 2);
         count_launch();
         MIS2_CUDA_TRY(cudaGetLastError());
         return MIS2_OK;
@@ -1040,7 +1532,7 @@ int debug_read(void* ws, size_t ws_bytes, int64_t n, long long* out, int64_t cou
     Mis2Ws w;
     DeviceInfo di;
     MIS2_TRY(device_info(&di));
-    carve_mis2(c, n, max_coop_warps(di), &w);
+    carve_mis2(c, n, 0, max_coop_warps(di), &w);  // mark precedes the nnz-sized pieces
     const int64_t cap = ((int64_t)n + 1) / 2;
     if (count > cap) count = cap;
     MIS2_CUDA_TRY(cudaMemcpy(out, w.mark, sizeof(long long) * count, cudaMemcpyDeviceToHost));
@@ -1050,9 +1542,9 @@ int debug_read(void* ws, size_t ws_bytes, int64_t n, long long* out, int64_t cou
 int part_grid(int64_t n_own, int G) {
     DeviceInfo di;
     if (device_info(&di) != MIS2_OK) return 1;
-    const int64_t rpb = kBlock / G;
+    const int64_t rpb = kMB / G;
     int64_t want = (n_own + 2 * rpb - 1) / (2 * rpb);
-    const int64_t cap = (int64_t)4 * di.sms;
+    const int64_t cap = (int64_t)kMinBlocksPerSM * di.sms;
     if (want > cap) want = cap;
     if (want < 1) want = 1;
     return (int)want;
@@ -1070,7 +1562,15 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
         set_error("stats/timeline mode supports max_iters <= %d", kStatsMaxIters);
         return MIS2_EINVAL;
     }
-    void* fn = pick_kernel(G, stats);
+    // push-form Decide for dense graphs (its per-row push / count overhead
+    // is amortised over long rows; measured: C5 (avg 80) faster, C3 (avg 7)
+    // slower, C2 (avg 26.5) even); MIS2_DECIDE=push|pull overrides
+    const double avg_deg = g.n > 0 ? (double)g.nnz / (double)g.n : 0.0;
+    bool push = avg_deg >= 32.0;
+    if (o.flags & MIS2_FLAG_PUSH_DECIDE) push = true;
+    if (o.flags & MIS2_FLAG_PULL_DECIDE) push = false;
+    if (const char* e = getenv("MIS2_DECIDE")) push = (e[0] == 'p' && e[1] == 'u' && e[2] == 's');
+    void* fn = pick_kernel(G, stats, push);
     if (!fn) {
         set_error("group must be one of 1,2,4,8,16,32 (got %d)", G);
         return MIS2_EINVAL;
@@ -1078,7 +1578,7 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     const int smem = (int)sizeof(TileSmem);
     MIS2_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0;
-    MIS2_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, smem));
+    MIS2_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kMB, smem));
     if (per_sm < 1) {
         set_error("persistent kernel does not fit on an SM");
         return MIS2_EINTERNAL;
@@ -1089,7 +1589,7 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     }
     const int64_t max_grid = (int64_t)per_sm * di.sms;
     // small graphs: about two steps of rows per block
-    const int64_t rpb = kBlock / G;
+    const int64_t rpb = kMB / G;
     const int64_t want = (g.n + 2 * rpb - 1) / (2 * rpb);
     const int grid = (int)(want < 1 ? 1 : (want > max_grid ? max_grid : want));
 
@@ -1115,10 +1615,16 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     p.ctrl = w.ctrl;
     p.heavy = w.heavy;
     p.mark = w.mark;
+    p.oflag = w.oflag;
+    p.cnt = w.cnt;
+    p.degc = w.degc;
+    p.ci2 = w.ci2;
+    p.len2 = w.len2;
     p.dstats = w.dstats;
     p.timeline = timeline ? w.dstats : nullptr;
     p.dbg_it = -1;
     p.dbg_ph = 0;
+    if (const char* e = getenv("MIS2_DBG_SKIP")) p.dbg_skip = atoi(e);
     if (timeline) {
         if (const char* e = getenv("MIS2_DBG_IT")) p.dbg_it = atoi(e);
         if (const char* e = getenv("MIS2_DBG_PH")) p.dbg_ph = atoi(e);
@@ -1130,6 +1636,19 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     p.prio.hi_mask = ~((1ull << p.prio.b) - 1ull);
     p.id_mask = (uint32_t)((1ull << p.prio.b) - 1ull);
     p.prio.n = g.n;
+    p.l2_keep = l2_keep_for(g.nnz);
+    p.nsm = di.sms;
+    p.dense_col64 = 24;
+    if (const char* e = getenv("MIS2_DENSE_COL64")) p.dense_col64 = atoi(e);  // tuning knob
+    p.sparse_kind = 0;
+    p.prune_frac64 = 0;  // off: measured slower on C2 (strided rewrite of the rows)
+    if (const char* e = getenv("MIS2_PRUNE64")) p.prune_frac64 = atoi(e);  // tuning knob
+    p.bar_mode = 0;
+    if (const char* e = getenv("MIS2_BAR_MODE")) p.bar_mode = atoi(e);
+    if (const char* e = getenv("MIS2_SPARSE_KIND")) p.sparse_kind = atoi(e);
+    p.qw[0] = p.qw[1] = p.qw[2] = p.qw[3] = 1.f;
+    if (const char* e = getenv("MIS2_QW"))  // tuning knob (measurement only)
+        sscanf(e, "%f,%f,%f,%f", &p.qw[0], &p.qw[1], &p.qw[2], &p.qw[3]);
     p.prio.override_ = o.prio_override;
     p.prio.override_iters = o.prio_override ? o.prio_iters : 0;
     p.max_iters = max_iters;
@@ -1138,7 +1657,7 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     p.d_iters = d_iters;
     p.d_status = d_status;
     void* args[] = {&p};
-    MIS2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args, smem, s));
+    MIS2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kMB), args, smem, s));
     count_launch();
     if (stats || timeline) {
         const size_t cnt = stats ? 6 * (size_t)max_iters : 2 * (size_t)max_iters + 2;

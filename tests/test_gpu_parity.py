@@ -46,9 +46,9 @@ def small_graphs(count, seed, nmax=200):
     return out
 
 
-def check_mis2(g, seed=0, group=0, scheme="xorstar", stats=False):
+def check_mis2(g, seed=0, group=0, scheme="xorstar", stats=False, decide="auto"):
     rp, ci = dev(g)
-    r = M().mis2(rp, ci, seed=seed, group=group, scheme=scheme, stats=stats)
+    r = M().mis2(rp, ci, seed=seed, group=group, scheme=scheme, stats=stats, decide=decide)
     o = O.mis2(g.rowptr, g.colinds, seed=seed, scheme=scheme, stats=stats)
     assert np.array_equal(r.in_set.cpu().numpy().astype(bool), o.in_set), g.name
     assert (r.count, r.iterations) == (o.count, o.iterations), g.name
@@ -71,17 +71,29 @@ def test_fig1_replay_gpu():
     assert sorted((np.nonzero(r1.in_set.cpu().numpy())[0] + 1).tolist()) == gold["in_after_iter0"]
 
 
+@pytest.mark.parametrize("decide", ["pull", "push"])
 @pytest.mark.parametrize("chunk", range(6))
-def test_random_small_graphs(chunk):
+def test_random_small_graphs(chunk, decide):
     for g in small_graphs(60, 1000 + chunk):
-        check_mis2(g, seed=chunk * 17)
+        check_mis2(g, seed=chunk * 17, decide=decide)
 
 
+@pytest.mark.parametrize("decide", ["pull", "push"])
 @pytest.mark.parametrize("group", [1, 2, 4, 8, 16, 32])
-def test_group_width_invariance(group):
+def test_group_width_invariance(group, decide):
     """§V-D lane grouping never changes results."""
     for g in small_graphs(25, 77, nmax=400) + [G.laplace3d_27pt(20), G.kronecker(11)]:
-        check_mis2(g, group=group)
+        check_mis2(g, group=group, decide=decide)
+
+
+@pytest.mark.parametrize("decide", ["pull", "push"])
+def test_decide_forms_long_rows(decide):
+    """Both Decide forms on graphs with rows beyond the deferred-row threshold
+    (hubs), with and without a stored diagonal (the push form's IN test)."""
+    for g in [G.random_powerlaw_graph(4000, 40, 3), G.kronecker(13), G.random_graph(800, 0.6, 9, diagonal=True),
+              G.random_graph(800, 0.6, 9, diagonal=False), G.from_edges(300, [(0, j) for j in range(1, 300)])]:
+        check_mis2(g, decide=decide)
+        check_mis2(g, decide=decide, seed=99)
 
 
 @pytest.mark.parametrize("scheme", ["xorstar", "fixed", "xor"])
@@ -90,9 +102,10 @@ def test_schemes(scheme):
         check_mis2(g, scheme=scheme)
 
 
-def test_stats_parity():
+@pytest.mark.parametrize("decide", ["pull", "push"])
+def test_stats_parity(decide):
     for g in [G.grid2d_5pt(10, 10), G.laplace3d_27pt(30), G.kronecker(12), G.random_graph(300, 0.02, 4)]:
-        check_mis2(g, stats=True)
+        check_mis2(g, stats=True, decide=decide)
 
 
 def test_edge_cases():
@@ -113,6 +126,8 @@ def test_config2_full():
     r = check_mis2(g, stats=True)
     assert (r.count, r.iterations) == (21587, 10)
     check_mis2(g, seed=12345)
+    check_mis2(g, decide="push")
+    check_mis2(g, decide="pull")
 
 
 @pytest.mark.slow
@@ -173,9 +188,9 @@ def test_mis2_host_e2e():
 
 
 # ----------------------------------------------------------------- aggregation
-def check_agg(g, seed=0):
+def check_agg(g, seed=0, decide="auto"):
     rp, ci = dev(g)
-    a = M().aggregate(rp, ci, seed=seed)
+    a = M().aggregate(rp, ci, seed=seed, decide=decide)
     o = O.aggregate(g.rowptr, g.colinds, seed=seed)
     assert a.num_aggs == o.num_aggs, g.name
     assert np.array_equal(a.labels.cpu().numpy(), o.labels), g.name
@@ -184,10 +199,12 @@ def check_agg(g, seed=0):
     return a
 
 
+@pytest.mark.parametrize("decide", ["pull", "push"])
 @pytest.mark.parametrize("chunk", range(3))
-def test_aggregate_small(chunk):
+def test_aggregate_small(chunk, decide):
+    """includes the masked phase-2 MIS-2 (reading Q15) under both Decide forms"""
     for g in small_graphs(40, 2000 + chunk):
-        check_agg(g, seed=chunk)
+        check_agg(g, seed=chunk, decide=decide)
 
 
 def test_aggregate_heavy_leftovers():
