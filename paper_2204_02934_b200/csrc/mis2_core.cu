@@ -270,6 +270,7 @@ __device__ __forceinline__ uint64_t row_min(const uint64_t* __restrict__ T, cons
         for (int q = 0; q < B; q++) tt[q] = T[x[min(j + q * G, last)]];
 #pragma unroll
         for (int q = 0; q < B; q++) m = tt[q] < m ? tt[q] : m;
+        if (m == kIN) break;  // IN is the least word: the row's M is OUT whatever follows
     }
     return m;
 }
@@ -346,6 +347,7 @@ __device__ __forceinline__ void row_decide(const uint32_t* __restrict__ M, const
         for (int q = 0; q < B; q++) mm[q] = M[x[min(j + q * G, last)]];
 #pragma unroll
         for (int q = 0; q < B; q++) decide_acc(mm[q], vid1, any_out, all_eq);
+        if (any_out) break;  // the row is OUT whatever follows
     }
 }
 
