@@ -207,6 +207,16 @@ int mis2_comm_set_graph(mis2_comm* c, int64_t n_global, const int64_t* rowptr_h,
                         void* stream);
 int mis2_dist_mis2(mis2_comm* c, const mis2_opts* o, uint8_t* in_set, int64_t* count, int32_t* iters,
                    void* stream);
+/* Alg. 3 over the partition, bit-identical to mis2_aggregate():
+ * both MIS-2 calls partitioned, roots numbered by a global exclusive prefix
+ * of per-part counts (allgather), root / accepted-root ids and labels
+ * exchanged as ghost halos before the passes that read them, phase-3
+ * aggregate sizes summed over the parts (allreduce).  labels: device int32,
+ * this rank's n_own rows (NCCL) or all n rows (LOCAL), GLOBAL aggregate ids.
+ * stats (host int64[8] or NULL) as mis2_aggregate's.  Collective call.
+ * MIS2_FLAG_BASIC and prio_override are not supported (MIS2_EINVAL). */
+int mis2_dist_aggregate(mis2_comm* c, const mis2_opts* o, int32_t* labels, int64_t* num_aggs, int64_t* stats,
+                        void* stream);
 /* rows [lo, hi) and ghost count of local part `part` (NCCL: part 0) */
 int mis2_comm_part_info(mis2_comm* c, int part, int64_t* lo, int64_t* hi, int64_t* n_ghost);
 int mis2_comm_destroy(mis2_comm* c);

@@ -33,7 +33,8 @@ DECIDE = {"auto": 0, "push": FLAG_PUSH_DECIDE, "pull": FLAG_PULL_DECIDE}
 EXPORTS = ["mis2_opts_default", "mis2_workspace_size", "mis2", "mis2_async", "mis2_host", "mis2_aggregate",
            "mis2_coarsen", "mis2_validate_graph", "mis2_last_launch_count", "mis2_strerror", "mis2_last_error",
            "mis2_version", "mis2_comm_unique_id", "mis2_comm_init_nccl", "mis2_comm_init_local",
-           "mis2_comm_set_graph", "mis2_dist_mis2", "mis2_comm_part_info", "mis2_comm_destroy", "mis2_plan_part"]
+           "mis2_comm_set_graph", "mis2_dist_mis2", "mis2_dist_aggregate", "mis2_comm_part_info", "mis2_comm_destroy",
+           "mis2_plan_part"]
 
 
 class Mis2Error(RuntimeError):
@@ -76,6 +77,7 @@ def lib():
         L.mis2_aggregate.argtypes = [P, P, P, P, P, P, P, SZ, P]
         L.mis2_coarsen.argtypes = [P, P, I64, P, P, I64, P, P, SZ, P]
         L.mis2_validate_graph.argtypes = [P, P, SZ, P]
+        L.mis2_dist_aggregate.argtypes = [P, P, P, P, P, P]
         L.mis2_last_launch_count.restype = I64
         L.mis2_strerror.restype = ctypes.c_char_p
         L.mis2_strerror.argtypes = [ctypes.c_int]
@@ -376,6 +378,18 @@ class Comm:
         _check(lib().mis2_dist_mis2(self.h, ctypes.byref(o), in_set.data_ptr(), ctypes.byref(cnt), ctypes.byref(its),
                                     _stream()), "mis2_dist_mis2")
         return int(cnt.value), int(its.value)
+
+    def aggregate(self, labels, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0):
+        """Alg. 3 over the partition (``mis2_dist_aggregate``): fills ``labels``
+        (int32 CUDA tensor: this rank's rows, or all rows for local parts)
+        with global aggregate ids; returns (num_aggs, stats dict)."""
+        o = _opts(seed, scheme, max_iters, group)
+        na = ctypes.c_int64(0)
+        st = np.zeros(8, dtype=np.int64)
+        _check(lib().mis2_dist_aggregate(self.h, ctypes.byref(o), labels.data_ptr(), ctypes.byref(na),
+                                         st.ctypes.data, _stream()), "mis2_dist_aggregate")
+        keys = ["mis1", "iters1", "mis2", "iters2", "accepted2", "leftovers", "n1", "num_aggs"]
+        return int(na.value), dict(zip(keys, map(int, st)))
 
     def close(self):
         if self.h:

@@ -356,6 +356,61 @@ static void rows(int G, int64_t n, int sms, cudaStream_t s, int which, const mis
     }
 }
 
+// ---- raw-array launchers of the row kernels, for the partitioned driver
+// (dist.cu): rows are a partition's owned rows, colinds are local indices
+// and every array read through colinds holds the ghosts after the owned rows.
+static int64_t row_blocks(int G, int64_t n, int sms) {
+    const int64_t rows_per_block = (int64_t)(kBlock / 32) * (32 / G);
+    int64_t blocks = (n + rows_per_block - 1) / rows_per_block;
+    if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+    return blocks < 1 ? 1 : blocks;
+}
+#define AGG_DISPATCH(G, CALL)                  \
+    switch (G) {                               \
+        case 1: { constexpr int GG = 1; CALL; } break;  \
+        case 2: { constexpr int GG = 2; CALL; } break;  \
+        case 4: { constexpr int GG = 4; CALL; } break;  \
+        case 8: { constexpr int GG = 8; CALL; } break;  \
+        case 16: { constexpr int GG = 16; CALL; } break; \
+        default: { constexpr int GG = 32; CALL; } break; \
+    }
+void agg_phase1(int G, int64_t n, const int64_t* rowptr, const int32_t* colinds, const uint8_t* in1,
+                const int32_t* rid, int32_t* labels, int* err, int sms, cudaStream_t s) {
+    const unsigned b = (unsigned)row_blocks(G, n, sms);
+    AGG_DISPATCH(G, (k_phase1<GG><<<b, kBlock, 0, s>>>(n, rowptr, colinds, in1, rid, labels, nullptr, err)));
+    count_launch();
+}
+void agg_accept(int G, int64_t n, const int64_t* rowptr, const int32_t* colinds, const uint8_t* in2,
+                const int32_t* labels, uint8_t* acc, int sms, cudaStream_t s) {
+    const unsigned b = (unsigned)row_blocks(G, n, sms);
+    AGG_DISPATCH(G, (k_phase2_accept<GG><<<b, kBlock, 0, s>>>(n, rowptr, colinds, in2, labels, acc)));
+    count_launch();
+}
+void agg_phase2_label(int G, int64_t n, const int64_t* rowptr, const int32_t* colinds, const uint8_t* acc,
+                      const int32_t* aid, const int32_t* d_n1, int32_t* labels, int* err, int sms, cudaStream_t s) {
+    const unsigned b = (unsigned)row_blocks(G, n, sms);
+    AGG_DISPATCH(G, (k_phase2_label<GG><<<b, kBlock, 0, s>>>(n, rowptr, colinds, acc, aid, d_n1, labels, nullptr, err)));
+    count_launch();
+}
+void agg_tent_size(int64_t n, const int32_t* labels, int32_t* tent, int32_t* size, unsigned long long* left, int sms,
+                   cudaStream_t s) {
+    int64_t blocks = (n + kBlock - 1) / kBlock;
+    if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+    if (blocks < 1) blocks = 1;
+    k_tent_size<<<(unsigned)blocks, kBlock, 0, s>>>(n, labels, tent, size, left);
+    count_launch();
+}
+void agg_phase3(int G, int64_t n, const int64_t* rowptr, const int32_t* colinds, const int32_t* tent,
+                const int32_t* size, int32_t* labels, int32_t* heavy, int* heavy_cnt, int* err, int sms,
+                cudaStream_t s) {
+    const unsigned b = (unsigned)row_blocks(G, n, sms);
+    AGG_DISPATCH(G, (k_phase3<GG><<<b, kBlock, 0, s>>>(n, rowptr, colinds, tent, size, labels, heavy, heavy_cnt, err)));
+    count_launch();
+    k_phase3_heavy<<<sms * 4, kBlock, 0, s>>>(rowptr, colinds, tent, size, labels, heavy, heavy_cnt, err);
+    count_launch();
+}
+#undef AGG_DISPATCH
+
 int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int64_t* num_aggs, int32_t* roots,
                   int64_t* stats, void* ws, size_t ws_bytes, cudaStream_t s, size_t* bytes_needed) {
     DeviceInfo di;

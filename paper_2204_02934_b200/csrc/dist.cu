@@ -156,9 +156,30 @@ __global__ void k_pack_u32(const uint32_t* __restrict__ src, const int32_t* __re
         dst[i] = src[idx[i]];
 }
 
+__global__ void k_pack_u8(const uint8_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t cnt,
+                          uint8_t* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+// x[v] += off for v < n (local prefix -> global aggregate numbering)
+__global__ void k_add_i32(int32_t* __restrict__ x, int64_t n, int32_t off) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] += off;
+}
+__global__ void k_set_i32(int32_t* p, int32_t v) { *p = v; }
+
 }  // namespace
 
 // ------------------------------------------------------------------ handles
+// per-part state of the partitioned aggregation (allocated on first use)
+struct AggPart {
+    uint8_t *in1 = nullptr, *in2 = nullptr, *acc = nullptr;  // [n_own + n_ghost]
+    int32_t *rid = nullptr, *aid = nullptr, *lab = nullptr, *tent = nullptr;  // [n_own + n_ghost]
+    int32_t* size = nullptr;   // [n_global + 1] aggregate sizes (LOCAL: one array shared by all parts)
+    int32_t* heavy = nullptr;  // [n_own]
+    void* scan_tmp = nullptr;
+    long long* scal = nullptr; // [16]: 0 n_local(int32 at 0), 1 err, 2 heavy_cnt, 3 leftovers, 4 n1 (int32)
+};
 struct mis2_comm {
     bool local = false;
     int nparts = 1;  // P
@@ -173,6 +194,7 @@ struct mis2_comm {
     std::vector<uint32_t*> sendM;
     std::vector<int32_t*> send_idx_d;
     unsigned long long* d_sum = nullptr;  // NCCL allreduce buffer
+    std::vector<AggPart> agg;              // partitioned aggregation state
 };
 
 static int dev_alloc(mis2_comm* c, void** p, size_t bytes) {
@@ -190,6 +212,7 @@ static void free_parts(mis2_comm* c) {
     c->sendM.clear();
     c->send_idx_d.clear();
     c->d_sum = nullptr;
+    c->agg.clear();
 }
 
 // upload one planned part
@@ -279,6 +302,69 @@ static int exchange(mis2_comm* c, int which, cudaStream_t s) {
             NCCL_TRY(c->api, c->api->Recv(dst + es * (d.n_own + h.recv_off[q]), h.recv_cnt[q], ty, q, c->nccl, s));
     }
     NCCL_TRY(c->api, c->api->GroupEnd());
+    return MIS2_OK;
+}
+
+// ghost values of a per-part array of es-byte elements (1 or 4): arr[i] is
+// part i's local array [owned | ghosts]; the send buffers of T are scratch
+static int exchange_arr(mis2_comm* c, const std::vector<void*>& arr, int es, cudaStream_t s) {
+    const int P = c->nparts;
+    const int L = (int)c->dev.size();
+    for (int i = 0; i < L; i++) {
+        const int64_t ns = (int64_t)c->hp[i].send_idx.size();
+        if (!ns) continue;
+        const int blocks = (int)std::min<int64_t>((ns + 255) / 256, 1024);
+        if (es == 1) k_pack_u8<<<blocks, 256, 0, s>>>((const uint8_t*)arr[i], c->send_idx_d[i], ns, (uint8_t*)c->sendT[i]);
+        else k_pack_u32<<<blocks, 256, 0, s>>>((const uint32_t*)arr[i], c->send_idx_d[i], ns, (uint32_t*)c->sendT[i]);
+        count_launch();
+    }
+    MIS2_CUDA_TRY(cudaGetLastError());
+    if (c->local) {
+        for (int p = 0; p < P; p++) {
+            char* dst = (char*)arr[p];
+            for (int q = 0; q < P; q++) {
+                const int64_t cnt = c->hp[p].recv_cnt[q];
+                if (!cnt || q == p) continue;
+                const char* src = (const char*)c->sendT[q] + es * c->hp[q].send_off[p];
+                MIS2_CUDA_TRY(cudaMemcpyAsync(dst + es * (c->dev[p].n_own + c->hp[p].recv_off[q]), src, es * cnt,
+                                              cudaMemcpyDeviceToDevice, s));
+            }
+        }
+        return MIS2_OK;
+    }
+    const HostPart& h = c->hp[0];
+    const PartDev& d = c->dev[0];
+    const ncclDataType_t ty = es == 1 ? ncclUint8 : ncclInt32;
+    char* dst = (char*)arr[0];
+    const char* sb = (const char*)c->sendT[0];
+    NCCL_TRY(c->api, c->api->GroupStart());
+    for (int q = 0; q < P; q++) {
+        if (q == c->rank) continue;
+        if (h.send_cnt[q]) NCCL_TRY(c->api, c->api->Send(sb + es * h.send_off[q], h.send_cnt[q], ty, q, c->nccl, s));
+        if (h.recv_cnt[q])
+            NCCL_TRY(c->api, c->api->Recv(dst + es * (d.n_own + h.recv_off[q]), h.recv_cnt[q], ty, q, c->nccl, s));
+    }
+    NCCL_TRY(c->api, c->api->GroupEnd());
+    return MIS2_OK;
+}
+
+// per-part int64 values -> all of them on the host, in part order
+static int gather_counts(mis2_comm* c, const std::vector<int64_t>& mine, std::vector<int64_t>& all, cudaStream_t s) {
+    const int P = c->nparts;
+    all.assign(P, 0);
+    if (c->local) {
+        for (int p = 0; p < P; p++) all[p] = mine[p];
+        return MIS2_OK;
+    }
+    int64_t *d_in, *d_all;
+    MIS2_CUDA_TRY(cudaMalloc(&d_in, sizeof(int64_t)));
+    MIS2_CUDA_TRY(cudaMalloc(&d_all, sizeof(int64_t) * P));
+    MIS2_CUDA_TRY(cudaMemcpyAsync(d_in, &mine[0], sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    NCCL_TRY(c->api, c->api->AllGather(d_in, d_all, 1, ncclInt64, c->nccl, s));
+    MIS2_CUDA_TRY(cudaMemcpyAsync(all.data(), d_all, sizeof(int64_t) * P, cudaMemcpyDeviceToHost, s));
+    MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFree(d_in);
+    cudaFree(d_all);
     return MIS2_OK;
 }
 
@@ -453,24 +539,12 @@ int mis2_comm_set_graph(mis2_comm* c, int64_t n_global, const int64_t* rowptr_h,
     return MIS2_OK;
 }
 
-int mis2_dist_mis2(mis2_comm* c, const mis2_opts* o, uint8_t* in_set, int64_t* count, int32_t* iters, void* stream) {
-    reset_launches();
-    if (!c || !count || !iters || c->dev.empty()) {
-        set_error("bad arguments (graph not set?)");
-        return MIS2_EINVAL;
-    }
-    if (c->n_global > 0 && !in_set) {
-        set_error("null in_set");
-        return MIS2_EINVAL;
-    }
-    mis2_opts def;
-    mis2_opts_default(&def);
-    const mis2_opts& opt = o ? *o : def;
-    if (opt.prio_override) {
-        set_error("prio_override is not supported by the partitioned driver");
-        return MIS2_EINVAL;
-    }
-    cudaStream_t s = (cudaStream_t)stream;
+}  // extern "C"
+
+// Alg. 1 over the partition.  in_sets[i] = part i's owned mask; labels[i]
+// (or empty) = part i's phase-2 mask (active iff < 0, owned rows).
+static int dist_mis2_run(mis2_comm* c, const mis2_opts& opt, const std::vector<uint8_t*>& in_sets,
+                         const std::vector<const int32_t*>& labels, int64_t* count, int32_t* iters, cudaStream_t s) {
     const int max_iters = max_iters_for(c->n_global, opt.max_iters);
     const int L = (int)c->dev.size();
     for (int i = 0; i < L; i++) {
@@ -478,7 +552,8 @@ int mis2_dist_mis2(mis2_comm* c, const mis2_opts* o, uint8_t* in_set, int64_t* c
         d.seed = opt.seed;
         d.scheme = opt.scheme;
         if (opt.group) d.G = opt.group;
-        d.in_set = c->local ? in_set + c->hp[i].lo : in_set;
+        d.labels = labels.empty() ? nullptr : labels[i];
+        d.in_set = in_sets[i];
         MIS2_CUDA_TRY(cudaMemsetAsync(d.ctr, 0, sizeof(unsigned long long) * 8, s));
         MIS2_TRY(part_step(d, kPartInit, 0, s));
     }
@@ -509,6 +584,234 @@ int mis2_dist_mis2(mis2_comm* c, const mis2_opts* o, uint8_t* in_set, int64_t* c
     *iters = it;
     if (status != MIS2_OK) set_error("MIS-2 did not converge within max_iters");
     return status;
+}
+
+static int agg_alloc(mis2_comm* c) {
+    if (!c->agg.empty()) return MIS2_OK;
+    const int L = (int)c->dev.size();
+    c->agg.resize(L);
+    int32_t* shared_size = nullptr;
+    for (int i = 0; i < L; i++) {
+        AggPart& a = c->agg[i];
+        const PartDev& d = c->dev[i];
+        const int64_t nl = d.n_own + d.n_ghost + 1;
+        void* p;
+        MIS2_TRY(dev_alloc(c, &p, nl)); a.in1 = (uint8_t*)p;
+        MIS2_TRY(dev_alloc(c, &p, nl)); a.in2 = (uint8_t*)p;
+        MIS2_TRY(dev_alloc(c, &p, nl)); a.acc = (uint8_t*)p;
+        MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * nl)); a.rid = (int32_t*)p;
+        MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * nl)); a.aid = (int32_t*)p;
+        MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * nl)); a.lab = (int32_t*)p;
+        MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * nl)); a.tent = (int32_t*)p;
+        MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * (d.n_own + 1))); a.heavy = (int32_t*)p;
+        MIS2_TRY(dev_alloc(c, &p, scan_ws_bytes(d.n_own))); a.scan_tmp = p;
+        MIS2_TRY(dev_alloc(c, &p, sizeof(long long) * 16)); a.scal = (long long*)p;
+        if (!c->local || i == 0) {
+            MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * (c->n_global + 1)));
+            shared_size = (int32_t*)p;
+        }
+        a.size = shared_size;  // LOCAL: every part adds into the one global histogram
+    }
+    return MIS2_OK;
+}
+
+// Alg. 3 over the partition, bit-identical to mis2_aggregate():
+// the two MIS-2 calls run partitioned; roots are numbered by a global
+// exclusive prefix (per-part counts gathered); every array read through a
+// neighbour is completed with its ghost values before the pass that reads
+// it; the aggregate sizes of phase 3 are summed over the parts.
+static int dist_aggregate_run(mis2_comm* c, const mis2_opts& opt, const std::vector<int32_t*>& labels_out,
+                              int64_t* num_aggs, int64_t* stats, cudaStream_t s) {
+    MIS2_TRY(agg_alloc(c));
+    DeviceInfo di;
+    MIS2_TRY(device_info(&di));
+    const int L = (int)c->dev.size();
+    std::vector<void*> v_in1(L), v_acc(L), v_rid(L), v_aid(L), v_lab(L);
+    std::vector<uint8_t*> in1(L), in2(L);
+    std::vector<const int32_t*> labs(L);
+    for (int i = 0; i < L; i++) {
+        AggPart& a = c->agg[i];
+        v_in1[i] = a.in1; v_acc[i] = a.acc; v_rid[i] = a.rid; v_aid[i] = a.aid; v_lab[i] = a.lab;
+        in1[i] = a.in1; in2[i] = a.in2; labs[i] = a.lab;
+        MIS2_CUDA_TRY(cudaMemsetAsync(a.scal, 0, sizeof(long long) * 16, s));
+    }
+    auto scal_i32 = [&](int i, int slot) { return (int32_t*)&c->agg[i].scal[slot]; };
+    // local counts (int32 device scalar at slot) -> global exclusive offsets and the total
+    auto offsets = [&](int slot, std::vector<int64_t>& off, int64_t& total) -> int {
+        std::vector<int64_t> mine(L, 0);
+        for (int i = 0; i < L; i++) {
+            int32_t v = 0;
+            MIS2_CUDA_TRY(cudaMemcpyAsync(&v, scal_i32(i, slot), sizeof(v), cudaMemcpyDeviceToHost, s));
+            MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+            mine[i] = v;
+        }
+        std::vector<int64_t> all;
+        MIS2_TRY(gather_counts(c, mine, all, s));
+        const int P = c->nparts;
+        std::vector<int64_t> ex(P + 1, 0);
+        for (int q = 0; q < P; q++) ex[q + 1] = ex[q] + all[q];
+        off.assign(L, 0);
+        for (int i = 0; i < L; i++) off[i] = ex[c->local ? i : c->rank];
+        total = ex[P];
+        return MIS2_OK;
+    };
+
+    // ---- phase 1: M1 = MIS2(G); roots numbered in vertex order; pull labels
+    int64_t cnt1 = 0, cnt2 = 0;
+    int32_t it1 = 0, it2 = 0;
+    MIS2_TRY(dist_mis2_run(c, opt, in1, {}, &cnt1, &it1, s));
+    for (int i = 0; i < L; i++)
+        MIS2_TRY(scan_flags(c->agg[i].in1, c->dev[i].n_own, c->agg[i].rid, scal_i32(i, 0), c->agg[i].scan_tmp, s));
+    std::vector<int64_t> off1;
+    int64_t n1 = 0;
+    MIS2_TRY(offsets(0, off1, n1));
+    for (int i = 0; i < L; i++) {
+        const int64_t no = c->dev[i].n_own;
+        if (off1[i] && no) {
+            k_add_i32<<<(unsigned)std::min<int64_t>((no + 255) / 256, 4096), 256, 0, s>>>(c->agg[i].rid, no, (int32_t)off1[i]);
+            count_launch();
+        }
+    }
+    MIS2_TRY(exchange_arr(c, v_in1, 1, s));
+    MIS2_TRY(exchange_arr(c, v_rid, 4, s));
+    for (int i = 0; i < L; i++) {
+        const PartDev& d = c->dev[i];
+        agg_phase1(d.G, d.n_own, d.rowptr, d.colinds, c->agg[i].in1, c->agg[i].rid, c->agg[i].lab,
+                   (int*)scal_i32(i, 2), di.sms, s);
+    }
+    // ---- phase 2: M2 = MIS2(G \ aggregated) (reading Q15); accept >= 2 unaggregated neighbours
+    MIS2_TRY(dist_mis2_run(c, opt, in2, labs, &cnt2, &it2, s));
+    MIS2_TRY(exchange_arr(c, v_lab, 4, s));
+    for (int i = 0; i < L; i++) {
+        const PartDev& d = c->dev[i];
+        agg_accept(d.G, d.n_own, d.rowptr, d.colinds, c->agg[i].in2, c->agg[i].lab, c->agg[i].acc, di.sms, s);
+        MIS2_TRY(scan_flags(c->agg[i].acc, d.n_own, c->agg[i].aid, scal_i32(i, 0), c->agg[i].scan_tmp, s));
+    }
+    std::vector<int64_t> off2;
+    int64_t n2 = 0;
+    MIS2_TRY(offsets(0, off2, n2));
+    for (int i = 0; i < L; i++) {
+        const int64_t no = c->dev[i].n_own;
+        if (off2[i] && no) {
+            k_add_i32<<<(unsigned)std::min<int64_t>((no + 255) / 256, 4096), 256, 0, s>>>(c->agg[i].aid, no, (int32_t)off2[i]);
+            count_launch();
+        }
+        k_set_i32<<<1, 1, 0, s>>>(scal_i32(i, 8), (int32_t)n1);
+        count_launch();
+    }
+    MIS2_TRY(exchange_arr(c, v_acc, 1, s));
+    MIS2_TRY(exchange_arr(c, v_aid, 4, s));
+    for (int i = 0; i < L; i++) {
+        const PartDev& d = c->dev[i];
+        agg_phase2_label(d.G, d.n_own, d.rowptr, d.colinds, c->agg[i].acc, c->agg[i].aid, scal_i32(i, 8),
+                         c->agg[i].lab, (int*)scal_i32(i, 2), di.sms, s);
+    }
+    // ---- phase 3: frozen labels (ghosts too); sizes summed over the parts
+    MIS2_TRY(exchange_arr(c, v_lab, 4, s));
+    const int64_t na = n1 + n2;
+    for (int i = 0; i < L; i++) {
+        if (!c->local || i == 0) MIS2_CUDA_TRY(cudaMemsetAsync(c->agg[i].size, 0, sizeof(int32_t) * (na + 1), s));
+    }
+    for (int i = 0; i < L; i++) {
+        const PartDev& d = c->dev[i];
+        AggPart& a = c->agg[i];
+        agg_tent_size(d.n_own, a.lab, a.tent, a.size, (unsigned long long*)&a.scal[3], di.sms, s);
+        if (d.n_ghost)
+            MIS2_CUDA_TRY(cudaMemcpyAsync(a.tent + d.n_own, a.lab + d.n_own, sizeof(int32_t) * d.n_ghost,
+                                          cudaMemcpyDeviceToDevice, s));
+    }
+    if (!c->local && na > 0)
+        NCCL_TRY(c->api, c->api->AllReduce(c->agg[0].size, c->agg[0].size, (size_t)na, ncclInt32, ncclSum, c->nccl, s));
+    for (int i = 0; i < L; i++) {
+        const PartDev& d = c->dev[i];
+        AggPart& a = c->agg[i];
+        agg_phase3(d.G, d.n_own, d.rowptr, d.colinds, a.tent, a.size, a.lab, a.heavy, (int*)scal_i32(i, 4),
+                   (int*)scal_i32(i, 2), di.sms, s);
+        if (d.n_own)
+            MIS2_CUDA_TRY(cudaMemcpyAsync(labels_out[i], a.lab, sizeof(int32_t) * d.n_own, cudaMemcpyDeviceToDevice, s));
+    }
+    MIS2_CUDA_TRY(cudaGetLastError());
+    // errors and leftovers over all parts
+    long long err = 0, left = 0;
+    for (int i = 0; i < L; i++) {
+        long long h[16];
+        MIS2_CUDA_TRY(cudaMemcpyAsync(h, c->agg[i].scal, sizeof(h), cudaMemcpyDeviceToHost, s));
+        MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+        err |= ((const int32_t*)h)[2];
+        left += h[3];
+    }
+    if (!c->local) {
+        std::vector<int64_t> e1(1, err), l1(1, left), ea, la;
+        MIS2_TRY(gather_counts(c, e1, ea, s));
+        MIS2_TRY(gather_counts(c, l1, la, s));
+        err = 0;
+        left = 0;
+        for (int64_t x : ea) err |= x;
+        for (int64_t x : la) left += x;
+    }
+    if (err) {
+        set_error("aggregation invariant failed (flags 0x%llx): input graph not symmetric?", (long long)err);
+        return MIS2_EINTERNAL;
+    }
+    *num_aggs = na;
+    if (stats) {
+        stats[0] = cnt1;
+        stats[1] = it1;
+        stats[2] = cnt2;
+        stats[3] = it2;
+        stats[4] = n2;
+        stats[5] = left;
+        stats[6] = n1;
+        stats[7] = na;
+    }
+    return MIS2_OK;
+}
+
+extern "C" {
+
+int mis2_dist_mis2(mis2_comm* c, const mis2_opts* o, uint8_t* in_set, int64_t* count, int32_t* iters, void* stream) {
+    reset_launches();
+    if (!c || !count || !iters || c->dev.empty()) {
+        set_error("bad arguments (graph not set?)");
+        return MIS2_EINVAL;
+    }
+    if (c->n_global > 0 && !in_set) {
+        set_error("null in_set");
+        return MIS2_EINVAL;
+    }
+    mis2_opts def;
+    mis2_opts_default(&def);
+    const mis2_opts& opt = o ? *o : def;
+    if (opt.prio_override) {
+        set_error("prio_override is not supported by the partitioned driver");
+        return MIS2_EINVAL;
+    }
+    std::vector<uint8_t*> ins(c->dev.size());
+    for (size_t i = 0; i < c->dev.size(); i++) ins[i] = c->local ? in_set + c->hp[i].lo : in_set;
+    return dist_mis2_run(c, opt, ins, {}, count, iters, (cudaStream_t)stream);
+}
+
+int mis2_dist_aggregate(mis2_comm* c, const mis2_opts* o, int32_t* labels, int64_t* num_aggs, int64_t* stats,
+                        void* stream) {
+    reset_launches();
+    if (!c || !num_aggs || c->dev.empty()) {
+        set_error("bad arguments (graph not set?)");
+        return MIS2_EINVAL;
+    }
+    if (c->n_global > 0 && !labels) {
+        set_error("null labels");
+        return MIS2_EINVAL;
+    }
+    mis2_opts def;
+    mis2_opts_default(&def);
+    const mis2_opts& opt = o ? *o : def;
+    if (opt.prio_override || (opt.flags & MIS2_FLAG_BASIC)) {
+        set_error("prio_override / MIS2_FLAG_BASIC are not supported by the partitioned driver");
+        return MIS2_EINVAL;
+    }
+    std::vector<int32_t*> outs(c->dev.size());
+    for (size_t i = 0; i < c->dev.size(); i++) outs[i] = c->local ? labels + c->hp[i].lo : labels;
+    return dist_aggregate_run(c, opt, outs, num_aggs, stats, (cudaStream_t)stream);
 }
 
 int mis2_comm_part_info(mis2_comm* c, int part, int64_t* lo, int64_t* hi, int64_t* n_ghost) {

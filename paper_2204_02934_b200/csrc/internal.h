@@ -118,6 +118,19 @@ int run_coarsen(const mis2_graph& g, const int32_t* labels, int64_t na, int64_t*
                 cudaStream_t s, size_t* bytes_needed);
 int run_validate(const mis2_graph& g, void* ws, size_t ws_bytes, cudaStream_t s, size_t* bytes_needed);
 
+// aggregation row kernels on raw arrays (aggregate.cu), for the partitioned driver
+void agg_phase1(int G, int64_t n, const int64_t* rowptr, const int32_t* colinds, const uint8_t* in1,
+                const int32_t* rid, int32_t* labels, int* err, int sms, cudaStream_t s);
+void agg_accept(int G, int64_t n, const int64_t* rowptr, const int32_t* colinds, const uint8_t* in2,
+                const int32_t* labels, uint8_t* acc, int sms, cudaStream_t s);
+void agg_phase2_label(int G, int64_t n, const int64_t* rowptr, const int32_t* colinds, const uint8_t* acc,
+                      const int32_t* aid, const int32_t* d_n1, int32_t* labels, int* err, int sms, cudaStream_t s);
+void agg_tent_size(int64_t n, const int32_t* labels, int32_t* tent, int32_t* size, unsigned long long* left, int sms,
+                   cudaStream_t s);
+void agg_phase3(int G, int64_t n, const int64_t* rowptr, const int32_t* colinds, const int32_t* tent,
+                const int32_t* size, int32_t* labels, int32_t* heavy, int* heavy_cnt, int* err, int sms,
+                cudaStream_t s);
+
 // device-wide exclusive scan of 0/1 (uint8) flags -> int32 prefix, total to *d_total
 size_t scan_ws_bytes(int64_t n);
 int scan_flags(const uint8_t* flags, int64_t n, int32_t* prefix, int32_t* d_total, void* tmp,

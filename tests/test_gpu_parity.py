@@ -325,6 +325,35 @@ def test_partitioned_config2_8parts():
     assert torch.equal(out, r.in_set) and (cnt, its) == (r.count, r.iterations)
 
 
+@pytest.mark.parametrize("nparts", [1, 2, 3, 5, 8])
+def test_partitioned_aggregate_local_transport(nparts):
+    """Alg. 3 over P partitions (mis2_dist_aggregate, halo exchanges of root
+    ids / labels, global root numbering, summed aggregate sizes): labels,
+    count and all statistics bit-identical to the oracle."""
+    gs = [G.config_graph(0), G.laplace3d_27pt(16), G.kronecker(11), G.random_graph(600, 0.02, 8),
+          G.elasticity3d(5), G.random_powerlaw_graph(3000, 30, 5), G.from_edges(5, [])]
+    for g in gs:
+        for seed in (0, 7):
+            c = M().Comm.local_parts(nparts).set_graph(g.n, g.rowptr, g.colinds)
+            lab = torch.empty(max(g.n, 1), dtype=torch.int32, device="cuda")
+            na, st = c.aggregate(lab, seed=seed)
+            c.close()
+            o = O.aggregate(g.rowptr, g.colinds, seed=seed)
+            assert na == o.num_aggs, (g.name, nparts)
+            assert np.array_equal(lab[: g.n].cpu().numpy(), o.labels), (g.name, nparts)
+            assert st == o.stats, (g.name, nparts, st, o.stats)
+
+
+def test_partitioned_aggregate_config2_8parts():
+    g = G.config_graph(1)
+    c = M().Comm.local_parts(8).set_graph(g.n, g.rowptr, g.colinds)
+    lab = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    na, st = c.aggregate(lab)
+    rp, ci = dev(g)
+    a = M().aggregate(rp, ci)
+    assert na == a.num_aggs and torch.equal(lab, a.labels) and st == a.stats
+
+
 @pytest.mark.slow
 def test_partitioned_config3_4parts():
     g = G.config_graph(2)
