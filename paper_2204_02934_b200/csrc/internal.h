@@ -67,8 +67,6 @@ struct Mis2Ws {
     uint8_t* oflag;     // push-form Decide state (mis2_core.cu)
     uint32_t* cnt;
     uint32_t* degc;
-    int32_t* len2;      // pruned row lengths
-    int32_t* ci2;       // pruned adjacency (nnz entries; carved by carve_mis2_adj)
     unsigned long long* ctrl;  // [0]=barrier, [1..4]=ring of |wl1| sums, [5]=count, [6]=ticket
     long long* dstats;         // [kStatsMaxIters * 6]
     long long* scal;           // [8] host-visible scalars of mis2()/mis2_host()

@@ -83,20 +83,12 @@ struct MisParams {
     uint8_t* oflag;       // push-form Decide: some w in N[v] got M_w = OUT this iteration
     uint32_t* cnt;        // push-form Decide: |{w in N[v] : M_w = T_v}| this iteration
     uint32_t* degc;       // |N[v] ∩ active| (closed), written by the column pass of iteration 0
-    int32_t* ci2;         // pruned adjacency (same offsets as colinds), see row_min_prune
-    int32_t* len2;        // pruned row length, -1: row not pruned (long rows)
     unsigned int* mark;   // stats only
     long long* dstats;    // stats only
     long long* timeline;  // MIS2_FLAG_TIMELINE only
     float l2_keep;        // fraction of each block's colinds span kept in L2 (evict_last)
-    int dense_col64;
-    int sparse_kind;      // 0: per-row staged sparse_phase, 1: direct sparse_col
-    int prune_frac64;     // prune adjacency once |worklist_1| < prune_frac64/64 of the active vertices (0: never)
-    int bar_mode;         // grid barrier polling (common.cuh grid_barrier)      // column phase is dense if |worklist_2 segment| >= dense_col64/64 of the range
-    float qw[4];          // relative speed of the k-th co-resident block of an SM (row-range weights)
-    int nsm;
+    int push_iters;       // PUSH kernels: iterations it < push_iters use the push-form Decide
     int dbg_it, dbg_ph;   // MIS2_FLAG_TIMELINE: sparse phase instrumented into `mark`
-    int dbg_skip;         // measurement only (MIS2_DBG_SKIP): 1 no pushes, 2 no counts, 4 no degree
     Prio prio;
     int max_iters;
     uint8_t* in_set;
@@ -300,36 +292,6 @@ __device__ __forceinline__ uint64_t row_min_deg(const uint64_t* __restrict__ T, 
     return m;
 }
 
-// Refresh Column of one row (thread per row) that also writes the row's
-// entries with T_w != OUT to out[0..k) and returns k.  A neighbour decided
-// OUT never changes a later minimum (OUT is the largest word) and never
-// needs a push, so later column passes may read the pruned row instead; a
-// row with an IN neighbour leaves worklist_2 in this pass, so dropping
-// nothing else is needed.  The same minimum results (exactly).  In place
-// (out == x) is safe: a batch is read before any of it is written, and
-// k <= entries read.
-__device__ __forceinline__ uint64_t row_min_prune(const uint64_t* __restrict__ T, const int32_t* x, int len,
-                                                  uint64_t m, int32_t* out, int& k) {
-    constexpr int B = 8;
-    const int last = len - 1;
-    k = 0;
-    for (int j = 0; j < len; j += B) {
-        uint64_t tt[B];
-        int32_t ww[B];
-#pragma unroll
-        for (int q = 0; q < B; q++) {
-            ww[q] = x[min(j + q, last)];
-            tt[q] = T[ww[q]];
-        }
-#pragma unroll
-        for (int q = 0; q < B; q++) {
-            m = tt[q] < m ? tt[q] : m;
-            if (j + q <= last && tt[q] != kOUT) out[k++] = ww[q];
-        }
-    }
-    return m;
-}
-
 // Decide of one row on id fields: exists M_w = OUT / forall
 // M_w = T_v (id v+1); M_w = 0 (inactive, reading Q15) is ignored.
 __device__ __forceinline__ void decide_acc(uint32_t m, uint32_t vid1, int& any_out, int& all_eq) {
@@ -371,8 +333,7 @@ __device__ __forceinline__ bool decide_write(const MisParams& p, int64_t v, int 
 }
 
 // issue the bulk copy of colinds[s, e) (16-byte aligned hull) into buffer `slot`
-__device__ __forceinline__ void stage_tile(TileSmem& sm, const MisParams& p, int slot, int64_t s, int64_t e,
-                                           const int32_t* src) {
+__device__ __forceinline__ void stage_tile(TileSmem& sm, const MisParams& p, int slot, int64_t s, int64_t e) {
     const int64_t sal = s & ~(int64_t)3;
     const int64_t nnz4 = p.nnz & ~(int64_t)3;
     const int64_t ecp = (e + 3) & ~(int64_t)3;
@@ -384,7 +345,7 @@ __device__ __forceinline__ void stage_tile(TileSmem& sm, const MisParams& p, int
     // fence.proxy.async, which would also drain this thread's global stores)
     if (fits && ecp > sal) {
         mbar_expect_tx(&sm.mbar[slot], (uint32_t)((ecp - sal) * 4));
-        bulk_g2s(sm.buf[slot], src + sal, (uint32_t)((ecp - sal) * 4), &sm.mbar[slot], sm.pol);
+        bulk_g2s(sm.buf[slot], p.colinds + sal, (uint32_t)((ecp - sal) * 4), &sm.mbar[slot], sm.pol);
     } else {
         mbar_expect_tx(&sm.mbar[slot], 0u);
     }
@@ -407,24 +368,17 @@ __device__ __forceinline__ void push_out(const MisParams& p, const int32_t* x, i
 
 template <int GG, int PH, bool PUSH>
 __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int sub, int64_t v, const int32_t* x,
-                                            int len, uint64_t tv, int it, uint64_t fi_next, int prune = 0,
-                                            int64_t s = 0) {
+                                            int len, uint64_t tv, int it, uint64_t fi_next) {
     bool keep = false;
     if (PH == 0) {
         uint64_t m = (act && sub == 0) ? tv : kOUT;  // closed neighbourhood (Q1)
         int dc = 0;
         if (act && len > 0) {
-            if (GG == 1 && prune) {
-                int k = 0;
-                m = row_min_prune(p.T, x, len, m, p.ci2 + s, k);
-                p.len2[v] = k;
-            } else if (PUSH && it == 0 && p.labels) {
+            if (PUSH && it == 0 && p.labels) {
                 m = row_min_deg<GG>(p.T, x, len, sub, m, p.gbase + v, dc);
             } else {
                 m = row_min<GG>(p.T, x, len, sub, m);
             }
-        } else if (GG == 1 && prune && act) {
-            p.len2[v] = 0;
         }
         m = group_min<GG>(m);
         const uint32_t mf = m_field(m, p.id_mask);
@@ -689,10 +643,8 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
 // PH = 1: Decide over worklist_1 (T_v undecided)
 template <int G, bool STATS, int PH, bool PUSH = false>
 __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, int64_t bhi, int32_t* lout,
-                           uint32_t& ph, uint64_t fi_next, int prune = 0) {
+                           uint32_t& ph, uint64_t fi_next) {
     constexpr int RPB = kMB / G;
-    // prune 1: read colinds, write the pruned rows; 2: read and rewrite the pruned rows
-    const int32_t* src = (G == 1 && prune == 2) ? p.ci2 : p.colinds;
     const int t = threadIdx.x, g = t / G, sub = t % G;
     const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
     Stat st;
@@ -707,7 +659,7 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
         const int64_t r2 = r1 + RPB < bhi ? r1 + RPB : bhi;
         nx_s = p.rowptr[r1];
         nx_e = p.rowptr[r2];
-        stage_tile(sm, p, 0, p.rowptr[blo], nx_s, src);
+        stage_tile(sm, p, 0, p.rowptr[blo], nx_s);
     }
     const bool dbg = p.timeline && it == p.dbg_it && PH == p.dbg_ph && threadIdx.x == 0;
     long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
@@ -728,14 +680,11 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
     int64_t ns0 = 0, ne0 = 0;
     uint64_t ntv = kOUT;
     uint32_t nmv = kM_OUT;
-    int32_t nl2 = -1;
-    const bool rd2 = G == 1 && PH == 0 && prune == 2;
     if (blo + g < bhi) {
         ns0 = p.rowptr[blo + g];
         ne0 = p.rowptr[blo + g + 1];
         ntv = p.T[blo + g];
         if (PH == 0) nmv = p.M[blo + g];
-        if (rd2) nl2 = p.len2[blo + g];
     }
     for (int64_t k = 0; k < nsteps; k++) {
         const int slot = (int)(k & 1);
@@ -750,7 +699,7 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
                 nx_s = p.rowptr[r2];
                 nx_e = p.rowptr[r3];
             }
-            stage_tile(sm, p, slot ^ 1, s1, e1, src);
+            stage_tile(sm, p, slot ^ 1, s1, e1);
         }
         // this tile's row bounds and status were loaded one step ahead; load
         // the next tile's now (a phase writes only rows of the tile it is
@@ -759,7 +708,6 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
         const bool valid = v < bhi;
         const int64_t s = ns0, e = ne0;
         const uint64_t tv = ntv;
-        const int32_t l2 = nl2;
         bool act = false;
         if (valid) act = PH == 0 ? (nmv != kM_OUT && nmv != 0u) : (tv != kIN && tv != kOUT);
         {
@@ -769,20 +717,16 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
                 ne0 = p.rowptr[vn + 1];
                 ntv = p.T[vn];
                 if (PH == 0) nmv = p.M[vn];
-                if (rd2) nl2 = p.len2[vn];
             }
         }
-        const int64_t len = (rd2 && l2 >= 0) ? (int64_t)l2 : e - s;
-        if (defer_long<G>(sm, p, blo, act, sub, v, len)) {
-            act = false;
-            if (G == 1 && prune == 1) p.len2[v] = -1;  // long rows stay unpruned (read from colinds)
-        }
+        const int64_t len = e - s;
+        if (defer_long<G>(sm, p, blo, act, sub, v, len)) act = false;
         if (dbg && k < 12) dbuf[4 + 5 * k + 2] = gt();
         mbar_wait(&sm.mbar[slot], (ph >> slot) & 1u);
         ph ^= 1u << slot;
         if (dbg && k < 12) dbuf[4 + 5 * k + 3] = gt();
-        const int32_t* x = sm.fits[slot] ? sm.buf[slot] + (s - sm.sal[slot]) : src + s;
-        const bool keep = process_row<G, PH, PUSH>(p, act, sub, v, x, (int)len, tv, it, fi_next, prune == 1, s);
+        const int32_t* x = sm.fits[slot] ? sm.buf[slot] + (s - sm.sal[slot]) : p.colinds + s;
+        const bool keep = process_row<G, PH, PUSH>(p, act, sub, v, x, (int)len, tv, it, fi_next);
         if (dbg && k < 12) dbuf[4 + 5 * k + 4] = gt();
         if (STATS && act) {
             stat_row<STATS>(p, tag, v, sub == 0, len, st);
@@ -813,10 +757,7 @@ static_assert(kSlotRegion > 0 && (kSlotRegion % 4) == 0, "sparse layout");
 
 template <int G, bool STATS, int PH, bool PUSH = false>
 __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, const int32_t* lin, int nin,
-                            int32_t* lout, uint32_t& ph, uint64_t fi_next, int prune = 0) {
-    // prune 2: rows are read from the pruned adjacency (ci2, len2)
-    const bool rd2 = G == 1 && PH == 0 && prune == 2;
-    const int32_t* src = rd2 ? p.ci2 : p.colinds;
+                            int32_t* lout, uint32_t& ph, uint64_t fi_next) {
     constexpr int GS = G * 2 <= 32 ? G * 2 : 32;
     constexpr int RPBS = kMB / GS;
     constexpr int SLOT = (kSlotRegion / RPBS) & ~3;
@@ -860,7 +801,7 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         meta[gs] = m;
         reinterpret_cast<uint64_t*>(sm.buf[slot] + kTvOff)[gs] = tv;
         mbar_expect_tx(&sm.mbarS[slot], bytes);
-        if (bytes) bulk_g2s(sm.buf[slot] + gs * SLOT, src + sal, bytes, &sm.mbarS[slot], sm.pol);
+        if (bytes) bulk_g2s(sm.buf[slot] + gs * SLOT, p.colinds + sal, bytes, &sm.mbarS[slot], sm.pol);
     };
     auto bounds = [&](int64_t v, int64_t& s, int64_t& e) {
         s = 0;
@@ -868,10 +809,6 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         if (v >= 0) {
             s = p.rowptr[v];
             e = p.rowptr[v + 1];
-            if (rd2) {
-                const int32_t l2 = p.len2[v];
-                if (l2 >= 0) e = s + l2;
-            }
         }
     };
 
@@ -922,7 +859,7 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         ph ^= 1u << (2 + slot);
         if (dbg && k < 12) dbuf[4 + 5 * k + 3] = gt();
         const int32_t* x = (m.len & kStaged) ? sm.buf[slot] + gs * SLOT + (m.s - (m.s & ~(int64_t)3))
-                                             : src + m.s;
+                                             : p.colinds + m.s;
         const bool keep = process_row<GS, PH, PUSH>(p, act, sub, v, x, len, tv, it, fi_next);
         if (dbg && k < 12) dbuf[4 + 5 * k + 4] = gt();
         if (STATS && act) {
@@ -938,74 +875,6 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
     }
     if (dbg) dbuf[3] = gt();
     return finish_phase<STATS, PH, PUSH>(sm, p, it, blo, lout, fi_next, st);
-}
-
-// ------------------------------------------------------------ sparse column (direct)
-// Refresh Column over the block's compacted worklist_2 with GS lanes per
-// row, colinds read straight from global memory (L1-cached): no staging, so
-// a pass is only limited by the neighbour gathers.  The worklist entry and
-// row bounds of the next pass are loaded while the current one gathers.
-template <int GS, bool STATS, bool PUSH>
-__device__ int sparse_col(TileSmem& sm, const MisParams& p, int it, int64_t blo, const int32_t* lin, int nin,
-                          int32_t* lout, int prune = 0) {
-    const bool rd2 = GS == 1 && prune == 2;
-    const int32_t* src = rd2 ? p.ci2 : p.colinds;
-    constexpr int RPS = kMB / GS;
-    const int t = threadIdx.x, gs = t / GS, sub = t % GS;
-    const unsigned tag = 2u * (unsigned)it + 1u;
-    Stat st;
-    if (t == 0) {
-        sm.cnt = 0;
-        sm.hcount = 0;
-    }
-    __syncthreads();
-    const int npass = (nin + RPS - 1) / RPS;
-    auto row_of = [&](int k) -> int64_t {
-        const int idx = k * RPS + gs;
-        return (k < npass && idx < nin) ? (int64_t)lin[blo + idx] : -1;
-    };
-    int64_t v = row_of(0), vn = row_of(1);
-    int64_t s = 0, e = 0;
-    uint64_t tv = kOUT;
-    int32_t l2 = -1;
-    if (v >= 0) {
-        s = p.rowptr[v];
-        e = p.rowptr[v + 1];
-        tv = p.T[v];
-        if (rd2) l2 = p.len2[v];
-    }
-    for (int k = 0; k < npass; k++) {
-        // prefetch: worklist entry two passes ahead, bounds one pass ahead
-        const int64_t vnn = row_of(k + 2);
-        int64_t sn = 0, en = 0;
-        uint64_t tvn = kOUT;
-        int32_t l2n = -1;
-        if (vn >= 0) {
-            sn = p.rowptr[vn];
-            en = p.rowptr[vn + 1];
-            tvn = p.T[vn];
-            if (rd2) l2n = p.len2[vn];
-        }
-        bool act = v >= 0;
-        const int64_t len = (rd2 && l2 >= 0) ? (int64_t)l2 : e - s;
-        if (defer_long<GS>(sm, p, blo, act, sub, v, len)) {
-            act = false;
-            if (GS == 1 && prune == 1) p.len2[v] = -1;
-        }
-        const bool keep = process_row<GS, 0, PUSH>(p, act, sub, act ? v : 0, src + s, (int)len, tv, it, 0, prune == 1, s);
-        if (STATS && act) {
-            stat_row<STATS>(p, tag, v, sub == 0, len, st);
-            stat_nbrs<STATS>(p, tag, p.colinds + s, len, sub, GS, st);
-        }
-        append(sm, keep, (int32_t)(v < 0 ? 0 : v), lout, blo);
-        v = vn;
-        vn = vnn;
-        s = sn;
-        e = en;
-        tv = tvn;
-        l2 = l2n;
-    }
-    return finish_phase<STATS, 0, PUSH>(sm, p, it, blo, lout, 0, st);
 }
 
 // ------------------------------------------------------------ push-form Decide
@@ -1163,35 +1032,19 @@ __device__ __forceinline__ void stamp(const MisParams& p, int slot) {
     }
 }
 
-// Row range of block b: contiguous, proportional to qw[b / nsm] (the
-// co-resident blocks of an SM are not scheduled fairly; block b + k*nsm is
-// the k-th block placed on its SM).  wrange(B) = n exactly.
-__device__ __forceinline__ int64_t wrange(const MisParams& p, int64_t b, int64_t B) {
-    const int64_t S = p.nsm > 0 ? p.nsm : B;
-    double acc = 0.0, tot = 0.0;
-#pragma unroll
-    for (int c = 0; c < 4; c++) {
-        int64_t cnt = B - c * S;
-        cnt = cnt < 0 ? 0 : (cnt > S ? S : cnt);
-        if (c == 3) cnt = B - 3 * S > 0 ? B - 3 * S : 0;  // any further blocks share the last weight
-        int64_t mine = b - c * S;
-        mine = mine < 0 ? 0 : (mine > cnt ? cnt : mine);
-        tot += (double)cnt * p.qw[c];
-        acc += (double)mine * p.qw[c];
-    }
-    return acc >= tot ? p.n : (int64_t)((double)p.n * acc / tot);
-}
-
 // ------------------------------------------------------------ the kernel
-// PUSH: push-form Decide (the column pass pushes / counts, decide_push
-// touches no edges); otherwise the pull form of Alg. 1 as written.
+// PUSH: iterations it < p.push_iters use the push-form Decide (the column
+// pass pushes / counts, decide_push touches no edges); all others -- and
+// every iteration of a !PUSH kernel -- the pull form of Alg. 1 as written.
+// The switch needs no conversion: the push state (oflag, cnt) is only
+// written and read by push iterations and cnt is cleared by decide_push.
 template <int G, bool STATS, bool PUSH>
 __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
     const int t = threadIdx.x;
     const int64_t B = gridDim.x;
-    const int64_t blo = wrange(p, blockIdx.x, B), bhi = wrange(p, blockIdx.x + 1, B);
+    const int64_t blo = p.n * blockIdx.x / B, bhi = p.n * (blockIdx.x + 1) / B;
     unsigned int* bar = (unsigned int*)&p.ctrl[0];
     unsigned long long* ring = &p.ctrl[1];
 
@@ -1221,7 +1074,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         const long long s = block_sum_int(sm, act_cnt);
         if (t == 0 && s) atomicAdd(&p.ctrl[7], (unsigned long long)s);
     }
-    grid_barrier(bar, p.bar_mode);
+    grid_barrier(bar);
     stamp(p, 0);
     const unsigned long long n_active = ld_acquire_u64(&p.ctrl[7]);
 
@@ -1229,42 +1082,33 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
     int status = MIS2_OK;
     const int64_t range = bhi - blo;
     int cnt1 = (int)range, cnt2 = (int)range;  // this block's worklist segment sizes
-    unsigned long long wl1_global = n_active;   // |worklist_1| before this iteration
-    bool pruned = false;
     while (n_active > 0) {  // while worklist_1 != {}
         const int cur = it & 1;
         // ---- Refresh Column over worklist_2
-        const bool dense2 = (it == 0) || (int64_t)cnt2 * 64 >= range * p.dense_col64;
-        constexpr int GS = G == 1 ? 4 : (G * 2 <= 32 ? G * 2 : 32);
-        // adjacency pruning (row_min_prune): from the first iteration in
-        // which fewer than prune_frac of the active vertices are undecided
-        int prune = 0;
-        if (G == 1 && PUSH && !STATS && p.prune_frac64 > 0) {
-            if (pruned) prune = 2;
-            else if (it > 0 && wl1_global * 64 < n_active * (unsigned long long)p.prune_frac64) prune = 1;
+        const bool push = PUSH && it < p.push_iters;
+        const bool dense2 = (it == 0) || (int64_t)cnt2 * kDenseDen >= range * kDenseNum;
+        if (push) {
+            cnt2 = dense2 ? dense_phase<G, STATS, 0, PUSH>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0)
+                          : sparse_phase<G, STATS, 0, PUSH>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
+        } else {
+            cnt2 = dense2 ? dense_phase<G, STATS, 0, false>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0)
+                          : sparse_phase<G, STATS, 0, false>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
         }
-        if (dense2) cnt2 = dense_phase<G, STATS, 0, PUSH>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0, prune);
-        else if (prune == 1) cnt2 = sparse_col<1, STATS, PUSH>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], prune);
-        else if (prune == 2) cnt2 = sparse_phase<G, STATS, 0, PUSH>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0, prune);
-        else if (p.sparse_kind == 1) cnt2 = sparse_col<GS, STATS, PUSH>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1]);
-        else cnt2 = sparse_phase<G, STATS, 0, PUSH>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
-        if (prune) pruned = true;
-        grid_barrier(bar, p.bar_mode);
+        grid_barrier(bar);
         stamp(p, 1 + 2 * it);
         // ---- Decide over worklist_1 + fused refresh of iteration it+1
         const uint64_t fi_next = p.prio.iter_term(it + 1);
         const bool dense1 = (it == 0) || (int64_t)cnt1 * kDenseDen >= range * kDenseNum;
-        if (PUSH) cnt1 = decide_push<STATS>(sm, p, it, blo, bhi, p.L1[cur], cnt1, dense1, p.L1[cur ^ 1], fi_next);
+        if (push) cnt1 = decide_push<STATS>(sm, p, it, blo, bhi, p.L1[cur], cnt1, dense1, p.L1[cur ^ 1], fi_next);
         else if (dense1) cnt1 = dense_phase<G, STATS, 1>(sm, p, it, blo, bhi, p.L1[cur ^ 1], ph, fi_next);
         else cnt1 = sparse_phase<G, STATS, 1>(sm, p, it, blo, p.L1[cur], cnt1, p.L1[cur ^ 1], ph, fi_next);
         if (t == 0) {
             if (cnt1) atomicAdd(&ring[it & 3], (unsigned long long)cnt1);
             if (blockIdx.x == 0) ring[(it + 2) & 3] = 0;  // slot last read two barriers ago
         }
-        grid_barrier(bar, p.bar_mode);
+        grid_barrier(bar);
         stamp(p, 2 + 2 * it);
         const unsigned long long remaining = ld_acquire_u64(&ring[it & 3]);
-        wl1_global = remaining;
         it++;
         if (remaining == 0) break;
         if (it >= p.max_iters) {  // reading Q12
@@ -1448,8 +1292,6 @@ void carve_mis2(Carve& c, int64_t n, int64_t nnz, int max_warps, Mis2Ws* w) {
     w->oflag = c.take<uint8_t>((size_t)n + 1);
     w->cnt = c.take<uint32_t>((size_t)n + 1);
     w->degc = c.take<uint32_t>((size_t)n + 1);
-    w->len2 = c.take<int32_t>((size_t)n + 1);
-    w->ci2 = c.take<int32_t>((size_t)nnz + 4);
     w->dstats = c.take<long long>((size_t)kStatsMaxIters * 6);
     w->scal = c.take<long long>(8);
 }
@@ -1564,15 +1406,19 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
         set_error("stats/timeline mode supports max_iters <= %d", kStatsMaxIters);
         return MIS2_EINVAL;
     }
-    // push-form Decide for dense graphs (its per-row push / count overhead
-    // is amortised over long rows; measured: C5 (avg 80) faster, C3 (avg 7)
-    // slower, C2 (avg 26.5) even); MIS2_DECIDE=push|pull overrides
+    // Decide form per iteration: push (its per-row push / count overhead
+    // amortised over long rows) for every iteration of a dense graph; for a
+    // medium one only in iteration 0, where no M is OUT yet (nothing to
+    // push) and the pull form's full second sweep over all rows is replaced
+    // by one count per row; pull otherwise.  Measured on C5 (avg degree 80),
+    // C2 (26.5), C3 (7).  MIS2_FLAG_PUSH_DECIDE / PULL_DECIDE force a form
+    // (MIS2_PUSH_ITERS: measurement knob).
     const double avg_deg = g.n > 0 ? (double)g.nnz / (double)g.n : 0.0;
-    bool push = avg_deg >= 32.0;
-    if (o.flags & MIS2_FLAG_PUSH_DECIDE) push = true;
-    if (o.flags & MIS2_FLAG_PULL_DECIDE) push = false;
-    if (const char* e = getenv("MIS2_DECIDE")) push = (e[0] == 'p' && e[1] == 'u' && e[2] == 's');
-    void* fn = pick_kernel(G, stats, push);
+    int push_iters = avg_deg >= 32.0 ? max_iters : (avg_deg >= 16.0 ? 1 : 0);
+    if (o.flags & MIS2_FLAG_PUSH_DECIDE) push_iters = max_iters;
+    if (o.flags & MIS2_FLAG_PULL_DECIDE) push_iters = 0;
+    if (const char* e = getenv("MIS2_PUSH_ITERS")) push_iters = atoi(e);
+    void* fn = pick_kernel(G, stats, push_iters > 0);
     if (!fn) {
         set_error("group must be one of 1,2,4,8,16,32 (got %d)", G);
         return MIS2_EINVAL;
@@ -1620,13 +1466,10 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     p.oflag = w.oflag;
     p.cnt = w.cnt;
     p.degc = w.degc;
-    p.ci2 = w.ci2;
-    p.len2 = w.len2;
     p.dstats = w.dstats;
     p.timeline = timeline ? w.dstats : nullptr;
     p.dbg_it = -1;
     p.dbg_ph = 0;
-    if (const char* e = getenv("MIS2_DBG_SKIP")) p.dbg_skip = atoi(e);
     if (timeline) {
         if (const char* e = getenv("MIS2_DBG_IT")) p.dbg_it = atoi(e);
         if (const char* e = getenv("MIS2_DBG_PH")) p.dbg_ph = atoi(e);
@@ -1639,18 +1482,7 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     p.id_mask = (uint32_t)((1ull << p.prio.b) - 1ull);
     p.prio.n = g.n;
     p.l2_keep = l2_keep_for(g.nnz);
-    p.nsm = di.sms;
-    p.dense_col64 = 24;
-    if (const char* e = getenv("MIS2_DENSE_COL64")) p.dense_col64 = atoi(e);  // tuning knob
-    p.sparse_kind = 0;
-    p.prune_frac64 = 0;  // off: measured slower on C2 (strided rewrite of the rows)
-    if (const char* e = getenv("MIS2_PRUNE64")) p.prune_frac64 = atoi(e);  // tuning knob
-    p.bar_mode = 0;
-    if (const char* e = getenv("MIS2_BAR_MODE")) p.bar_mode = atoi(e);
-    if (const char* e = getenv("MIS2_SPARSE_KIND")) p.sparse_kind = atoi(e);
-    p.qw[0] = p.qw[1] = p.qw[2] = p.qw[3] = 1.f;
-    if (const char* e = getenv("MIS2_QW"))  // tuning knob (measurement only)
-        sscanf(e, "%f,%f,%f,%f", &p.qw[0], &p.qw[1], &p.qw[2], &p.qw[3]);
+    p.push_iters = push_iters;
     p.prio.override_ = o.prio_override;
     p.prio.override_iters = o.prio_override ? o.prio_iters : 0;
     p.max_iters = max_iters;

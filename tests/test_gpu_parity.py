@@ -78,7 +78,7 @@ def test_random_small_graphs(chunk, decide):
         check_mis2(g, seed=chunk * 17, decide=decide)
 
 
-@pytest.mark.parametrize("decide", ["pull", "push"])
+@pytest.mark.parametrize("decide", ["pull", "push", "auto"])
 @pytest.mark.parametrize("group", [1, 2, 4, 8, 16, 32])
 def test_group_width_invariance(group, decide):
     """§V-D lane grouping never changes results."""
