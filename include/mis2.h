@@ -217,6 +217,17 @@ int mis2_dist_mis2(mis2_comm* c, const mis2_opts* o, uint8_t* in_set, int64_t* c
  * MIS2_FLAG_BASIC and prio_override are not supported (MIS2_EINVAL). */
 int mis2_dist_aggregate(mis2_comm* c, const mis2_opts* o, int32_t* labels, int64_t* num_aggs, int64_t* stats,
                         void* stream);
+/* Coarse graph of the partitioned graph given its aggregate labels
+ * (as produced by mis2_dist_aggregate: this rank's rows (NCCL) or all rows
+ * (LOCAL), global ids in [0, num_aggs)).  Every part builds the coarse edges
+ * of its own rows (ghost labels exchanged first); the per-part coarse CSRs
+ * are allgathered and merged, so the result -- identical to mis2_coarsen()
+ * on the whole graph -- is REPLICATED on every rank: c_rowptr int64
+ * [num_aggs + 1] and c_colinds int32 [cap], device.  Two-call convention as
+ * mis2_coarsen (MIS2_ERANGE with *c_nnz set when cap is too small; c_colinds
+ * may be NULL).  Scratch is allocated internally.  Collective call. */
+int mis2_dist_coarsen(mis2_comm* c, const int32_t* labels, int64_t num_aggs, int64_t* c_rowptr,
+                      int32_t* c_colinds, int64_t cap, int64_t* c_nnz, void* stream);
 /* rows [lo, hi) and ghost count of local part `part` (NCCL: part 0) */
 int mis2_comm_part_info(mis2_comm* c, int part, int64_t* lo, int64_t* hi, int64_t* n_ghost);
 int mis2_comm_destroy(mis2_comm* c);

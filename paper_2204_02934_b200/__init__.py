@@ -33,7 +33,7 @@ DECIDE = {"auto": 0, "push": FLAG_PUSH_DECIDE, "pull": FLAG_PULL_DECIDE}
 EXPORTS = ["mis2_opts_default", "mis2_workspace_size", "mis2", "mis2_async", "mis2_host", "mis2_aggregate",
            "mis2_coarsen", "mis2_validate_graph", "mis2_last_launch_count", "mis2_strerror", "mis2_last_error",
            "mis2_version", "mis2_comm_unique_id", "mis2_comm_init_nccl", "mis2_comm_init_local",
-           "mis2_comm_set_graph", "mis2_dist_mis2", "mis2_dist_aggregate", "mis2_comm_part_info", "mis2_comm_destroy",
+           "mis2_comm_set_graph", "mis2_dist_mis2", "mis2_dist_aggregate", "mis2_dist_coarsen", "mis2_comm_part_info", "mis2_comm_destroy",
            "mis2_plan_part"]
 
 
@@ -78,6 +78,7 @@ def lib():
         L.mis2_coarsen.argtypes = [P, P, I64, P, P, I64, P, P, SZ, P]
         L.mis2_validate_graph.argtypes = [P, P, SZ, P]
         L.mis2_dist_aggregate.argtypes = [P, P, P, P, P, P]
+        L.mis2_dist_coarsen.argtypes = [P, P, I64, P, P, I64, P, P]
         L.mis2_last_launch_count.restype = I64
         L.mis2_strerror.restype = ctypes.c_char_p
         L.mis2_strerror.argtypes = [ctypes.c_int]
@@ -390,6 +391,41 @@ class Comm:
                                          st.ctypes.data, _stream()), "mis2_dist_aggregate")
         keys = ["mis1", "iters1", "mis2", "iters2", "accepted2", "leftovers", "n1", "num_aggs"]
         return int(na.value), dict(zip(keys, map(int, st)))
+
+    def coarsen(self, labels, num_aggs: int):
+        """Coarse graph of the partitioned graph (``mis2_dist_coarsen``),
+        replicated on every rank: (crow int64, ccol int32) CUDA tensors."""
+        torch = _torch()
+        dev = labels.device
+        crow = torch.empty(num_aggs + 1, dtype=torch.int64, device=dev)
+        cnnz = ctypes.c_int64(0)
+        L = lib()
+        rc = L.mis2_dist_coarsen(self.h, labels.data_ptr(), num_aggs, crow.data_ptr(), None, 0, ctypes.byref(cnnz),
+                                 _stream())
+        _check(rc, "mis2_dist_coarsen(count)", allow=(ERANGE,))
+        ccol = torch.empty(max(cnnz.value, 1), dtype=torch.int32, device=dev)
+        rc = L.mis2_dist_coarsen(self.h, labels.data_ptr(), num_aggs, crow.data_ptr(), ccol.data_ptr(), ccol.numel(),
+                                 ctypes.byref(cnnz), _stream())
+        _check(rc, "mis2_dist_coarsen")
+        return crow, ccol[: cnnz.value]
+
+    def multilevel(self, labels, threshold: int = 1000, max_levels: int = 32, seed: int = 0):
+        """Multilevel coarsening of the partitioned graph (NEXT-3): level 0
+        aggregated and coarsened over the partition (mis2_dist_aggregate +
+        mis2_dist_coarsen), the replicated coarse graph (~1/70 of the fine
+        one on the elasticity graphs) continued on this GPU by ``multilevel``.
+        ``labels`` receives the level-0 labels.  Returns the same
+        (levels, final CSR) as ``multilevel`` on the whole graph."""
+        n = self.n_global
+        if n < threshold:
+            return [], None
+        na, _ = self.aggregate(labels, seed=seed)
+        levels = [(n, None, na)]
+        if na == n or max_levels <= 1:
+            return levels, None
+        crow, ccol = self.coarsen(labels, na)
+        more, fin, _ = multilevel(crow, ccol, threshold=threshold, max_levels=max_levels - 1, seed=seed)
+        return levels + more, fin
 
     def close(self):
         if self.h:

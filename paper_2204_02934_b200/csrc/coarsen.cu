@@ -231,7 +231,8 @@ int run_coarsen(const mis2_graph& g, const int32_t* labels, int64_t na, int64_t*
     DeviceInfo di;
     MIS2_TRY(device_info(&di));
     const int64_t n = g.n;
-    const int64_t nab = bytes_needed ? n : na;  // sizing uses the bound na <= n
+    // sizing uses the bound na <= n (the partitioned driver sizes with n = max(rows, na))
+    const int64_t nab = bytes_needed ? n : na;
     Carve c(ws, ws_bytes);
     unsigned long long* seglen = c.take<unsigned long long>((size_t)nab + 1);
     int64_t* sptr = c.take<int64_t>((size_t)nab + 2);
@@ -244,7 +245,7 @@ int run_coarsen(const mis2_graph& g, const int32_t* labels, int64_t na, int64_t*
     int* scal = c.take<int>(16);
     if (bytes_needed) { *bytes_needed = c.off; return MIS2_OK; }
     if (!c.ok()) { set_error("workspace too small: need %zu bytes", c.off); return MIS2_ENOMEM; }
-    if (na < 0 || na > n || (n > 0 && na == 0)) { set_error("num_aggs out of range"); return MIS2_EINVAL; }
+    if (na < 0 || na > nab || (n > 0 && na == 0)) { set_error("num_aggs out of range"); return MIS2_EINVAL; }
 
     const int G = choose_group(g.n, g.nnz, 0);
     int64_t blocks = (n + kBlock - 1) / kBlock;

@@ -167,6 +167,16 @@ __global__ void k_add_i32(int32_t* __restrict__ x, int64_t n, int32_t off) {
         x[i] += off;
 }
 __global__ void k_set_i32(int32_t* p, int32_t v) { *p = v; }
+// labels of the stacked per-part coarse rows: row i is coarse row i mod na
+__global__ void k_mod_labels(int32_t* __restrict__ lab, int64_t n, int64_t na) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        lab[i] = (int32_t)(i % na);
+}
+// dst[i] = src[i] + off (int64), i < cnt
+__global__ void k_shift_i64(const int64_t* __restrict__ src, int64_t cnt, int64_t off, int64_t* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i] + off;
+}
 
 }  // namespace
 
@@ -789,6 +799,137 @@ int mis2_dist_mis2(mis2_comm* c, const mis2_opts* o, uint8_t* in_set, int64_t* c
     std::vector<uint8_t*> ins(c->dev.size());
     for (size_t i = 0; i < c->dev.size(); i++) ins[i] = c->local ? in_set + c->hp[i].lo : in_set;
     return dist_mis2_run(c, opt, ins, {}, count, iters, (cudaStream_t)stream);
+}
+
+// RAII device scratch for the coarsening steps
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() { if (p) cudaFree(p); }
+    int alloc(size_t bytes) {
+        if (cudaMalloc(&p, bytes < 256 ? 256 : bytes) != cudaSuccess) {
+            set_error("cudaMalloc(%zu) failed", bytes);
+            return MIS2_ECUDA;
+        }
+        return MIS2_OK;
+    }
+};
+
+// coarse rows (per-part edges) of one part: run_coarsen on its rows with the
+// labels of its ghosts filled in (the coarse rows of aggregates it does not
+// touch stay empty)
+static int part_coarse(const PartDev& d, const int32_t* lab, int64_t na, DevBuf& crow, DevBuf& ccol, int64_t& nnz,
+                       cudaStream_t s) {
+    mis2_graph gl{d.n_own, d.nnz, d.rowptr, d.colinds};
+    mis2_graph gs{std::max<int64_t>(d.n_own, na), d.nnz, nullptr, nullptr};
+    size_t wsb = 0;
+    MIS2_TRY(run_coarsen(gs, nullptr, 0, nullptr, nullptr, 0, nullptr, nullptr, 0, s, &wsb));
+    DevBuf ws;
+    MIS2_TRY(ws.alloc(wsb));
+    MIS2_TRY(crow.alloc(sizeof(int64_t) * (na + 1)));
+    int rc = run_coarsen(gl, lab, na, (int64_t*)crow.p, nullptr, 0, &nnz, ws.p, wsb, s, nullptr);
+    if (rc != MIS2_ERANGE && rc != MIS2_OK) return rc;
+    MIS2_TRY(ccol.alloc(sizeof(int32_t) * (nnz + 1)));
+    return run_coarsen(gl, lab, na, (int64_t*)crow.p, (int32_t*)ccol.p, nnz, &nnz, ws.p, wsb, s, nullptr);
+}
+
+// The coarse graph of a partitioned graph, replicated on every part:
+// each part builds the coarse rows its fine rows contribute (ghost labels
+// exchanged first), the per-part coarse CSRs are stacked (allgather; LOCAL:
+// already on the device) and merged by one more coarsening of the stacked
+// graph with row label i mod na -- the union of each coarse row's edge sets,
+// sorted and deduplicated: exactly mis2_coarsen() of the whole graph.
+static int dist_coarsen_run(mis2_comm* c, const std::vector<const int32_t*>& labels_in, int64_t na, int64_t* c_rowptr,
+                            int32_t* c_colinds, int64_t cap, int64_t* c_nnz, cudaStream_t s) {
+    MIS2_TRY(agg_alloc(c));
+    const int L = (int)c->dev.size();
+    const int P = c->nparts;
+    std::vector<void*> v_lab(L);
+    for (int i = 0; i < L; i++) {
+        v_lab[i] = c->agg[i].lab;
+        if (c->dev[i].n_own)
+            MIS2_CUDA_TRY(cudaMemcpyAsync(c->agg[i].lab, labels_in[i], sizeof(int32_t) * c->dev[i].n_own,
+                                          cudaMemcpyDeviceToDevice, s));
+    }
+    MIS2_TRY(exchange_arr(c, v_lab, 4, s));
+    std::vector<DevBuf> crow(L), ccol(L);
+    std::vector<int64_t> nnz(L, 0);
+    for (int i = 0; i < L; i++) MIS2_TRY(part_coarse(c->dev[i], c->agg[i].lab, na, crow[i], ccol[i], nnz[i], s));
+    // stacked graph: P * na rows
+    std::vector<int64_t> all_nnz;
+    MIS2_TRY(gather_counts(c, nnz, all_nnz, s));
+    int64_t tot = 0, mx = 0;
+    for (int64_t x : all_nnz) {
+        tot += x;
+        mx = std::max(mx, x);
+    }
+    const int64_t ns = (int64_t)P * na;
+    DevBuf srow, scol, slab;
+    MIS2_TRY(srow.alloc(sizeof(int64_t) * (ns + 1)));
+    MIS2_TRY(slab.alloc(sizeof(int32_t) * (ns + 1)));
+    int64_t* sr = (int64_t*)srow.p;
+    const unsigned gb = (unsigned)std::min<int64_t>((na + 256) / 256 + 1, 4096);
+    if (c->local) {
+        MIS2_TRY(scol.alloc(sizeof(int32_t) * (tot + 1)));
+        int64_t off = 0;
+        for (int p = 0; p < P; p++) {
+            k_shift_i64<<<gb, 256, 0, s>>>((const int64_t*)crow[p].p, na, off, sr + (int64_t)p * na);
+            count_launch();
+            if (nnz[p])
+                MIS2_CUDA_TRY(cudaMemcpyAsync((int32_t*)scol.p + off, ccol[p].p, sizeof(int32_t) * nnz[p],
+                                              cudaMemcpyDeviceToDevice, s));
+            off += nnz[p];
+        }
+        MIS2_CUDA_TRY(cudaMemcpyAsync(sr + ns, &tot, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    } else {
+        // allgather of the row pointers and of the (padded) coarse columns
+        DevBuf arow, pcol;
+        MIS2_TRY(arow.alloc(sizeof(int64_t) * (na + 1) * P));
+        MIS2_TRY(pcol.alloc(sizeof(int32_t) * (mx + 1)));
+        MIS2_TRY(scol.alloc(sizeof(int32_t) * ((mx + 1) * P)));
+        if (nnz[0]) MIS2_CUDA_TRY(cudaMemcpyAsync(pcol.p, ccol[0].p, sizeof(int32_t) * nnz[0], cudaMemcpyDeviceToDevice, s));
+        NCCL_TRY(c->api, c->api->AllGather(crow[0].p, arow.p, (size_t)(na + 1), ncclInt64, c->nccl, s));
+        NCCL_TRY(c->api, c->api->AllGather(pcol.p, scol.p, (size_t)(mx + 1), ncclInt32, c->nccl, s));
+        for (int p = 0; p < P; p++) {
+            k_shift_i64<<<gb, 256, 0, s>>>((const int64_t*)arow.p + (int64_t)p * (na + 1), na, (int64_t)p * (mx + 1),
+                                           sr + (int64_t)p * na);
+            count_launch();
+        }
+        const int64_t last = (int64_t)(P - 1) * (mx + 1) + all_nnz[P - 1];
+        MIS2_CUDA_TRY(cudaMemcpyAsync(sr + ns, &last, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        MIS2_CUDA_TRY(cudaStreamSynchronize(s));  // `last` is a host stack value
+    }
+    k_mod_labels<<<(unsigned)std::min<int64_t>((ns + 255) / 256 + 1, 4096), 256, 0, s>>>((int32_t*)slab.p, ns, na);
+    count_launch();
+    MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+    const int64_t snnz = c->local ? tot : (int64_t)P * (mx + 1);
+    mis2_graph gm{ns, snnz, sr, (const int32_t*)scol.p};
+    size_t wsb = 0;
+    MIS2_TRY(run_coarsen(gm, nullptr, 0, nullptr, nullptr, 0, nullptr, nullptr, 0, s, &wsb));
+    DevBuf ws;
+    MIS2_TRY(ws.alloc(wsb));
+    return run_coarsen(gm, (const int32_t*)slab.p, na, c_rowptr, c_colinds, cap, c_nnz, ws.p, wsb, s, nullptr);
+}
+
+int mis2_dist_coarsen(mis2_comm* c, const int32_t* labels, int64_t num_aggs, int64_t* c_rowptr, int32_t* c_colinds,
+                      int64_t cap, int64_t* c_nnz, void* stream) {
+    reset_launches();
+    if (!c || c->dev.empty() || !c_rowptr || !c_nnz || cap < 0 || num_aggs < 0 || (c->n_global > 0 && !labels)) {
+        set_error("bad arguments (graph not set?)");
+        return MIS2_EINVAL;
+    }
+    if (c->n_global > 0 && num_aggs == 0) {
+        set_error("num_aggs out of range");
+        return MIS2_EINVAL;
+    }
+    if (c->n_global == 0) {
+        *c_nnz = 0;
+        return cudaMemsetAsync(c_rowptr, 0, sizeof(int64_t) * (num_aggs + 1), (cudaStream_t)stream) == cudaSuccess
+                   ? MIS2_OK
+                   : MIS2_ECUDA;
+    }
+    std::vector<const int32_t*> ins(c->dev.size());
+    for (size_t i = 0; i < c->dev.size(); i++) ins[i] = c->local ? labels + c->hp[i].lo : labels;
+    return dist_coarsen_run(c, ins, num_aggs, c_rowptr, c_colinds, cap, c_nnz, (cudaStream_t)stream);
 }
 
 int mis2_dist_aggregate(mis2_comm* c, const mis2_opts* o, int32_t* labels, int64_t* num_aggs, int64_t* stats,

@@ -250,7 +250,15 @@ def _agg_rank_main(rank, world, port, name, seed, outdir):
         lab[v] = best[2]
     labs = [None] * world
     dist.all_gather_object(labs, lab[:n_own])
+    # coarse graph (csrc/dist.cu dist_coarsen_run): ghost labels, the coarse
+    # edges of this rank's rows, allgather, union per coarse row
+    halo(lab)
+    edges = {(int(lab[v]), int(lab[w])) for v in range(n_own) for w in nbrs[v] if lab[v] != lab[w]}
+    alle = [None] * world
+    dist.all_gather_object(alle, sorted(edges))
     if rank == 0:
+        merged = sorted(set().union(*[set(map(tuple, e)) for e in alle]))
+        np.save(os.path.join(outdir, f"coarse_{name}_{seed}.npy"), np.asarray(merged, dtype=np.int64).reshape(-1, 2))
         np.save(os.path.join(outdir, f"agg_{name}_{seed}.npy"), np.concatenate(labs))
         with open(os.path.join(outdir, f"agg_{name}_{seed}.na"), "w") as fh:
             fh.write(str(na))
@@ -260,7 +268,8 @@ def _agg_rank_main(rank, world, port, name, seed, outdir):
 @pytest.mark.parametrize("name", ["c1", "lap", "er", "elast"])
 @pytest.mark.parametrize("world", [2, 3])
 def test_partitioned_aggregation_protocol_gloo(name, world, tmp_path):
-    """Alg. 3 under the partitioned exchange schedule == monolithic oracle."""
+    """Alg. 3 and the coarse graph under the partitioned exchange schedule ==
+    monolithic oracle."""
     import torch.multiprocessing as mp
     seed = 0 if world == 2 else 777
     mp.spawn(_agg_rank_main, args=(world, _free_port(), name, seed, str(tmp_path)), nprocs=world, join=True)
@@ -269,3 +278,6 @@ def test_partitioned_aggregation_protocol_gloo(name, world, tmp_path):
     g = _graphs()[name]
     o = O.aggregate(g.rowptr, g.colinds, seed=seed)
     assert na == o.num_aggs and np.array_equal(got, o.labels)
+    crow, ccol = O.coarsen(g.rowptr, g.colinds, o.labels, o.num_aggs)
+    want = np.stack([np.repeat(np.arange(o.num_aggs), np.diff(crow)), ccol], axis=1) if len(ccol) else np.zeros((0, 2))
+    assert np.array_equal(np.load(tmp_path / f"coarse_{name}_{seed}.npy"), want)

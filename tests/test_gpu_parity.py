@@ -354,6 +354,29 @@ def test_partitioned_aggregate_config2_8parts():
     assert na == a.num_aggs and torch.equal(lab, a.labels) and st == a.stats
 
 
+@pytest.mark.parametrize("nparts", [1, 2, 3, 8])
+def test_partitioned_coarsen_and_multilevel(nparts):
+    """mis2_dist_coarsen (per-part coarse rows, stacked and merged) equals
+    mis2_coarsen / the oracle; the partitioned multilevel equals the
+    single-GPU one level by level (NEXT-3)."""
+    for g in [G.config_graph(0), G.laplace3d_27pt(14), G.elasticity3d(7), G.random_graph(400, 0.03, 2),
+              G.kronecker(10)]:
+        c = M().Comm.local_parts(nparts).set_graph(g.n, g.rowptr, g.colinds)
+        lab = torch.empty(max(g.n, 1), dtype=torch.int32, device="cuda")
+        na, _ = c.aggregate(lab)
+        crow, ccol = c.coarsen(lab, na)
+        oa = O.aggregate(g.rowptr, g.colinds)
+        orow, ocol = O.coarsen(g.rowptr, g.colinds, oa.labels, oa.num_aggs)
+        assert np.array_equal(crow.cpu().numpy(), orow) and np.array_equal(ccol.cpu().numpy(), ocol), (g.name, nparts)
+        rp, ci = dev(g)
+        lv1, fin1, _ = M().multilevel(rp, ci, threshold=50)
+        lv, fin = c.multilevel(lab, threshold=50)
+        c.close()
+        assert [l[0] for l in lv] == [l[0] for l in lv1] and [l[2] for l in lv] == [l[2] for l in lv1], g.name
+        if fin is not None:
+            assert torch.equal(fin[0], fin1[0]) and torch.equal(fin[1], fin1[1])
+
+
 @pytest.mark.slow
 def test_partitioned_config3_4parts():
     g = G.config_graph(2)
