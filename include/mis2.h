@@ -69,6 +69,11 @@ extern "C" {
                                        w for its argmin; Decide then reads no neighbour).  Default:
                                        push iff nnz/n >= 32.  Never changes results. */
 #define MIS2_FLAG_PULL_DECIDE 0x10u /* force the pull form (Alg. 1 as written).  Never changes results. */
+#define MIS2_FLAG_KEYS 0x20u     /* use 32-bit column keys (top 32 bits of the status word, ties
+                                    resolved on the full words): half the gather bytes, for
+                                    random-access graphs whose status words exceed L2; off by
+                                    default.  Never changes results. */
+#define MIS2_FLAG_NO_KEYS 0x40u  /* never use the 32-bit column keys.  Never changes results. */
 #define MIS2_FLAG_TIMELINE 0x2u  /* measurement aid: mis2()'s `stats` receives int64 device
                                     timestamps (ns, %globaltimer) taken by block 0 after
                                     the init phase and after every grid barrier:

@@ -28,6 +28,9 @@ FLAG_BASIC = 4
 FLAG_PUSH_DECIDE = 8
 FLAG_PULL_DECIDE = 16
 DECIDE = {"auto": 0, "push": FLAG_PUSH_DECIDE, "pull": FLAG_PULL_DECIDE}
+FLAG_KEYS = 32
+FLAG_NO_KEYS = 64
+KEYS = {"auto": 0, "on": FLAG_KEYS, "off": FLAG_NO_KEYS}
 
 # every symbol include/mis2.h declares
 EXPORTS = ["mis2_opts_default", "mis2_workspace_size", "mis2", "mis2_async", "mis2_host", "mis2_aggregate",
@@ -147,14 +150,15 @@ def _graph(rowptr, colinds):
     return _Graph(n, nnz, rowptr.data_ptr(), colinds.data_ptr() if nnz else None), n, nnz
 
 
-def _opts(seed=0, scheme="xorstar", max_iters=0, group=0, validate=False, prio_override=None, decide="auto"):
+def _opts(seed=0, scheme="xorstar", max_iters=0, group=0, validate=False, prio_override=None, decide="auto",
+          keys="auto"):
     o = _Opts()
     lib().mis2_opts_default(ctypes.byref(o))
     o.seed = seed & ((1 << 64) - 1)
     o.scheme = SCHEMES[scheme]
     o.max_iters = max_iters
     o.group = group
-    o.flags = (FLAG_VALIDATE if validate else 0) | DECIDE[decide]
+    o.flags = (FLAG_VALIDATE if validate else 0) | DECIDE[decide] | KEYS[keys]
     if prio_override is not None:
         o.prio_override = prio_override.data_ptr()
         o.prio_iters = prio_override.shape[0]
@@ -173,13 +177,13 @@ class Mis2Result:
 
 def mis2(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
          validate: bool = False, prio_override=None, stats: bool = False, allow_partial: bool = False,
-         out=None, timeline: bool = False, decide: str = "auto") -> Mis2Result:
+         out=None, timeline: bool = False, decide: str = "auto", keys: str = "auto") -> Mis2Result:
     """Alg. 1 through ``mis2()`` of the C ABI."""
     torch = _torch()
     g, n, nnz = _graph(rowptr, colinds)
     if prio_override is not None:
         prio_override = prio_override.to(device=rowptr.device, dtype=torch.int64).contiguous()
-    o = _opts(seed, scheme, max_iters, group, validate, prio_override, decide)
+    o = _opts(seed, scheme, max_iters, group, validate, prio_override, decide, keys)
     ws, wsb = workspace(OP_MIS2, n, nnz)
     in_set = out if out is not None else torch.empty(max(n, 1), dtype=torch.uint8, device=rowptr.device)
     cnt, its = ctypes.c_int64(0), ctypes.c_int32(0)
@@ -246,12 +250,12 @@ class AggResult:
 
 
 def aggregate(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
-              validate: bool = False, basic: bool = False, decide: str = "auto") -> AggResult:
+              validate: bool = False, basic: bool = False, decide: str = "auto", keys: str = "auto") -> AggResult:
     """Alg. 3, or Alg. 2 with basic=True,
     through ``mis2_aggregate()``."""
     torch = _torch()
     g, n, nnz = _graph(rowptr, colinds)
-    o = _opts(seed, scheme, max_iters, group, validate, decide=decide)
+    o = _opts(seed, scheme, max_iters, group, validate, decide=decide, keys=keys)
     if basic:
         o.flags |= FLAG_BASIC
     ws, wsb = workspace(OP_AGGREGATE, n, nnz)

@@ -67,6 +67,7 @@ struct Mis2Ws {
     uint8_t* oflag;     // push-form Decide state (mis2_core.cu)
     uint32_t* cnt;
     uint32_t* degc;
+    uint32_t* K;        // 32-bit column keys (mis2_core.cu kkey)
     unsigned long long* ctrl;  // [0]=barrier, [1..4]=ring of |wl1| sums, [5]=count, [6]=ticket
     long long* dstats;         // [kStatsMaxIters * 6]
     long long* scal;           // [8] host-visible scalars of mis2()/mis2_host()

@@ -75,6 +75,7 @@ struct MisParams {
     const int32_t* __restrict__ labels;  // phase-2 mask (active iff labels[v] < 0) or null
     uint64_t* T;                         // row status T_v (64-bit packed word, Eq. 1)
     uint32_t* M;                         // column status M_v, stored as its id field (see below)
+    uint32_t* K;                         // 32-bit column keys of T (kkey) or null (KEYS kernels only)
     uint32_t id_mask;                    // 2^b - 1
     int32_t* L1[2];                      // worklist_1, double buffered, per-block segments
     int32_t* L2[2];                      // worklist_2
@@ -292,6 +293,37 @@ __device__ __forceinline__ uint64_t row_min_deg(const uint64_t* __restrict__ T, 
     return m;
 }
 
+// Refresh Column on 32-bit keys (KEYS: p.K != null): the gathers read
+// K_w = kkey(T_w) -- half the bytes of T, so K of a 16.7M-vertex graph stays
+// L2-resident where T does not.  Two minima are kept: of (K_w, w) and of
+// (K_w, ~w); their key parts are the least key, their id parts the least and
+// the greatest id holding it.  Different ids = a tie in the key class, which
+// the caller resolves on the full words.
+__device__ __forceinline__ uint64_t key_lo(uint32_t k, uint32_t w) { return ((uint64_t)k << 32) | w; }
+__device__ __forceinline__ uint64_t key_hi(uint32_t k, uint32_t w) { return ((uint64_t)k << 32) | (~w); }
+template <int G>
+__device__ __forceinline__ void row_min_keys(const uint32_t* __restrict__ K, const int32_t* x, int len, int sub,
+                                             uint64_t& k1, uint64_t& k2) {
+    constexpr int B = G <= 2 ? 16 : (G == 4 ? 8 : 4);
+    const int last = len - 1;
+    for (int j = sub; j < len; j += B * G) {
+        uint32_t kk[B];
+        int32_t ww[B];
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            ww[q] = x[min(j + q * G, last)];
+            kk[q] = K[ww[q]];
+        }
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            const uint64_t a = key_lo(kk[q], (uint32_t)ww[q]), b = key_hi(kk[q], (uint32_t)ww[q]);
+            k1 = a < k1 ? a : k1;
+            k2 = b < k2 ? b : k2;
+        }
+        if ((k1 >> 32) == 0u) break;  // an IN neighbour: M is OUT
+    }
+}
+
 // Decide of one row on id fields: exists M_w = OUT / forall
 // M_w = T_v (id v+1); M_w = 0 (inactive, reading Q15) is ignored.
 __device__ __forceinline__ void decide_acc(uint32_t m, uint32_t vid1, int& any_out, int& all_eq) {
@@ -318,17 +350,32 @@ __device__ __forceinline__ uint32_t m_field(uint64_t m, uint32_t id_mask) {
     return (m == kIN || m == kOUT) ? kM_OUT : (uint32_t)m & id_mask;
 }
 
+// 32-bit column key of a status word (KEYS kernels): IN -> 0, OUT -> all
+// ones, an undecided word -> its top 32 bits clamped to [1, 2^32 - 2].  The
+// key order agrees with the word order except inside a class of equal keys,
+// which the column pass detects and resolves on the full words (row_min_keys).
+__device__ __forceinline__ uint32_t kkey(uint64_t t) {
+    if (t == kIN) return 0u;
+    if (t == kOUT) return 0xffffffffu;
+    const uint32_t k = (uint32_t)(t >> 32);
+    return k == 0u ? 1u : (k == 0xffffffffu ? 0xfffffffeu : k);
+}
+__device__ __forceinline__ void set_T(const MisParams& p, int64_t v, uint64_t t) {
+    p.T[v] = t;
+    if (p.K) p.K[v] = kkey(t);
+}
+
 __device__ __forceinline__ bool decide_write(const MisParams& p, int64_t v, int any_out, int all_eq, int it,
                                              uint64_t fi_next) {
     if (any_out) {
-        p.T[v] = kOUT;
+        set_T(p, v, kOUT);
         return false;
     }
     if (all_eq) {
-        p.T[v] = kIN;
+        set_T(p, v, kIN);
         return false;
     }
-    p.T[v] = p.prio.word(it + 1, fi_next, p.gbase + v);  // fused Refresh Row
+    set_T(p, v, p.prio.word(it + 1, fi_next, p.gbase + v));  // fused Refresh Row
     return true;
 }
 
@@ -371,17 +418,39 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
                                             int len, uint64_t tv, int it, uint64_t fi_next) {
     bool keep = false;
     if (PH == 0) {
-        uint64_t m = (act && sub == 0) ? tv : kOUT;  // closed neighbourhood (Q1)
+        uint32_t mf;
         int dc = 0;
-        if (act && len > 0) {
-            if (PUSH && it == 0 && p.labels) {
-                m = row_min_deg<GG>(p.T, x, len, sub, m, p.gbase + v, dc);
-            } else {
-                m = row_min<GG>(p.T, x, len, sub, m);
+        if (p.K && !(PUSH && it == 0 && p.labels)) {
+            // keys (single GPU: local ids are global ids)
+            uint64_t k1 = ~0ull, k2 = ~0ull;
+            if (act && sub == 0) {  // closed neighbourhood (Q1)
+                k1 = key_lo(kkey(tv), (uint32_t)v);
+                k2 = key_hi(kkey(tv), (uint32_t)v);
             }
+            if (act && len > 0) row_min_keys<GG>(p.K, x, len, sub, k1, k2);
+            k1 = group_min<GG>(k1);
+            k2 = group_min<GG>(k2);
+            const uint32_t kmin = (uint32_t)(k1 >> 32);
+            const bool tie = act && kmin != 0u && kmin != 0xffffffffu && (uint32_t)k1 != ~(uint32_t)k2;
+            mf = (kmin == 0u || kmin == 0xffffffffu) ? kM_OUT : (uint32_t)k1 + 1u;
+            if (__any_sync(kFull, tie)) {  // equal keys: the full words decide
+                uint64_t m = (tie && sub == 0) ? tv : kOUT;
+                if (tie && len > 0) m = row_min<GG>(p.T, x, len, sub, m);
+                m = group_min<GG>(m);
+                if (tie) mf = m_field(m, p.id_mask);
+            }
+        } else {
+            uint64_t m = (act && sub == 0) ? tv : kOUT;  // closed neighbourhood (Q1)
+            if (act && len > 0) {
+                if (PUSH && it == 0 && p.labels) {
+                    m = row_min_deg<GG>(p.T, x, len, sub, m, p.gbase + v, dc);
+                } else {
+                    m = row_min<GG>(p.T, x, len, sub, m);
+                }
+            }
+            m = group_min<GG>(m);
+            mf = m_field(m, p.id_mask);
         }
-        m = group_min<GG>(m);
-        const uint32_t mf = m_field(m, p.id_mask);
         if (PUSH) {
             // the warp pushes its OUT rows one after another, 32 entries at a time
             const int lane = threadIdx.x & 31;
@@ -460,10 +529,12 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
     char* base_ptr = reinterpret_cast<char*>(sm.buf[0]);
     int64_t* pref = reinterpret_cast<int64_t*>(base_ptr);              // [kMB + 1]
     int64_t* rs = pref + (kMB + 1);                                  // [kMB] row starts
-    unsigned long long* acc = reinterpret_cast<unsigned long long*>(rs + kMB);  // [kMB] PH 0 min
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(rs + kMB);  // [kMB] PH 0 min (word or key_lo)
     int32_t* rv = reinterpret_cast<int32_t*>(acc + kMB);             // [kMB] rows
-    int32_t* anyo = rv + kMB;                                        // [kMB] PH 1 exists OUT
-    int32_t* alle = anyo + kMB;                                      // [kMB] PH 1 forall equal
+    int32_t* anyo = rv + kMB;                                        // [kMB] PH 1 exists OUT / PH 0 push flag
+    int32_t* alle = anyo + kMB;                                      // [kMB] PH 1 forall equal / PH 0 degree
+    unsigned long long* acc2 = reinterpret_cast<unsigned long long*>(alle + kMB);  // [kMB] PH 0 key_hi min
+    const bool keys = PH == 0 && p.K && !(PUSH && it == 0 && p.labels);
     for (int hb = 0; hb < nh; hb += kMB) {
         const int cnt = min(kMB, nh - hb);
         int64_t v = 0, s = 0, len = 0;
@@ -474,7 +545,13 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
             rv[t] = (int32_t)v;
             rs[t] = s;
             if (PH == 0) {
-                acc[t] = p.T[v];  // closed neighbourhood (Q1)
+                const uint64_t tv = p.T[v];  // closed neighbourhood (Q1)
+                if (keys) {
+                    acc[t] = key_lo(kkey(tv), (uint32_t)v);
+                    acc2[t] = key_hi(kkey(tv), (uint32_t)v);
+                } else {
+                    acc[t] = tv;
+                }
                 if (PUSH) alle[t] = 0;  // active-neighbour count (iteration 0)
             } else {
                 const uint32_t mv = p.M[v];
@@ -506,92 +583,129 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
             __syncthreads();
         }
         const int64_t total = pref[kMB];
-        // each thread takes 8 consecutive entries per round and keeps a
+        // Each thread takes 8 consecutive entries per round and keeps a
         // running accumulator for its current row; one shared atomic per row
-        // change (a hub row is reduced almost entirely in registers)
-        int cur = -1;
-        uint64_t cmin = kOUT;
-        int cany = 0, call = 1, cdeg = 0;
-        const bool count_deg = PUSH && PH == 0 && it == 0 && p.labels;
-        auto flush = [&]() {
-            if (cur < 0) return;
-            if (PH == 0) {
-                if (cmin < acc[cur]) atomicMin(&acc[cur], (unsigned long long)cmin);
-                if (count_deg && cdeg) atomicAdd(&alle[cur], cdeg);
-            } else {
-                if (cany) anyo[cur] = 1;
-                if (!call) alle[cur] = 0;
+        // change (a hub row is reduced almost entirely in registers).
+        // use_keys: PH 0 on keys; only_rows: restrict to rows with rv_mask set
+        // (the exact re-pass of key ties, anyo[] marks them).
+        auto flat_pass = [&](bool use_keys, bool only_marked) {
+            int cur = -1;
+            uint64_t cmin = kOUT, cmin2 = kOUT;
+            int cany = 0, call = 1, cdeg = 0;
+            const bool count_deg = PUSH && PH == 0 && it == 0 && p.labels && !only_marked;
+            auto flush = [&]() {
+                if (cur < 0) return;
+                if (PH == 0) {
+                    if (cmin < acc[cur]) atomicMin(&acc[cur], (unsigned long long)cmin);
+                    if (use_keys && cmin2 < acc2[cur]) atomicMin(&acc2[cur], (unsigned long long)cmin2);
+                    if (count_deg && cdeg) atomicAdd(&alle[cur], cdeg);
+                } else {
+                    if (cany) anyo[cur] = 1;
+                    if (!call) alle[cur] = 0;
+                }
+            };
+            for (int64_t c = (int64_t)t * 8; c < total; c += (int64_t)kMB * 8) {
+                int r = 0;
+                {
+                    int lo = 0, hi = cnt;  // last row with pref[row] <= c
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (pref[mid] <= c) lo = mid; else hi = mid;
+                    }
+                    r = lo;
+                }
+                int32_t rr[8], ww[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int64_t idx = c + u;
+                    rr[u] = -1;
+                    ww[u] = 0;
+                    if (idx < total) {
+                        while (pref[r + 1] <= idx) r++;
+                        if (!only_marked || anyo[r]) {
+                            rr[u] = r;
+                            ww[u] = p.colinds[rs[r] + (idx - pref[r])];
+                        }
+                    }
+                }
+                if (PH == 0) {
+                    uint64_t tv[8];
+                    if (use_keys) {
+#pragma unroll
+                        for (int u = 0; u < 8; u++) tv[u] = rr[u] >= 0 ? (uint64_t)p.K[ww[u]] : 0xffffffffull;
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 8; u++) tv[u] = rr[u] >= 0 ? p.T[ww[u]] : kOUT;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        if (rr[u] < 0) continue;
+                        if (rr[u] != cur) {
+                            flush();
+                            cur = rr[u];
+                            cmin = kOUT;
+                            cmin2 = kOUT;
+                            cdeg = 0;
+                        }
+                        if (use_keys) {
+                            const uint64_t a = key_lo((uint32_t)tv[u], (uint32_t)ww[u]);
+                            const uint64_t b = key_hi((uint32_t)tv[u], (uint32_t)ww[u]);
+                            cmin = a < cmin ? a : cmin;
+                            cmin2 = b < cmin2 ? b : cmin2;
+                        } else {
+                            cmin = tv[u] < cmin ? tv[u] : cmin;
+                            if (count_deg) cdeg += (tv[u] != kOUT) & (ww[u] != rv[cur]);
+                        }
+                    }
+                } else {
+                    uint32_t mm[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) mm[u] = rr[u] >= 0 ? p.M[ww[u]] : 0u;
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        if (rr[u] < 0) continue;
+                        if (rr[u] != cur) {
+                            flush();
+                            cur = rr[u];
+                            cany = 0;
+                            call = 1;
+                        }
+                        const uint32_t vid1 = (uint32_t)(p.gbase + rv[cur]) + 1u;
+                        cany |= (mm[u] == kM_OUT);
+                        call &= (mm[u] == vid1) | (mm[u] == 0u);
+                    }
+                }
+                if (STATS && !only_marked) {
+#pragma unroll
+                    for (int u = 0; u < 8; u++)
+                        if (rr[u] >= 0 && atomicMax(&p.mark[ww[u]], tag) < tag) st.d++;
+                }
             }
+            flush();
+            __syncthreads();
         };
-        for (int64_t c = (int64_t)t * 8; c < total; c += (int64_t)kMB * 8) {
-            int r = 0;
-            {
-                int lo = 0, hi = cnt;  // last row with pref[row] <= c
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (pref[mid] <= c) lo = mid; else hi = mid;
-                }
-                r = lo;
+        flat_pass(keys, false);
+        if (keys) {  // key ties: the full words of those rows decide
+            int tie = 0;
+            if (t < cnt) {
+                const uint32_t kmin = (uint32_t)(acc[t] >> 32);
+                tie = kmin != 0u && kmin != 0xffffffffu && (uint32_t)acc[t] != ~(uint32_t)acc2[t];
+                anyo[t] = tie;
+                if (tie) acc[t] = p.T[v];
             }
-            int32_t rr[8], ww[8];
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const int64_t idx = c + u;
-                rr[u] = -1;
-                ww[u] = 0;
-                if (idx < total) {
-                    while (pref[r + 1] <= idx) r++;
-                    rr[u] = r;
-                    ww[u] = p.colinds[rs[r] + (idx - pref[r])];
-                }
-            }
-            if (PH == 0) {
-                uint64_t tv[8];
-#pragma unroll
-                for (int u = 0; u < 8; u++) tv[u] = rr[u] >= 0 ? p.T[ww[u]] : kOUT;
-#pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    if (rr[u] < 0) continue;
-                    if (rr[u] != cur) {
-                        flush();
-                        cur = rr[u];
-                        cmin = kOUT;
-                        cdeg = 0;
-                    }
-                    cmin = tv[u] < cmin ? tv[u] : cmin;
-                    if (count_deg) cdeg += (tv[u] != kOUT) & (ww[u] != rv[cur]);
-                }
-            } else {
-                uint32_t mm[8];
-#pragma unroll
-                for (int u = 0; u < 8; u++) mm[u] = rr[u] >= 0 ? p.M[ww[u]] : 0u;
-#pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    if (rr[u] < 0) continue;
-                    if (rr[u] != cur) {
-                        flush();
-                        cur = rr[u];
-                        cany = 0;
-                        call = 1;
-                    }
-                    const uint32_t vid1 = (uint32_t)(p.gbase + rv[cur]) + 1u;
-                    cany |= (mm[u] == kM_OUT);
-                    call &= (mm[u] == vid1) | (mm[u] == 0u);
-                }
-            }
-            if (STATS) {
-#pragma unroll
-                for (int u = 0; u < 8; u++)
-                    if (rr[u] >= 0 && atomicMax(&p.mark[ww[u]], tag) < tag) st.d++;
-            }
+            if (__syncthreads_or(tie)) flat_pass(false, true);
         }
-        flush();
-        __syncthreads();
         bool keep = false;
         int any_push = 0;
         if (t < cnt) {
             if (PH == 0) {
-                const uint32_t mf = m_field(acc[t], p.id_mask);
+                uint32_t mf;
+                if (keys && !anyo[t]) {
+                    const uint32_t kmin = (uint32_t)(acc[t] >> 32);
+                    mf = (kmin == 0u || kmin == 0xffffffffu) ? kM_OUT : (uint32_t)acc[t] + 1u;
+                } else {
+                    mf = m_field(acc[t], p.id_mask);
+                }
                 p.M[v] = mf;
                 keep = (mf != kM_OUT);
                 if (PUSH) {
@@ -977,10 +1091,10 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, int64_t blo
                     }
                 }
                 if (later) {
-                } else if (fl[u]) p.T[v] = kOUT;
-                else if (in) p.T[v] = kIN;
+                } else if (fl[u]) set_T(p, v, kOUT);
+                else if (in) set_T(p, v, kIN);
                 else {
-                    p.T[v] = p.prio.word(it + 1, fi_next, p.gbase + v);
+                    set_T(p, v, p.prio.word(it + 1, fi_next, p.gbase + v));
                     keep = true;
                 }
                 if (STATS) {
@@ -1007,9 +1121,9 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, int64_t blo
             bool keep = false;
             if (lane == 0) {
                 if (found) {
-                    p.T[v] = kIN;
+                    set_T(p, v, kIN);
                 } else {
-                    p.T[v] = p.prio.word(it + 1, fi_next, p.gbase + v);
+                    set_T(p, v, p.prio.word(it + 1, fi_next, p.gbase + v));
                     keep = true;
                 }
             }
@@ -1065,7 +1179,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         int act_cnt = 0;
         for (int64_t v = blo + t; v < bhi; v += kMB) {
             const bool act = p.labels ? (p.labels[v] < 0) : true;
-            p.T[v] = act ? p.prio.word(0, fi0, p.gbase + v) : kOUT;
+            set_T(p, v, act ? p.prio.word(0, fi0, p.gbase + v) : kOUT);
             p.M[v] = act ? kPending : 0u;  // 0 = inactive sentinel (reading Q15)
             p.oflag[v] = 0;
             p.cnt[v] = 0u;
@@ -1292,6 +1406,7 @@ void carve_mis2(Carve& c, int64_t n, int64_t nnz, int max_warps, Mis2Ws* w) {
     w->oflag = c.take<uint8_t>((size_t)n + 1);
     w->cnt = c.take<uint32_t>((size_t)n + 1);
     w->degc = c.take<uint32_t>((size_t)n + 1);
+    w->K = c.take<uint32_t>((size_t)n + 1);
     w->dstats = c.take<long long>((size_t)kStatsMaxIters * 6);
     w->scal = c.take<long long>(8);
 }
@@ -1456,6 +1571,16 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     p.labels = labels;
     p.T = w.T;
     p.M = w.M;
+    // 32-bit column keys: off by default -- the two 64-bit minima per entry
+    // cost more ALU than the halved gather bytes save on the stencil configs
+    // (C2 387 -> 451 us, C3 5.6 -> 6.5 ms, C5 8.2 -> 10.1 ms); they help only
+    // random-access graphs whose T does not fit L2 (C4 101 -> 86 ms).
+    // MIS2_FLAG_KEYS / MIS2_FLAG_NO_KEYS force (results identical).
+    bool keys = false;
+    if (o.flags & MIS2_FLAG_KEYS) keys = true;
+    if (o.flags & MIS2_FLAG_NO_KEYS) keys = false;
+    if (const char* e = getenv("MIS2_KEYS")) keys = atoi(e) != 0;  // measurement knob
+    p.K = keys ? w.K : nullptr;
     for (int i = 0; i < 2; i++) {
         p.L1[i] = w.L1[i];
         p.L2[i] = w.L2[i];

@@ -46,9 +46,9 @@ def small_graphs(count, seed, nmax=200):
     return out
 
 
-def check_mis2(g, seed=0, group=0, scheme="xorstar", stats=False, decide="auto"):
+def check_mis2(g, seed=0, group=0, scheme="xorstar", stats=False, decide="auto", keys="auto"):
     rp, ci = dev(g)
-    r = M().mis2(rp, ci, seed=seed, group=group, scheme=scheme, stats=stats, decide=decide)
+    r = M().mis2(rp, ci, seed=seed, group=group, scheme=scheme, stats=stats, decide=decide, keys=keys)
     o = O.mis2(g.rowptr, g.colinds, seed=seed, scheme=scheme, stats=stats)
     assert np.array_equal(r.in_set.cpu().numpy().astype(bool), o.in_set), g.name
     assert (r.count, r.iterations) == (o.count, o.iterations), g.name
@@ -84,6 +84,21 @@ def test_group_width_invariance(group, decide):
     """§V-D lane grouping never changes results."""
     for g in small_graphs(25, 77, nmax=400) + [G.laplace3d_27pt(20), G.kronecker(11)]:
         check_mis2(g, group=group, decide=decide)
+
+
+@pytest.mark.parametrize("keys", ["on", "off"])
+@pytest.mark.parametrize("decide", ["pull", "push"])
+def test_column_keys(decide, keys):
+    """32-bit column keys (ties in the key class resolved on the full words)
+    on random / power-law / stencil graphs, every lane-group width, hub rows;
+    the Fixed scheme's and the Fig. 1-like small-id words make ties frequent."""
+    gs = small_graphs(40, 4242, nmax=300) + [G.laplace3d_27pt(12), G.kronecker(12),
+                                           G.random_powerlaw_graph(4000, 40, 3)]
+    for g in gs:
+        check_mis2(g, decide=decide, keys=keys)
+        check_mis2(g, decide=decide, keys=keys, seed=5, scheme="fixed")
+    for grp in (1, 4, 32):
+        check_mis2(G.kronecker(11), group=grp, decide=decide, keys=keys)
 
 
 @pytest.mark.parametrize("decide", ["pull", "push"])
