@@ -215,3 +215,30 @@ def config_graph(i: int) -> Graph:
 
 def num_threads() -> int:
     return int(_load().gen_num_threads())
+
+
+def spd_values(g: Graph, seed: int = 0):
+    """Seeded symmetric, strictly diagonally dominant (hence SPD) values on
+    the pattern of g, diagonal inserted where missing: the synthetic matrices
+    of the Alg. 4 (cluster Gauss-Seidel) tests and bench.  Off-diagonal
+    a_ij = a_ji = -(0.5 + 0.5 u(min(i,j), max(i,j))), u a splitmix64 hash in
+    [0, 1); a_ii = 1 + sum_j |a_ij|.  Returns (Graph with diagonal, vals f64).
+    Input generation only (no method arithmetic)."""
+    gd = add_diagonal(g)
+    n = gd.n
+    rows = np.repeat(np.arange(n, dtype=np.uint64), np.diff(gd.rowptr).astype(np.int64))
+    cols = gd.colinds.astype(np.uint64)
+    lo, hi = np.minimum(rows, cols), np.maximum(rows, cols)
+    with np.errstate(over="ignore"):
+        z = lo * np.uint64(0x9E3779B97F4A7C15) + hi + np.uint64(seed & ((1 << 64) - 1))
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    u = (z >> np.uint64(11)).astype(np.float64) / float(1 << 53)
+    vals = -(0.5 + 0.5 * u)
+    diag = rows == cols
+    vals[diag] = 0.0
+    rowsum = np.zeros(n)
+    np.add.at(rowsum, rows.astype(np.int64), np.abs(vals))
+    vals[diag] = 1.0 + rowsum[rows[diag].astype(np.int64)]
+    return gd, vals

@@ -70,6 +70,10 @@ def _load():
         lib.orc_coarsen_basic.restype = ctypes.c_int
         lib.orc_coarsen.argtypes = [i64, p, p, p, i64, p, p, i64, p]
         lib.orc_coarsen.restype = ctypes.c_int
+        lib.orc_color_jp.argtypes = [i64, p, p, u64, p, p]
+        lib.orc_color_jp.restype = ctypes.c_int
+        lib.orc_cluster_sgs.argtypes = [i64, p, p, p, p, i64, p, i32, p, p, ctypes.c_int, ctypes.c_int]
+        lib.orc_cluster_sgs.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -228,3 +232,55 @@ def multilevel(rowptr, colinds, threshold: int = 1000, max_levels: int = 32, see
             break
         rp, ci = coarsen(rp, ci, agg.labels, agg.num_aggs)
     return levels, (rp, ci)
+
+
+# --- Alg. 4 -----------------------------------------------------
+def color_jp(rowptr, colinds, seed: int = 0):
+    """Deterministic greedy colouring (reading Q30): (colour int32[n], ncolors)."""
+    lib = _load()
+    rowptr, colinds = _csr(rowptr, colinds)
+    n = rowptr.shape[0] - 1
+    color = np.zeros(max(n, 1), dtype=np.int32)
+    nc = ctypes.c_int32(0)
+    rc = lib.orc_color_jp(n, _p(rowptr), _p(colinds), seed & ((1 << 64) - 1), _p(color), ctypes.byref(nc))
+    if rc != OK:
+        raise OracleError(rc, "color_jp")
+    return color[:n], int(nc.value)
+
+
+def cluster_sgs(rowptr, colinds, vals, labels, num_aggs, ccolor, ncolors, b, x0=None, sweeps: int = 1,
+                direction: str = "symmetric"):
+    """Alg. 4 apply / SGS (reading Q31) in fp64 from x0
+    (default 0): returns x."""
+    lib = _load()
+    rowptr, colinds = _csr(rowptr, colinds)
+    n = rowptr.shape[0] - 1
+    vals = np.ascontiguousarray(vals, dtype=np.float64)
+    if vals.shape[0] == 0:
+        vals = np.zeros(1)
+    labels = np.ascontiguousarray(labels, dtype=np.int32)
+    ccolor = np.ascontiguousarray(ccolor, dtype=np.int32)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros(max(n, 1)) if x0 is None else np.array(x0, dtype=np.float64, copy=True)
+    d = {"symmetric": 0, "forward": 1, "backward": 2}[direction]
+    rc = lib.orc_cluster_sgs(n, _p(rowptr), _p(colinds), _p(vals), _p(labels if n else np.zeros(1, np.int32)),
+                             num_aggs, _p(ccolor if len(ccolor) else np.zeros(1, np.int32)), ncolors, _p(b), _p(x),
+                             sweeps, d)
+    if rc != OK:
+        raise OracleError(rc, "cluster_sgs")
+    return x[:n]
+
+
+def cgs_setup(rowptr, colinds, seed: int = 0, point: bool = False):
+    """Alg. 4 setup: clusters = Alg. 3 aggregates (or single rows when
+    point=True, point multicolor GS), coloured on the coarse graph.
+    Returns (labels, num_aggs, ccolor, ncolors)."""
+    n = len(rowptr) - 1
+    if point:
+        labels, na = np.arange(n, dtype=np.int32), n
+    else:
+        a = aggregate(rowptr, colinds, seed=seed)
+        labels, na = a.labels, a.num_aggs
+    crow, ccol = coarsen(rowptr, colinds, labels, na)
+    ccolor, nc = color_jp(crow, ccol, seed=seed)
+    return labels, na, ccolor, nc

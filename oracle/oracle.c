@@ -467,3 +467,139 @@ int orc_coarsen(int64_t n, const int64_t* rowptr, const int32_t* colinds, const 
     if (!c_colinds || cap < total) return -7;
     return ORC_OK;
 }
+
+/* ---------------------------------------------------------------------------
+ * Alg. 4 "Cluster Multicolor Gauss-Seidel" (§III-C).
+ *
+ * Setup line "colorsets <- color(A_c)": the paper colours the
+ * coarse graph with a greedy colouring ("setup time is dominated by
+ * greedy graph coloring") without fixing the algorithm; reading Q30: the
+ * deterministic parallel greedy of Jones-Plassmann, priorities = the MIS-2
+ * status words of iteration 0 (word(0, v), seed as given, b of this graph).
+ * Round r: every uncoloured vertex whose word is smaller than the words of
+ * all its uncoloured neighbours (as of the start of the round) takes the
+ * smallest colour not used by an already coloured neighbour.  Diagonal
+ * entries are ignored.  Plain loops in round order.
+ * ------------------------------------------------------------------------- */
+int orc_color_jp(int64_t n, const int64_t* rowptr, const int32_t* colinds, uint64_t seed, int32_t* color,
+                 int32_t* ncolors) {
+    if (n < 0 || !color || !ncolors) return ORC_EINVAL;
+    const int b = orc_bits(n);
+    uint64_t* w = (uint64_t*)malloc(sizeof(uint64_t) * ((size_t)n + 1));
+    unsigned char* cand = (unsigned char*)malloc((size_t)n + 1);
+    unsigned char* used = NULL;
+    size_t used_cap = 0;
+    if (!w || !cand) { free(w); free(cand); return ORC_ENOMEM; }
+    for (int64_t v = 0; v < n; v++) {
+        w[v] = orc_word(ORC_SCHEME_XORSTAR, 0, v, seed, b);
+        color[v] = -1;
+    }
+    int64_t left = n;
+    int32_t nc = 0;
+    int rc = ORC_OK;
+    while (left > 0) {
+        /* candidates of this round, from the colouring at its start */
+        for (int64_t v = 0; v < n; v++) {
+            cand[v] = 0;
+            if (color[v] >= 0) continue;
+            int ok = 1;
+            for (int64_t j = rowptr[v]; j < rowptr[v + 1] && ok; j++) {
+                const int64_t u = colinds[j];
+                if (u != v && color[u] < 0 && w[u] < w[v]) ok = 0;
+            }
+            cand[v] = (unsigned char)ok;
+        }
+        for (int64_t v = 0; v < n; v++) {
+            if (!cand[v]) continue;
+            const size_t deg = (size_t)(rowptr[v + 1] - rowptr[v]);
+            if (deg + 2 > used_cap) {
+                free(used);
+                used_cap = 2 * deg + 2;
+                used = (unsigned char*)malloc(used_cap);
+                if (!used) { rc = ORC_ENOMEM; break; }
+            }
+            memset(used, 0, deg + 2);
+            for (int64_t j = rowptr[v]; j < rowptr[v + 1]; j++) {
+                const int64_t u = colinds[j];
+                if (u != v && color[u] >= 0 && !cand[u] && (size_t)color[u] <= deg) used[color[u]] = 1;
+            }
+            int32_t c = 0;
+            while (used[c]) c++;
+            color[v] = c;
+            if (c + 1 > nc) nc = c + 1;
+            left--;
+        }
+        if (rc != ORC_OK) break;
+    }
+    free(w);
+    free(cand);
+    free(used);
+    *ncolors = nc;
+    return rc;
+}
+
+/* Alg. 4 apply and its symmetric form ("looping over the
+ * colors twice: first forward and then backward ... the order of row updates
+ * within each cluster are reversed during the backward loop").  Row i belongs
+ * to cluster labels[i]; cluster a has colour ccolor[a].  For each colour (in
+ * order), for each cluster of that colour (independent: any order), for each
+ * row of the cluster in ascending (forward) / descending (backward) order:
+ *     r = b_i - sum_j A_ij x_j        (stored column order)
+ *     x_i = x_i + r / A_ii            (reading Q31: the standard GS update;
+ *                                      P:349's literal "x_i <- r/A_ii" with r
+ *                                      including the diagonal term double
+ *                                      counts it)
+ * direction: 0 symmetric (forward then backward), 1 forward, 2 backward;
+ * `sweeps` repetitions.  A_ii must be present and nonzero (else EINVAL). */
+int orc_cluster_sgs(int64_t n, const int64_t* rowptr, const int32_t* colinds, const double* vals,
+                    const int32_t* labels, int64_t na, const int32_t* ccolor, int32_t ncolors, const double* b,
+                    double* x, int sweeps, int direction) {
+    if (n < 0 || na < 0 || ncolors < 0 || sweeps < 0 || direction < 0 || direction > 2) return ORC_EINVAL;
+    double* diag = (double*)malloc(sizeof(double) * ((size_t)n + 1));
+    int64_t* mptr = (int64_t*)calloc((size_t)na + 2, sizeof(int64_t));
+    int64_t* mem = (int64_t*)malloc(sizeof(int64_t) * ((size_t)n + 1));
+    if (!diag || !mptr || !mem) { free(diag); free(mptr); free(mem); return ORC_ENOMEM; }
+    int rc = ORC_OK;
+    for (int64_t i = 0; i < n && rc == ORC_OK; i++) {
+        diag[i] = 0.0;
+        for (int64_t j = rowptr[i]; j < rowptr[i + 1]; j++)
+            if (colinds[j] == i) diag[i] = vals[j];
+        if (diag[i] == 0.0 || labels[i] < 0 || labels[i] >= na) rc = ORC_EINVAL;
+    }
+    /* rows of each cluster, ascending */
+    if (rc == ORC_OK) {
+        for (int64_t i = 0; i < n; i++) mptr[labels[i] + 1]++;
+        for (int64_t a = 0; a < na; a++) mptr[a + 1] += mptr[a];
+        int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * ((size_t)na + 1));
+        if (!fill) rc = ORC_ENOMEM;
+        else {
+            memcpy(fill, mptr, sizeof(int64_t) * (size_t)na);
+            for (int64_t i = 0; i < n; i++) mem[fill[labels[i]]++] = i;
+            free(fill);
+        }
+    }
+    for (int s = 0; s < sweeps && rc == ORC_OK; s++) {
+        for (int pass = 0; pass < 2; pass++) {
+            const int backward = (direction == 2) || (direction == 0 && pass == 1);
+            if (direction == 1 && pass == 1) break;
+            if (direction == 2 && pass == 1) break;
+            for (int32_t ci = 0; ci < ncolors; ci++) {
+                const int32_t col = backward ? ncolors - 1 - ci : ci;
+                for (int64_t a = 0; a < na; a++) {
+                    if (ccolor[a] != col) continue;
+                    const int64_t k0 = mptr[a], k1 = mptr[a + 1];
+                    for (int64_t t = 0; t < k1 - k0; t++) {
+                        const int64_t i = mem[backward ? k1 - 1 - t : k0 + t];
+                        double r = b[i];
+                        for (int64_t j = rowptr[i]; j < rowptr[i + 1]; j++) r -= vals[j] * x[colinds[j]];
+                        x[i] = x[i] + r / diag[i];
+                    }
+                }
+            }
+        }
+    }
+    free(diag);
+    free(mptr);
+    free(mem);
+    return rc;
+}

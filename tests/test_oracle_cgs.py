@@ -1,0 +1,119 @@
+"""Pins of the Alg. 4 oracle (cluster multicolor Gauss-Seidel):
+the colouring against the properties that define a greedy colouring, the
+sweeps against textbook Gauss-Seidel written as triangular solves (scipy) on
+the colour/cluster ordering, and the symmetric form against the symmetry of
+its operator."""
+import numpy as np
+import pytest
+import scipy.linalg as sla
+import scipy.sparse as sp
+
+import mis2gen as G
+import oracle as O
+
+
+def dense(g, vals):
+    return sp.csr_matrix((vals, g.colinds, g.rowptr), shape=(g.n, g.n)).toarray()
+
+
+def graphs():
+    return [G.grid2d_5pt(7, 6), G.laplace3d_7pt(5), G.laplace3d_27pt(5), G.random_graph(80, 0.08, 3),
+            G.random_powerlaw_graph(120, 5, 2), G.elasticity3d(3)]
+
+
+@pytest.mark.parametrize("seed", [0, 31])
+def test_coloring_is_a_greedy_coloring(seed):
+    for g in graphs() + [G.from_edges(9, [])]:
+        color, nc = O.color_jp(g.rowptr, g.colinds, seed=seed)
+        deg = np.diff(g.rowptr)
+        assert nc == (color.max() + 1 if g.n else 0)
+        for v in range(g.n):
+            nb = [u for u in g.colinds[g.rowptr[v]:g.rowptr[v + 1]] if u != v]
+            assert all(color[u] != color[v] for u in nb)              # proper (distance 1)
+            assert set(range(color[v])) <= {color[u] for u in nb}      # greedy: every smaller colour is taken
+            assert color[v] <= deg[v]
+        assert np.array_equal(color, O.color_jp(g.rowptr, g.colinds, seed=seed)[0])
+
+
+def test_coloring_closed_forms():
+    kn = G.from_edges(6, [(i, j) for i in range(6) for j in range(i + 1, 6)])
+    c, nc = O.color_jp(kn.rowptr, kn.colinds)
+    assert nc == 6 and sorted(c) == list(range(6))
+    e = G.from_edges(5, [])
+    c, nc = O.color_jp(e.rowptr, e.colinds)
+    assert nc == 1 and not c.any()
+
+
+def gs_order_solve(A, b, x, order, backward=False):
+    """Gauss-Seidel over the rows in `order` as one triangular solve: with P the
+    permutation, (D + L_P) x_new = b - U_P x_old in the permuted system."""
+    P = np.asarray(order)
+    Ap, bp, xp = A[np.ix_(P, P)], b[P], x[P]
+    if not backward:
+        lower = np.tril(Ap)
+        xn = sla.solve_triangular(lower, bp - np.triu(Ap, 1) @ xp, lower=True)
+    else:
+        upper = np.triu(Ap)
+        xn = sla.solve_triangular(upper, bp - np.tril(Ap, -1) @ xp, lower=False)
+    out = np.empty_like(x)
+    out[P] = xn
+    return out
+
+
+@pytest.mark.parametrize("point", [False, True])
+def test_sweeps_equal_ordered_gauss_seidel(point):
+    rng = np.random.default_rng(4)
+    for g0 in graphs():
+        g, vals = G.spd_values(g0, seed=7)
+        A = dense(g, vals)
+        labels, na, ccolor, nc = O.cgs_setup(g.rowptr, g.colinds, point=point)
+        # the same-colour clusters share no edge (independence of clusters)
+        rows = np.repeat(np.arange(g.n), np.diff(g.rowptr))
+        same = (ccolor[labels[rows]] == ccolor[labels[g.colinds]]) & (labels[rows] != labels[g.colinds])
+        assert not same.any()
+        order = sorted(range(g.n), key=lambda i: (ccolor[labels[i]], labels[i], i))
+        b = rng.standard_normal(g.n)
+        x0 = rng.standard_normal(g.n)
+        fw = O.cluster_sgs(g.rowptr, g.colinds, vals, labels, na, ccolor, nc, b, x0, 1, "forward")
+        want = gs_order_solve(A, b, x0, order)
+        assert np.allclose(fw, want, rtol=1e-11, atol=1e-12)
+        bw = O.cluster_sgs(g.rowptr, g.colinds, vals, labels, na, ccolor, nc, b, x0, 1, "backward")
+        assert np.allclose(bw, gs_order_solve(A, b, x0, order, backward=True), rtol=1e-11, atol=1e-12)
+        sym = O.cluster_sgs(g.rowptr, g.colinds, vals, labels, na, ccolor, nc, b, x0, 1, "symmetric")
+        assert np.allclose(sym, gs_order_solve(A, b, want, order, backward=True), rtol=1e-11, atol=1e-12)
+
+
+def test_diagonal_matrix_and_single_cluster():
+    g, vals = G.spd_values(G.from_edges(7, []), seed=1)
+    b = np.arange(1.0, 8.0)
+    lab = np.arange(7, dtype=np.int32)
+    x = O.cluster_sgs(g.rowptr, g.colinds, vals, lab, 7, np.zeros(7, np.int32), 1, b, None, 1, "forward")
+    assert np.array_equal(x, b / vals)  # exact: x_i = b_i / A_ii
+    # one cluster with every row, one colour = classical sequential GS
+    g, vals = G.spd_values(G.laplace3d_7pt(4), seed=2)
+    A = dense(g, vals)
+    b = np.linspace(-1, 1, g.n)
+    one = np.zeros(g.n, np.int32)
+    x = O.cluster_sgs(g.rowptr, g.colinds, vals, one, 1, np.zeros(1, np.int32), 1, b, None, 1, "forward")
+    assert np.allclose(x, sla.solve_triangular(np.tril(A), b, lower=True), rtol=1e-12, atol=1e-14)
+
+
+def test_symmetric_sweep_is_a_symmetric_operator_and_converges():
+    rng = np.random.default_rng(9)
+    g, vals = G.spd_values(G.laplace3d_27pt(4), seed=3)
+    A = dense(g, vals)
+    labels, na, ccolor, nc = O.cgs_setup(g.rowptr, g.colinds)
+    for _ in range(10):
+        b1, b2 = rng.standard_normal(g.n), rng.standard_normal(g.n)
+        m1 = O.cluster_sgs(g.rowptr, g.colinds, vals, labels, na, ccolor, nc, b1)
+        m2 = O.cluster_sgs(g.rowptr, g.colinds, vals, labels, na, ccolor, nc, b2)
+        assert abs(m1 @ b2 - b1 @ m2) <= 1e-12 * max(1.0, abs(m1 @ b2))
+    # SGS on SPD A contracts the error in the energy norm
+    b = rng.standard_normal(g.n)
+    xs = np.linalg.solve(A, b)
+    x = np.zeros(g.n)
+    err = [np.sqrt((x - xs) @ A @ (x - xs))]
+    for _ in range(10):
+        x = O.cluster_sgs(g.rowptr, g.colinds, vals, labels, na, ccolor, nc, b, x, 1)
+        err.append(np.sqrt((x - xs) @ A @ (x - xs)))
+    assert all(e2 < e1 for e1, e2 in zip(err, err[1:]))
