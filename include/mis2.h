@@ -246,6 +246,38 @@ int mis2_plan_part(int64_t n_global, int nparts, int part, const int64_t* rowptr
                    const int32_t* colinds_global, int64_t* n_ghost, int64_t* ghost_ids, int64_t* req_counts,
                    int32_t* colinds_local);
 
+/* ------------------------------------------------------------------------
+ * Alg. 4 "Cluster Multicolor Gauss-Seidel" (§III-C).
+ *
+ * mis2_color: deterministic greedy colouring of a graph (reading Q30:
+ * Jones-Plassmann rounds, priorities = the MIS-2 status words of iteration 0
+ * with `seed`; every vertex takes the smallest colour none of its
+ * earlier-coloured neighbours has).  color: device int32[n]; *ncolors on
+ * return (synchronises the stream).  Scratch is allocated internally.
+ *
+ * mis2_cgs_setup: Alg. 4's setup.  labels (device int32[n]) and
+ * num_aggs give the clusters (e.g. mis2_aggregate), `coarse` their coarse
+ * graph (mis2_coarsen; device CSR with num_aggs rows), coloured with
+ * mis2_color; labels == NULL gives point multicolor Gauss-Seidel (every row
+ * its own cluster, the graph itself coloured).  vals: device f64[nnz], A_ii
+ * must be stored and nonzero (MIS2_EINVAL otherwise).  g, vals must stay
+ * valid while the handle is used; the handle owns its cluster / colour-set
+ * arrays (freed by mis2_cgs_destroy).
+ *
+ * mis2_cgs_apply: `sweeps` sweeps on x (device f64[n], in place) for the
+ * right-hand side b (device f64[n]): direction 1 forward (colours and rows
+ * ascending), 2 backward (both descending), 0 symmetric (forward then
+ * backward).  Row update x_i += (b_i - A_i x) / A_ii (reading Q31).  Clusters
+ * of one colour are updated concurrently; enqueued on `stream`.
+ * ---------------------------------------------------------------------- */
+typedef struct mis2_cgs mis2_cgs;
+int mis2_color(const mis2_graph* g, uint64_t seed, int32_t* color, int32_t* ncolors, void* stream);
+int mis2_cgs_setup(const mis2_graph* g, const double* vals, const int32_t* labels, int64_t num_aggs,
+                   const mis2_graph* coarse, uint64_t seed, mis2_cgs** out, void* stream);
+int mis2_cgs_ncolors(const mis2_cgs* h);
+int mis2_cgs_apply(mis2_cgs* h, const double* b, double* x, int sweeps, int direction, void* stream);
+int mis2_cgs_destroy(mis2_cgs* h);
+
 /* Number of kernel launches issued by the last call on this thread
  * (measurement aid for bench.py's "gpu_launches"). */
 int64_t mis2_last_launch_count(void);

@@ -37,7 +37,7 @@ EXPORTS = ["mis2_opts_default", "mis2_workspace_size", "mis2", "mis2_async", "mi
            "mis2_coarsen", "mis2_validate_graph", "mis2_last_launch_count", "mis2_strerror", "mis2_last_error",
            "mis2_version", "mis2_comm_unique_id", "mis2_comm_init_nccl", "mis2_comm_init_local",
            "mis2_comm_set_graph", "mis2_dist_mis2", "mis2_dist_aggregate", "mis2_dist_coarsen", "mis2_comm_part_info", "mis2_comm_destroy",
-           "mis2_plan_part"]
+           "mis2_plan_part", "mis2_color", "mis2_cgs_setup", "mis2_cgs_ncolors", "mis2_cgs_apply", "mis2_cgs_destroy"]
 
 
 class Mis2Error(RuntimeError):
@@ -82,6 +82,11 @@ def lib():
         L.mis2_validate_graph.argtypes = [P, P, SZ, P]
         L.mis2_dist_aggregate.argtypes = [P, P, P, P, P, P]
         L.mis2_dist_coarsen.argtypes = [P, P, I64, P, P, I64, P, P]
+        L.mis2_color.argtypes = [P, ctypes.c_uint64, P, P, P]
+        L.mis2_cgs_setup.argtypes = [P, P, P, I64, P, ctypes.c_uint64, P, P]
+        L.mis2_cgs_ncolors.argtypes = [P]
+        L.mis2_cgs_apply.argtypes = [P, P, P, I32, I32, P]
+        L.mis2_cgs_destroy.argtypes = [P]
         L.mis2_last_launch_count.restype = I64
         L.mis2_strerror.restype = ctypes.c_char_p
         L.mis2_strerror.argtypes = [ctypes.c_int]
@@ -434,6 +439,64 @@ class Comm:
     def close(self):
         if self.h:
             lib().mis2_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------- Alg. 4
+def color(rowptr, colinds, seed: int = 0):
+    """Deterministic greedy colouring (``mis2_color``, reading Q30): returns
+    (int32 CUDA colours, ncolors)."""
+    torch = _torch()
+    g, n, nnz = _graph(rowptr, colinds)
+    out = torch.empty(max(n, 1), dtype=torch.int32, device=rowptr.device)
+    nc = ctypes.c_int32(0)
+    _check(lib().mis2_color(ctypes.byref(g), seed & ((1 << 64) - 1), out.data_ptr(), ctypes.byref(nc), _stream()),
+           "mis2_color")
+    return out[:n], int(nc.value)
+
+
+class ClusterSGS:
+    """Alg. 4 cluster multicolor Gauss-Seidel (``mis2_cgs_*``): clusters =
+    ``labels`` (e.g. ``aggregate``) coloured on their coarse graph, or
+    point multicolor GS when ``labels`` is None.  ``apply`` runs sweeps in
+    place on a float64 CUDA vector."""
+
+    DIRS = {"symmetric": 0, "forward": 1, "backward": 2}
+
+    def __init__(self, rowptr, colinds, vals, labels=None, num_aggs: int = 0, coarse=None, seed: int = 0):
+        self._keep = (rowptr, colinds, vals, labels, coarse)
+        g, n, nnz = _graph(rowptr, colinds)
+        self.n = n
+        cg = None
+        if labels is not None:
+            if coarse is None:
+                coarse = coarsen(rowptr, colinds, labels, num_aggs)
+                self._keep = (rowptr, colinds, vals, labels, coarse)
+            cg, _, _ = _graph(*coarse)
+        h = ctypes.c_void_p()
+        _check(lib().mis2_cgs_setup(ctypes.byref(g), vals.data_ptr(), labels.data_ptr() if labels is not None else None,
+                                    num_aggs, ctypes.byref(cg) if cg is not None else None,
+                                    seed & ((1 << 64) - 1), ctypes.byref(h), _stream()), "mis2_cgs_setup")
+        self.h = h
+        self.ncolors = int(lib().mis2_cgs_ncolors(h))
+
+    def apply(self, b, x=None, sweeps: int = 1, direction: str = "symmetric"):
+        torch = _torch()
+        if x is None:
+            x = torch.zeros(max(self.n, 1), dtype=torch.float64, device=b.device)
+        _check(lib().mis2_cgs_apply(self.h, b.data_ptr(), x.data_ptr(), sweeps, self.DIRS[direction], _stream()),
+               "mis2_cgs_apply")
+        return x
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().mis2_cgs_destroy(self.h)
             self.h = None
 
     def __del__(self):

@@ -1,0 +1,408 @@
+// cgs.cu -- Alg. 4 "Cluster Multicolor Gauss-Seidel" (§III-C):
+// the colouring of the coarse graph (setup), the cluster / colour-set
+// structure and the symmetric sweeps.
+//
+// Colouring (reading Q30): Jones-Plassmann rounds with the MIS-2 status
+// words of iteration 0 as priorities -- in round r every uncoloured vertex
+// whose word is below the words of all its neighbours uncoloured at the
+// start of the round takes the smallest colour no earlier-coloured neighbour
+// has.  Candidates of one round are never adjacent, so a round is one
+// race-free pass (a vertex coloured in round r records r, and "uncoloured at
+// the start of round r" = "coloured in round >= r").
+//
+// Sweeps: one launch per colour and direction; a warp per cluster of the
+// colour walks the cluster's rows in order (ascending forward, descending
+// backward); a row's residual r = b_i - A_i x is summed by the lanes
+// (fixed order: lane-strided partial sums, then a tree), and lane 0 applies
+// x_i += r / A_ii (reading Q31: the standard update; P:349's literal
+// "x_i <- r/A_ii" double counts the diagonal).  Clusters of one colour share
+// no edge, so they run concurrently without touching each other's x.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace mis2k {
+
+__global__ void k_color_init(int64_t n, Prio pr, uint64_t* __restrict__ W, int32_t* __restrict__ cround,
+                             int32_t* __restrict__ color) {
+    const uint64_t fi0 = pr.iter_term(0);
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        W[v] = pr.word(0, fi0, v);
+        cround[v] = 0x7fffffff;
+        color[v] = -1;
+    }
+}
+
+__global__ void k_color_round(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colinds,
+                              const uint64_t* __restrict__ W, int32_t* __restrict__ cround,
+                              int32_t* __restrict__ color, int r, unsigned long long* colored, int* maxc) {
+    int done = 0, mc = -1;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        if (cround[v] < r) continue;  // coloured in an earlier round
+        const uint64_t wv = W[v];
+        const int64_t s = rowptr[v], e = rowptr[v + 1];
+        bool cand = true;
+        uint64_t mask = 0;
+        for (int64_t j = s; j < e && cand; j++) {
+            const int32_t u = colinds[j];
+            if (u == v) continue;
+            const int32_t ru = cround[u];
+            if (ru >= r) {
+                if (W[u] < wv) cand = false;  // an uncoloured neighbour of higher priority
+            } else {
+                const int32_t cu = color[u];
+                if (cu < 64) mask |= 1ull << cu;
+            }
+        }
+        if (!cand) continue;
+        int32_t c;
+        if (mask != ~0ull) {
+            c = __ffsll((long long)~mask) - 1;
+        } else {  // more than 64 colours around: smallest free colour >= 64
+            c = 64;
+            for (;;) {
+                bool taken = false;
+                for (int64_t j = s; j < e && !taken; j++) {
+                    const int32_t u = colinds[j];
+                    if (u != v && cround[u] < r && color[u] == c) taken = true;
+                }
+                if (!taken) break;
+                c++;
+            }
+        }
+        color[v] = c;
+        cround[v] = r;
+        done++;
+        mc = max(mc, c);
+    }
+    done = group_sum<32>(done);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mc = max(mc, __shfl_xor_sync(kFull, mc, off));
+    if ((threadIdx.x & 31) == 0) {
+        if (done) atomicAdd(colored, (unsigned long long)done);
+        if (mc >= 0) atomicMax(maxc, mc);
+    }
+}
+
+// rows per cluster (pass 1) / placed at an atomically reserved slot (pass 2)
+__global__ void k_count_i32(int64_t n, const int32_t* __restrict__ key, unsigned long long* __restrict__ cnt) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&cnt[key[i]], 1ull);
+}
+__global__ void k_scatter_i32(int64_t n, const int32_t* __restrict__ key, unsigned long long* __restrict__ cursor,
+                              int32_t* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[atomicAdd(&cursor[key[i]], 1ull)] = (int32_t)i;
+}
+// ascending rows inside each cluster: block bitonic of the segment in shared memory
+constexpr int kSegMax = 4096;
+__global__ void k_sort_segments(int64_t na, const int64_t* __restrict__ ptr, int32_t* __restrict__ rows, int* err) {
+    __shared__ int32_t x[kSegMax];
+    for (int64_t a = blockIdx.x; a < na; a += gridDim.x) {
+        const int64_t s = ptr[a], len = ptr[a + 1] - s;
+        if (len <= 1) continue;
+        if (len > kSegMax) {
+            if (threadIdx.x == 0) atomicOr(err, 1);
+            continue;
+        }
+        int P = 1;
+        while (P < len) P <<= 1;
+        for (int i = threadIdx.x; i < P; i += blockDim.x) x[i] = i < len ? rows[s + i] : 0x7fffffff;
+        __syncthreads();
+        for (int k = 2; k <= P; k <<= 1)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
+                    const int lo = 2 * i - (i & (j - 1)), hi = lo + j;
+                    const bool up = (lo & k) == 0;
+                    const int32_t p = x[lo], q = x[hi];
+                    if ((p > q) == up) {
+                        x[lo] = q;
+                        x[hi] = p;
+                    }
+                }
+                __syncthreads();
+            }
+        for (int i = threadIdx.x; i < len; i += blockDim.x) rows[s + i] = x[i];
+        __syncthreads();
+    }
+}
+__global__ void k_diag(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colinds,
+                       const double* __restrict__ vals, double* __restrict__ diag, int* err) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double d = 0.0;
+        for (int64_t j = rowptr[i]; j < rowptr[i + 1]; j++)
+            if (colinds[j] == i) d = vals[j];
+        diag[i] = d;
+        if (d == 0.0) atomicOr(err, 2);
+    }
+}
+__global__ void k_iota(int64_t n, int32_t* __restrict__ x, int64_t* __restrict__ ptr) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < n) x[i] = (int32_t)i;
+        ptr[i] = i;
+    }
+}
+
+// One colour of a sweep: a warp per cluster of the colour.
+__global__ void k_cgs_color(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colinds,
+                            const double* __restrict__ vals, const double* __restrict__ diag,
+                            const int64_t* __restrict__ cptr, const int32_t* __restrict__ crows,
+                            const int32_t* __restrict__ cset, int64_t set_lo, int64_t set_hi,
+                            const double* __restrict__ b, double* __restrict__ x, int backward) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t k = set_lo + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < set_hi; k += nw) {
+        const int32_t a = cset[k];
+        const int64_t r0 = cptr[a], r1 = cptr[a + 1];
+        for (int64_t t = 0; t < r1 - r0; t++) {
+            const int64_t i = crows[backward ? r1 - 1 - t : r0 + t];
+            const int64_t s = rowptr[i], e = rowptr[i + 1];
+            double acc = 0.0;
+            for (int64_t j = s + lane; j < e; j += 32) acc += vals[j] * x[colinds[j]];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
+            if (lane == 0) x[i] = x[i] + (b[i] - acc) / diag[i];
+            __syncwarp();
+        }
+    }
+}
+
+}  // namespace mis2k
+
+using namespace mis2h;
+using namespace mis2k;
+
+struct mis2_cgs {
+    int64_t n = 0, na = 0;
+    int32_t ncolors = 0;
+    mis2_graph g{};
+    const double* vals = nullptr;
+    std::vector<void*> allocs;
+    double* diag = nullptr;
+    int64_t* cptr = nullptr;   // [na+1] rows of cluster a: crows[cptr[a] .. cptr[a+1])
+    int32_t* crows = nullptr;  // [n] ascending inside a cluster
+    int32_t* cset = nullptr;   // [na] clusters grouped by colour
+    std::vector<int64_t> csptr;  // host [ncolors+1]
+};
+
+namespace {
+
+int cgs_alloc(mis2_cgs* h, void** p, size_t bytes) {
+    MIS2_CUDA_TRY(cudaMalloc(p, bytes < 256 ? 256 : bytes));
+    h->allocs.push_back(*p);
+    return MIS2_OK;
+}
+
+unsigned grid_for(int64_t n, int sms) {
+    int64_t b = (n + 255) / 256;
+    if (b > (int64_t)sms * 16) b = (int64_t)sms * 16;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+// the colouring (reading Q30) with internally allocated scratch
+int color_graph(const mis2_graph& g, uint64_t seed, int32_t* color, int32_t* ncolors, cudaStream_t s) {
+    DeviceInfo di;
+    MIS2_TRY(device_info(&di));
+    const int64_t n = g.n;
+    if (n == 0) {
+        *ncolors = 0;
+        return MIS2_OK;
+    }
+    uint64_t* W;
+    int32_t* cround;
+    unsigned long long* ctr;
+    MIS2_CUDA_TRY(cudaMallocAsync((void**)&W, sizeof(uint64_t) * n, s));
+    MIS2_CUDA_TRY(cudaMallocAsync((void**)&cround, sizeof(int32_t) * n, s));
+    MIS2_CUDA_TRY(cudaMallocAsync((void**)&ctr, 64, s));
+    Prio pr{};
+    pr.scheme = MIS2_SCHEME_XORSTAR;
+    pr.b = bits_for(n);
+    pr.seed = seed;
+    pr.hi_mask = ~((1ull << pr.b) - 1ull);
+    pr.n = n;
+    const unsigned gb = grid_for(n, di.sms);
+    k_color_init<<<gb, 256, 0, s>>>(n, pr, W, cround, color);
+    count_launch();
+    MIS2_CUDA_TRY(cudaMemsetAsync(ctr, 0, 64, s));
+    int rc = MIS2_OK;
+    unsigned long long colored = 0;
+    for (int r = 0; colored < (unsigned long long)n; r++) {
+        k_color_round<<<gb, 256, 0, s>>>(n, g.rowptr, g.colinds, W, cround, color, r, ctr, (int*)(ctr + 1));
+        count_launch();
+        if (cudaMemcpyAsync(&colored, ctr, sizeof(colored), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) {
+            rc = MIS2_ECUDA;
+            break;
+        }
+        if (r > n + 2) {  // every round colours at least the least uncoloured word
+            set_error("colouring did not terminate");
+            rc = MIS2_EINTERNAL;
+            break;
+        }
+    }
+    int maxc = -1;
+    if (rc == MIS2_OK) {
+        MIS2_CUDA_TRY(cudaMemcpyAsync(&maxc, ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+        MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+        *ncolors = maxc + 1;
+    }
+    cudaFreeAsync(W, s);
+    cudaFreeAsync(cround, s);
+    cudaFreeAsync(ctr, s);
+    return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mis2_color(const mis2_graph* g, uint64_t seed, int32_t* color, int32_t* ncolors, void* stream) {
+    reset_launches();
+    if (!g || !ncolors || g->n < 0 || (g->n > 0 && (!color || !g->rowptr)) || g->n > 2147483645LL) {
+        set_error("bad arguments");
+        return MIS2_EINVAL;
+    }
+    return color_graph(*g, seed, color, ncolors, (cudaStream_t)stream);
+}
+
+int mis2_cgs_setup(const mis2_graph* g, const double* vals, const int32_t* labels, int64_t num_aggs,
+                   const mis2_graph* coarse, uint64_t seed, mis2_cgs** out, void* stream) {
+    reset_launches();
+    if (!g || !out || g->n < 0 || (g->n > 0 && (!vals || !g->rowptr || !g->colinds)) ||
+        (labels && (!coarse || num_aggs < 1 || coarse->n != num_aggs)) || g->n > 2147483645LL) {
+        set_error("bad arguments");
+        return MIS2_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    DeviceInfo di;
+    MIS2_TRY(device_info(&di));
+    mis2_cgs* h = new mis2_cgs();
+    h->n = g->n;
+    h->g = *g;
+    h->vals = vals;
+    const bool point = labels == nullptr;
+    h->na = point ? g->n : num_aggs;
+    const int64_t n = h->n, na = h->na;
+    auto fail = [&](int rc) {
+        mis2_cgs_destroy(h);
+        return rc;
+    };
+    void* p;
+    int* err;
+    int rc;
+    if ((rc = cgs_alloc(h, &p, sizeof(double) * (n + 1))) != MIS2_OK) return fail(rc);
+    h->diag = (double*)p;
+    if ((rc = cgs_alloc(h, &p, sizeof(int64_t) * (na + 2))) != MIS2_OK) return fail(rc);
+    h->cptr = (int64_t*)p;
+    if ((rc = cgs_alloc(h, &p, sizeof(int32_t) * (n + 1))) != MIS2_OK) return fail(rc);
+    h->crows = (int32_t*)p;
+    if ((rc = cgs_alloc(h, &p, sizeof(int32_t) * (na + 1))) != MIS2_OK) return fail(rc);
+    h->cset = (int32_t*)p;
+    if ((rc = cgs_alloc(h, &p, 64)) != MIS2_OK) return fail(rc);
+    err = (int*)p;
+    int32_t* ccolor;
+    if ((rc = cgs_alloc(h, &p, sizeof(int32_t) * (na + 1))) != MIS2_OK) return fail(rc);
+    ccolor = (int32_t*)p;
+    unsigned long long* cnt;
+    const int64_t nk = std::max<int64_t>(na, 64) + 2;
+    if ((rc = cgs_alloc(h, &p, sizeof(unsigned long long) * nk)) != MIS2_OK) return fail(rc);
+    cnt = (unsigned long long*)p;
+    void* tmp;
+    if ((rc = cgs_alloc(h, &tmp, scan64_ws_bytes(nk))) != MIS2_OK) return fail(rc);
+    if (cudaMemsetAsync(err, 0, 64, s) != cudaSuccess) return fail(MIS2_ECUDA);
+    if (n) {
+        k_diag<<<grid_for(n, di.sms), 256, 0, s>>>(n, g->rowptr, g->colinds, vals, h->diag, err);
+        count_launch();
+    }
+    // colour the coarse graph (point: the graph itself)
+    if ((rc = color_graph(point ? *g : *coarse, seed, ccolor, &h->ncolors, s)) != MIS2_OK) return fail(rc);
+    // rows of each cluster, ascending
+    if (point) {
+        k_iota<<<grid_for(n + 1, di.sms), 256, 0, s>>>(n, h->crows, h->cptr);
+        count_launch();
+    } else if (n) {
+        if (cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * nk, s) != cudaSuccess) return fail(MIS2_ECUDA);
+        k_count_i32<<<grid_for(n, di.sms), 256, 0, s>>>(n, labels, cnt);
+        count_launch();
+        if ((rc = scan_counts64((const int64_t*)cnt, na, h->cptr, tmp, s)) != MIS2_OK) return fail(rc);
+        if (cudaMemcpyAsync(cnt, h->cptr, sizeof(int64_t) * na, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            return fail(MIS2_ECUDA);
+        k_scatter_i32<<<grid_for(n, di.sms), 256, 0, s>>>(n, labels, cnt, h->crows);
+        k_sort_segments<<<(unsigned)std::min<int64_t>(na, (int64_t)di.sms * 8), 256, 0, s>>>(na, h->cptr, h->crows, err);
+        count_launch(2);
+    }
+    // clusters grouped by colour
+    if (na) {
+        if (cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * nk, s) != cudaSuccess) return fail(MIS2_ECUDA);
+        k_count_i32<<<grid_for(na, di.sms), 256, 0, s>>>(na, ccolor, cnt);
+        count_launch();
+        std::vector<unsigned long long> hc(h->ncolors);
+        if (cudaMemcpyAsync(hc.data(), cnt, sizeof(unsigned long long) * h->ncolors, cudaMemcpyDeviceToHost, s) !=
+                cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return fail(MIS2_ECUDA);
+        h->csptr.assign(h->ncolors + 1, 0);
+        for (int c = 0; c < h->ncolors; c++) h->csptr[c + 1] = h->csptr[c] + (int64_t)hc[c];
+        if (cudaMemcpyAsync(cnt, h->csptr.data(), sizeof(int64_t) * h->ncolors, cudaMemcpyHostToDevice, s) !=
+            cudaSuccess)
+            return fail(MIS2_ECUDA);
+        k_scatter_i32<<<grid_for(na, di.sms), 256, 0, s>>>(na, ccolor, cnt, h->cset);
+        count_launch();
+    }
+    int herr = 0;
+    if (cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return fail(MIS2_ECUDA);
+    if (herr & 2) {
+        set_error("a diagonal entry A_ii is missing or zero");
+        return fail(MIS2_EINVAL);
+    }
+    if (herr & 1) {
+        set_error("a cluster has more than %d rows", kSegMax);
+        return fail(MIS2_EINTERNAL);
+    }
+    *out = h;
+    return MIS2_OK;
+}
+
+int mis2_cgs_ncolors(const mis2_cgs* h) { return h ? h->ncolors : -1; }
+
+int mis2_cgs_apply(mis2_cgs* h, const double* b, double* x, int sweeps, int direction, void* stream) {
+    reset_launches();
+    if (!h || sweeps < 0 || direction < 0 || direction > 2 || (h->n > 0 && (!b || !x))) {
+        set_error("bad arguments");
+        return MIS2_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    DeviceInfo di;
+    MIS2_TRY(device_info(&di));
+    for (int sw = 0; sw < sweeps; sw++) {
+        for (int pass = 0; pass < 2; pass++) {
+            if (pass == 1 && direction != 0) break;
+            const int backward = (direction == 2) || (direction == 0 && pass == 1);
+            for (int ci = 0; ci < h->ncolors; ci++) {
+                const int c = backward ? h->ncolors - 1 - ci : ci;
+                const int64_t lo = h->csptr[c], hi = h->csptr[c + 1];
+                if (hi <= lo) continue;
+                int64_t blocks = (hi - lo + 7) / 8;  // 8 warps per block, a warp per cluster
+                if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
+                k_cgs_color<<<(unsigned)blocks, 256, 0, s>>>(h->g.rowptr, h->g.colinds, h->vals, h->diag, h->cptr,
+                                                             h->crows, h->cset, lo, hi, b, x, backward);
+                count_launch();
+            }
+        }
+    }
+    MIS2_CUDA_TRY(cudaGetLastError());
+    return MIS2_OK;
+}
+
+int mis2_cgs_destroy(mis2_cgs* h) {
+    if (!h) return MIS2_OK;
+    for (void* p : h->allocs) cudaFree(p);
+    delete h;
+    return MIS2_OK;
+}
+
+}  // extern "C"

@@ -411,3 +411,57 @@ def test_coarsen_bitmap_path():
     labels[:na] = np.arange(na)
     labels[na: na + 2500] = 7  # aggregate 7 gets ~2500 members x ~60 neighbours
     check_coarsen(g, labels, na)
+
+
+# ------------------------------------------------------------------ Alg. 4
+def cgs_graphs():
+    return [G.grid2d_5pt(10, 10), G.laplace3d_7pt(9), G.laplace3d_27pt(8), G.random_graph(300, 0.03, 5),
+            G.random_powerlaw_graph(800, 8, 3), G.elasticity3d(4), G.kronecker(9)]
+
+
+@pytest.mark.parametrize("seed", [0, 17])
+def test_coloring_gpu(seed):
+    """mis2_color == the oracle's greedy colouring (reading Q30), bit-exact."""
+    for g in cgs_graphs() + [G.from_edges(20, []), G.from_edges(0, [])]:
+        rp, ci = dev(g)
+        c, nc = M().color(rp, ci, seed=seed)
+        oc, onc = O.color_jp(g.rowptr, g.colinds, seed=seed)
+        assert nc == onc and np.array_equal(c.cpu().numpy(), oc), g.name
+
+
+@pytest.mark.parametrize("point", [False, True])
+def test_cluster_sgs_gpu(point):
+    """Alg. 4 sweeps on the GPU == the oracle (fp64; only the order of the
+    row sums differs: relative 1e-12), forward / backward / symmetric,
+    several sweeps, point and MIS-2-aggregate clusters."""
+    rng = np.random.default_rng(11)
+    for g0 in cgs_graphs():
+        g, vals = G.spd_values(g0, seed=3)
+        rp, ci = dev(g)
+        vd = torch.from_numpy(vals).cuda()
+        if point:
+            cg = M().ClusterSGS(rp, ci, vd)
+            labels, na, ccolor, nc = O.cgs_setup(g.rowptr, g.colinds, point=True)
+        else:
+            a = M().aggregate(rp, ci)
+            cg = M().ClusterSGS(rp, ci, vd, labels=a.labels, num_aggs=a.num_aggs)
+            labels, na, ccolor, nc = O.cgs_setup(g.rowptr, g.colinds)
+            assert a.num_aggs == na
+        assert cg.ncolors == nc, g.name
+        b = rng.standard_normal(g.n)
+        x0 = rng.standard_normal(g.n)
+        for direction, sweeps in (("forward", 1), ("backward", 1), ("symmetric", 3)):
+            x = torch.from_numpy(x0.copy()).cuda()
+            cg.apply(torch.from_numpy(b).cuda(), x, sweeps=sweeps, direction=direction)
+            want = O.cluster_sgs(g.rowptr, g.colinds, vals, labels, na, ccolor, nc, b, x0, sweeps, direction)
+            got = x.cpu().numpy()
+            assert np.allclose(got, want, rtol=1e-12, atol=1e-12 * np.abs(want).max()), (g.name, direction)
+        cg.close()
+
+
+def test_cluster_sgs_errors():
+    g = G.grid2d_5pt(4, 4)  # no stored diagonal values -> A_ii missing
+    rp, ci = dev(G.strip_diagonal(g))
+    vals = torch.ones(int(ci.numel()), dtype=torch.float64, device="cuda")
+    with pytest.raises(M().Mis2Error):
+        M().ClusterSGS(rp, ci, vals)
