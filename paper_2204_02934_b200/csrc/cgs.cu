@@ -169,6 +169,21 @@ __global__ void k_cgs_color(const int64_t* __restrict__ rowptr, const int32_t* _
     }
 }
 
+// Point multicolor GS (every cluster one row): a thread per row of the colour.
+__global__ void k_pgs_color(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colinds,
+                            const double* __restrict__ vals, const double* __restrict__ diag,
+                            const int32_t* __restrict__ cset, int64_t set_lo, int64_t set_hi,
+                            const double* __restrict__ b, double* __restrict__ x) {
+    for (int64_t k = set_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < set_hi;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = cset[k];
+        const int64_t s = rowptr[i], e = rowptr[i + 1];
+        double acc = 0.0;
+        for (int64_t j = s; j < e; j++) acc += vals[j] * x[colinds[j]];
+        x[i] = x[i] + (b[i] - acc) / diag[i];
+    }
+}
+
 }  // namespace mis2k
 
 using namespace mis2h;
@@ -177,6 +192,7 @@ using namespace mis2k;
 struct mis2_cgs {
     int64_t n = 0, na = 0;
     int32_t ncolors = 0;
+    bool point = false;
     mis2_graph g{};
     const double* vals = nullptr;
     std::vector<void*> allocs;
@@ -283,6 +299,7 @@ int mis2_cgs_setup(const mis2_graph* g, const double* vals, const int32_t* label
     h->g = *g;
     h->vals = vals;
     const bool point = labels == nullptr;
+    h->point = point;
     h->na = point ? g->n : num_aggs;
     const int64_t n = h->n, na = h->na;
     auto fail = [&](int rc) {
@@ -386,10 +403,15 @@ int mis2_cgs_apply(mis2_cgs* h, const double* b, double* x, int sweeps, int dire
                 const int c = backward ? h->ncolors - 1 - ci : ci;
                 const int64_t lo = h->csptr[c], hi = h->csptr[c + 1];
                 if (hi <= lo) continue;
-                int64_t blocks = (hi - lo + 7) / 8;  // 8 warps per block, a warp per cluster
-                if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
-                k_cgs_color<<<(unsigned)blocks, 256, 0, s>>>(h->g.rowptr, h->g.colinds, h->vals, h->diag, h->cptr,
-                                                             h->crows, h->cset, lo, hi, b, x, backward);
+                if (h->point) {  // a thread per row
+                    k_pgs_color<<<grid_for(hi - lo, di.sms), 256, 0, s>>>(h->g.rowptr, h->g.colinds, h->vals,
+                                                                          h->diag, h->cset, lo, hi, b, x);
+                } else {
+                    int64_t blocks = (hi - lo + 7) / 8;  // 8 warps per block, a warp per cluster
+                    if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
+                    k_cgs_color<<<(unsigned)blocks, 256, 0, s>>>(h->g.rowptr, h->g.colinds, h->vals, h->diag,
+                                                                 h->cptr, h->crows, h->cset, lo, hi, b, x, backward);
+                }
                 count_launch();
             }
         }
