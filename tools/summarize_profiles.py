@@ -32,7 +32,7 @@ tot = sum(sum(v) for v in per.values())
 for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
     lines.append(f"| `{k[:90]}` | {len(v)} | {sum(v)/1e3:.1f} | {sum(v)/len(v)/1e3:.1f} | {100*sum(v)/tot:.1f}% |")
 mp = [ns for k, v in per.items() if "mis2_persistent<" in k and "1>" not in k.split("mis2_persistent")[1][:6] for ns in v]
-lines += ["", "Per timed step the only kernel of ours is `mis2k::mis2_persistent<1, false, false>` (1 launch; the",
+lines += ["", "Per timed step the only kernel of ours is `mis2k::mis2_persistent<1, false, true>` (1 launch; the",
           "per-call control-block memset and the between-step L2-flush fill are driver/torch operations).",
           "Its share of the step's GPU time is therefore ~100%, as in the CUDA-event timing."]
 open(os.path.join(out, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
@@ -73,8 +73,8 @@ if os.path.exists(rep):
     # per-source-line warp-stall attribution (tools/ncu_lines.py)
     try:
         txt = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), rep,
-                              "mis2_persistentILi1ELb0ELb0", "40"], capture_output=True, text=True).stdout
+                              "mis2_persistentILi1ELb0ELb1", "40"], capture_output=True, text=True).stdout
         open(os.path.join(out, f"{tag}_ncu_lines.txt"), "w").write(
-            "# warp-stall samples of mis2_persistent<1,false,false> by CUDA source line (innermost inlined line)\n" + txt)
+            "# warp-stall samples of mis2_persistent<1,false,true> (G=1, no stats, push-capable) by CUDA source line (innermost inlined line)\n" + txt)
     except Exception as e:  # pragma: no cover
         print("ncu_lines failed:", e)
