@@ -49,9 +49,12 @@ constexpr int kMinBlocksPerSM = kMW >= 16 ? 1 : 4;
 constexpr int kTileCap = (kMB >= 512 ? kMB / 2 : kMB) * 27;
 // rows longer than 8 gather batches of their lane group are deferred and
 // reduced by the whole block (flattened over all deferred rows of the block)
+#ifndef MIS2_HEAVY_BATCHES
+#define MIS2_HEAVY_BATCHES 8
+#endif
 template <int G>
 __host__ __device__ constexpr int heavy_len() {
-    return 8 * G * (G <= 2 ? 16 : (G == 4 ? 8 : 4));
+    return MIS2_HEAVY_BATCHES * G * (G <= 2 ? 16 : (G == 4 ? 8 : 4));
 }
 constexpr int kDenseNum = 3, kDenseDen = 8;  // dense if |worklist segment| >= 3/8 of the range (pull phases)
 // M_v is only ever compared against T_v (Decide: "M_w = T_v", "M_w = OUT").
@@ -107,6 +110,8 @@ struct __align__(16) TileSmem {
     uint64_t pol;    // L2 policy of this block's colinds span
     int cnt;         // survivors written this phase
     int hcount;
+    int hnext;       // deferred rows: next row for a warp
+    int nhuge;       // deferred rows too long for a warp
     uint64_t red64[kMW];
     int wred[kMW];
 };
@@ -511,10 +516,123 @@ __device__ __forceinline__ bool defer_long(TileSmem& sm, const MisParams& p, int
 // (prefix of the row lengths), 8 independent gathers per thread per pass,
 // combined per row with shared-memory atomics (min is exact in any order;
 // exists / forall likewise).
+// One deferred (long) row reduced by NT cooperating threads -- a warp
+// (NT = 32) or the whole block (NT = kMB) -- each issuing 8 independent,
+// coalesced colinds loads and 8 gathers per pass (indices clamped to the
+// row's last entry: min / exists / forall are idempotent).  Writes the row's
+// result like process_row; returns the survivor flag (valid in thread 0 of
+// the group).  All NT threads must call it.
+template <int NT>
+__device__ __forceinline__ uint64_t nt_min(TileSmem& sm, uint64_t x) {
+    if (NT == 32) return group_min<32>(x);
+    return block_min_u64(sm, x);
+}
+template <int NT>
+__device__ __forceinline__ int nt_sum(TileSmem& sm, int x) {
+    if (NT == 32) return group_sum<32>(x);
+    return (int)block_sum_int(sm, x);
+}
+template <int NT, bool STATS, int PH, bool PUSH>
+__device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_next, int64_t v, Stat& st,
+                          unsigned tag) {
+    const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
+    const int64_t s = p.rowptr[v], len = p.rowptr[v + 1] - s;
+    const int32_t* x = p.colinds + s;
+    const int64_t last = len - 1;
+    bool keep = false;
+    if (STATS) {
+        stat_row<STATS>(p, tag, v, tid == 0, len, st);
+        stat_nbrs<STATS>(p, tag, x, len, tid, NT, st);
+    }
+    if (PH == 0) {
+        const uint64_t tv = p.T[v];
+        const bool count_deg = PUSH && it == 0 && p.labels;
+        const bool keys = p.K && !count_deg;
+        uint32_t mf;
+        int dc = 0;
+        bool exact = !keys;
+        if (keys) {
+            uint64_t k1 = tid == 0 ? key_lo(kkey(tv), (uint32_t)v) : ~0ull;
+            uint64_t k2 = tid == 0 ? key_hi(kkey(tv), (uint32_t)v) : ~0ull;
+            for (int64_t j = tid; j < len; j += (int64_t)NT * 8) {
+                int32_t ww[8];
+                uint32_t kk[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) ww[u] = x[min(j + (int64_t)u * NT, last)];
+#pragma unroll
+                for (int u = 0; u < 8; u++) kk[u] = p.K[ww[u]];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const uint64_t a = key_lo(kk[u], (uint32_t)ww[u]), b = key_hi(kk[u], (uint32_t)ww[u]);
+                    k1 = a < k1 ? a : k1;
+                    k2 = b < k2 ? b : k2;
+                }
+            }
+            k1 = nt_min<NT>(sm, k1);
+            k2 = nt_min<NT>(sm, k2);
+            const uint32_t kmin = (uint32_t)(k1 >> 32);
+            mf = (kmin == 0u || kmin == 0xffffffffu) ? kM_OUT : (uint32_t)k1 + 1u;
+            exact = kmin != 0u && kmin != 0xffffffffu && (uint32_t)k1 != ~(uint32_t)k2;  // a key tie
+        }
+        if (exact) {
+            uint64_t m = tid == 0 ? tv : kOUT;  // closed neighbourhood (Q1)
+            for (int64_t j = tid; j < len; j += (int64_t)NT * 8) {
+                int32_t ww[8];
+                uint64_t tt[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) ww[u] = x[min(j + (int64_t)u * NT, last)];
+#pragma unroll
+                for (int u = 0; u < 8; u++) tt[u] = p.T[ww[u]];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    m = tt[u] < m ? tt[u] : m;
+                    if (count_deg) dc += (j + (int64_t)u * NT <= last) & (tt[u] != kOUT) & ((int64_t)ww[u] != v);
+                }
+            }
+            m = nt_min<NT>(sm, m);
+            mf = m_field(m, p.id_mask);
+            if (count_deg) dc = nt_sum<NT>(sm, dc);
+        }
+        if (PUSH) {
+            if (mf == kM_OUT) {  // mark N[v] (push-form Decide)
+                for (int64_t j = tid; j < len; j += NT) p.oflag[x[j]] = 1;
+                if (tid == 0) p.oflag[v] = 1;
+            } else if (tid == 0) {
+                atomicAdd(&p.cnt[(int64_t)(mf - 1u) - p.gbase], 1u);
+            }
+            if (count_deg && tid == 0) p.degc[v] = (uint32_t)dc + 1u;
+        }
+        if (tid == 0) {
+            p.M[v] = mf;
+            keep = mf != kM_OUT;
+        }
+    } else {
+        const uint32_t vid1 = (uint32_t)(p.gbase + v) + 1u;
+        int any_out = 0, all_eq = 1;
+        if (tid == 0) decide_acc(p.M[v], vid1, any_out, all_eq);
+        for (int64_t j = tid; j < len; j += (int64_t)NT * 8) {
+            uint32_t mm[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) mm[u] = p.M[x[min(j + (int64_t)u * NT, last)]];
+#pragma unroll
+            for (int u = 0; u < 8; u++) decide_acc(mm[u], vid1, any_out, all_eq);
+            if (any_out) break;  // the row is OUT whatever follows
+        }
+        any_out = nt_sum<NT>(sm, any_out) > 0;
+        all_eq = nt_sum<NT>(sm, !all_eq) == 0;
+        if (tid == 0) keep = decide_write(p, v, any_out, all_eq, it, fi_next);
+    }
+    return keep;
+}
+
+// Deferred long rows, stats flush, survivor count.  Warps take deferred rows
+// from a shared counter and reduce one row each; rows longer than
+// kHugeRow are reduced afterwards by the whole block, one at a time.
+constexpr int kHugeRow = 32768;
 template <bool STATS, int PH, bool PUSH>
 __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, int32_t* lout, uint64_t fi_next,
                             Stat& st) {
-    const int t = threadIdx.x;
+    const int t = threadIdx.x, lane = t & 31;
     const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
     __syncthreads();
     const int nh = sm.hcount;
@@ -526,211 +644,34 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         dbuf[60] = (long long)ns;
         dbuf[61] = nh;
     }
-    char* base_ptr = reinterpret_cast<char*>(sm.buf[0]);
-    int64_t* pref = reinterpret_cast<int64_t*>(base_ptr);              // [kMB + 1]
-    int64_t* rs = pref + (kMB + 1);                                  // [kMB] row starts
-    unsigned long long* acc = reinterpret_cast<unsigned long long*>(rs + kMB);  // [kMB] PH 0 min (word or key_lo)
-    int32_t* rv = reinterpret_cast<int32_t*>(acc + kMB);             // [kMB] rows
-    int32_t* anyo = rv + kMB;                                        // [kMB] PH 1 exists OUT / PH 0 push flag
-    int32_t* alle = anyo + kMB;                                      // [kMB] PH 1 forall equal / PH 0 degree
-    unsigned long long* acc2 = reinterpret_cast<unsigned long long*>(alle + kMB);  // [kMB] PH 0 key_hi min
-    const bool keys = PH == 0 && p.K && !(PUSH && it == 0 && p.labels);
-    for (int hb = 0; hb < nh; hb += kMB) {
-        const int cnt = min(kMB, nh - hb);
-        int64_t v = 0, s = 0, len = 0;
-        if (t < cnt) {
-            v = p.heavy[blo + hb + t];
-            s = p.rowptr[v];
-            len = p.rowptr[v + 1] - s;
-            rv[t] = (int32_t)v;
-            rs[t] = s;
-            if (PH == 0) {
-                const uint64_t tv = p.T[v];  // closed neighbourhood (Q1)
-                if (keys) {
-                    acc[t] = key_lo(kkey(tv), (uint32_t)v);
-                    acc2[t] = key_hi(kkey(tv), (uint32_t)v);
-                } else {
-                    acc[t] = tv;
-                }
-                if (PUSH) alle[t] = 0;  // active-neighbour count (iteration 0)
-            } else {
-                const uint32_t mv = p.M[v];
-                const uint32_t vid1 = (uint32_t)(p.gbase + v) + 1u;
-                anyo[t] = (mv == kM_OUT);
-                alle[t] = (mv == vid1) | (mv == 0u);
-            }
-            if (STATS) stat_row<STATS>(p, tag, v, true, len, st);
-        }
-        // exclusive prefix of the lengths (int64)
-        {
-            const int lane = t & 31, warp = t >> 5;
-            long long inc = len;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const long long y = __shfl_up_sync(kFull, inc, off);
-                if (lane >= off) inc += y;
-            }
-            if (lane == 31) sm.red64[warp] = (uint64_t)inc;
-            __syncthreads();
-            long long wb = 0, tot = 0;
-#pragma unroll
-            for (int w = 0; w < kMW; w++) {
-                wb += (w < warp) ? (long long)sm.red64[w] : 0;
-                tot += (long long)sm.red64[w];
-            }
-            pref[t] = wb + inc - len;
-            if (t == 0) pref[kMB] = tot;
-            __syncthreads();
-        }
-        const int64_t total = pref[kMB];
-        // Each thread takes 8 consecutive entries per round and keeps a
-        // running accumulator for its current row; one shared atomic per row
-        // change (a hub row is reduced almost entirely in registers).
-        // use_keys: PH 0 on keys; only_rows: restrict to rows with rv_mask set
-        // (the exact re-pass of key ties, anyo[] marks them).
-        auto flat_pass = [&](bool use_keys, bool only_marked) {
-            int cur = -1;
-            uint64_t cmin = kOUT, cmin2 = kOUT;
-            int cany = 0, call = 1, cdeg = 0;
-            const bool count_deg = PUSH && PH == 0 && it == 0 && p.labels && !only_marked;
-            auto flush = [&]() {
-                if (cur < 0) return;
-                if (PH == 0) {
-                    if (cmin < acc[cur]) atomicMin(&acc[cur], (unsigned long long)cmin);
-                    if (use_keys && cmin2 < acc2[cur]) atomicMin(&acc2[cur], (unsigned long long)cmin2);
-                    if (count_deg && cdeg) atomicAdd(&alle[cur], cdeg);
-                } else {
-                    if (cany) anyo[cur] = 1;
-                    if (!call) alle[cur] = 0;
-                }
-            };
-            for (int64_t c = (int64_t)t * 8; c < total; c += (int64_t)kMB * 8) {
-                int r = 0;
-                {
-                    int lo = 0, hi = cnt;  // last row with pref[row] <= c
-                    while (hi - lo > 1) {
-                        const int mid = (lo + hi) >> 1;
-                        if (pref[mid] <= c) lo = mid; else hi = mid;
-                    }
-                    r = lo;
-                }
-                int32_t rr[8], ww[8];
-#pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const int64_t idx = c + u;
-                    rr[u] = -1;
-                    ww[u] = 0;
-                    if (idx < total) {
-                        while (pref[r + 1] <= idx) r++;
-                        if (!only_marked || anyo[r]) {
-                            rr[u] = r;
-                            ww[u] = p.colinds[rs[r] + (idx - pref[r])];
-                        }
-                    }
-                }
-                if (PH == 0) {
-                    uint64_t tv[8];
-                    if (use_keys) {
-#pragma unroll
-                        for (int u = 0; u < 8; u++) tv[u] = rr[u] >= 0 ? (uint64_t)p.K[ww[u]] : 0xffffffffull;
-                    } else {
-#pragma unroll
-                        for (int u = 0; u < 8; u++) tv[u] = rr[u] >= 0 ? p.T[ww[u]] : kOUT;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; u++) {
-                        if (rr[u] < 0) continue;
-                        if (rr[u] != cur) {
-                            flush();
-                            cur = rr[u];
-                            cmin = kOUT;
-                            cmin2 = kOUT;
-                            cdeg = 0;
-                        }
-                        if (use_keys) {
-                            const uint64_t a = key_lo((uint32_t)tv[u], (uint32_t)ww[u]);
-                            const uint64_t b = key_hi((uint32_t)tv[u], (uint32_t)ww[u]);
-                            cmin = a < cmin ? a : cmin;
-                            cmin2 = b < cmin2 ? b : cmin2;
-                        } else {
-                            cmin = tv[u] < cmin ? tv[u] : cmin;
-                            if (count_deg) cdeg += (tv[u] != kOUT) & (ww[u] != rv[cur]);
-                        }
-                    }
-                } else {
-                    uint32_t mm[8];
-#pragma unroll
-                    for (int u = 0; u < 8; u++) mm[u] = rr[u] >= 0 ? p.M[ww[u]] : 0u;
-#pragma unroll
-                    for (int u = 0; u < 8; u++) {
-                        if (rr[u] < 0) continue;
-                        if (rr[u] != cur) {
-                            flush();
-                            cur = rr[u];
-                            cany = 0;
-                            call = 1;
-                        }
-                        const uint32_t vid1 = (uint32_t)(p.gbase + rv[cur]) + 1u;
-                        cany |= (mm[u] == kM_OUT);
-                        call &= (mm[u] == vid1) | (mm[u] == 0u);
-                    }
-                }
-                if (STATS && !only_marked) {
-#pragma unroll
-                    for (int u = 0; u < 8; u++)
-                        if (rr[u] >= 0 && atomicMax(&p.mark[ww[u]], tag) < tag) st.d++;
-                }
-            }
-            flush();
-            __syncthreads();
-        };
-        flat_pass(keys, false);
-        if (keys) {  // key ties: the full words of those rows decide
-            int tie = 0;
-            if (t < cnt) {
-                const uint32_t kmin = (uint32_t)(acc[t] >> 32);
-                tie = kmin != 0u && kmin != 0xffffffffu && (uint32_t)acc[t] != ~(uint32_t)acc2[t];
-                anyo[t] = tie;
-                if (tie) acc[t] = p.T[v];
-            }
-            if (__syncthreads_or(tie)) flat_pass(false, true);
-        }
-        bool keep = false;
-        int any_push = 0;
-        if (t < cnt) {
-            if (PH == 0) {
-                uint32_t mf;
-                if (keys && !anyo[t]) {
-                    const uint32_t kmin = (uint32_t)(acc[t] >> 32);
-                    mf = (kmin == 0u || kmin == 0xffffffffu) ? kM_OUT : (uint32_t)acc[t] + 1u;
-                } else {
-                    mf = m_field(acc[t], p.id_mask);
-                }
-                p.M[v] = mf;
-                keep = (mf != kM_OUT);
-                if (PUSH) {
-                    anyo[t] = !keep;
-                    any_push = !keep;
-                    if (keep) atomicAdd(&p.cnt[(int64_t)(mf - 1u) - p.gbase], 1u);
-                    else p.oflag[v] = 1;
-                    if (it == 0 && p.labels) p.degc[v] = (uint32_t)alle[t] + 1u;
-                }
-            } else {
-                keep = decide_write(p, v, anyo[t], alle[t], it, fi_next);
-            }
-        }
-        append(sm, keep, (int32_t)v, lout, blo);
-        if (PUSH && PH == 0 && __syncthreads_or(any_push)) {  // push OUT along the rows whose M became OUT
-            for (int64_t c = t; c < total; c += kMB) {
-                int lo = 0, hi = cnt;
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (pref[mid] <= c) lo = mid; else hi = mid;
-                }
-                if (anyo[lo]) p.oflag[p.colinds[rs[lo] + (c - pref[lo])]] = 1;
-            }
+    int32_t* huge = sm.buf[0];  // rows for the whole block (<= nh <= the buffer)
+    if (nh > 0) {
+        if (t == 0) {
+            sm.hnext = 0;
+            sm.nhuge = 0;
         }
         __syncthreads();
+        for (;;) {
+            int i = 0;
+            if (lane == 0) i = atomicAdd(&sm.hnext, 1);
+            i = __shfl_sync(kFull, i, 0);
+            if (i >= nh) break;
+            const int64_t v = p.heavy[blo + i];
+            const int64_t len = p.rowptr[v + 1] - p.rowptr[v];
+            if (len > kHugeRow && nh <= 2 * kTileCap) {
+                if (lane == 0) huge[atomicAdd(&sm.nhuge, 1)] = (int32_t)v;
+                continue;
+            }
+            const bool keep = heavy_row<32, STATS, PH, PUSH>(sm, p, it, fi_next, v, st, tag);
+            append(sm, keep && lane == 0, (int32_t)v, lout, blo);
+        }
+        __syncthreads();
+        const int nb = sm.nhuge;
+        for (int k = 0; k < nb; k++) {
+            const int64_t v = huge[k];
+            const bool keep = heavy_row<kMB, STATS, PH, PUSH>(sm, p, it, fi_next, v, st, tag);
+            append(sm, keep && t == 0, (int32_t)v, lout, blo);
+        }
     }
     stats_flush<STATS>(p, it, PH == 0 ? 1 : 0, st);
     if (dbg) {
