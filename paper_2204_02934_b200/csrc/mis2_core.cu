@@ -49,12 +49,20 @@ constexpr int kMinBlocksPerSM = kMW >= 16 ? 1 : 4;
 constexpr int kTileCap = (kMB >= 512 ? kMB / 2 : kMB) * 27;
 // rows longer than 8 gather batches of their lane group are deferred and
 // reduced by the whole block (flattened over all deferred rows of the block)
+// independent gathers per lane per batch of the row loops
+#ifndef MIS2_B1
+#define MIS2_B1 9  // measured: 9 is best on C2 (27 entries = 3 batches, 373 us vs 388 at 16) and near-best on C3
+#endif
+template <int G>
+__host__ __device__ constexpr int gather_batch() {
+    return G == 1 ? MIS2_B1 : (G == 2 ? 16 : (G == 4 ? 8 : 4));
+}
 #ifndef MIS2_HEAVY_BATCHES
 #define MIS2_HEAVY_BATCHES 8
 #endif
 template <int G>
 __host__ __device__ constexpr int heavy_len() {
-    return MIS2_HEAVY_BATCHES * G * (G <= 2 ? 16 : (G == 4 ? 8 : 4));
+    return MIS2_HEAVY_BATCHES * G * gather_batch<G>();
 }
 constexpr int kDenseNum = 3, kDenseDen = 8;  // dense if |worklist segment| >= 3/8 of the range (pull phases)
 // M_v is only ever compared against T_v (Decide: "M_w = T_v", "M_w = OUT").
@@ -260,7 +268,7 @@ __device__ __forceinline__ void stats_flush(const MisParams& p, int it, int slot
 template <int G>
 __device__ __forceinline__ uint64_t row_min(const uint64_t* __restrict__ T, const int32_t* x, int len, int sub,
                                             uint64_t m) {
-    constexpr int B = G <= 2 ? 16 : (G == 4 ? 8 : 4);
+    constexpr int B = gather_batch<G>();
     const int last = len - 1;
     for (int j = sub; j < len; j += B * G) {
         uint64_t tt[B];
@@ -279,7 +287,7 @@ __device__ __forceinline__ uint64_t row_min(const uint64_t* __restrict__ T, cons
 template <int G>
 __device__ __forceinline__ uint64_t row_min_deg(const uint64_t* __restrict__ T, const int32_t* x, int len, int sub,
                                                 uint64_t m, int64_t self, int& dc) {
-    constexpr int B = G <= 2 ? 16 : (G == 4 ? 8 : 4);
+    constexpr int B = gather_batch<G>();
     const int last = len - 1;
     for (int j = sub; j < len; j += B * G) {
         uint64_t tt[B];
@@ -309,7 +317,7 @@ __device__ __forceinline__ uint64_t key_hi(uint32_t k, uint32_t w) { return ((ui
 template <int G>
 __device__ __forceinline__ void row_min_keys(const uint32_t* __restrict__ K, const int32_t* x, int len, int sub,
                                              uint64_t& k1, uint64_t& k2) {
-    constexpr int B = G <= 2 ? 16 : (G == 4 ? 8 : 4);
+    constexpr int B = gather_batch<G>();
     const int last = len - 1;
     for (int j = sub; j < len; j += B * G) {
         uint32_t kk[B];
@@ -338,7 +346,7 @@ __device__ __forceinline__ void decide_acc(uint32_t m, uint32_t vid1, int& any_o
 template <int G>
 __device__ __forceinline__ void row_decide(const uint32_t* __restrict__ M, const int32_t* x, int len, int sub,
                                            uint32_t vid1, int& any_out, int& all_eq) {
-    constexpr int B = G <= 2 ? 16 : (G == 4 ? 8 : 4);
+    constexpr int B = gather_batch<G>();
     const int last = len - 1;
     for (int j = sub; j < len; j += B * G) {
         uint32_t mm[B];
