@@ -53,9 +53,12 @@ constexpr int kTileCap = (kMB >= 512 ? kMB / 2 : kMB) * 27;
 #ifndef MIS2_B1
 #define MIS2_B1 9  // measured: 9 is best on C2 (27 entries = 3 batches, 373 us vs 388 at 16) and near-best on C3
 #endif
+#ifndef MIS2_B4
+#define MIS2_B4 11  // measured on C5 (81-entry rows over 4 lanes = 2 batches): 7.95 ms vs 8.24 at 8
+#endif
 template <int G>
 __host__ __device__ constexpr int gather_batch() {
-    return G == 1 ? MIS2_B1 : (G == 2 ? 16 : (G == 4 ? 8 : 4));
+    return G == 1 ? MIS2_B1 : (G == 2 ? 16 : (G == 4 ? MIS2_B4 : 4));
 }
 #ifndef MIS2_HEAVY_BATCHES
 #define MIS2_HEAVY_BATCHES 8
