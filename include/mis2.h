@@ -71,8 +71,9 @@ extern "C" {
 #define MIS2_FLAG_PULL_DECIDE 0x10u /* force the pull form (Alg. 1 as written).  Never changes results. */
 #define MIS2_FLAG_KEYS 0x20u     /* use 32-bit column keys (top 32 bits of the status word, ties
                                     resolved on the full words): half the gather bytes, for
-                                    random-access graphs whose status words exceed L2; off by
-                                    default.  Never changes results. */
+                                    random-access graphs whose status words exceed L2.  Default:
+                                    used iff 8n > 64 MB and the largest degree exceeds 16x the
+                                    average.  Never changes results. */
 #define MIS2_FLAG_NO_KEYS 0x40u  /* never use the 32-bit column keys.  Never changes results. */
 #define MIS2_FLAG_TIMELINE 0x2u  /* measurement aid: mis2()'s `stats` receives int64 device
                                     timestamps (ns, %globaltimer) taken by block 0 after

@@ -89,7 +89,8 @@ struct MisParams {
     const int32_t* __restrict__ labels;  // phase-2 mask (active iff labels[v] < 0) or null
     uint64_t* T;                         // row status T_v (64-bit packed word, Eq. 1)
     uint32_t* M;                         // column status M_v, stored as its id field (see below)
-    uint32_t* K;                         // 32-bit column keys of T (kkey) or null (KEYS kernels only)
+    uint32_t* K;                         // 32-bit column keys of T (kkey), maintained when non-null
+    int keys_mode;                       // K non-null: 1 = use the keys, 0 = use them iff the degrees are skewed
     uint32_t id_mask;                    // 2^b - 1
     int32_t* L1[2];                      // worklist_1, double buffered, per-block segments
     int32_t* L2[2];                      // worklist_2
@@ -111,6 +112,10 @@ struct MisParams {
     int32_t* d_iters;
     int32_t* d_status;
 };
+
+// per block: the column passes use the 32-bit keys (decided once per call,
+// after the init phase; see the kernel)
+__shared__ int s_use_keys;
 
 struct __align__(16) TileSmem {
     int32_t buf[2][kTileCap + 8];
@@ -436,7 +441,7 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
     if (PH == 0) {
         uint32_t mf;
         int dc = 0;
-        if (p.K && !(PUSH && it == 0 && p.labels)) {
+        if (p.K && s_use_keys && !(PUSH && it == 0 && p.labels)) {
             // keys (single GPU: local ids are global ids)
             uint64_t k1 = ~0ull, k2 = ~0ull;
             if (act && sub == 0) {  // closed neighbourhood (Q1)
@@ -558,7 +563,7 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
     if (PH == 0) {
         const uint64_t tv = p.T[v];
         const bool count_deg = PUSH && it == 0 && p.labels;
-        const bool keys = p.K && !count_deg;
+        const bool keys = p.K && s_use_keys && !count_deg;
         uint32_t mf;
         int dc = 0;
         bool exact = !keys;
@@ -1129,6 +1134,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
     {
         const uint64_t fi0 = p.prio.iter_term(0);
         int act_cnt = 0;
+        int64_t maxdeg = 0;
         for (int64_t v = blo + t; v < bhi; v += kMB) {
             const bool act = p.labels ? (p.labels[v] < 0) : true;
             set_T(p, v, act ? p.prio.word(0, fi0, p.gbase + v) : kOUT);
@@ -1136,13 +1142,27 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
             p.oflag[v] = 0;
             p.cnt[v] = 0u;
             act_cnt += act;
+            if (p.K && !p.keys_mode) maxdeg = max(maxdeg, p.rowptr[v + 1] - p.rowptr[v]);
         }
         const long long s = block_sum_int(sm, act_cnt);
         if (t == 0 && s) atomicAdd(&p.ctrl[7], (unsigned long long)s);
+        if (p.K && !p.keys_mode) {
+            const uint64_t bm = ~block_min_u64(sm, ~(uint64_t)maxdeg);  // block max
+            if (t == 0 && bm) atomicMax(&p.ctrl[8], (unsigned long long)bm);
+        }
     }
     grid_barrier(bar);
     stamp(p, 0);
     const unsigned long long n_active = ld_acquire_u64(&p.ctrl[7]);
+    // 32-bit column keys for skewed degree distributions: random neighbour
+    // ids gather from all of T, which does not stay in L2 (C4); on meshes the
+    // extra key arithmetic costs more than the halved bytes save
+    if (t == 0) {
+        int use = 0;
+        if (p.K) use = p.keys_mode ? 1 : (double)ld_acquire_u64(&p.ctrl[8]) > 16.0 * (double)p.nnz / (double)p.n;
+        s_use_keys = use;
+    }
+    __syncthreads();
 
     int it = 0;
     int status = MIS2_OK;
@@ -1523,16 +1543,19 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     p.labels = labels;
     p.T = w.T;
     p.M = w.M;
-    // 32-bit column keys: off by default -- the two 64-bit minima per entry
-    // cost more ALU than the halved gather bytes save on the stencil configs
-    // (C2 387 -> 451 us, C3 5.6 -> 6.5 ms, C5 8.2 -> 10.1 ms); they help only
-    // random-access graphs whose T does not fit L2 (C4 101 -> 86 ms).
+    // 32-bit column keys: the two 64-bit minima per entry cost more ALU than
+    // the halved gather bytes save on the stencil configs (C2 387 -> 451 us,
+    // C3 5.6 -> 6.5 ms, C5 8.2 -> 10.1 ms); they help random-access graphs
+    // whose T does not fit L2 (C4 92 -> 77 ms).  Automatic: candidates are
+    // graphs with 8n > 64 MB; the kernel then uses the keys iff the largest
+    // degree exceeds 16x the average (skewed, random access).
     // MIS2_FLAG_KEYS / MIS2_FLAG_NO_KEYS force (results identical).
-    bool keys = false;
-    if (o.flags & MIS2_FLAG_KEYS) keys = true;
-    if (o.flags & MIS2_FLAG_NO_KEYS) keys = false;
-    if (const char* e = getenv("MIS2_KEYS")) keys = atoi(e) != 0;  // measurement knob
+    int keys = (double)g.n * 8.0 > 64.0 * 1048576.0 ? 2 : 0;  // 2 = decide on the device
+    if (o.flags & MIS2_FLAG_KEYS) keys = 1;
+    if (o.flags & MIS2_FLAG_NO_KEYS) keys = 0;
+    if (const char* e = getenv("MIS2_KEYS")) keys = atoi(e);  // measurement knob
     p.K = keys ? w.K : nullptr;
+    p.keys_mode = keys == 1 ? 1 : 0;
     for (int i = 0; i < 2; i++) {
         p.L1[i] = w.L1[i];
         p.L2[i] = w.L2[i];
