@@ -145,7 +145,10 @@ __global__ void k_iota(int64_t n, int32_t* __restrict__ x, int64_t* __restrict__
     }
 }
 
-// One colour of a sweep: a warp per cluster of the colour.
+// One colour of a sweep: a warp per cluster of the colour.  The structure
+// of the next row (its index, bounds, first 32 column ids and values, b_i,
+// A_ii) is loaded while the current row gathers x, so a row costs one
+// dependent gather + the lane reduction.
 __global__ void k_cgs_color(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colinds,
                             const double* __restrict__ vals, const double* __restrict__ diag,
                             const int64_t* __restrict__ cptr, const int32_t* __restrict__ crows,
@@ -155,16 +158,45 @@ __global__ void k_cgs_color(const int64_t* __restrict__ rowptr, const int32_t* _
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t k = set_lo + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < set_hi; k += nw) {
         const int32_t a = cset[k];
-        const int64_t r0 = cptr[a], r1 = cptr[a + 1];
-        for (int64_t t = 0; t < r1 - r0; t++) {
-            const int64_t i = crows[backward ? r1 - 1 - t : r0 + t];
-            const int64_t s = rowptr[i], e = rowptr[i + 1];
-            double acc = 0.0;
-            for (int64_t j = s + lane; j < e; j += 32) acc += vals[j] * x[colinds[j]];
+        const int64_t r0 = cptr[a], r1 = cptr[a + 1], nr = r1 - r0;
+        auto row_at = [&](int64_t t) { return (int64_t)crows[backward ? r1 - 1 - t : r0 + t]; };
+        // structure of row t (lane-distributed first 32 entries)
+        int64_t i = 0, s = 0, e = 0;
+        int32_t cj = 0;
+        double vj = 0.0, bi = 0.0, di = 1.0;
+        auto load = [&](int64_t t, int64_t& ii, int64_t& ss, int64_t& ee, int32_t& c, double& v, double& bb,
+                        double& dd) {
+            ii = row_at(t);
+            ss = rowptr[ii];
+            ee = rowptr[ii + 1];
+            c = 0;
+            v = 0.0;
+            if (ss + lane < ee) {
+                c = colinds[ss + lane];
+                v = vals[ss + lane];
+            }
+            bb = b[ii];
+            dd = diag[ii];
+        };
+        if (nr > 0) load(0, i, s, e, cj, vj, bi, di);
+        for (int64_t t = 0; t < nr; t++) {
+            int64_t i2 = 0, s2 = 0, e2 = 0;
+            int32_t cj2 = 0;
+            double vj2 = 0.0, bi2 = 0.0, di2 = 1.0;
+            if (t + 1 < nr) load(t + 1, i2, s2, e2, cj2, vj2, bi2, di2);
+            double acc = (s + lane < e) ? vj * x[cj] : 0.0;
+            for (int64_t j = s + 32 + lane; j < e; j += 32) acc += vals[j] * x[colinds[j]];
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
-            if (lane == 0) x[i] = x[i] + (b[i] - acc) / diag[i];
+            if (lane == 0) x[i] = x[i] + (bi - acc) / di;
             __syncwarp();
+            i = i2;
+            s = s2;
+            e = e2;
+            cj = cj2;
+            vj = vj2;
+            bi = bi2;
+            di = di2;
         }
     }
 }
