@@ -88,6 +88,20 @@ def test_group_width_invariance(group, decide):
 
 @pytest.mark.parametrize("keys", ["on", "off"])
 @pytest.mark.parametrize("decide", ["pull", "push"])
+def test_huge_rows_block_path(decide, keys):
+    """Rows beyond a warp's share (> 32768 entries) are reduced by the whole
+    block (finish_phase): two hubs joined to a sparse random graph."""
+    n = 90000
+    rng = np.random.default_rng(5)
+    e = [(0, j) for j in range(1, 40001)] + [(1, j) for j in range(30000, 75000)]
+    e += [tuple(x) for x in rng.integers(2, n, size=(60000, 2)) if x[0] != x[1]]
+    g = G.from_edges(n, e)
+    check_mis2(g, decide=decide, keys=keys)
+    check_mis2(g, decide=decide, keys=keys, seed=3)
+
+
+@pytest.mark.parametrize("keys", ["on", "off"])
+@pytest.mark.parametrize("decide", ["pull", "push"])
 def test_column_keys(decide, keys):
     """32-bit column keys (ties in the key class resolved on the full words)
     on random / power-law / stencil graphs, every lane-group width, hub rows;
