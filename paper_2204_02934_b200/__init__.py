@@ -283,12 +283,16 @@ def coarsen(rowptr, colinds, labels, num_aggs: int):
     crow = torch.empty(num_aggs + 1, dtype=torch.int64, device=rowptr.device)
     cnnz = ctypes.c_int64(0)
     L = lib()
-    rc = L.mis2_coarsen(ctypes.byref(g), labels.data_ptr(), num_aggs, crow.data_ptr(), None, 0, ctypes.byref(cnnz),
-                        ws.data_ptr(), wsb, _stream())
-    _check(rc, "mis2_coarsen(count)", allow=(ERANGE,))
-    ccol = torch.empty(max(cnnz.value, 1), dtype=torch.int32, device=rowptr.device)
-    rc = L.mis2_coarsen(ctypes.byref(g), labels.data_ptr(), num_aggs, crow.data_ptr(), ccol.data_ptr(),
-                        ccol.numel(), ctypes.byref(cnnz), ws.data_ptr(), wsb, _stream())
+    # one call with a capacity guess (coarse graphs are far sparser than the
+    # fine one); the two-call convention (MIS2_ERANGE + exact size) otherwise
+    cap = max(4096, min(nnz, num_aggs * num_aggs), nnz // 8) if nnz else 1
+    ccol = torch.empty(cap, dtype=torch.int32, device=rowptr.device)
+    rc = L.mis2_coarsen(ctypes.byref(g), labels.data_ptr(), num_aggs, crow.data_ptr(), ccol.data_ptr(), cap,
+                        ctypes.byref(cnnz), ws.data_ptr(), wsb, _stream())
+    if rc == ERANGE:
+        ccol = torch.empty(max(cnnz.value, 1), dtype=torch.int32, device=rowptr.device)
+        rc = L.mis2_coarsen(ctypes.byref(g), labels.data_ptr(), num_aggs, crow.data_ptr(), ccol.data_ptr(),
+                            ccol.numel(), ctypes.byref(cnnz), ws.data_ptr(), wsb, _stream())
     _check(rc, "mis2_coarsen")
     return crow, ccol[: cnnz.value]
 

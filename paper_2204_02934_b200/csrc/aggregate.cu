@@ -168,7 +168,68 @@ __global__ void k_phase3(int64_t n, const int64_t* __restrict__ rowptr, const in
     if (left) { s = rowptr[v]; e = rowptr[v + 1]; }
     const bool is_heavy = left && (e - s) > kHeavyDeg;
     int bc = 0, bs = 0, ba = -1;
-    if (left && !is_heavy) {
+    bool done = false;
+    if (G == 1 && left && !is_heavy) {
+        // one pass: the distinct candidate aggregates and their couplings
+        // in registers (a leftover sees few aggregates); more than 8 -> the
+        // quadratic pass below
+        int32_t lab[8];
+        int cnt[8];
+        int nl = 0;
+        bool overflow = false;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            lab[q] = -1;
+            cnt[q] = 0;
+        }
+        for (int64_t j0 = s; j0 < e; j0 += 8) {
+            int32_t aa[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int64_t j = j0 + u;
+                aa[u] = -1;
+                if (j < e) {
+                    const int32_t w = colinds[j];
+                    aa[u] = (w != v) ? tent[w] : -1;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int32_t a = aa[u];
+                if (a < 0) continue;
+                bool found = false;
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    if (lab[q] == a) {
+                        cnt[q]++;
+                        found = true;
+                    }
+                if (!found) {
+                    if (nl < 8) {
+#pragma unroll
+                        for (int q = 0; q < 8; q++)
+                            if (q == nl) {
+                                lab[q] = a;
+                                cnt[q] = 1;
+                            }
+                        nl++;
+                    } else {
+                        overflow = true;
+                    }
+                }
+            }
+        }
+        if (!overflow) {
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+                if (q < nl) {
+                    const int sz = size[lab[q]];
+                    if (better(cnt[q], sz, lab[q], bc, bs, ba)) { bc = cnt[q]; bs = sz; ba = lab[q]; }
+                }
+            done = true;
+        }
+    }
+    if (left && !is_heavy && !done) {
         for (int64_t j = s + sub; j < e; j += G) {
             const int32_t u = colinds[j];
             const int32_t a = (u != v) ? tent[u] : -1;

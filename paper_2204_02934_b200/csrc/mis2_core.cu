@@ -1130,21 +1130,45 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
     }
     uint32_t ph = 0u;  // mbarrier phase bits: 0,1 dense buffers; 2,3 sparse buffers
 
-    // worklists <- 0..|V|; Refresh Row of iteration 0
+    // worklists <- 0..|V|; Refresh Row of iteration 0.
+    // A masked call (phase 2 of Alg. 3) also lists its active rows, so its
+    // first passes can be sparse (the active rows are a small fraction).
+    int act_block = 0;
     {
         const uint64_t fi0 = p.prio.iter_term(0);
         int act_cnt = 0;
         int64_t maxdeg = 0;
-        for (int64_t v = blo + t; v < bhi; v += kMB) {
-            const bool act = p.labels ? (p.labels[v] < 0) : true;
-            set_T(p, v, act ? p.prio.word(0, fi0, p.gbase + v) : kOUT);
-            p.M[v] = act ? kPending : 0u;  // 0 = inactive sentinel (reading Q15)
-            p.oflag[v] = 0;
-            p.cnt[v] = 0u;
+        if (t == 0) sm.cnt = 0;
+        __syncthreads();
+        for (int64_t base = blo; base < bhi; base += kMB) {
+            const int64_t v = base + t;
+            const bool in = v < bhi;
+            const bool act = in && (p.labels ? (p.labels[v] < 0) : true);
+            if (in) {
+                set_T(p, v, act ? p.prio.word(0, fi0, p.gbase + v) : kOUT);
+                p.M[v] = act ? kPending : 0u;  // 0 = inactive sentinel (reading Q15)
+                p.oflag[v] = 0;
+                p.cnt[v] = 0u;
+                if (p.K && !p.keys_mode) maxdeg = max(maxdeg, p.rowptr[v + 1] - p.rowptr[v]);
+            }
             act_cnt += act;
-            if (p.K && !p.keys_mode) maxdeg = max(maxdeg, p.rowptr[v + 1] - p.rowptr[v]);
+            if (p.labels) {  // worklist_1 = worklist_2 = the active rows
+                const unsigned ball = __ballot_sync(kFull, act);
+                if (ball) {
+                    const int lane = t & 31, leader = __ffs(ball) - 1;
+                    int pos = 0;
+                    if (lane == leader) pos = atomicAdd(&sm.cnt, __popc(ball));
+                    pos = __shfl_sync(kFull, pos, leader);
+                    if (act) {
+                        const int64_t at = blo + pos + __popc(ball & lanemask_lt());
+                        p.L1[0][at] = (int32_t)v;
+                        p.L2[0][at] = (int32_t)v;
+                    }
+                }
+            }
         }
         const long long s = block_sum_int(sm, act_cnt);
+        act_block = (int)s;
         if (t == 0 && s) atomicAdd(&p.ctrl[7], (unsigned long long)s);
         if (p.K && !p.keys_mode) {
             const uint64_t bm = ~block_min_u64(sm, ~(uint64_t)maxdeg);  // block max
@@ -1167,12 +1191,13 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
     int it = 0;
     int status = MIS2_OK;
     const int64_t range = bhi - blo;
-    int cnt1 = (int)range, cnt2 = (int)range;  // this block's worklist segment sizes
+    // this block's worklist segment sizes (a masked call starts from its lists)
+    int cnt1 = p.labels ? act_block : (int)range, cnt2 = cnt1;
     while (n_active > 0) {  // while worklist_1 != {}
         const int cur = it & 1;
         // ---- Refresh Column over worklist_2
         const bool push = PUSH && it < p.push_iters;
-        const bool dense2 = (it == 0) || (int64_t)cnt2 * kDenseDen >= range * kDenseNum;
+        const bool dense2 = (it == 0 && !p.labels) || (int64_t)cnt2 * kDenseDen >= range * kDenseNum;
         if (push) {
             cnt2 = dense2 ? dense_phase<G, STATS, 0, PUSH>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0)
                           : sparse_phase<G, STATS, 0, PUSH>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
@@ -1184,7 +1209,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         stamp(p, 1 + 2 * it);
         // ---- Decide over worklist_1 + fused refresh of iteration it+1
         const uint64_t fi_next = p.prio.iter_term(it + 1);
-        const bool dense1 = (it == 0) || (int64_t)cnt1 * kDenseDen >= range * kDenseNum;
+        const bool dense1 = (it == 0 && !p.labels) || (int64_t)cnt1 * kDenseDen >= range * kDenseNum;
         if (push) cnt1 = decide_push<STATS>(sm, p, it, blo, bhi, p.L1[cur], cnt1, dense1, p.L1[cur ^ 1], fi_next);
         else if (dense1) cnt1 = dense_phase<G, STATS, 1>(sm, p, it, blo, bhi, p.L1[cur ^ 1], ph, fi_next);
         else cnt1 = sparse_phase<G, STATS, 1>(sm, p, it, blo, p.L1[cur], cnt1, p.L1[cur ^ 1], ph, fi_next);
