@@ -22,6 +22,8 @@ enum AggErr : int { kErrTwoRoots = 1, kErrPhase2Conflict = 2, kErrNoCandidate = 
 
 #define ROWS_END }
 
+constexpr int kBatch = 8;  // gathers in flight per lane (row_batched)
+
 // Phase 1: roots = MIS-2; every root and its neighbours get the
 // root's id (pull form: each vertex looks for its unique root neighbour).
 template <int G>
@@ -32,16 +34,15 @@ __global__ void k_phase1(int64_t n, const int64_t* __restrict__ rowptr, const in
     int found = -1;
     int bad = 0;
     const bool root = valid && in1[v];
-    if (valid && !root) {
-        for (int64_t j = rowptr[v] + sub; j < rowptr[v + 1]; j += G) {
-            const int32_t w = colinds[j];
-            if (w != v && in1[w]) {
-                const int r = rid[w];
-                if (found >= 0 && found != r) bad = 1;
-                found = r;
-            }
-        }
-    }
+    if (valid && !root)
+        row_batched<G, kBatch>(rowptr[v], rowptr[v + 1], sub, colinds, [&](int32_t w) { return in1[w]; },
+                               [&](int32_t w, uint8_t x) {
+                                   if (w != v && x) {
+                                       const int r = rid[w];
+                                       if (found >= 0 && found != r) bad = 1;
+                                       found = r;
+                                   }
+                               });
     // combine: all lanes that found a root must agree (roots are >= 3 apart)
     int mx = found, mn = found < 0 ? 0x7fffffff : found;
 #pragma unroll
@@ -72,10 +73,8 @@ __global__ void k_phase2_accept(int64_t n, const int64_t* __restrict__ rowptr,
     const bool r = valid && in2[v];
     int cnt = 0;
     if (r)
-        for (int64_t j = rowptr[v] + sub; j < rowptr[v + 1]; j += G) {
-            const int32_t w = colinds[j];
-            cnt += (w != v && labels[w] < 0);
-        }
+        row_batched<G, kBatch>(rowptr[v], rowptr[v + 1], sub, colinds, [&](int32_t w) { return labels[w]; },
+                               [&](int32_t w, int32_t x) { cnt += (w != v && x < 0); });
     cnt = group_sum<G>(cnt);
     if (valid && sub == 0) acc[v] = (r && cnt >= 2) ? 1 : 0;
     ROWS_END
@@ -94,13 +93,13 @@ __global__ void k_phase2_label(int64_t n, const int64_t* __restrict__ rowptr,
     const bool root = un && acc[v];
     int found = -1, bad = 0;
     if (un && !root)
-        for (int64_t j = rowptr[v] + sub; j < rowptr[v + 1]; j += G) {
-            const int32_t w = colinds[j];
-            if (w != v && acc[w]) {
-                if (found >= 0 && found != aid[w]) bad = 1;
-                found = aid[w];
-            }
-        }
+        row_batched<G, kBatch>(rowptr[v], rowptr[v + 1], sub, colinds, [&](int32_t w) { return acc[w]; },
+                               [&](int32_t w, uint8_t x) {
+                                   if (w != v && x) {
+                                       if (found >= 0 && found != aid[w]) bad = 1;
+                                       found = aid[w];
+                                   }
+                               });
     int mx = found, mn = found < 0 ? 0x7fffffff : found;
 #pragma unroll
     for (int off = G / 2; off > 0; off >>= 1) {
@@ -169,10 +168,12 @@ __global__ void k_phase3(int64_t n, const int64_t* __restrict__ rowptr, const in
     const bool is_heavy = left && (e - s) > kHeavyDeg;
     int bc = 0, bs = 0, ba = -1;
     bool done = false;
-    if (G == 1 && left && !is_heavy) {
-        // one pass: the distinct candidate aggregates and their couplings
-        // in registers (a leftover sees few aggregates); more than 8 -> the
-        // quadratic pass below
+    {
+        // one pass: each lane keeps the distinct candidate aggregates of its
+        // entries (stride G) and their couplings in registers (a leftover sees
+        // few aggregates); the group then adds up the lanes' counts by
+        // shuffles.  A lane with more than 8 -> the group takes the quadratic
+        // pass below.
         int32_t lab[8];
         int cnt[8];
         int nl = 0;
@@ -182,49 +183,66 @@ __global__ void k_phase3(int64_t n, const int64_t* __restrict__ rowptr, const in
             lab[q] = -1;
             cnt[q] = 0;
         }
-        for (int64_t j0 = s; j0 < e; j0 += 8) {
-            int32_t aa[8];
+        if (left && !is_heavy) {
+            for (int64_t j0 = s + sub; j0 < e; j0 += 8 * G) {
+                int32_t aa[8];
 #pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const int64_t j = j0 + u;
-                aa[u] = -1;
-                if (j < e) {
-                    const int32_t w = colinds[j];
-                    aa[u] = (w != v) ? tent[w] : -1;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const int32_t a = aa[u];
-                if (a < 0) continue;
-                bool found = false;
-#pragma unroll
-                for (int q = 0; q < 8; q++)
-                    if (lab[q] == a) {
-                        cnt[q]++;
-                        found = true;
+                for (int u = 0; u < 8; u++) {
+                    const int64_t j = j0 + (int64_t)u * G;
+                    aa[u] = -1;
+                    if (j < e) {
+                        const int32_t w = colinds[j];
+                        aa[u] = (w != v) ? tent[w] : -1;
                     }
-                if (!found) {
-                    if (nl < 8) {
+                }
 #pragma unroll
-                        for (int q = 0; q < 8; q++)
-                            if (q == nl) {
-                                lab[q] = a;
-                                cnt[q] = 1;
-                            }
-                        nl++;
-                    } else {
-                        overflow = true;
+                for (int u = 0; u < 8; u++) {
+                    const int32_t a = aa[u];
+                    if (a < 0) continue;
+                    bool found = false;
+#pragma unroll
+                    for (int q = 0; q < 8; q++)
+                        if (lab[q] == a) {
+                            cnt[q]++;
+                            found = true;
+                        }
+                    if (!found) {
+                        if (nl < 8) {
+#pragma unroll
+                            for (int q = 0; q < 8; q++)
+                                if (q == nl) {
+                                    lab[q] = a;
+                                    cnt[q] = 1;
+                                }
+                            nl++;
+                        } else {
+                            overflow = true;
+                        }
                     }
                 }
             }
         }
-        if (!overflow) {
+        int tot[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) tot[q] = cnt[q];
+#pragma unroll 1
+        for (int r = 1; r < G; r++) {
+            overflow |= __shfl_xor_sync(kFull, (int)overflow, r) != 0;
+#pragma unroll
+            for (int q2 = 0; q2 < 8; q2++) {
+                const int32_t l2 = __shfl_xor_sync(kFull, lab[q2], r);
+                const int c2 = __shfl_xor_sync(kFull, cnt[q2], r);
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    if (l2 >= 0 && lab[q] == l2) tot[q] += c2;
+            }
+        }
+        if (left && !is_heavy && !overflow) {
 #pragma unroll
             for (int q = 0; q < 8; q++)
                 if (q < nl) {
                     const int sz = size[lab[q]];
-                    if (better(cnt[q], sz, lab[q], bc, bs, ba)) { bc = cnt[q]; bs = sz; ba = lab[q]; }
+                    if (better(tot[q], sz, lab[q], bc, bs, ba)) { bc = tot[q]; bs = sz; ba = lab[q]; }
                 }
             done = true;
         }

@@ -5,12 +5,13 @@
 // Device pipeline (no global sort of all nnz keys):
 //   1. seglen[a] = sum of stored row lengths of a's members
 //   2. sptr = exclusive scan(seglen)
-//   3. every fine row u appends labels[adj(u)] (own label -> sentinel) into
-//      its aggregate's segment at an atomically reserved offset
-//   4. per segment: sort + unique in shared memory (warp-per-segment for
-//      <= 256 entries); longer segments: block-level shared-memory hash set of
-//      the distinct labels, then sort of the uniques; segments with more than
-//      2048 distinct labels use an na-bit bitmap (ordered compaction = sorted unique)
+//   3. every fine row u appends the distinct labels of adj(u) other than its
+//      own (per-lane register lists) into its aggregate's segment at an
+//      atomically reserved offset
+//   4. per segment: shared-memory hash set of the distinct labels, then the
+//      uniques in sorted order (warp per segment up to 4096 entries / 255
+//      distinct; else a block per segment up to 2047 distinct); segments with
+//      more distinct labels use an na-bit bitmap (ordered compaction = sorted unique)
 //   5. c_rowptr = exclusive scan(unique counts); copy out.
 #include "common.cuh"
 #include "internal.h"
@@ -18,7 +19,6 @@
 namespace mis2k {
 
 constexpr int32_t kSent = 0x7fffffff;
-constexpr int kWarpSeg = 256;
 
 __global__ void k_check_labels(int64_t n, const int32_t* __restrict__ labels, int64_t na, int* err) {
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
@@ -35,6 +35,13 @@ __global__ void k_seglen(int64_t n, const int64_t* __restrict__ rowptr, const in
     }
 }
 
+// Each lane keeps the distinct labels (!= own) of its entries in a register
+// list of kFillList; a full list is flushed to the segment at an atomically
+// reserved offset.  Typical rows touch 2-4 aggregates, so the segments hold a
+// few entries per fine row instead of its degree (duplicates across lanes and
+// flushes remain; step 4 removes them).  A segment's used length is
+// cursor[a] - sptr[a] <= its capacity seglen[a].
+constexpr int kFillList = 8;
 template <int G>
 __global__ void k_fill(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colinds,
                        const int32_t* __restrict__ labels, unsigned long long* __restrict__ cursor,
@@ -46,21 +53,44 @@ __global__ void k_fill(int64_t n, const int64_t* __restrict__ rowptr, const int3
     for (int64_t base = gwarp * RPW; base < n; base += nwarps * RPW) {
         const int64_t v = base + grp;
         const bool valid = v < n;
-        int64_t s = 0, e = 0;
+        int32_t lst[kFillList];
+        int cnt = 0;
         int32_t a = 0;
-        unsigned long long pos = 0;
         if (valid) {
-            s = rowptr[v];
-            e = rowptr[v + 1];
+            const int64_t s = rowptr[v], e = rowptr[v + 1];
             a = labels[v];
-            if (sub == 0 && e > s) pos = atomicAdd(&cursor[a], (unsigned long long)(e - s));
+            row_batched<G, 8>(s, e, sub, colinds, [&](int32_t w) { return labels[w]; }, [&](int32_t, int32_t b) {
+                if (b == a) return;
+                bool found = false;
+#pragma unroll
+                for (int k = 0; k < kFillList; k++) found |= (k < cnt) && lst[k] == b;
+                if (found) return;
+                if (cnt == kFillList) {
+                    const unsigned long long pos = atomicAdd(&cursor[a], (unsigned long long)kFillList);
+#pragma unroll
+                    for (int k = 0; k < kFillList; k++) buf[pos + k] = lst[k];
+                    cnt = 0;
+                }
+#pragma unroll
+                for (int k = 0; k < kFillList; k++)
+                    if (k == cnt) lst[k] = b;
+                cnt++;
+            });
         }
-        pos = __shfl_sync(kFull, pos, lane - sub);
-        if (valid)
-            for (int64_t j = s + sub; j < e; j += G) {
-                const int32_t b = labels[colinds[j]];
-                buf[pos + (j - s)] = (b == a) ? kSent : b;
-            }
+        // one reservation per row for the lanes' final lists
+        int incl = cnt;
+#pragma unroll
+        for (int off = 1; off < G; off <<= 1) {
+            const int y = __shfl_up_sync(kFull, incl, off, G);
+            if (sub >= off) incl += y;
+        }
+        const int tot = __shfl_sync(kFull, incl, G - 1, G);
+        unsigned long long pos = 0;
+        if (sub == G - 1 && tot > 0) pos = atomicAdd(&cursor[a], (unsigned long long)tot);
+        pos = __shfl_sync(kFull, pos, G - 1, G) + (unsigned long long)(incl - cnt);
+#pragma unroll
+        for (int k = 0; k < kFillList; k++)
+            if (k < cnt) buf[pos + k] = lst[k];
     }
 }
 
@@ -80,60 +110,87 @@ __device__ __forceinline__ void bitonic(int32_t* x, int P, int tid, int nthreads
     }
 }
 
-// warp per segment, segments of <= kWarpSeg entries
-__global__ void k_sort_warp(int64_t na, const int64_t* __restrict__ sptr, int32_t* __restrict__ buf,
-                            int64_t* __restrict__ ucnt, int32_t* __restrict__ big, int* big_cnt) {
-    __shared__ int32_t sm[kWarpsPerBlock][kWarpSeg];
+// warp per segment: the distinct labels go through a per-warp shared-memory
+// hash set (a coarse row of a stencil graph has ~27 distinct neighbours
+// against ~60-100 segment entries), then each unique is placed by its rank
+// among the uniques (O(u) broadcast reads per unique).  Segments longer than
+// kWarpSegMax entries or with kWarpUniq or more distinct labels are marked
+// ucnt = -1 for the block kernel.
+constexpr int kWarpHash = 512;
+constexpr int kWarpUniq = 256;
+constexpr int64_t kWarpSegMax = 4096;
+__global__ void k_dedupe_warp(int64_t na, const int64_t* __restrict__ sptr, const unsigned long long* __restrict__ send,
+                              int32_t* __restrict__ buf, int64_t* __restrict__ ucnt) {
+    __shared__ int32_t hs[kWarpsPerBlock][kWarpHash];
+    __shared__ int32_t uqs[kWarpsPerBlock][kWarpUniq];
+    __shared__ int s_cnt[kWarpsPerBlock];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int32_t* x = sm[warp];
+    int32_t* h = hs[warp];
+    int32_t* uq = uqs[warp];
     const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
     for (int64_t a = (int64_t)blockIdx.x * kWarpsPerBlock + warp; a < na; a += nwarps) {
-        const int64_t s = sptr[a], len = sptr[a + 1] - s;
-        if (len > kWarpSeg) {
-            if (lane == 0) ucnt[a] = -1;  // handled by the block / bitmap kernels
+        const int64_t s = sptr[a], len = (int64_t)send[a] - s;
+        if (len > kWarpSegMax) {
+            if (lane == 0) ucnt[a] = -1;
             continue;
         }
-        int P = 1;
-        while (P < len) P <<= 1;
-        for (int i = lane; i < P; i += 32) x[i] = i < len ? buf[s + i] : kSent;
+        for (int i = lane; i < kWarpHash; i += 32) h[i] = -1;
+        if (lane == 0) s_cnt[warp] = 0;
         __syncwarp();
-        bitonic(x, P, lane, 32, true);
-        int c = 0;
-        for (int base = 0; base < P; base += 32) {
-            const int i = base + lane;
-            const int32_t xi = x[i < P ? i : 0];
-            const bool first = i < P && xi != kSent && (i == 0 || x[i - 1] != xi);
-            const unsigned ball = __ballot_sync(kFull, first);
-            if (first) buf[s + c + __popc(ball & lanemask_lt())] = xi;
-            c += __popc(ball);
+        for (int64_t j = lane; j < len; j += 32) {
+            if (*(volatile int*)&s_cnt[warp] >= kWarpUniq) break;  // overflow: block path
+            const int32_t b = buf[s + j];
+            uint32_t slot = ((uint32_t)b * 2654435761u) >> 23;  // 9-bit hash
+            for (;;) {
+                const int32_t prev = atomicCAS(&h[slot], -1, b);
+                if (prev == -1) {
+                    const int k = atomicAdd(&s_cnt[warp], 1);
+                    if (k < kWarpUniq) uq[k] = b;
+                    break;
+                }
+                if (prev == b) break;
+                slot = (slot + 1) & (kWarpHash - 1);
+            }
         }
-        if (lane == 0) ucnt[a] = c;
+        __syncwarp();
+        const int cnt = *(volatile int*)&s_cnt[warp];
+        if (cnt >= kWarpUniq) {
+            if (lane == 0) ucnt[a] = -1;
+            __syncwarp();
+            continue;
+        }
+        for (int i = lane; i < cnt; i += 32) {
+            const int32_t x = uq[i];
+            int r = 0;
+            for (int k = 0; k < cnt; k++) r += uq[k] < x;
+            buf[s + r] = x;
+        }
+        if (lane == 0) ucnt[a] = cnt;
         __syncwarp();
     }
-    (void)big; (void)big_cnt;
 }
 
-// block per segment longer than kWarpSeg: the distinct labels are collected
+// block per segment the warp kernel marked (ucnt = -1): the distinct labels are collected
 // in a shared-memory hash set (coarse rows have few distinct neighbours, e.g.
 // ~17 per aggregate on the elasticity graph against ~5.7K entries), then only
 // the uniques are sorted.  Segments with more than kMaxUniq distinct labels go
 // to `big` (bitmap path).
 constexpr int kHashCap = 4096;
 constexpr int kMaxUniq = 2048;
-__global__ void k_dedupe_block(int64_t na, const int64_t* __restrict__ sptr, int32_t* __restrict__ buf,
+__global__ void k_dedupe_block(int64_t na, const int64_t* __restrict__ sptr, const unsigned long long* __restrict__ send,
+                               int32_t* __restrict__ buf,
                                int64_t* __restrict__ ucnt, int32_t* __restrict__ big, int* big_cnt) {
     __shared__ int32_t keys[kHashCap];
     __shared__ int32_t uq[kMaxUniq];
     __shared__ int s_cnt;
     for (int64_t a = blockIdx.x; a < na; a += gridDim.x) {
-        const int64_t s = sptr[a], len = sptr[a + 1] - s;
-        if (len <= kWarpSeg) continue;
+        if (ucnt[a] >= 0) continue;
+        const int64_t s = sptr[a], len = (int64_t)send[a] - s;
         for (int i = threadIdx.x; i < kHashCap; i += blockDim.x) keys[i] = -1;
         if (threadIdx.x == 0) s_cnt = 0;
         __syncthreads();
         for (int64_t j = s + threadIdx.x; j < s + len; j += blockDim.x) {
             const int32_t b = buf[j];
-            if (b == kSent) continue;
             if (*(volatile int*)&s_cnt >= kMaxUniq) break;  // overflow: bitmap path below
             uint32_t slot = ((uint32_t)b * 2654435761u) >> 20;  // 12-bit hash
             for (;;) {
@@ -167,17 +224,18 @@ __global__ void k_dedupe_block(int64_t na, const int64_t* __restrict__ sptr, int
 
 // one block handles one long segment via an na-bit bitmap
 __global__ void k_bitmap_segment(const int32_t* __restrict__ big, int idx, const int64_t* __restrict__ sptr,
+                                 const unsigned long long* __restrict__ send,
                                  int32_t* __restrict__ buf, int64_t* __restrict__ ucnt, unsigned* __restrict__ bm,
                                  int64_t na) {
     __shared__ int s_w[32 + 1];
     const int64_t a = big[idx];
-    const int64_t s = sptr[a], e = sptr[a + 1];
+    const int64_t s = sptr[a], e = (int64_t)send[a];
     const int64_t words = (na + 31) / 32;
     for (int64_t i = threadIdx.x; i < words; i += blockDim.x) bm[i] = 0;
     __syncthreads();
     for (int64_t j = s + threadIdx.x; j < e; j += blockDim.x) {
         const int32_t b = buf[j];
-        if (b != kSent) atomicOr(&bm[b >> 5], 1u << (b & 31));
+        atomicOr(&bm[b >> 5], 1u << (b & 31));
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -279,10 +337,10 @@ int run_coarsen(const mis2_graph& g, const int32_t* labels, int64_t na, int64_t*
         int64_t wb = (na + kWarpsPerBlock - 1) / kWarpsPerBlock;
         if (wb > (int64_t)di.sms * 32) wb = (int64_t)di.sms * 32;
         if (wb < 1) wb = 1;
-        k_sort_warp<<<(unsigned)wb, kBlock, 0, s>>>(na, sptr, buf, ucnt, big, &scal[1]);
+        k_dedupe_warp<<<(unsigned)wb, kBlock, 0, s>>>(na, sptr, cursor, buf, ucnt);
         int64_t bb = na < (int64_t)di.sms * 8 ? na : (int64_t)di.sms * 8;
         if (bb < 1) bb = 1;
-        k_dedupe_block<<<(unsigned)bb, kBlock, 0, s>>>(na, sptr, buf, ucnt, big, &scal[1]);
+        k_dedupe_block<<<(unsigned)bb, kBlock, 0, s>>>(na, sptr, cursor, buf, ucnt, big, &scal[1]);
         count_launch(2);
     }
     int hs[16];
@@ -290,7 +348,7 @@ int run_coarsen(const mis2_graph& g, const int32_t* labels, int64_t na, int64_t*
     MIS2_CUDA_TRY(cudaStreamSynchronize(s));
     if (hs[0]) { set_error("labels out of [0, num_aggs)"); return MIS2_EINVAL; }
     for (int i = 0; i < hs[1]; i++) {
-        k_bitmap_segment<<<1, 1024, 0, s>>>(big, i, sptr, buf, ucnt, bm, na);
+        k_bitmap_segment<<<1, 1024, 0, s>>>(big, i, sptr, cursor, buf, ucnt, bm, na);
         count_launch();
     }
     MIS2_TRY(scan_counts64(ucnt, na, c_rowptr, tmp, s));

@@ -146,4 +146,25 @@ __device__ __forceinline__ long long block_sum_warps(long long warp_val, long lo
     return s;
 }
 
+// Visits the entries j = s + sub, s + sub + G, ... < e of a row with U column
+// loads, then U gathers ld(w), in flight per batch; use(w, ld(w)) in order.
+template <int G, int U, class Load, class Use>
+__device__ __forceinline__ void row_batched(int64_t s, int64_t e, int sub, const int32_t* __restrict__ colinds,
+                                            Load ld, Use use) {
+    for (int64_t j0 = s + sub; j0 < e; j0 += (int64_t)U * G) {
+        int32_t w[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t j = j0 + (int64_t)u * G;
+            w[u] = j < e ? colinds[j] : -1;
+        }
+        decltype(ld(0)) x[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) x[u] = w[u] >= 0 ? ld(w[u]) : decltype(ld(0))();
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (w[u] >= 0) use(w[u], x[u]);
+    }
+}
+
 }  // namespace mis2k
