@@ -137,11 +137,21 @@ __global__ void k_dedupe_warp(int64_t na, const int64_t* __restrict__ sptr, cons
         for (int i = lane; i < kWarpHash; i += 32) h[i] = -1;
         if (lane == 0) s_cnt[warp] = 0;
         __syncwarp();
-        for (int64_t j = lane; j < len; j += 32) {
-            if (*(volatile int*)&s_cnt[warp] >= kWarpUniq) break;  // overflow: block path
-            const int32_t b = buf[s + j];
+        for (int64_t j0 = 0; j0 < len; j0 += 32) {
+            if (__any_sync(kFull, *(volatile int*)&s_cnt[warp] >= kWarpUniq)) break;  // overflow: block path
+            const int64_t j = j0 + lane;
+            const int32_t b = j < len ? buf[s + j] : -1;
+            // one lane per distinct value of the chunk inserts it
+            const unsigned m = __match_any_sync(kFull, b);
+            if (b < 0 || (m & lanemask_lt())) continue;
             uint32_t slot = ((uint32_t)b * 2654435761u) >> 23;  // 9-bit hash
             for (;;) {
+                const int32_t cur = ((volatile int32_t*)h)[slot];
+                if (cur == b) break;
+                if (cur != -1) {
+                    slot = (slot + 1) & (kWarpHash - 1);
+                    continue;
+                }
                 const int32_t prev = atomicCAS(&h[slot], -1, b);
                 if (prev == -1) {
                     const int k = atomicAdd(&s_cnt[warp], 1);
