@@ -31,6 +31,13 @@ _lib = None
 
 OK, EINVAL, ENOMEM, ENOTCONVERGED, EASSERT, ERANGE = 0, -1, -2, -6, -9, -7
 SCHEMES = {"xorstar": 0, "fixed": 1, "xor": 2}
+WORD32 = 0x10  # scheme modifier: status words of width 32 (reading Q32)
+
+
+def _scheme(scheme: str, word_bits: int) -> int:
+    if word_bits not in (32, 64):
+        raise ValueError(word_bits)
+    return SCHEMES[scheme] | (WORD32 if word_bits == 32 else 0)
 IN = 0
 OUT = (1 << 64) - 1
 UNAGG = -1
@@ -111,8 +118,8 @@ def pack(priority: int, vid: int, b: int) -> int:
     return int(_load().orc_pack(priority, vid, b))
 
 
-def word(it: int, v: int, n: int, seed: int = 0, scheme: str = "xorstar") -> int:
-    return int(_load().orc_word(SCHEMES[scheme], it, v, seed, bits(n)))
+def word(it: int, v: int, n: int, seed: int = 0, scheme: str = "xorstar", word_bits: int = 64) -> int:
+    return int(_load().orc_word(_scheme(scheme, word_bits), it, v, seed, bits(n)))
 
 
 # --- Alg. 1 ---------------------------------------------------------------
@@ -129,8 +136,9 @@ class Mis2Result:
 
 def mis2(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0,
          active=None, prio_override=None, stats: bool = False, state: bool = False,
-         allow_partial: bool = False) -> Mis2Result:
-    """Alg. 1 on CSR (rowptr int64, colinds int32)."""
+         allow_partial: bool = False, word_bits: int = 64) -> Mis2Result:
+    """Alg. 1 on CSR (rowptr int64, colinds int32); word_bits = the
+    status-word width W (64, or the paper's 32: reading Q32)."""
     lib = _load()
     rowptr, colinds = _csr(rowptr, colinds)
     n = rowptr.shape[0] - 1
@@ -148,7 +156,7 @@ def mis2(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int
         po = np.ascontiguousarray(prio_override, dtype=np.uint64)
         pi = po.shape[0]
         po = po.reshape(-1)
-    rc = lib.orc_mis2(n, _p(rowptr), _p(colinds), seed, SCHEMES[scheme], mi, _p(act), _p(po), pi,
+    rc = lib.orc_mis2(n, _p(rowptr), _p(colinds), seed, _scheme(scheme, word_bits), mi, _p(act), _p(po), pi,
                       _p(in_set), ctypes.byref(cnt), ctypes.byref(its), _p(st), _p(T), _p(M))
     if rc not in (OK, ENOTCONVERGED) or (rc == ENOTCONVERGED and not allow_partial):
         raise OracleError(rc, "mis2")
@@ -166,7 +174,8 @@ class AggResult:
     stats: dict = field(default_factory=dict)
 
 
-def aggregate(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0) -> AggResult:
+def aggregate(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0,
+              word_bits: int = 64) -> AggResult:
     """Alg. 3 (P:289-319)."""
     lib = _load()
     rowptr, colinds = _csr(rowptr, colinds)
@@ -175,7 +184,7 @@ def aggregate(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters
     roots = np.zeros(max(n, 1), dtype=np.int32)
     na = ctypes.c_int64(0)
     st = np.zeros(8, dtype=np.int64)
-    rc = lib.orc_aggregate(n, _p(rowptr), _p(colinds), seed, SCHEMES[scheme], max_iters, _p(labels),
+    rc = lib.orc_aggregate(n, _p(rowptr), _p(colinds), seed, _scheme(scheme, word_bits), max_iters, _p(labels),
                            ctypes.byref(na), _p(roots), _p(st))
     if rc != OK:
         raise OracleError(rc, "aggregate")

@@ -34,6 +34,10 @@
 #define ORC_SCHEME_XORSTAR 0 /* h(i,v) = f(f(i^seed) ^ f(v)), f = xorshift64*  (used) */
 #define ORC_SCHEME_FIXED 1   /* Bell et al.: priorities drawn once: f(seed ^ f(v)) */
 #define ORC_SCHEME_XOR 2     /* same as XORSTAR with f = plain xorshift64 */
+/* Scheme modifier: status words of the paper's width W = 32 ("the
+ * same width as the vertex ids"; reading Q32): the priority is taken from the
+ * high 32 bits of h, IN = 0, OUT = 2^32 - 1.  Needs b <= 31. */
+#define ORC_WORD32 0x10
 
 /* ---------------------------------------------------------------------------
  * §V-A Pseudo-random priorities: "h(iter, v) = f(f(iter) ⊕ f(v))";
@@ -75,8 +79,9 @@ int orc_bits(int64_t n) {
 uint64_t orc_pack(uint64_t priority, int64_t id, int b) { return (priority << b) | (uint64_t)(id + 1); }
 
 uint64_t orc_word(int scheme, uint64_t iter, int64_t v, uint64_t seed, int b) {
-    uint64_t h = orc_h(scheme, iter, (uint64_t)v, seed);
-    return orc_pack(h >> b, v, b); /* = (h & ~(2^b - 1)) | (v + 1) */
+    uint64_t h = orc_h(scheme & ~ORC_WORD32, iter, (uint64_t)v, seed);
+    if (scheme & ORC_WORD32) h >>= 32; /* a W = 32 hash: the high half of h (Q5, Q32) */
+    return orc_pack(h >> b, v, b);     /* = (h & ~(2^b - 1)) | (v + 1) */
 }
 
 /* ---------------------------------------------------------------------------
@@ -107,6 +112,8 @@ int orc_mis2(int64_t n, const int64_t* rowptr, const int32_t* colinds, uint64_t 
              uint64_t* M_out) {
     if (n < 0 || (n > 0 && (!rowptr || !colinds)) || !in_set || !count || !iters) return ORC_EINVAL;
     const int b = orc_bits(n);
+    const uint64_t OUT = (scheme & ORC_WORD32) ? 0xFFFFFFFFULL : ORC_OUT; /* UINT_MAX of width W */
+    if ((scheme & ORC_WORD32) && b > 31) return ORC_EINVAL;
     if (max_iters <= 0) max_iters = 10 * b + 20; /* reading Q12 */
 
     uint64_t* T = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(n + 1));
@@ -123,7 +130,7 @@ int orc_mis2(int64_t n, const int64_t* rowptr, const int32_t* colinds, uint64_t 
 #define ACTIVE(w) (active == NULL || active[w])
     /* IN <- 0; OUT <- UINT_MAX.  Vertices outside worklist_2 keep
      * M = OUT (reading Q9); inactive vertices are never read. */
-    for (int64_t v = 0; v < n; v++) { T[v] = ORC_OUT; M[v] = ORC_OUT; }
+    for (int64_t v = 0; v < n; v++) { T[v] = OUT; M[v] = OUT; }
     /* worklist_1 <- 0..|V|, worklist_2 <- 0..|V| */
     int64_t n1 = 0, n2 = 0;
     for (int64_t v = 0; v < n; v++)
@@ -171,7 +178,7 @@ int orc_mis2(int64_t n, const int64_t* rowptr, const int32_t* colinds, uint64_t 
                 int64_t w = colinds[j];
                 if (ACTIVE(w) && T[w] < m) m = T[w];
             }
-            if (m == ORC_IN) m = ORC_OUT;
+            if (m == ORC_IN) m = OUT;
             M[v] = m;
         }
 
@@ -181,24 +188,24 @@ int orc_mis2(int64_t n, const int64_t* rowptr, const int32_t* colinds, uint64_t 
         for (int64_t k = 0; k < n1; k++) {
             int64_t v = wl1[k];
             const uint64_t tv = T[v];
-            int any_out = (M[v] == ORC_OUT);
+            int any_out = (M[v] == OUT);
             int all_eq = (M[v] == tv);
             for (int64_t j = rowptr[v]; j < rowptr[v + 1]; j++) {
                 int64_t w = colinds[j];
                 if (!ACTIVE(w)) continue;
-                if (M[w] == ORC_OUT) any_out = 1;
+                if (M[w] == OUT) any_out = 1;
                 if (M[w] != tv) all_eq = 0;
             }
-            if (any_out) T[v] = ORC_OUT;
+            if (any_out) T[v] = OUT;
             else if (all_eq) T[v] = ORC_IN;
         }
 
         /* Compact worklists: ascending order kept */
         int64_t k1 = 0, k2 = 0;
         for (int64_t k = 0; k < n1; k++)
-            if (T[wl1[k]] != ORC_IN && T[wl1[k]] != ORC_OUT) wl1[k1++] = wl1[k];
+            if (T[wl1[k]] != ORC_IN && T[wl1[k]] != OUT) wl1[k1++] = wl1[k];
         for (int64_t k = 0; k < n2; k++)
-            if (M[wl2[k]] != ORC_OUT) wl2[k2++] = wl2[k];
+            if (M[wl2[k]] != OUT) wl2[k2++] = wl2[k];
         n1 = k1;
         n2 = k2;
         iter++;

@@ -45,10 +45,13 @@ def py_bits(n: int) -> int:
     return (n + 1).bit_length()
 
 
-def py_word(it: int, v: int, n: int, seed: int = 0) -> int:
+def py_word(it: int, v: int, n: int, seed: int = 0, word_bits: int = 64) -> int:
+    """Eq. 1 with word width W = word_bits: the priority field is the
+    top W - b bits of the W-bit hash, and a W = 32 hash is the high half of
+    the 64-bit one (readings Q5, Q32)."""
     b = py_bits(n)
-    h = py_f(py_f(it ^ seed) ^ py_f(v))
-    return (h & ~((1 << b) - 1) & MASK64) | (v + 1)
+    h = py_f(py_f(it ^ seed) ^ py_f(v)) >> (64 - word_bits)
+    return (h >> b << b) | (v + 1)
 
 
 def adjacency_sets(rowptr, colinds):
@@ -95,7 +98,7 @@ def square_pattern(rowptr, colinds):
     return ((A @ A) > 0).tocsr()
 
 
-def luby_g2(rowptr, colinds, seed=0, active=None, prio=None, max_iters=500):
+def luby_g2(rowptr, colinds, seed=0, active=None, prio=None, max_iters=500, word_bits=64):
     """Luby (distance-1) on explicit G^2 (closed), priorities word(k, v).
 
     Iteration k, U = undecided at its start:
@@ -118,7 +121,7 @@ def luby_g2(rowptr, colinds, seed=0, active=None, prio=None, max_iters=500):
         if prio is not None and it < len(prio):
             w = {int(v): (int(prio[it][v]) << py_bits(n)) | (int(v) + 1) for v in U}
         else:
-            w = {int(v): py_word(it, int(v), n, seed) for v in U}
+            w = {int(v): py_word(it, int(v), n, seed, word_bits) for v in U}
         new_status = status.copy()
         for v in U:
             nb = S2.indices[S2.indptr[v]:S2.indptr[v + 1]]
