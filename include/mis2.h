@@ -75,6 +75,14 @@ extern "C" {
                                     used iff 8n > 64 MB and the largest degree exceeds 16x the
                                     average.  Never changes results. */
 #define MIS2_FLAG_NO_KEYS 0x40u  /* never use the 32-bit column keys.  Never changes results. */
+#define MIS2_FLAG_WORD32 0x80u  /* status words of the paper's width W = 32 (Eq. 1;
+                                    reading Q32): undecided T_v = (h32 & ~(2^b - 1)) | (v + 1) with
+                                    h32 = the HIGH 32 bits of h, IN = 0, OUT = 2^32 - 1.  Requires
+                                    b = ceil(log2(n + 2)) <= 31 (else MIS2_EINVAL).  Changes results
+                                    (fewer priority bits, more ties broken by id); stored
+                                    zero-extended in the 64-bit arrays, which orders every word
+                                    exactly as 32-bit storage would (results identical to a
+                                    32-bit implementation).  MIS-2 / aggregation / partitioned. */
 #define MIS2_FLAG_TIMELINE 0x2u  /* measurement aid: mis2()'s `stats` receives int64 device
                                     timestamps (ns, %globaltimer) taken by block 0 after
                                     the init phase and after every grid barrier:

@@ -31,6 +31,8 @@ DECIDE = {"auto": 0, "push": FLAG_PUSH_DECIDE, "pull": FLAG_PULL_DECIDE}
 FLAG_KEYS = 32
 FLAG_NO_KEYS = 64
 KEYS = {"auto": 0, "on": FLAG_KEYS, "off": FLAG_NO_KEYS}
+FLAG_WORD32 = 128
+WORD_BITS = {64: 0, 32: FLAG_WORD32}
 
 # every symbol include/mis2.h declares
 EXPORTS = ["mis2_opts_default", "mis2_workspace_size", "mis2", "mis2_async", "mis2_host", "mis2_aggregate",
@@ -156,14 +158,14 @@ def _graph(rowptr, colinds):
 
 
 def _opts(seed=0, scheme="xorstar", max_iters=0, group=0, validate=False, prio_override=None, decide="auto",
-          keys="auto"):
+          keys="auto", word_bits=64):
     o = _Opts()
     lib().mis2_opts_default(ctypes.byref(o))
     o.seed = seed & ((1 << 64) - 1)
     o.scheme = SCHEMES[scheme]
     o.max_iters = max_iters
     o.group = group
-    o.flags = (FLAG_VALIDATE if validate else 0) | DECIDE[decide] | KEYS[keys]
+    o.flags = (FLAG_VALIDATE if validate else 0) | DECIDE[decide] | KEYS[keys] | WORD_BITS[word_bits]
     if prio_override is not None:
         o.prio_override = prio_override.data_ptr()
         o.prio_iters = prio_override.shape[0]
@@ -182,13 +184,14 @@ class Mis2Result:
 
 def mis2(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
          validate: bool = False, prio_override=None, stats: bool = False, allow_partial: bool = False,
-         out=None, timeline: bool = False, decide: str = "auto", keys: str = "auto") -> Mis2Result:
+         out=None, timeline: bool = False, decide: str = "auto", keys: str = "auto",
+         word_bits: int = 64) -> Mis2Result:
     """Alg. 1 through ``mis2()`` of the C ABI."""
     torch = _torch()
     g, n, nnz = _graph(rowptr, colinds)
     if prio_override is not None:
         prio_override = prio_override.to(device=rowptr.device, dtype=torch.int64).contiguous()
-    o = _opts(seed, scheme, max_iters, group, validate, prio_override, decide, keys)
+    o = _opts(seed, scheme, max_iters, group, validate, prio_override, decide, keys, word_bits)
     ws, wsb = workspace(OP_MIS2, n, nnz)
     in_set = out if out is not None else torch.empty(max(n, 1), dtype=torch.uint8, device=rowptr.device)
     cnt, its = ctypes.c_int64(0), ctypes.c_int32(0)
@@ -255,12 +258,13 @@ class AggResult:
 
 
 def aggregate(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
-              validate: bool = False, basic: bool = False, decide: str = "auto", keys: str = "auto") -> AggResult:
+              validate: bool = False, basic: bool = False, decide: str = "auto", keys: str = "auto",
+              word_bits: int = 64) -> AggResult:
     """Alg. 3, or Alg. 2 with basic=True,
     through ``mis2_aggregate()``."""
     torch = _torch()
     g, n, nnz = _graph(rowptr, colinds)
-    o = _opts(seed, scheme, max_iters, group, validate, decide=decide, keys=keys)
+    o = _opts(seed, scheme, max_iters, group, validate, decide=decide, keys=keys, word_bits=word_bits)
     if basic:
         o.flags |= FLAG_BASIC
     ws, wsb = workspace(OP_AGGREGATE, n, nnz)
@@ -386,18 +390,20 @@ class Comm:
                "mis2_comm_part_info")
         return lo.value, hi.value, ng.value
 
-    def mis2(self, in_set, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0):
-        o = _opts(seed, scheme, max_iters, group)
+    def mis2(self, in_set, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
+             word_bits: int = 64):
+        o = _opts(seed, scheme, max_iters, group, word_bits=word_bits)
         cnt, its = ctypes.c_int64(0), ctypes.c_int32(0)
         _check(lib().mis2_dist_mis2(self.h, ctypes.byref(o), in_set.data_ptr(), ctypes.byref(cnt), ctypes.byref(its),
                                     _stream()), "mis2_dist_mis2")
         return int(cnt.value), int(its.value)
 
-    def aggregate(self, labels, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0):
+    def aggregate(self, labels, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
+                  word_bits: int = 64):
         """Alg. 3 over the partition (``mis2_dist_aggregate``): fills ``labels``
         (int32 CUDA tensor: this rank's rows, or all rows for local parts)
         with global aggregate ids; returns (num_aggs, stats dict)."""
-        o = _opts(seed, scheme, max_iters, group)
+        o = _opts(seed, scheme, max_iters, group, word_bits=word_bits)
         na = ctypes.c_int64(0)
         st = np.zeros(8, dtype=np.int64)
         _check(lib().mis2_dist_aggregate(self.h, ctypes.byref(o), labels.data_ptr(), ctypes.byref(na),

@@ -56,7 +56,10 @@ static int check_opts(const mis2_opts* o, int64_t n) {
         return MIS2_EINVAL;
     }
     if (o->prio_override && o->prio_iters < 0) { set_error("prio_iters < 0"); return MIS2_EINVAL; }
-    (void)n;
+    if ((o->flags & MIS2_FLAG_WORD32) && bits_for(n) > 31) {
+        set_error("MIS2_FLAG_WORD32 needs ceil(log2(n + 2)) <= 31");
+        return MIS2_EINVAL;
+    }
     return MIS2_OK;
 }
 

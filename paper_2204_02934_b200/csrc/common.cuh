@@ -34,6 +34,7 @@ struct Prio {
     int b;
     uint64_t seed;
     uint64_t hi_mask;           // ~(2^b - 1)
+    int hshift;                 // 0: W = 64; 32: W = 32, priority from the high half of h (Q32)
     int64_t n;
     const uint64_t* override_;  // test-only (Fig. 1 replay)
     int override_iters;
@@ -51,7 +52,7 @@ struct Prio {
         if (scheme == MIS2_SCHEME_FIXED) h = xs64star(seed ^ xs64star((uint64_t)v));
         else if (scheme == MIS2_SCHEME_XOR) h = xs64(fi ^ xs64((uint64_t)v));
         else h = xs64star(fi ^ xs64star((uint64_t)v));
-        return (h & hi_mask) | (uint64_t)(v + 1);
+        return ((h >> hshift) & hi_mask) | (uint64_t)(v + 1);
     }
 };
 

@@ -561,6 +561,7 @@ static int dist_mis2_run(mis2_comm* c, const mis2_opts& opt, const std::vector<u
         PartDev& d = c->dev[i];
         d.seed = opt.seed;
         d.scheme = opt.scheme;
+        d.hshift = (opt.flags & MIS2_FLAG_WORD32) ? 32 : 0;
         if (opt.group) d.G = opt.group;
         d.labels = labels.empty() ? nullptr : labels[i];
         d.in_set = in_sets[i];
@@ -796,6 +797,10 @@ int mis2_dist_mis2(mis2_comm* c, const mis2_opts* o, uint8_t* in_set, int64_t* c
         set_error("prio_override is not supported by the partitioned driver");
         return MIS2_EINVAL;
     }
+    if ((opt.flags & MIS2_FLAG_WORD32) && bits_for(c->n_global) > 31) {
+        set_error("MIS2_FLAG_WORD32 needs ceil(log2(n + 2)) <= 31");
+        return MIS2_EINVAL;
+    }
     std::vector<uint8_t*> ins(c->dev.size());
     for (size_t i = 0; i < c->dev.size(); i++) ins[i] = c->local ? in_set + c->hp[i].lo : in_set;
     return dist_mis2_run(c, opt, ins, {}, count, iters, (cudaStream_t)stream);
@@ -948,6 +953,10 @@ int mis2_dist_aggregate(mis2_comm* c, const mis2_opts* o, int32_t* labels, int64
     const mis2_opts& opt = o ? *o : def;
     if (opt.prio_override || (opt.flags & MIS2_FLAG_BASIC)) {
         set_error("prio_override / MIS2_FLAG_BASIC are not supported by the partitioned driver");
+        return MIS2_EINVAL;
+    }
+    if ((opt.flags & MIS2_FLAG_WORD32) && bits_for(c->n_global) > 31) {
+        set_error("MIS2_FLAG_WORD32 needs ceil(log2(n + 2)) <= 31");
         return MIS2_EINVAL;
     }
     std::vector<int32_t*> outs(c->dev.size());

@@ -100,7 +100,7 @@ struct PartDev {
     unsigned long long* ctr; // [0] active, [1] |wl1| this iteration, [2] count
     int32_t* heavy;          // n_own deferred long rows
     uint8_t* in_set;         // n_own
-    int grid, G, scheme;
+    int grid, G, scheme, hshift;
     uint64_t seed;
 };
 enum { kPartInit = 0, kPartColumn = 1, kPartDecide = 2, kPartFinal = 3 };

@@ -1437,6 +1437,7 @@ static MisParams part_params(const PartDev& d) {
         p.L2[i] = d.L2[i];
     }
     p.prio.scheme = d.scheme;
+    p.prio.hshift = d.hshift;
     p.prio.b = bits_for(d.n_global);
     p.prio.seed = d.seed;
     p.prio.hi_mask = ~((1ull << p.prio.b) - 1ull);
@@ -1579,6 +1580,7 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     if (o.flags & MIS2_FLAG_KEYS) keys = 1;
     if (o.flags & MIS2_FLAG_NO_KEYS) keys = 0;
     if (const char* e = getenv("MIS2_KEYS")) keys = atoi(e);  // measurement knob
+    if (o.flags & MIS2_FLAG_WORD32) keys = 0;  // the keys are the words' high halves
     p.K = keys ? w.K : nullptr;
     p.keys_mode = keys == 1 ? 1 : 0;
     for (int i = 0; i < 2; i++) {
@@ -1601,6 +1603,7 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
         if (p.dbg_it >= 0) MIS2_CUDA_TRY(cudaMemsetAsync(w.mark, 0, sizeof(long long) * 64 * kMaxDbgBlocks, s));
     }
     p.prio.scheme = o.scheme;
+    p.prio.hshift = (o.flags & MIS2_FLAG_WORD32) ? 32 : 0;
     p.prio.b = bits_for(g.n);
     p.prio.seed = o.seed;
     p.prio.hi_mask = ~((1ull << p.prio.b) - 1ull);

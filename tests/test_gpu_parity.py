@@ -46,10 +46,11 @@ def small_graphs(count, seed, nmax=200):
     return out
 
 
-def check_mis2(g, seed=0, group=0, scheme="xorstar", stats=False, decide="auto", keys="auto"):
+def check_mis2(g, seed=0, group=0, scheme="xorstar", stats=False, decide="auto", keys="auto", word_bits=64):
     rp, ci = dev(g)
-    r = M().mis2(rp, ci, seed=seed, group=group, scheme=scheme, stats=stats, decide=decide, keys=keys)
-    o = O.mis2(g.rowptr, g.colinds, seed=seed, scheme=scheme, stats=stats)
+    r = M().mis2(rp, ci, seed=seed, group=group, scheme=scheme, stats=stats, decide=decide, keys=keys,
+                 word_bits=word_bits)
+    o = O.mis2(g.rowptr, g.colinds, seed=seed, scheme=scheme, stats=stats, word_bits=word_bits)
     assert np.array_equal(r.in_set.cpu().numpy().astype(bool), o.in_set), g.name
     assert (r.count, r.iterations) == (o.count, o.iterations), g.name
     if stats:
@@ -217,10 +218,10 @@ def test_mis2_host_e2e():
 
 
 # ----------------------------------------------------------------- aggregation
-def check_agg(g, seed=0, decide="auto"):
+def check_agg(g, seed=0, decide="auto", word_bits=64):
     rp, ci = dev(g)
-    a = M().aggregate(rp, ci, seed=seed, decide=decide)
-    o = O.aggregate(g.rowptr, g.colinds, seed=seed)
+    a = M().aggregate(rp, ci, seed=seed, decide=decide, word_bits=word_bits)
+    o = O.aggregate(g.rowptr, g.colinds, seed=seed, word_bits=word_bits)
     assert a.num_aggs == o.num_aggs, g.name
     assert np.array_equal(a.labels.cpu().numpy(), o.labels), g.name
     assert np.array_equal(a.roots.cpu().numpy(), o.roots), g.name
@@ -479,3 +480,37 @@ def test_cluster_sgs_errors():
     vals = torch.ones(int(ci.numel()), dtype=torch.float64, device="cuda")
     with pytest.raises(M().Mis2Error):
         M().ClusterSGS(rp, ci, vals)
+
+
+# ----------------------------------------------------------------- W = 32 status words (§8 f2)
+@pytest.mark.parametrize("decide", ["pull", "push"])
+@pytest.mark.parametrize("chunk", range(2))
+def test_word32_small_graphs(chunk, decide):
+    """MIS2_FLAG_WORD32 (reading Q32): bit-exact with the oracle's
+    32-bit words, every scheme, both Decide forms."""
+    for k, g in enumerate(small_graphs(30, 5000 + chunk)):
+        check_mis2(g, seed=k, scheme=("xorstar", "fixed", "xor")[k % 3], decide=decide, word_bits=32, stats=True)
+
+
+@pytest.mark.parametrize("keys", ["auto", "on"])
+def test_word32_structured_and_config2(keys):
+    for g in [G.laplace3d_7pt(30), G.elasticity3d(8), G.kronecker(12), G.random_powerlaw_graph(3000, 30, 5)]:
+        check_mis2(g, keys=keys, word_bits=32)
+    check_mis2(G.config_graph(1), keys=keys, word_bits=32)
+
+
+def test_word32_aggregate_and_partitioned():
+    for g in small_graphs(15, 5100) + [G.laplace3d_27pt(16), G.kronecker(11)]:
+        check_agg(g, word_bits=32)
+    for g in [G.laplace3d_27pt(16), G.random_powerlaw_graph(2000, 6, 4)]:
+        for nparts in (2, 5):
+            c = M().Comm.local_parts(nparts).set_graph(g.n, g.rowptr, g.colinds)
+            out = torch.empty(max(g.n, 1), dtype=torch.uint8, device="cuda")
+            cnt, its = c.mis2(out, word_bits=32)
+            lab = torch.empty(max(g.n, 1), dtype=torch.int32, device="cuda")
+            na, st = c.aggregate(lab, word_bits=32)
+            c.close()
+            o = O.mis2(g.rowptr, g.colinds, word_bits=32)
+            assert np.array_equal(out[: g.n].cpu().numpy().astype(bool), o.in_set) and (cnt, its) == (o.count, o.iterations)
+            oa = O.aggregate(g.rowptr, g.colinds, word_bits=32)
+            assert na == oa.num_aggs and np.array_equal(lab[: g.n].cpu().numpy(), oa.labels) and st == oa.stats
