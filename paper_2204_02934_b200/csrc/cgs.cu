@@ -25,76 +25,165 @@
 
 namespace mis2k {
 
-__global__ void k_color_init(int64_t n, Prio pr, uint64_t* __restrict__ W, int32_t* __restrict__ cround,
-                             int32_t* __restrict__ color) {
+// All rounds of the colouring in one cooperative launch (grid barrier
+// between rounds): round 0 visits every vertex, later rounds the vertices
+// left uncoloured (a worklist compacted with one atomic per warp, counts in a
+// ring of three).  G lanes per row with batched gathers; the decision is the
+// Jones-Plassmann rule of reading Q30: a vertex coloured in round r records r,
+// so "uncoloured at the start of round r" is cround >= r and the round is
+// race-free; the free colour comes from a 64-bit mask of the neighbours'
+// colours, with a scan beyond 64.
+struct ColorState {
+    uint64_t* W;
+    int32_t* cround;
+    int32_t* color;
+    int32_t* wl[2];
+    unsigned int* bar;
+    unsigned long long* cnt;  // [3] ring of worklist lengths
+    int* maxc;
+    int* err;
+};
+
+template <int G>
+__global__ void __launch_bounds__(256, 5) k_color_persistent(int64_t n, const int64_t* __restrict__ rowptr,
+                                                          const int32_t* __restrict__ colinds, Prio pr,
+                                                          ColorState st) {
+    constexpr int RPW = 32 / G;
+    const int lane = threadIdx.x & 31, grp = lane / G, sub = lane % G;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint64_t fi0 = pr.iter_term(0);
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-        W[v] = pr.word(0, fi0, v);
-        cround[v] = 0x7fffffff;
-        color[v] = -1;
+        st.W[v] = pr.word(0, fi0, v);
+        st.cround[v] = 0x7fffffff;
+        st.color[v] = -1;
     }
-}
-
-__global__ void k_color_round(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colinds,
-                              const uint64_t* __restrict__ W, int32_t* __restrict__ cround,
-                              int32_t* __restrict__ color, int r, unsigned long long* colored, int* maxc) {
-    int done = 0, mc = -1;
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-        if (cround[v] < r) continue;  // coloured in an earlier round
-        const uint64_t wv = W[v];
-        const int64_t s = rowptr[v], e = rowptr[v + 1];
-        bool cand = true;
-        uint64_t mask = 0;
-        for (int64_t j = s; j < e && cand; j++) {
-            const int32_t u = colinds[j];
-            if (u == v) continue;
-            const int32_t ru = cround[u];
-            if (ru >= r) {
-                if (W[u] < wv) cand = false;  // an uncoloured neighbour of higher priority
-            } else {
-                const int32_t cu = color[u];
-                if (cu < 64) mask |= 1ull << cu;
+    if (blockIdx.x == 0 && threadIdx.x < 3) st.cnt[threadIdx.x] = 0;
+    grid_barrier(st.bar);
+    const int32_t* cr = st.cround;
+    const uint64_t* Wp = st.W;
+    const int32_t* cl = st.color;
+    int64_t m = n;
+    for (int r = 0;; r++) {
+        const int32_t* in = (r & 1) ? st.wl[1] : st.wl[0];  // no dynamic index into the parameter
+        int32_t* out = (r & 1) ? st.wl[0] : st.wl[1];
+        unsigned long long* ocnt = st.cnt + (r % 3);
+        if (blockIdx.x == 0 && threadIdx.x == 0) st.cnt[(r + 1) % 3] = 0;
+        int mc = -1;
+        for (int64_t base = gwarp * RPW; base < m; base += nwarps * RPW) {
+            const int64_t idx = base + grp;
+            const bool valid = idx < m;
+            int64_t v = 0, s = 0, e = 0;
+            uint64_t wv = 0;
+            if (valid) {
+                v = (r == 0) ? idx : in[idx];
+                s = rowptr[v];
+                e = rowptr[v + 1];
+                wv = st.W[v];
             }
-        }
-        if (!cand) continue;
-        int32_t c;
-        if (mask != ~0ull) {
-            c = __ffsll((long long)~mask) - 1;
-        } else {  // more than 64 colours around: smallest free colour >= 64
-            c = 64;
-            for (;;) {
-                bool taken = false;
-                for (int64_t j = s; j < e && !taken; j++) {
-                    const int32_t u = colinds[j];
-                    if (u != v && cround[u] < r && color[u] == c) taken = true;
-                }
-                if (!taken) break;
-                c++;
-            }
-        }
-        color[v] = c;
-        cround[v] = r;
-        done++;
-        mc = max(mc, c);
-    }
-    done = group_sum<32>(done);
+            bool cand = true;
+            uint64_t mask = 0;
+            // batches of 8 entries per lane, three levels of independent
+            // loads (column ids, rounds, then words or colours); a lane stops
+            // at its first uncoloured neighbour with a smaller word
+            if (valid)
+                for (int64_t j0 = s + sub; j0 < e && cand; j0 += 8 * G) {
+                    int32_t uu[8], ru[8];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) mc = max(mc, __shfl_xor_sync(kFull, mc, off));
-    if ((threadIdx.x & 31) == 0) {
-        if (done) atomicAdd(colored, (unsigned long long)done);
-        if (mc >= 0) atomicMax(maxc, mc);
+                    for (int q = 0; q < 8; q++) {
+                        const int64_t j = j0 + (int64_t)q * G;
+                        uu[q] = j < e ? colinds[j] : -1;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; q++) ru[q] = (uu[q] >= 0 && uu[q] != v) ? cr[uu[q]] : -1;
+#pragma unroll
+                    for (int q = 0; q < 8; q++) {
+                        if (ru[q] >= r) {
+                            if (Wp[uu[q]] < wv) cand = false;
+                        } else if (ru[q] >= 0) {
+                            const int32_t cu = cl[uu[q]];
+                            if (cu < 64) mask |= 1ull << cu;
+                        }
+                    }
+                }
+#pragma unroll
+            for (int off = G / 2; off > 0; off >>= 1) {
+                const int oc = __shfl_xor_sync(kFull, (int)cand, off);  // every lane shuffles
+                cand = cand && oc;
+                mask |= __shfl_xor_sync(kFull, mask, off);
+            }
+            bool keep = false;
+            if (valid && sub == 0) {
+                if (cand) {
+                    int32_t c;
+                    if (mask != ~0ull) {
+                        c = __ffsll((long long)~mask) - 1;
+                    } else {  // more than 64 colours around: smallest free colour >= 64
+                        c = 64;
+                        for (;;) {
+                            bool taken = false;
+                            for (int64_t j = s; j < e && !taken; j++) {
+                                const int32_t u = colinds[j];
+                                if (u != v && st.cround[u] < r && st.color[u] == c) taken = true;
+                            }
+                            if (!taken) break;
+                            c++;
+                        }
+                    }
+                    st.color[v] = c;
+                    st.cround[v] = r;
+                    mc = max(mc, c);
+                } else {
+                    keep = true;
+                }
+            }
+            const unsigned ball = __ballot_sync(kFull, keep);
+            if (ball) {
+                unsigned long long pos = 0;
+                if (lane == 0) pos = atomicAdd(ocnt, (unsigned long long)__popc(ball));
+                pos = __shfl_sync(kFull, pos, 0);
+                if (keep) out[pos + __popc(ball & lanemask_lt())] = (int32_t)v;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mc = max(mc, __shfl_xor_sync(kFull, mc, off));
+        if (lane == 0 && mc >= 0) atomicMax(st.maxc, mc);
+        grid_barrier(st.bar);
+        m = (int64_t)*(volatile unsigned long long*)ocnt;
+        if (m == 0) break;
+        if (r > n + 2) {  // every round colours at least the least uncoloured word
+            if (blockIdx.x == 0 && threadIdx.x == 0) *st.err = 1;
+            break;
+        }
     }
 }
 
-// rows per cluster (pass 1) / placed at an atomically reserved slot (pass 2)
+// rows per cluster (pass 1) / placed at an atomically reserved slot (pass 2);
+// lanes of a warp with the same key share one atomic (__match_any_sync: a
+// colour histogram has ~20 keys for 10^6 entries)
 __global__ void k_count_i32(int64_t n, const int32_t* __restrict__ key, unsigned long long* __restrict__ cnt) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(&cnt[key[i]], 1ull);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        const int32_t k = i < n ? key[i] : -1;
+        const unsigned m = __match_any_sync(kFull, k);
+        if (k >= 0 && !(m & lanemask_lt())) atomicAdd(&cnt[k], (unsigned long long)__popc(m));
+    }
 }
 __global__ void k_scatter_i32(int64_t n, const int32_t* __restrict__ key, unsigned long long* __restrict__ cursor,
                               int32_t* __restrict__ out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        out[atomicAdd(&cursor[key[i]], 1ull)] = (int32_t)i;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        const int32_t k = i < n ? key[i] : -1;
+        const unsigned m = __match_any_sync(kFull, k);
+        const int leader = __ffs(m) - 1;
+        unsigned long long pos = 0;
+        if (k >= 0 && lane == leader) pos = atomicAdd(&cursor[k], (unsigned long long)__popc(m));
+        pos = __shfl_sync(kFull, pos, leader);
+        if (k >= 0) out[pos + __popc(m & lanemask_lt())] = (int32_t)i;
+    }
 }
 // ascending rows inside each cluster: block bitonic of the segment in shared memory
 constexpr int kSegMax = 4096;
@@ -258,46 +347,61 @@ int color_graph(const mis2_graph& g, uint64_t seed, int32_t* color, int32_t* nco
         *ncolors = 0;
         return MIS2_OK;
     }
-    uint64_t* W;
-    int32_t* cround;
-    unsigned long long* ctr;
-    MIS2_CUDA_TRY(cudaMallocAsync((void**)&W, sizeof(uint64_t) * n, s));
-    MIS2_CUDA_TRY(cudaMallocAsync((void**)&cround, sizeof(int32_t) * n, s));
-    MIS2_CUDA_TRY(cudaMallocAsync((void**)&ctr, 64, s));
+    ColorState st;
+    char* ctr;
+    MIS2_CUDA_TRY(cudaMallocAsync((void**)&st.W, sizeof(uint64_t) * n, s));
+    MIS2_CUDA_TRY(cudaMallocAsync((void**)&st.cround, sizeof(int32_t) * n, s));
+    MIS2_CUDA_TRY(cudaMallocAsync((void**)&st.wl[0], sizeof(int32_t) * n, s));
+    MIS2_CUDA_TRY(cudaMallocAsync((void**)&st.wl[1], sizeof(int32_t) * n, s));
+    MIS2_CUDA_TRY(cudaMallocAsync((void**)&ctr, 256, s));
+    MIS2_CUDA_TRY(cudaMemsetAsync(ctr, 0, 256, s));
+    st.color = color;
+    st.bar = (unsigned int*)ctr;
+    st.cnt = (unsigned long long*)(ctr + 64);
+    st.maxc = (int*)(ctr + 128);
+    st.err = (int*)(ctr + 132);
+    MIS2_CUDA_TRY(cudaMemsetAsync(st.maxc, 0xff, sizeof(int), s));  // -1
     Prio pr{};
     pr.scheme = MIS2_SCHEME_XORSTAR;
     pr.b = bits_for(n);
     pr.seed = seed;
     pr.hi_mask = ~((1ull << pr.b) - 1ull);
     pr.n = n;
-    const unsigned gb = grid_for(n, di.sms);
-    k_color_init<<<gb, 256, 0, s>>>(n, pr, W, cround, color);
+    const int G = choose_group(n, g.nnz, 0);
+    void* fn;
+    switch (G) {
+        case 1: fn = (void*)k_color_persistent<1>; break;
+        case 2: fn = (void*)k_color_persistent<2>; break;
+        case 4: fn = (void*)k_color_persistent<4>; break;
+        case 8: fn = (void*)k_color_persistent<8>; break;
+        case 16: fn = (void*)k_color_persistent<16>; break;
+        default: fn = (void*)k_color_persistent<32>; break;
+    }
+    int per_sm = 0;
+    MIS2_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+    int64_t grid = (int64_t)per_sm * di.sms;
+    const int64_t need = (n + (256 / G) - 1) / (256 / G);
+    if (grid > need) grid = need;
+    if (grid < 1) grid = 1;
+    const mis2_graph gg = g;
+    int64_t nn = n;
+    void* args[] = {&nn, (void*)&gg.rowptr, (void*)&gg.colinds, &pr, &st};
+    MIS2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(256), args, 0, s));
     count_launch();
-    MIS2_CUDA_TRY(cudaMemsetAsync(ctr, 0, 64, s));
+    int hv[2] = {-1, 0};
     int rc = MIS2_OK;
-    unsigned long long colored = 0;
-    for (int r = 0; colored < (unsigned long long)n; r++) {
-        k_color_round<<<gb, 256, 0, s>>>(n, g.rowptr, g.colinds, W, cround, color, r, ctr, (int*)(ctr + 1));
-        count_launch();
-        if (cudaMemcpyAsync(&colored, ctr, sizeof(colored), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-            cudaStreamSynchronize(s) != cudaSuccess) {
-            rc = MIS2_ECUDA;
-            break;
-        }
-        if (r > n + 2) {  // every round colours at least the least uncoloured word
-            set_error("colouring did not terminate");
-            rc = MIS2_EINTERNAL;
-            break;
-        }
+    MIS2_CUDA_TRY(cudaMemcpyAsync(hv, st.maxc, sizeof(hv), cudaMemcpyDeviceToHost, s));
+    MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+    if (hv[1]) {
+        set_error("colouring did not terminate");
+        rc = MIS2_EINTERNAL;
+    } else {
+        *ncolors = hv[0] + 1;
     }
-    int maxc = -1;
-    if (rc == MIS2_OK) {
-        MIS2_CUDA_TRY(cudaMemcpyAsync(&maxc, ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
-        MIS2_CUDA_TRY(cudaStreamSynchronize(s));
-        *ncolors = maxc + 1;
-    }
-    cudaFreeAsync(W, s);
-    cudaFreeAsync(cround, s);
+    cudaFreeAsync(st.W, s);
+    cudaFreeAsync(st.cround, s);
+    cudaFreeAsync(st.wl[0], s);
+    cudaFreeAsync(st.wl[1], s);
     cudaFreeAsync(ctr, s);
     return rc;
 }
@@ -341,25 +445,26 @@ int mis2_cgs_setup(const mis2_graph* g, const double* vals, const int32_t* label
     void* p;
     int* err;
     int rc;
-    if ((rc = cgs_alloc(h, &p, sizeof(double) * (n + 1))) != MIS2_OK) return fail(rc);
-    h->diag = (double*)p;
-    if ((rc = cgs_alloc(h, &p, sizeof(int64_t) * (na + 2))) != MIS2_OK) return fail(rc);
-    h->cptr = (int64_t*)p;
-    if ((rc = cgs_alloc(h, &p, sizeof(int32_t) * (n + 1))) != MIS2_OK) return fail(rc);
-    h->crows = (int32_t*)p;
-    if ((rc = cgs_alloc(h, &p, sizeof(int32_t) * (na + 1))) != MIS2_OK) return fail(rc);
-    h->cset = (int32_t*)p;
-    if ((rc = cgs_alloc(h, &p, 64)) != MIS2_OK) return fail(rc);
-    err = (int*)p;
     int32_t* ccolor;
-    if ((rc = cgs_alloc(h, &p, sizeof(int32_t) * (na + 1))) != MIS2_OK) return fail(rc);
-    ccolor = (int32_t*)p;
     unsigned long long* cnt;
-    const int64_t nk = std::max<int64_t>(na, 64) + 2;
-    if ((rc = cgs_alloc(h, &p, sizeof(unsigned long long) * nk)) != MIS2_OK) return fail(rc);
-    cnt = (unsigned long long*)p;
     void* tmp;
-    if ((rc = cgs_alloc(h, &tmp, scan64_ws_bytes(nk))) != MIS2_OK) return fail(rc);
+    const int64_t nk = std::max<int64_t>(na, 64) + 2;
+    // one allocation for the handle's arrays and the setup scratch
+    auto layout = [&](Carve& c) {
+        h->diag = c.take<double>((size_t)n + 1);
+        h->cptr = c.take<int64_t>((size_t)na + 2);
+        h->crows = c.take<int32_t>((size_t)n + 1);
+        h->cset = c.take<int32_t>((size_t)na + 1);
+        err = c.take<int>(16);
+        ccolor = c.take<int32_t>((size_t)na + 1);
+        cnt = c.take<unsigned long long>((size_t)nk);
+        tmp = c.take<char>(scan64_ws_bytes(nk));
+    };
+    Carve dry(nullptr, 0);
+    layout(dry);
+    if ((rc = cgs_alloc(h, &p, dry.off)) != MIS2_OK) return fail(rc);
+    Carve cv(p, dry.off);
+    layout(cv);
     if (cudaMemsetAsync(err, 0, 64, s) != cudaSuccess) return fail(MIS2_ECUDA);
     if (n) {
         k_diag<<<grid_for(n, di.sms), 256, 0, s>>>(n, g->rowptr, g->colinds, vals, h->diag, err);
