@@ -291,17 +291,44 @@ __global__ void k_cgs_color(const int64_t* __restrict__ rowptr, const int32_t* _
 }
 
 // Point multicolor GS (every cluster one row): a thread per row of the colour.
+// Point GS, one colour: G lanes per row (coalesced row reads, 8 independent
+// gathers of x in flight per lane), lane-strided partial sums added by a
+// shuffle tree (fixed order, so the sweep is deterministic).
+template <int G>
 __global__ void k_pgs_color(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colinds,
                             const double* __restrict__ vals, const double* __restrict__ diag,
                             const int32_t* __restrict__ cset, int64_t set_lo, int64_t set_hi,
                             const double* __restrict__ b, double* __restrict__ x) {
-    for (int64_t k = set_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < set_hi;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = cset[k];
-        const int64_t s = rowptr[i], e = rowptr[i + 1];
+    constexpr int RPW = 32 / G;
+    const int lane = threadIdx.x & 31, grp = lane / G, sub = lane % G;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (int64_t base = set_lo + gwarp * RPW; base < set_hi; base += nwarps * RPW) {
+        const int64_t k = base + grp;
+        const bool valid = k < set_hi;
+        int64_t i = 0;
         double acc = 0.0;
-        for (int64_t j = s; j < e; j++) acc += vals[j] * x[colinds[j]];
-        x[i] = x[i] + (b[i] - acc) / diag[i];
+        if (valid) {
+            i = cset[k];
+            const int64_t s = rowptr[i], e = rowptr[i + 1];
+            for (int64_t j0 = s + sub; j0 < e; j0 += 8 * G) {
+                int32_t c[8];
+                double a[8], xv[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const int64_t j = j0 + (int64_t)q * G;
+                    c[q] = j < e ? colinds[j] : -1;
+                    a[q] = j < e ? vals[j] : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; q++) xv[q] = c[q] >= 0 ? x[c[q]] : 0.0;
+#pragma unroll
+                for (int q = 0; q < 8; q++) acc += a[q] * xv[q];
+            }
+        }
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
+        if (valid && sub == 0) x[i] = x[i] + (b[i] - acc) / diag[i];
     }
 }
 
@@ -541,8 +568,20 @@ int mis2_cgs_apply(mis2_cgs* h, const double* b, double* x, int sweeps, int dire
                 const int64_t lo = h->csptr[c], hi = h->csptr[c + 1];
                 if (hi <= lo) continue;
                 if (h->point) {  // a thread per row
-                    k_pgs_color<<<grid_for(hi - lo, di.sms), 256, 0, s>>>(h->g.rowptr, h->g.colinds, h->vals,
-                                                                          h->diag, h->cset, lo, hi, b, x);
+                    const double avg = h->n ? (double)h->g.nnz / (double)h->n : 0.0;
+                    const int G = avg < 4 ? 1 : avg < 8 ? 2 : avg < 16 ? 4 : avg < 40 ? 8 : avg < 100 ? 16 : 32;
+                    int64_t blocks = ((hi - lo) * G + 255) / 256;
+                    if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
+                    if (blocks < 1) blocks = 1;
+                    const dim3 gb((unsigned)blocks), tb(256);
+                    switch (G) {
+                        case 1: k_pgs_color<1><<<gb, tb, 0, s>>>(h->g.rowptr, h->g.colinds, h->vals, h->diag, h->cset, lo, hi, b, x); break;
+                        case 2: k_pgs_color<2><<<gb, tb, 0, s>>>(h->g.rowptr, h->g.colinds, h->vals, h->diag, h->cset, lo, hi, b, x); break;
+                        case 4: k_pgs_color<4><<<gb, tb, 0, s>>>(h->g.rowptr, h->g.colinds, h->vals, h->diag, h->cset, lo, hi, b, x); break;
+                        case 8: k_pgs_color<8><<<gb, tb, 0, s>>>(h->g.rowptr, h->g.colinds, h->vals, h->diag, h->cset, lo, hi, b, x); break;
+                        case 16: k_pgs_color<16><<<gb, tb, 0, s>>>(h->g.rowptr, h->g.colinds, h->vals, h->diag, h->cset, lo, hi, b, x); break;
+                        default: k_pgs_color<32><<<gb, tb, 0, s>>>(h->g.rowptr, h->g.colinds, h->vals, h->diag, h->cset, lo, hi, b, x); break;
+                    }
                 } else {
                     int64_t blocks = (hi - lo + 7) / 8;  // 8 warps per block, a warp per cluster
                     if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
