@@ -474,6 +474,35 @@ def test_cluster_sgs_gpu(point):
         cg.close()
 
 
+@pytest.mark.parametrize("size", [5, 32, 33, 64, 65, 90])
+def test_cluster_sgs_given_clusters(size):
+    """Clusters given by the caller: rows in blocks of `size` (clusters of
+    up to 90 rows, rows of a cluster adjacent to each other), against the
+    oracle with the same clusters and the oracle's colouring of the oracle's
+    coarse graph."""
+    rng = np.random.default_rng(size)
+    for g0 in [G.laplace3d_27pt(7), G.grid2d_5pt(20, 13), G.random_graph(400, 0.02, 9)]:
+        g, vals = G.spd_values(g0, seed=5)
+        labels = (np.arange(g.n) // size).astype(np.int32)
+        na = int(labels.max()) + 1
+        crow, ccol = O.coarsen(g.rowptr, g.colinds, labels, na)
+        ccolor, nc = O.color_jp(crow, ccol)
+        rp, ci = dev(g)
+        coarse = (torch.from_numpy(np.asarray(crow, dtype=np.int64)).cuda(),
+                  torch.from_numpy(np.asarray(ccol, dtype=np.int32)).cuda())
+        cg = M().ClusterSGS(rp, ci, torch.from_numpy(vals).cuda(), labels=torch.from_numpy(labels).cuda(),
+                            num_aggs=na, coarse=coarse)
+        assert cg.ncolors == nc
+        b = rng.standard_normal(g.n)
+        x0 = rng.standard_normal(g.n)
+        for direction in ("forward", "backward", "symmetric"):
+            x = torch.from_numpy(x0.copy()).cuda()
+            cg.apply(torch.from_numpy(b).cuda(), x, sweeps=2, direction=direction)
+            want = O.cluster_sgs(g.rowptr, g.colinds, vals, labels, na, ccolor, nc, b, x0, 2, direction)
+            assert np.allclose(x.cpu().numpy(), want, rtol=1e-12, atol=1e-12 * np.abs(want).max()), (g.name, direction)
+        cg.close()
+
+
 def test_cluster_sgs_errors():
     g = G.grid2d_5pt(4, 4)  # no stored diagonal values -> A_ii missing
     rp, ci = dev(G.strip_diagonal(g))
