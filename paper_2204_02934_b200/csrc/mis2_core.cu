@@ -1521,13 +1521,16 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     }
     // Decide form per iteration: push (its per-row push / count overhead
     // amortised over long rows) for every iteration of a dense graph; for a
-    // medium one only in iteration 0, where no M is OUT yet (nothing to
-    // push) and the pull form's full second sweep over all rows is replaced
-    // by one count per row; pull otherwise.  Measured on C5 (avg degree 80),
-    // C2 (26.5), C3 (7).  MIS2_FLAG_PUSH_DECIDE / PULL_DECIDE force a form
-    // (MIS2_PUSH_ITERS: measurement knob).
+    // medium one in iterations 0 and 1: in iteration 0 no M is OUT yet
+    // (nothing to push) and the pull form's full second sweep over all rows
+    // is replaced by one count per row; in iteration 1 ~99% of the rows are
+    // still undecided, so the pull Decide is again a full sweep (C2 push
+    // iterations 1 / 2 / 3: 376.8 / 374.8 / 374.9 us).  Pull otherwise.
+    // Measured on C5 (avg degree 80), C2 (26.5), C3 (7).
+    // MIS2_FLAG_PUSH_DECIDE / PULL_DECIDE force a form (MIS2_PUSH_ITERS:
+    // measurement knob).
     const double avg_deg = g.n > 0 ? (double)g.nnz / (double)g.n : 0.0;
-    int push_iters = avg_deg >= 32.0 ? max_iters : (avg_deg >= 16.0 ? 1 : 0);
+    int push_iters = avg_deg >= 32.0 ? max_iters : (avg_deg >= 16.0 ? 2 : 0);
     if (o.flags & MIS2_FLAG_PUSH_DECIDE) push_iters = max_iters;
     if (o.flags & MIS2_FLAG_PULL_DECIDE) push_iters = 0;
     if (const char* e = getenv("MIS2_PUSH_ITERS")) push_iters = atoi(e);
