@@ -154,6 +154,12 @@ __device__ __forceinline__ void group_best(int& c, int& s, int& a) {
 }
 
 constexpr int kHeavyDeg = 512;
+#ifndef MIS2_P3LIST
+#define MIS2_P3LIST 8
+#endif
+// distinct candidate aggregates kept per lane in phase 3 (C5 aggregation
+// 18.4 / 20.4 / 26.1 ms with 8 / 12 / 16: register pressure beyond 8)
+constexpr int kP3List = MIS2_P3LIST;
 
 // Phase 3 for leftover rows of degree <= kHeavyDeg: each lane
 // takes candidate entries and counts their coupling over the whole row.
@@ -174,12 +180,12 @@ __global__ void k_phase3(int64_t n, const int64_t* __restrict__ rowptr, const in
         // few aggregates); the group then adds up the lanes' counts by
         // shuffles.  A lane with more than 8 -> the group takes the quadratic
         // pass below.
-        int32_t lab[8];
-        int cnt[8];
+        int32_t lab[kP3List];
+        int cnt[kP3List];
         int nl = 0;
         bool overflow = false;
 #pragma unroll
-        for (int q = 0; q < 8; q++) {
+        for (int q = 0; q < kP3List; q++) {
             lab[q] = -1;
             cnt[q] = 0;
         }
@@ -201,15 +207,15 @@ __global__ void k_phase3(int64_t n, const int64_t* __restrict__ rowptr, const in
                     if (a < 0) continue;
                     bool found = false;
 #pragma unroll
-                    for (int q = 0; q < 8; q++)
+                    for (int q = 0; q < kP3List; q++)
                         if (lab[q] == a) {
                             cnt[q]++;
                             found = true;
                         }
                     if (!found) {
-                        if (nl < 8) {
+                        if (nl < kP3List) {
 #pragma unroll
-                            for (int q = 0; q < 8; q++)
+                            for (int q = 0; q < kP3List; q++)
                                 if (q == nl) {
                                     lab[q] = a;
                                     cnt[q] = 1;
@@ -222,24 +228,24 @@ __global__ void k_phase3(int64_t n, const int64_t* __restrict__ rowptr, const in
                 }
             }
         }
-        int tot[8];
+        int tot[kP3List];
 #pragma unroll
-        for (int q = 0; q < 8; q++) tot[q] = cnt[q];
+        for (int q = 0; q < kP3List; q++) tot[q] = cnt[q];
 #pragma unroll 1
         for (int r = 1; r < G; r++) {
             overflow |= __shfl_xor_sync(kFull, (int)overflow, r) != 0;
 #pragma unroll
-            for (int q2 = 0; q2 < 8; q2++) {
+            for (int q2 = 0; q2 < kP3List; q2++) {
                 const int32_t l2 = __shfl_xor_sync(kFull, lab[q2], r);
                 const int c2 = __shfl_xor_sync(kFull, cnt[q2], r);
 #pragma unroll
-                for (int q = 0; q < 8; q++)
+                for (int q = 0; q < kP3List; q++)
                     if (l2 >= 0 && lab[q] == l2) tot[q] += c2;
             }
         }
         if (left && !is_heavy && !overflow) {
 #pragma unroll
-            for (int q = 0; q < 8; q++)
+            for (int q = 0; q < kP3List; q++)
                 if (q < nl) {
                     const int sz = size[lab[q]];
                     if (better(tot[q], sz, lab[q], bc, bs, ba)) { bc = tot[q]; bs = sz; ba = lab[q]; }
