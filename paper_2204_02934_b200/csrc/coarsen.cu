@@ -41,7 +41,12 @@ __global__ void k_seglen(int64_t n, const int64_t* __restrict__ rowptr, const in
 // few entries per fine row instead of its degree (duplicates across lanes and
 // flushes remain; step 4 removes them).  A segment's used length is
 // cursor[a] - sptr[a] <= its capacity seglen[a].
-constexpr int kFillList = 8;
+#ifndef MIS2_FILL_LIST
+#define MIS2_FILL_LIST 6
+#endif
+// list size measured (coarsen ms, C5 / C2 / C3): 4 -> 2.69 / 0.284 / 4.33,
+// 6 -> 2.70 / 0.275 / 4.31, 8 -> ~2.9 / 0.275 / 4.38, 12 -> 3.72 / 0.300 / 4.49
+constexpr int kFillList = MIS2_FILL_LIST;
 template <int G>
 __global__ void k_fill(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colinds,
                        const int32_t* __restrict__ labels, unsigned long long* __restrict__ cursor,
