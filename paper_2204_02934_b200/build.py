@@ -11,8 +11,9 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmis2.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=default", "-shared",
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=default",
          "--expt-relaxed-constexpr", "-Xptxas", "-O3"]
+OBJDIR = os.path.join(HERE, "build")
 
 
 def nccl_include():
@@ -41,11 +42,40 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
+def _headers():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))) + [
+        os.path.join(HERE, "..", "include", "mis2.h")]
+
+
+def _compile(src: str, inc: str, verbose: bool) -> str:
+    """One translation unit -> build/<name>.o (skipped when newer than its source and the headers)."""
+    obj = os.path.join(OBJDIR, os.path.basename(src)[:-3] + ".o")
+    if os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(p) for p in [src, *_headers()]):
+        return obj
+    tmp = obj + f".tmp{os.getpid()}"
+    cmd = [NVCC, *ARCH, *FLAGS, "-I", inc, "-c", "-o", tmp, src]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+    os.replace(tmp, obj)
+    return obj
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Translation units compile in parallel (one nvcc per .cu), then one link."""
     if not force and not stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJDIR, exist_ok=True)
+    if force:
+        for o in glob.glob(os.path.join(OBJDIR, "*.o")):
+            os.remove(o)
+    inc = nccl_include()
+    srcs = sources()
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(lambda s: _compile(s, inc, verbose), srcs))
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", nccl_include(), "-o", tmp, *sources(), "-ldl"]
+    cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs, "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

@@ -1,0 +1,1303 @@
+// mis2_kernel.cuh -- device code of Alg. 1 (MIS-2, §III-A): the
+// persistent kernel template and the per-phase kernel template of the
+// partitioned driver.  Included by mis2_core.cu (host side, types only) and
+// instantiated per lane-group width G in mis2_g<G>.cu (parallel build).
+#pragma once
+// cooperatively launched sm_100a kernel.
+//
+// Design:
+//  * Each thread block owns a contiguous vertex range [blo, bhi) and works
+//    through it in steps of RPB = 256/G rows, G lanes per CSR row
+//    (§V-D "SIMD parallelism", with a tunable group width).
+//  * worklist_1 / worklist_2 (§V-B) live in the block's slice of
+//    int32[n] arrays, double buffered (in -> out) and compacted with warp
+//    ballots + one shared-memory atomic per warp: no global scan, no global
+//    atomics, no block barrier per step.  The order inside a segment is
+//    free (reading Q11): every phase is a per-vertex function of the
+//    previous phase's arrays.
+//  * Dense phases (iteration 0, and any block whose worklist still covers
+//    >= 3/8 of its range) walk consecutive rows; the colinds of the next
+//    tile are streamed into shared memory by the Blackwell bulk-copy engine
+//    (cp.async.bulk + mbarrier complete_tx), double buffered, while the
+//    current tile gathers T / M.  Worklist membership is read from the
+//    status words (M_v != OUT for worklist_2, T_v undecided for worklist_1).
+//  * Sparse phases read the block's compacted worklist and process rows
+//    straight from global memory.  Rows longer than kHeavyDirect are
+//    deferred and reduced by the whole block.
+//  * Neighbour loops issue predicated batches of independent gathers.
+//  * Phases are separated by a grid-wide barrier; |worklist_1| == 0
+//    is tested on the device, so one call is 1 memset + 1 kernel launch.
+//  * Refresh Row of iteration i+1 is fused into Decide of
+//    iteration i; iteration 0's refresh is the init phase.
+//  * 64-bit status words (Eq. 1, reading Q6): a min is one compare.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace mis2k {
+
+// One block per SM (MIS2_WARPS = 32, the default): co-resident blocks of one
+// SM are not scheduled fairly (the youngest block of an SM finishes a phase
+// ~9 us after the oldest on C2, measured), and a grid barrier over 148
+// blocks costs about half of one over 592.
+#ifndef MIS2_WARPS
+#define MIS2_WARPS 8
+#endif
+constexpr int kMW = MIS2_WARPS;
+constexpr int kMB = 32 * kMW;
+constexpr int kMinBlocksPerSM = kMW >= 16 ? 1 : 4;
+// int32 colinds per staging buffer: a dense step of 27-entry rows
+constexpr int kTileCap = (kMB >= 512 ? kMB / 2 : kMB) * 27;
+// rows longer than 8 gather batches of their lane group are deferred and
+// reduced by the whole block (flattened over all deferred rows of the block)
+// independent gathers per lane per batch of the row loops
+#ifndef MIS2_B1
+#define MIS2_B1 9  // measured: 9 is best on C2 (27 entries = 3 batches, 373 us vs 388 at 16) and near-best on C3
+#endif
+#ifndef MIS2_B4
+#define MIS2_B4 11  // measured on C5 (81-entry rows over 4 lanes = 2 batches): 7.95 ms vs 8.24 at 8
+#endif
+template <int G>
+__host__ __device__ constexpr int gather_batch() {
+    return G == 1 ? MIS2_B1 : (G == 2 ? 16 : (G == 4 ? MIS2_B4 : 4));
+}
+#ifndef MIS2_HEAVY_BATCHES
+#define MIS2_HEAVY_BATCHES 8
+#endif
+template <int G>
+__host__ __device__ constexpr int heavy_len() {
+    return MIS2_HEAVY_BATCHES * G * gather_batch<G>();
+}
+constexpr int kDenseNum = 3, kDenseDen = 8;  // dense if |worklist segment| >= 3/8 of the range (pull phases)
+// M_v is only ever compared against T_v (Decide: "M_w = T_v", "M_w = OUT").
+// By Eq. 1 the low b bits of an undecided word are id+1, unique per vertex,
+// never 0 and never all ones (2^b - 1 > |V|), and M_w is always a
+// word of the CURRENT iteration (worklist_2 vertices are recomputed every
+// iteration, the others hold OUT).  Hence M_w = T_v  <=>  id(M_w) = v + 1 and
+// M_w = OUT <=> id(M_w) = all ones, so M is stored as a uint32 id field:
+//   kM_OUT   : M_v = OUT
+//   0        : inactive vertex (phase 2, reading Q15) -- ignored by Decide
+//   a + 1    : M_v = T_a (a = argmin of T over N[v])
+constexpr uint32_t kM_OUT = 0xffffffffu;
+constexpr uint32_t kPending = 1u;  // M of an active vertex before its first column pass
+
+struct MisParams {
+    int64_t n;       // rows processed (all of them, or the owned rows of a partition)
+    int64_t gbase;   // global id of local row 0 (0 on one GPU): hashes and ids use gbase + v
+    int64_t nnz;
+    const int64_t* __restrict__ rowptr;
+    const int32_t* __restrict__ colinds;
+    const int32_t* __restrict__ labels;  // phase-2 mask (active iff labels[v] < 0) or null
+    uint64_t* T;                         // row status T_v (64-bit packed word, Eq. 1)
+    uint32_t* M;                         // column status M_v, stored as its id field (see below)
+    uint32_t* K;                         // 32-bit column keys of T (kkey), maintained when non-null
+    int keys_mode;                       // K non-null: 1 = use the keys, 0 = use them iff the degrees are skewed
+    uint32_t id_mask;                    // 2^b - 1
+    int32_t* L1[2];                      // worklist_1, double buffered, per-block segments
+    int32_t* L2[2];                      // worklist_2
+    unsigned long long* ctrl;
+    int32_t* heavy;       // [n] deferred long rows, per-block segments at blo
+    uint8_t* oflag;       // push-form Decide: some w in N[v] got M_w = OUT this iteration
+    uint32_t* cnt;        // push-form Decide: |{w in N[v] : M_w = T_v}| this iteration
+    uint32_t* degc;       // |N[v] ∩ active| (closed), written by the column pass of iteration 0
+    unsigned int* mark;   // stats only
+    long long* dstats;    // stats only
+    long long* timeline;  // MIS2_FLAG_TIMELINE only
+    float l2_keep;        // fraction of each block's colinds span kept in L2 (evict_last)
+    int push_iters;       // PUSH kernels: iterations it < push_iters use the push-form Decide
+    int dbg_it, dbg_ph;   // MIS2_FLAG_TIMELINE: sparse phase instrumented into `mark`
+    Prio prio;
+    int max_iters;
+    uint8_t* in_set;
+    int64_t* d_count;
+    int32_t* d_iters;
+    int32_t* d_status;
+};
+
+// per block: the column passes use the 32-bit keys (decided once per call,
+// after the init phase; see the kernel)
+__shared__ int s_use_keys;
+
+struct __align__(16) TileSmem {
+    int32_t buf[2][kTileCap + 8];
+    unsigned long long mbar[2];   // dense tiles: one arrival (thread 0)
+    unsigned long long mbarS[2];  // sparse tiles: one arrival per row group
+    int64_t sal[2];  // 16-byte aligned colinds start of the staged span
+    int32_t fits[2];
+    uint64_t pol;    // L2 policy of this block's colinds span
+    int cnt;         // survivors written this phase
+    int hcount;
+    int hnext;       // deferred rows: next row for a warp
+    int nhuge;       // deferred rows too long for a warp
+    uint64_t red64[kMW];
+    int wred[kMW];
+};
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+// Blackwell bulk-copy engine: global -> shared, completion on an mbarrier
+// with an L2 eviction-priority policy (see l2_policy)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* b,
+                                         uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+        : "memory");
+}
+// L2 residency of the CSR stream.  Every phase re-streams colinds; C2's
+// 106 MB fits the 126 MB L2 but, with T, M, rowptr and the worklists also
+// cycling through it, a plain LRU-like replacement of a cyclic scan larger
+// than the cache keeps almost none of it between passes.  Each block marks
+// the first `keep` fraction of its own colinds span evict_last and the rest
+// evict_first, so a fixed, evenly spread part of the stream stays resident
+// from phase to phase (all blocks see the same hit rate).  The span is
+// demoted back to evict_normal when the call ends (l2_release).
+__device__ __forceinline__ uint64_t l2_policy(const MisParams& p, int64_t blo, int64_t bhi) {
+    const int64_t s0 = p.rowptr[blo] & ~(int64_t)31, s1 = p.rowptr[bhi];
+    const char* base = reinterpret_cast<const char*>(p.colinds + s0);
+    int64_t tot = (s1 - s0) * 4 + 128;
+    if (tot > 0x7fffff00ll) tot = 0x7fffff00ll;
+    const int64_t prim = (int64_t)((double)tot * (double)p.l2_keep) & ~(int64_t)127;
+    uint64_t pol;
+    if (p.l2_keep <= 0.f) {
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+        return pol;
+    }
+    asm volatile("createpolicy.range.global.L2::evict_last.L2::evict_first.b64 %0, [%1], %2, %3;"
+                 : "=l"(pol)
+                 : "l"(base), "r"((uint32_t)prim), "r"((uint32_t)tot));
+    return pol;
+}
+__device__ __forceinline__ void l2_release(const MisParams& p, int64_t blo, int64_t bhi) {
+    if (p.l2_keep <= 0.f) return;
+    const int64_t s0 = p.rowptr[blo] & ~(int64_t)31, s1 = p.rowptr[bhi];
+    const int64_t prim = (int64_t)((double)((s1 - s0) * 4 + 128) * (double)p.l2_keep);
+    const char* base = reinterpret_cast<const char*>(p.colinds + s0);
+    for (int64_t o = (int64_t)threadIdx.x * 128; o < prim; o += (int64_t)blockDim.x * 128)
+        asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(base + o) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ------------------------------------------------------------ block helpers
+// Warp-aggregated append of the group leaders' survivors to out[base + ...]
+// (one shared atomic per warp; order inside the segment is free, Q11).
+__device__ __forceinline__ void append(TileSmem& sm, bool keep, int32_t v, int32_t* out, int64_t base) {
+    const unsigned ball = __ballot_sync(kFull, keep);
+    if (ball == 0) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(ball) - 1;
+    int pos = 0;
+    if (lane == leader) pos = atomicAdd(&sm.cnt, __popc(ball));
+    pos = __shfl_sync(kFull, pos, leader);
+    if (keep) out[base + pos + __popc(ball & lanemask_lt())] = v;
+}
+
+__device__ __forceinline__ uint64_t block_min_u64(TileSmem& sm, uint64_t x) {
+    x = group_min<32>(x);
+    const int warp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) sm.red64[warp] = x;
+    __syncthreads();
+    uint64_t r = sm.red64[0];
+#pragma unroll
+    for (int w = 1; w < kMW; w++) r = sm.red64[w] < r ? sm.red64[w] : r;
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ long long block_sum_int(TileSmem& sm, int x) {
+    x = group_sum<32>(x);
+    if ((threadIdx.x & 31) == 0) sm.wred[threadIdx.x >> 5] = x;
+    __syncthreads();
+    long long s = 0;
+#pragma unroll
+    for (int w = 0; w < kMW; w++) s += sm.wred[w];
+    __syncthreads();
+    return s;
+}
+
+// ------------------------------------------------------------ statistics
+struct Stat {
+    long long r = 0, e = 0, d = 0;
+};
+template <bool STATS>
+__device__ __forceinline__ void stat_row(const MisParams& p, unsigned tag, int64_t v, bool leader, int64_t deg,
+                                         Stat& st) {
+    if (STATS && leader) {
+        st.r++;
+        st.e += deg;
+        if (atomicMax(&p.mark[v], tag) < tag) st.d++;
+    }
+}
+template <bool STATS>
+__device__ __forceinline__ void stat_nbrs(const MisParams& p, unsigned tag, const int32_t* x, int64_t len, int sub,
+                                          int stride, Stat& st) {
+    if (STATS)
+        for (int64_t j = sub; j < len; j += stride)
+            if (atomicMax(&p.mark[x[j]], tag) < tag) st.d++;
+}
+template <bool STATS>
+__device__ __forceinline__ void stats_flush(const MisParams& p, int it, int slot0, Stat st) {
+    if (!STATS) return;
+    st.r = warp_sum_ll(st.r);
+    st.e = warp_sum_ll(st.e);
+    st.d = warp_sum_ll(st.d);
+    if ((threadIdx.x & 31) == 0) {
+        long long* o = p.dstats + 6 * it;
+        if (st.r) atomicAdd((unsigned long long*)&o[slot0], (unsigned long long)st.r);
+        if (st.e) atomicAdd((unsigned long long*)&o[slot0 + 2], (unsigned long long)st.e);
+        if (st.d) atomicAdd((unsigned long long*)&o[slot0 + 4], (unsigned long long)st.d);
+    }
+}
+
+// ------------------------------------------------------------ row kernels
+// Refresh Column of one row: min of T over the row's entries x[0..len)
+// (x is shared memory or global; generic addressing), lanes sub, sub+G, ...
+// Indices past the row end are clamped to its last entry: min / exists /
+// forall are idempotent, so a repeated entry never changes the result and the
+// loads need no predicate.
+template <int G>
+__device__ __forceinline__ uint64_t row_min(const uint64_t* __restrict__ T, const int32_t* x, int len, int sub,
+                                            uint64_t m) {
+    constexpr int B = gather_batch<G>();
+    const int last = len - 1;
+    for (int j = sub; j < len; j += B * G) {
+        uint64_t tt[B];
+#pragma unroll
+        for (int q = 0; q < B; q++) tt[q] = T[x[min(j + q * G, last)]];
+#pragma unroll
+        for (int q = 0; q < B; q++) m = tt[q] < m ? tt[q] : m;
+        if (m == kIN) break;  // IN is the least word: the row's M is OUT whatever follows
+    }
+    return m;
+}
+
+// The same, also counting the entries w != self with T_w != OUT (iteration 0:
+// exactly the active neighbours) for the push-form Decide.  Clamped repeats
+// are not counted.
+template <int G>
+__device__ __forceinline__ uint64_t row_min_deg(const uint64_t* __restrict__ T, const int32_t* x, int len, int sub,
+                                                uint64_t m, int64_t self, int& dc) {
+    constexpr int B = gather_batch<G>();
+    const int last = len - 1;
+    for (int j = sub; j < len; j += B * G) {
+        uint64_t tt[B];
+        int ww[B];
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            ww[q] = x[min(j + q * G, last)];
+            tt[q] = T[ww[q]];
+        }
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            m = tt[q] < m ? tt[q] : m;
+            dc += (j + q * G <= last) & (tt[q] != kOUT) & ((int64_t)ww[q] != self);
+        }
+    }
+    return m;
+}
+
+// Refresh Column on 32-bit keys (KEYS: p.K != null): the gathers read
+// K_w = kkey(T_w) -- half the bytes of T, so K of a 16.7M-vertex graph stays
+// L2-resident where T does not.  Two minima are kept: of (K_w, w) and of
+// (K_w, ~w); their key parts are the least key, their id parts the least and
+// the greatest id holding it.  Different ids = a tie in the key class, which
+// the caller resolves on the full words.
+__device__ __forceinline__ uint64_t key_lo(uint32_t k, uint32_t w) { return ((uint64_t)k << 32) | w; }
+__device__ __forceinline__ uint64_t key_hi(uint32_t k, uint32_t w) { return ((uint64_t)k << 32) | (~w); }
+template <int G>
+__device__ __forceinline__ void row_min_keys(const uint32_t* __restrict__ K, const int32_t* x, int len, int sub,
+                                             uint64_t& k1, uint64_t& k2) {
+    constexpr int B = gather_batch<G>();
+    const int last = len - 1;
+    for (int j = sub; j < len; j += B * G) {
+        uint32_t kk[B];
+        int32_t ww[B];
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            ww[q] = x[min(j + q * G, last)];
+            kk[q] = K[ww[q]];
+        }
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            const uint64_t a = key_lo(kk[q], (uint32_t)ww[q]), b = key_hi(kk[q], (uint32_t)ww[q]);
+            k1 = a < k1 ? a : k1;
+            k2 = b < k2 ? b : k2;
+        }
+        if ((k1 >> 32) == 0u) break;  // an IN neighbour: M is OUT
+    }
+}
+
+// Decide of one row on id fields: exists M_w = OUT / forall
+// M_w = T_v (id v+1); M_w = 0 (inactive, reading Q15) is ignored.
+__device__ __forceinline__ void decide_acc(uint32_t m, uint32_t vid1, int& any_out, int& all_eq) {
+    any_out |= (m == kM_OUT);
+    all_eq &= (m == vid1) | (m == 0u);
+}
+template <int G>
+__device__ __forceinline__ void row_decide(const uint32_t* __restrict__ M, const int32_t* x, int len, int sub,
+                                           uint32_t vid1, int& any_out, int& all_eq) {
+    constexpr int B = gather_batch<G>();
+    const int last = len - 1;
+    for (int j = sub; j < len; j += B * G) {
+        uint32_t mm[B];
+#pragma unroll
+        for (int q = 0; q < B; q++) mm[q] = M[x[min(j + q * G, last)]];
+#pragma unroll
+        for (int q = 0; q < B; q++) decide_acc(mm[q], vid1, any_out, all_eq);
+        if (any_out) break;  // the row is OUT whatever follows
+    }
+}
+
+// M_v from the column minimum m (IN -> OUT)
+__device__ __forceinline__ uint32_t m_field(uint64_t m, uint32_t id_mask) {
+    return (m == kIN || m == kOUT) ? kM_OUT : (uint32_t)m & id_mask;
+}
+
+// 32-bit column key of a status word (KEYS kernels): IN -> 0, OUT -> all
+// ones, an undecided word -> its top 32 bits clamped to [1, 2^32 - 2].  The
+// key order agrees with the word order except inside a class of equal keys,
+// which the column pass detects and resolves on the full words (row_min_keys).
+__device__ __forceinline__ uint32_t kkey(uint64_t t) {
+    if (t == kIN) return 0u;
+    if (t == kOUT) return 0xffffffffu;
+    const uint32_t k = (uint32_t)(t >> 32);
+    return k == 0u ? 1u : (k == 0xffffffffu ? 0xfffffffeu : k);
+}
+__device__ __forceinline__ void set_T(const MisParams& p, int64_t v, uint64_t t) {
+    p.T[v] = t;
+    if (p.K) p.K[v] = kkey(t);
+}
+
+__device__ __forceinline__ bool decide_write(const MisParams& p, int64_t v, int any_out, int all_eq, int it,
+                                             uint64_t fi_next) {
+    if (any_out) {
+        set_T(p, v, kOUT);
+        return false;
+    }
+    if (all_eq) {
+        set_T(p, v, kIN);
+        return false;
+    }
+    set_T(p, v, p.prio.word(it + 1, fi_next, p.gbase + v));  // fused Refresh Row
+    return true;
+}
+
+// issue the bulk copy of colinds[s, e) (16-byte aligned hull) into buffer `slot`
+__device__ __forceinline__ void stage_tile(TileSmem& sm, const MisParams& p, int slot, int64_t s, int64_t e) {
+    const int64_t sal = s & ~(int64_t)3;
+    const int64_t nnz4 = p.nnz & ~(int64_t)3;
+    const int64_t ecp = (e + 3) & ~(int64_t)3;
+    const bool fits = (ecp - sal) <= kTileCap && ecp <= nnz4;
+    sm.sal[slot] = sal;
+    sm.fits[slot] = fits;
+    // no proxy fence: the buffer was only READ by the generic proxy before the
+    // __syncthreads that precedes this call (write-after-read needs no
+    // fence.proxy.async, which would also drain this thread's global stores)
+    if (fits && ecp > sal) {
+        mbar_expect_tx(&sm.mbar[slot], (uint32_t)((ecp - sal) * 4));
+        bulk_g2s(sm.buf[slot], p.colinds + sal, (uint32_t)((ecp - sal) * 4), &sm.mbar[slot], sm.pol);
+    } else {
+        mbar_expect_tx(&sm.mbar[slot], 0u);
+    }
+}
+
+// One row, GG lanes: Refresh Column (PH 0) or Decide (PH 1).  Returns the
+// survivor flag in the group leader.  Must be called by all lanes.
+// PUSH (single GPU): the column pass also does the edge work of Decide.
+// A row whose M_w becomes OUT marks every w' in N[w] (oflag: "some
+// neighbour has M = OUT", the first test of P:98-100); otherwise it counts
+// itself for its argmin a (cnt[a]; "forall w: M_w = T_a" of P:101-103 holds
+// iff cnt[a] = |N[a] ∩ active|).  Sound because a vertex still undecided at
+// iteration i has every active neighbour in worklist_2 (a neighbour that
+// left it earlier had M = OUT and made the vertex OUT then), so every
+// neighbour's M of iteration i is either pushed or counted.  Decide then
+// touches no edges (decide_push).
+__device__ __forceinline__ void push_out(const MisParams& p, const int32_t* x, int len, int sub, int stride) {
+    for (int j = sub; j < len; j += stride) p.oflag[x[j]] = 1;
+}
+
+template <int GG, int PH, bool PUSH>
+__device__ __forceinline__ bool process_row(const MisParams& p, bool act, int sub, int64_t v, const int32_t* x,
+                                            int len, uint64_t tv, int it, uint64_t fi_next) {
+    bool keep = false;
+    if (PH == 0) {
+        uint32_t mf;
+        int dc = 0;
+        if (p.K && s_use_keys && !(PUSH && it == 0 && p.labels)) {
+            // keys (single GPU: local ids are global ids)
+            uint64_t k1 = ~0ull, k2 = ~0ull;
+            if (act && sub == 0) {  // closed neighbourhood (Q1)
+                k1 = key_lo(kkey(tv), (uint32_t)v);
+                k2 = key_hi(kkey(tv), (uint32_t)v);
+            }
+            if (act && len > 0) row_min_keys<GG>(p.K, x, len, sub, k1, k2);
+            k1 = group_min<GG>(k1);
+            k2 = group_min<GG>(k2);
+            const uint32_t kmin = (uint32_t)(k1 >> 32);
+            const bool tie = act && kmin != 0u && kmin != 0xffffffffu && (uint32_t)k1 != ~(uint32_t)k2;
+            mf = (kmin == 0u || kmin == 0xffffffffu) ? kM_OUT : (uint32_t)k1 + 1u;
+            if (__any_sync(kFull, tie)) {  // equal keys: the full words decide
+                uint64_t m = (tie && sub == 0) ? tv : kOUT;
+                if (tie && len > 0) m = row_min<GG>(p.T, x, len, sub, m);
+                m = group_min<GG>(m);
+                if (tie) mf = m_field(m, p.id_mask);
+            }
+        } else {
+            uint64_t m = (act && sub == 0) ? tv : kOUT;  // closed neighbourhood (Q1)
+            if (act && len > 0) {
+                if (PUSH && it == 0 && p.labels) {
+                    m = row_min_deg<GG>(p.T, x, len, sub, m, p.gbase + v, dc);
+                } else {
+                    m = row_min<GG>(p.T, x, len, sub, m);
+                }
+            }
+            m = group_min<GG>(m);
+            mf = m_field(m, p.id_mask);
+        }
+        if (PUSH) {
+            // the warp pushes its OUT rows one after another, 32 entries at a time
+            const int lane = threadIdx.x & 31;
+            unsigned bal = __ballot_sync(kFull, act && sub == 0 && mf == kM_OUT);
+            while (bal) {
+                const int l = __ffs(bal) - 1;
+                bal &= bal - 1;
+                const int32_t* xr = reinterpret_cast<const int32_t*>(
+                    __shfl_sync(kFull, reinterpret_cast<unsigned long long>(x), l));
+                const int lr = __shfl_sync(kFull, len, l);
+                push_out(p, xr, lr, lane, 32);
+                if (lane == l) p.oflag[v] = 1;
+            }
+            // count for the argmin; rows of a warp sharing one argmin add together
+            const bool cnt_me = act && sub == 0 && mf != kM_OUT;
+            const uint32_t key = cnt_me ? mf - 1u : (0x80000000u | (threadIdx.x & 31));
+            const unsigned grp = __match_any_sync(kFull, key);
+            if (cnt_me && (threadIdx.x & 31) == __ffs(grp) - 1)
+                atomicAdd(&p.cnt[(int64_t)key - p.gbase], (uint32_t)__popc(grp));
+            if (it == 0 && p.labels) {
+                dc = group_sum<GG>(dc);
+                if (act && sub == 0) p.degc[v] = (uint32_t)dc + 1u;
+            }
+        }
+        if (act && sub == 0) {
+            p.M[v] = mf;
+            keep = (mf != kM_OUT);
+        }
+    } else {
+        int any_out = 0, all_eq = 1;
+        const uint32_t vid1 = (uint32_t)(p.gbase + v) + 1u;
+        if (act) {
+            if (sub == 0) decide_acc(p.M[v], vid1, any_out, all_eq);
+            if (len > 0) row_decide<GG>(p.M, x, len, sub, vid1, any_out, all_eq);
+        }
+        any_out = group_or<GG>(any_out);
+        all_eq = group_and<GG>(all_eq);
+        if (act && sub == 0) keep = decide_write(p, v, any_out, all_eq, it, fi_next);
+    }
+    return keep;
+}
+
+// defer a long row to whole-block processing (group leader decides, group agrees)
+template <int GG>
+__device__ __forceinline__ bool defer_long(TileSmem& sm, const MisParams& p, int64_t blo, bool act, int sub,
+                                           int64_t v, int64_t len) {
+    bool defer = false;
+    if (act && sub == 0 && len > heavy_len<GG>()) {
+        const int h = atomicAdd(&sm.hcount, 1);
+        p.heavy[blo + h] = (int32_t)v;  // at most one entry per row of the block's range
+        defer = true;
+    }
+    return __shfl_sync(kFull, defer, (threadIdx.x & 31) & ~(GG - 1));
+}
+
+// Deferred long rows, stats flush, survivor count.  The block reduces all its
+// deferred rows together: up to 256 rows per round, their entries flattened
+// (prefix of the row lengths), 8 independent gathers per thread per pass,
+// combined per row with shared-memory atomics (min is exact in any order;
+// exists / forall likewise).
+// One deferred (long) row reduced by NT cooperating threads -- a warp
+// (NT = 32) or the whole block (NT = kMB) -- each issuing 8 independent,
+// coalesced colinds loads and 8 gathers per pass (indices clamped to the
+// row's last entry: min / exists / forall are idempotent).  Writes the row's
+// result like process_row; returns the survivor flag (valid in thread 0 of
+// the group).  All NT threads must call it.
+template <int NT>
+__device__ __forceinline__ uint64_t nt_min(TileSmem& sm, uint64_t x) {
+    if (NT == 32) return group_min<32>(x);
+    return block_min_u64(sm, x);
+}
+template <int NT>
+__device__ __forceinline__ int nt_sum(TileSmem& sm, int x) {
+    if (NT == 32) return group_sum<32>(x);
+    return (int)block_sum_int(sm, x);
+}
+template <int NT, bool STATS, int PH, bool PUSH>
+__device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_next, int64_t v, Stat& st,
+                          unsigned tag) {
+    const int tid = NT == 32 ? (threadIdx.x & 31) : threadIdx.x;
+    const int64_t s = p.rowptr[v], len = p.rowptr[v + 1] - s;
+    const int32_t* x = p.colinds + s;
+    const int64_t last = len - 1;
+    bool keep = false;
+    if (STATS) {
+        stat_row<STATS>(p, tag, v, tid == 0, len, st);
+        stat_nbrs<STATS>(p, tag, x, len, tid, NT, st);
+    }
+    if (PH == 0) {
+        const uint64_t tv = p.T[v];
+        const bool count_deg = PUSH && it == 0 && p.labels;
+        const bool keys = p.K && s_use_keys && !count_deg;
+        uint32_t mf;
+        int dc = 0;
+        bool exact = !keys;
+        if (keys) {
+            uint64_t k1 = tid == 0 ? key_lo(kkey(tv), (uint32_t)v) : ~0ull;
+            uint64_t k2 = tid == 0 ? key_hi(kkey(tv), (uint32_t)v) : ~0ull;
+            for (int64_t j = tid; j < len; j += (int64_t)NT * 8) {
+                int32_t ww[8];
+                uint32_t kk[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) ww[u] = x[min(j + (int64_t)u * NT, last)];
+#pragma unroll
+                for (int u = 0; u < 8; u++) kk[u] = p.K[ww[u]];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const uint64_t a = key_lo(kk[u], (uint32_t)ww[u]), b = key_hi(kk[u], (uint32_t)ww[u]);
+                    k1 = a < k1 ? a : k1;
+                    k2 = b < k2 ? b : k2;
+                }
+            }
+            k1 = nt_min<NT>(sm, k1);
+            k2 = nt_min<NT>(sm, k2);
+            const uint32_t kmin = (uint32_t)(k1 >> 32);
+            mf = (kmin == 0u || kmin == 0xffffffffu) ? kM_OUT : (uint32_t)k1 + 1u;
+            exact = kmin != 0u && kmin != 0xffffffffu && (uint32_t)k1 != ~(uint32_t)k2;  // a key tie
+        }
+        if (exact) {
+            uint64_t m = tid == 0 ? tv : kOUT;  // closed neighbourhood (Q1)
+            for (int64_t j = tid; j < len; j += (int64_t)NT * 8) {
+                int32_t ww[8];
+                uint64_t tt[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) ww[u] = x[min(j + (int64_t)u * NT, last)];
+#pragma unroll
+                for (int u = 0; u < 8; u++) tt[u] = p.T[ww[u]];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    m = tt[u] < m ? tt[u] : m;
+                    if (count_deg) dc += (j + (int64_t)u * NT <= last) & (tt[u] != kOUT) & ((int64_t)ww[u] != v);
+                }
+            }
+            m = nt_min<NT>(sm, m);
+            mf = m_field(m, p.id_mask);
+            if (count_deg) dc = nt_sum<NT>(sm, dc);
+        }
+        if (PUSH) {
+            if (mf == kM_OUT) {  // mark N[v] (push-form Decide)
+                for (int64_t j = tid; j < len; j += NT) p.oflag[x[j]] = 1;
+                if (tid == 0) p.oflag[v] = 1;
+            } else if (tid == 0) {
+                atomicAdd(&p.cnt[(int64_t)(mf - 1u) - p.gbase], 1u);
+            }
+            if (count_deg && tid == 0) p.degc[v] = (uint32_t)dc + 1u;
+        }
+        if (tid == 0) {
+            p.M[v] = mf;
+            keep = mf != kM_OUT;
+        }
+    } else {
+        const uint32_t vid1 = (uint32_t)(p.gbase + v) + 1u;
+        int any_out = 0, all_eq = 1;
+        if (tid == 0) decide_acc(p.M[v], vid1, any_out, all_eq);
+        for (int64_t j = tid; j < len; j += (int64_t)NT * 8) {
+            uint32_t mm[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) mm[u] = p.M[x[min(j + (int64_t)u * NT, last)]];
+#pragma unroll
+            for (int u = 0; u < 8; u++) decide_acc(mm[u], vid1, any_out, all_eq);
+            if (any_out) break;  // the row is OUT whatever follows
+        }
+        any_out = nt_sum<NT>(sm, any_out) > 0;
+        all_eq = nt_sum<NT>(sm, !all_eq) == 0;
+        if (tid == 0) keep = decide_write(p, v, any_out, all_eq, it, fi_next);
+    }
+    return keep;
+}
+
+// Deferred long rows, stats flush, survivor count.  Warps take deferred rows
+// from a shared counter and reduce one row each; rows longer than
+// kHugeRow are reduced afterwards by the whole block, one at a time.
+constexpr int kHugeRow = 32768;
+template <bool STATS, int PH, bool PUSH>
+__device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, int32_t* lout, uint64_t fi_next,
+                            Stat& st) {
+    const int t = threadIdx.x, lane = t & 31;
+    const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
+    __syncthreads();
+    const int nh = sm.hcount;
+    const bool dbg = p.timeline && it == p.dbg_it && PH == p.dbg_ph && t == 0;
+    long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
+    if (dbg) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        dbuf[60] = (long long)ns;
+        dbuf[61] = nh;
+    }
+    int32_t* huge = sm.buf[0];  // rows for the whole block (<= nh <= the buffer)
+    if (nh > 0) {
+        if (t == 0) {
+            sm.hnext = 0;
+            sm.nhuge = 0;
+        }
+        __syncthreads();
+        for (;;) {
+            int i = 0;
+            if (lane == 0) i = atomicAdd(&sm.hnext, 1);
+            i = __shfl_sync(kFull, i, 0);
+            if (i >= nh) break;
+            const int64_t v = p.heavy[blo + i];
+            const int64_t len = p.rowptr[v + 1] - p.rowptr[v];
+            if (len > kHugeRow && nh <= 2 * kTileCap) {
+                if (lane == 0) huge[atomicAdd(&sm.nhuge, 1)] = (int32_t)v;
+                continue;
+            }
+            const bool keep = heavy_row<32, STATS, PH, PUSH>(sm, p, it, fi_next, v, st, tag);
+            append(sm, keep && lane == 0, (int32_t)v, lout, blo);
+        }
+        __syncthreads();
+        const int nb = sm.nhuge;
+        for (int k = 0; k < nb; k++) {
+            const int64_t v = huge[k];
+            const bool keep = heavy_row<kMB, STATS, PH, PUSH>(sm, p, it, fi_next, v, st, tag);
+            append(sm, keep && t == 0, (int32_t)v, lout, blo);
+        }
+    }
+    stats_flush<STATS>(p, it, PH == 0 ? 1 : 0, st);
+    if (dbg) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        dbuf[62] = (long long)ns;
+        long long e = 0;
+        for (int i = 0; i < nh; i++) {
+            const int64_t v = p.heavy[blo + i];
+            e += p.rowptr[v + 1] - p.rowptr[v];
+        }
+        dbuf[63] = e;
+    }
+    __syncthreads();
+    const int out = sm.cnt;
+    __syncthreads();
+    return out;
+}
+
+// ------------------------------------------------------------ dense phase
+// Consecutive rows of the block range, RPB = kMB/G per step; the step's
+// colinds span is bulk-copied into shared memory one step ahead.
+// PH = 0: Refresh Column over worklist_2 (M_v != OUT, active)
+// PH = 1: Decide over worklist_1 (T_v undecided)
+template <int G, bool STATS, int PH, bool PUSH = false>
+__device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, int64_t bhi, int32_t* lout,
+                           uint32_t& ph, uint64_t fi_next) {
+    constexpr int RPB = kMB / G;
+    const int t = threadIdx.x, g = t / G, sub = t % G;
+    const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
+    Stat st;
+    if (t == 0) {
+        sm.cnt = 0;
+        sm.hcount = 0;
+    }
+    const int64_t nsteps = (bhi - blo + RPB - 1) / RPB;
+    int64_t nx_s = 0, nx_e = 0;  // bounds of the next tile (thread 0), prefetched a step ahead
+    if (t == 0 && nsteps > 0) {
+        const int64_t r1 = blo + RPB < bhi ? blo + RPB : bhi;
+        const int64_t r2 = r1 + RPB < bhi ? r1 + RPB : bhi;
+        nx_s = p.rowptr[r1];
+        nx_e = p.rowptr[r2];
+        stage_tile(sm, p, 0, p.rowptr[blo], nx_s);
+    }
+    const bool dbg = p.timeline && it == p.dbg_it && PH == p.dbg_ph && threadIdx.x == 0;
+    long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
+    auto gt = []() {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        return (long long)ns;
+    };
+    if (dbg) {
+        dbuf[0] = gt();
+        dbuf[1] = nsteps;
+        dbuf[2] = bhi - blo;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        dbuf[59] = smid;
+    }
+    // prefetched row bounds / status of the next tile (this thread's row)
+    int64_t ns0 = 0, ne0 = 0;
+    uint64_t ntv = kOUT;
+    uint32_t nmv = kM_OUT;
+    if (blo + g < bhi) {
+        ns0 = p.rowptr[blo + g];
+        ne0 = p.rowptr[blo + g + 1];
+        ntv = p.T[blo + g];
+        if (PH == 0) nmv = p.M[blo + g];
+    }
+    for (int64_t k = 0; k < nsteps; k++) {
+        const int slot = (int)(k & 1);
+        if (dbg && k < 12) dbuf[4 + 5 * k] = gt();
+        __syncthreads();  // tile k-1 consumed: its buffer may be refilled
+        if (dbg && k < 12) dbuf[4 + 5 * k + 1] = gt();
+        if (t == 0 && k + 1 < nsteps) {
+            const int64_t s1 = nx_s, e1 = nx_e;
+            const int64_t r2 = blo + (k + 2) * RPB;
+            if (r2 < bhi) {
+                const int64_t r3 = r2 + RPB < bhi ? r2 + RPB : bhi;
+                nx_s = p.rowptr[r2];
+                nx_e = p.rowptr[r3];
+            }
+            stage_tile(sm, p, slot ^ 1, s1, e1);
+        }
+        // this tile's row bounds and status were loaded one step ahead; load
+        // the next tile's now (a phase writes only rows of the tile it is
+        // processing, so the prefetched words are current)
+        const int64_t v = blo + k * RPB + g;
+        const bool valid = v < bhi;
+        const int64_t s = ns0, e = ne0;
+        const uint64_t tv = ntv;
+        bool act = false;
+        if (valid) act = PH == 0 ? (nmv != kM_OUT && nmv != 0u) : (tv != kIN && tv != kOUT);
+        {
+            const int64_t vn = v + RPB;
+            if (vn < bhi) {
+                ns0 = p.rowptr[vn];
+                ne0 = p.rowptr[vn + 1];
+                ntv = p.T[vn];
+                if (PH == 0) nmv = p.M[vn];
+            }
+        }
+        const int64_t len = e - s;
+        if (defer_long<G>(sm, p, blo, act, sub, v, len)) act = false;
+        if (dbg && k < 12) dbuf[4 + 5 * k + 2] = gt();
+        mbar_wait(&sm.mbar[slot], (ph >> slot) & 1u);
+        ph ^= 1u << slot;
+        if (dbg && k < 12) dbuf[4 + 5 * k + 3] = gt();
+        const int32_t* x = sm.fits[slot] ? sm.buf[slot] + (s - sm.sal[slot]) : p.colinds + s;
+        const bool keep = process_row<G, PH, PUSH>(p, act, sub, v, x, (int)len, tv, it, fi_next);
+        if (dbg && k < 12) dbuf[4 + 5 * k + 4] = gt();
+        if (STATS && act) {
+            stat_row<STATS>(p, tag, v, sub == 0, len, st);
+            stat_nbrs<STATS>(p, tag, x, len, sub, G, st);
+        }
+        append(sm, keep, (int32_t)v, lout, blo);
+    }
+    if (dbg) dbuf[3] = gt();
+    return finish_phase<STATS, PH, PUSH>(sm, p, it, blo, lout, fi_next, st);
+}
+
+// ------------------------------------------------------------ sparse phase
+// Rows of the block's compacted worklist, RPBS = kMB/GS per step with
+// GS = 2G lanes per row.  Each group leader bulk-copies its own row into a
+// fixed shared-memory slot (16-byte aligned hull, <= SLOT entries) one step
+// ahead; rows that do not fit are read from global memory.
+struct __align__(16) SMeta {
+    int64_t s;    // rowptr[v]
+    int32_t v;    // vertex (-1: no row)
+    int32_t len;  // row length; bit 30 set: staged in the slot
+};
+constexpr int kMaxDbgBlocks = 1184;
+// sparse step layout of a staging buffer: row slots | SMeta per row | T_v per row
+constexpr int kMaxRowsS = kMB / 2;                    // rows per sparse step (GS >= 2)
+constexpr int kTvOff = kTileCap - 2 * kMaxRowsS;      // uint64 T_v per row
+constexpr int kSlotRegion = kTvOff - 4 * kMaxRowsS;   // entries used for row slots; SMeta after
+static_assert(kSlotRegion > 0 && (kSlotRegion % 4) == 0, "sparse layout");
+
+template <int G, bool STATS, int PH, bool PUSH = false>
+__device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, const int32_t* lin, int nin,
+                            int32_t* lout, uint32_t& ph, uint64_t fi_next) {
+    constexpr int GS = G * 2 <= 32 ? G * 2 : 32;
+    constexpr int RPBS = kMB / GS;
+    constexpr int SLOT = (kSlotRegion / RPBS) & ~3;
+    static_assert(RPBS * sizeof(SMeta) <= (kTileCap - kSlotRegion) * 4, "SMeta region too small");
+    constexpr int kStaged = 1 << 30;
+    const int t = threadIdx.x, gs = t / GS, sub = t % GS;
+    const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
+    Stat st;
+    if (t == 0) {
+        sm.cnt = 0;
+        sm.hcount = 0;
+    }
+    const int nsteps = (nin + RPBS - 1) / RPBS;
+    const int64_t nnz4 = p.nnz & ~(int64_t)3;
+
+    // Leaders pipeline the row metadata: worklist entry of tile j+3, row
+    // bounds of tile j+2 and T_v of tile j+1 are loaded while tile j is
+    // processed, so the copy of tile j+1 is issued without waiting on loads.
+    auto row_of = [&](int j) -> int64_t {
+        const int idx = j * RPBS + gs;
+        return (sub == 0 && j < nsteps && idx < nin) ? (int64_t)lin[blo + idx] : -1;
+    };
+    auto issue = [&](int slot, int64_t v, int64_t s, int64_t e, uint64_t tv) {
+        if (sub != 0) return;
+        SMeta* meta = reinterpret_cast<SMeta*>(sm.buf[slot] + kSlotRegion);
+        SMeta m;
+        m.v = -1;
+        m.s = 0;
+        m.len = 0;
+        uint32_t bytes = 0;
+        int64_t sal = 0;
+        if (v >= 0) {
+            sal = s & ~(int64_t)3;
+            const int64_t ecp = (e + 3) & ~(int64_t)3;
+            const bool fits = (ecp - sal) <= SLOT && ecp <= nnz4;
+            m.v = (int32_t)v;
+            m.s = s;
+            m.len = (int32_t)(e - s) | (fits ? kStaged : 0);
+            if (fits && ecp > sal) bytes = (uint32_t)((ecp - sal) * 4);
+        }
+        meta[gs] = m;
+        reinterpret_cast<uint64_t*>(sm.buf[slot] + kTvOff)[gs] = tv;
+        mbar_expect_tx(&sm.mbarS[slot], bytes);
+        if (bytes) bulk_g2s(sm.buf[slot] + gs * SLOT, p.colinds + sal, bytes, &sm.mbarS[slot], sm.pol);
+    };
+    auto bounds = [&](int64_t v, int64_t& s, int64_t& e) {
+        s = 0;
+        e = 0;
+        if (v >= 0) {
+            s = p.rowptr[v];
+            e = p.rowptr[v + 1];
+        }
+    };
+
+    // prologue
+    int64_t v1 = -1, s1 = 0, e1 = 0, v2 = -1, s2 = 0, e2 = 0, v3 = -1;
+    uint64_t tv1 = kOUT, tv2 = kOUT;
+    if (nsteps > 0) {
+        const int64_t v0 = row_of(0);
+        v1 = row_of(1);
+        v2 = row_of(2);
+        int64_t s0, e0;
+        bounds(v0, s0, e0);
+        bounds(v1, s1, e1);
+        const uint64_t tv0 = v0 >= 0 ? p.T[v0] : kOUT;
+        tv1 = v1 >= 0 ? p.T[v1] : kOUT;
+        issue(0, v0, s0, e0, tv0);
+    }
+    const bool dbg = p.timeline && it == p.dbg_it && PH == p.dbg_ph && threadIdx.x == 0;
+    long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
+    auto gt = []() {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        return (long long)ns;
+    };
+    if (dbg) {
+        dbuf[0] = gt();
+        dbuf[1] = nsteps;
+        dbuf[2] = nin;
+    }
+    for (int k = 0; k < nsteps; k++) {
+        const int slot = k & 1;
+        if (dbg && k < 12) dbuf[4 + 5 * k] = gt();
+        __syncthreads();  // metadata of tile k visible; buffer of tile k-1 free
+        if (dbg && k < 12) dbuf[4 + 5 * k + 1] = gt();
+        if (k + 1 < nsteps) issue(slot ^ 1, v1, s1, e1, tv1);  // no proxy fence needed (see stage_tile)
+        bounds(v2, s2, e2);     // prefetch for tile k+2
+        tv2 = v2 >= 0 ? p.T[v2] : kOUT;
+        v3 = row_of(k + 3);     // prefetch for tile k+3
+        const SMeta m = reinterpret_cast<const SMeta*>(sm.buf[slot] + kSlotRegion)[gs];
+        const bool valid = m.v >= 0;
+        const int64_t v = valid ? m.v : 0;
+        const int len = m.len & ~kStaged;
+        const uint64_t tv = reinterpret_cast<const uint64_t*>(sm.buf[slot] + kTvOff)[gs];
+        bool act = valid;
+        if (defer_long<GS>(sm, p, blo, act, sub, v, len)) act = false;
+        if (dbg && k < 12) dbuf[4 + 5 * k + 2] = gt();
+        mbar_wait(&sm.mbarS[slot], (ph >> (2 + slot)) & 1u);
+        ph ^= 1u << (2 + slot);
+        if (dbg && k < 12) dbuf[4 + 5 * k + 3] = gt();
+        const int32_t* x = (m.len & kStaged) ? sm.buf[slot] + gs * SLOT + (m.s - (m.s & ~(int64_t)3))
+                                             : p.colinds + m.s;
+        const bool keep = process_row<GS, PH, PUSH>(p, act, sub, v, x, len, tv, it, fi_next);
+        if (dbg && k < 12) dbuf[4 + 5 * k + 4] = gt();
+        if (STATS && act) {
+            stat_row<STATS>(p, tag, v, sub == 0, len, st);
+            stat_nbrs<STATS>(p, tag, x, len, sub, GS, st);
+        }
+        append(sm, keep, (int32_t)v, lout, blo);
+        v1 = v2;
+        s1 = s2;
+        e1 = e2;
+        tv1 = tv2;
+        v2 = v3;
+    }
+    if (dbg) dbuf[3] = gt();
+    return finish_phase<STATS, PH, PUSH>(sm, p, it, blo, lout, fi_next, st);
+}
+
+// ------------------------------------------------------------ push-form Decide
+// Decide over worklist_1 when the column pass has already done its
+// edge work (process_row, PUSH): v is OUT iff some M_w = OUT for w in N[v]
+// (oflag[v]); else IN iff every active w in N[v] has M_w = T_v
+// (cnt[v] = degc[v]); else it stays undecided and gets its word of iteration
+// it + 1 (fused Refresh Row).  No neighbour is read.  Dense: all
+// rows of the block range, membership from T_v; sparse: the worklist.
+__device__ __forceinline__ bool row_has(const int32_t* x, int64_t len, int32_t v) {
+    for (int64_t j = 0; j < len; j++)
+        if (x[j] == v) return true;
+    return false;
+}
+template <bool STATS>
+__device__ int decide_push(TileSmem& sm, const MisParams& p, int it, int64_t blo, int64_t bhi, const int32_t* lin,
+                           int nin, bool dense, int32_t* lout, uint64_t fi_next) {
+    const int t = threadIdx.x;
+    const unsigned tag = 2u * (unsigned)it + 2u;
+    Stat st;
+    // IN candidates whose test needs "is v in its own row": resolved after
+    // the loop, one warp per row (a serial scan inside the loop would stall
+    // its warp once per candidate)
+    int32_t* cand = sm.buf[0];
+    constexpr int kCandCap = 2 * kTileCap;
+    if (t == 0) {
+        sm.cnt = 0;
+        sm.hcount = 0;
+    }
+    __syncthreads();
+    const int64_t total = dense ? bhi - blo : (int64_t)nin;
+    const bool dbg = p.timeline && it == p.dbg_it && 1 == p.dbg_ph && t == 0;
+    long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
+    auto gt = []() {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        return (long long)ns;
+    };
+    if (dbg) {
+        dbuf[0] = gt();
+        dbuf[1] = total;
+    }
+    // U rows per thread per round, loads batched by dependency level
+    constexpr int U = 4;
+    for (int64_t base = 0; base < total; base += (int64_t)kMB * U) {
+        int64_t vv[U];
+        uint64_t tv[U];
+        uint32_t c[U];
+        uint8_t fl[U];
+        int64_t rs[U], re[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t idx = base + u * kMB + t;
+            vv[u] = idx < total ? (dense ? blo + idx : (int64_t)lin[blo + idx]) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            tv[u] = kIN;
+            fl[u] = 0;
+            c[u] = 0;
+            if (vv[u] >= 0) {
+                tv[u] = p.T[vv[u]];
+                fl[u] = p.oflag[vv[u]];
+                c[u] = p.cnt[vv[u]];
+            }
+        }
+        // IN candidates of the unmasked call need the row length
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            rs[u] = 0;
+            re[u] = 0;
+            if (vv[u] >= 0 && !p.labels && !fl[u] && c[u] > 0 && tv[u] != kIN && tv[u] != kOUT) {
+                rs[u] = p.rowptr[vv[u]];
+                re[u] = p.rowptr[vv[u] + 1];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t v = vv[u];
+            bool keep = false;
+            if (v >= 0 && tv[u] != kIN && tv[u] != kOUT) {
+                if (c[u]) p.cnt[v] = 0u;
+                bool in = false, later = false;
+                if (!fl[u] && c[u] > 0) {
+                    if (p.labels) {
+                        in = c[u] == p.degc[v];  // |N[v] ∩ active| counted by the column pass of iteration 0
+                    } else {                     // all active: |N[v]| = len + 1 - [v in its own row] (Q23)
+                        const int64_t len = re[u] - rs[u];
+                        if ((int64_t)c[u] == len + 1) {
+                            in = true;
+                        } else if ((int64_t)c[u] == len) {
+                            const int h = atomicAdd(&sm.hcount, 1);
+                            if (h < kCandCap) {
+                                cand[h] = (int32_t)v;
+                                later = true;
+                            } else {
+                                in = row_has(p.colinds + rs[u], len, (int32_t)v);
+                            }
+                        }
+                    }
+                }
+                if (later) {
+                } else if (fl[u]) set_T(p, v, kOUT);
+                else if (in) set_T(p, v, kIN);
+                else {
+                    set_T(p, v, p.prio.word(it + 1, fi_next, p.gbase + v));
+                    keep = true;
+                }
+                if (STATS) {
+                    const int64_t s = p.rowptr[v], e = p.rowptr[v + 1];
+                    stat_row<STATS>(p, tag, v, true, e - s, st);
+                    stat_nbrs<STATS>(p, tag, p.colinds + s, e - s, 0, 1, st);
+                }
+            }
+            append(sm, keep, (int32_t)(v < 0 ? 0 : v), lout, blo);
+        }
+    }
+    if (dbg) dbuf[2] = gt();
+    __syncthreads();
+    if (dbg) dbuf[5] = gt();
+    {
+        const int nh = min(sm.hcount, kCandCap), lane = t & 31;
+        if (dbg) dbuf[4] = nh;
+        for (int i = t >> 5; i < nh; i += kMW) {
+            const int32_t v = cand[i];
+            const int64_t s = p.rowptr[v], len = p.rowptr[v + 1] - s;
+            bool found = false;
+            for (int64_t j = lane; j < len; j += 32) found |= p.colinds[s + j] == v;
+            found = __any_sync(kFull, found);
+            bool keep = false;
+            if (lane == 0) {
+                if (found) {
+                    set_T(p, v, kIN);
+                } else {
+                    set_T(p, v, p.prio.word(it + 1, fi_next, p.gbase + v));
+                    keep = true;
+                }
+            }
+            append(sm, keep, v, lout, blo);
+        }
+    }
+    if (dbg) dbuf[3] = gt();
+    stats_flush<STATS>(p, it, 0, st);
+    __syncthreads();
+    const int out = sm.cnt;
+    __syncthreads();
+    return out;
+}
+
+__device__ __forceinline__ void stamp(const MisParams& p, int slot) {
+    if (p.timeline && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        p.timeline[slot] = (long long)ns;
+    }
+}
+
+// ------------------------------------------------------------ the kernel
+// PUSH: iterations it < p.push_iters use the push-form Decide (the column
+// pass pushes / counts, decide_push touches no edges); all others -- and
+// every iteration of a !PUSH kernel -- the pull form of Alg. 1 as written.
+// The switch needs no conversion: the push state (oflag, cnt) is only
+// written and read by push iterations and cnt is cleared by decide_push.
+template <int G, bool STATS, bool PUSH>
+__global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+    const int t = threadIdx.x;
+    const int64_t B = gridDim.x;
+    const int64_t blo = p.n * blockIdx.x / B, bhi = p.n * (blockIdx.x + 1) / B;
+    unsigned int* bar = (unsigned int*)&p.ctrl[0];
+    unsigned long long* ring = &p.ctrl[1];
+
+    if (t == 0) {
+        mbar_init(&sm.mbar[0], 1);
+        mbar_init(&sm.mbar[1], 1);
+        constexpr int kRowGroups = kMB / (G * 2 <= 32 ? G * 2 : 32);
+        mbar_init(&sm.mbarS[0], kRowGroups);
+        mbar_init(&sm.mbarS[1], kRowGroups);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        sm.pol = l2_policy(p, blo, bhi);
+    }
+    uint32_t ph = 0u;  // mbarrier phase bits: 0,1 dense buffers; 2,3 sparse buffers
+
+    // worklists <- 0..|V|; Refresh Row of iteration 0.
+    // A masked call (phase 2 of Alg. 3) also lists its active rows, so its
+    // first passes can be sparse (the active rows are a small fraction).
+    int act_block = 0;
+    {
+        const uint64_t fi0 = p.prio.iter_term(0);
+        int act_cnt = 0;
+        int64_t maxdeg = 0;
+        if (t == 0) sm.cnt = 0;
+        __syncthreads();
+        for (int64_t base = blo; base < bhi; base += kMB) {
+            const int64_t v = base + t;
+            const bool in = v < bhi;
+            const bool act = in && (p.labels ? (p.labels[v] < 0) : true);
+            if (in) {
+                set_T(p, v, act ? p.prio.word(0, fi0, p.gbase + v) : kOUT);
+                p.M[v] = act ? kPending : 0u;  // 0 = inactive sentinel (reading Q15)
+                p.oflag[v] = 0;
+                p.cnt[v] = 0u;
+                if (p.K && !p.keys_mode) maxdeg = max(maxdeg, p.rowptr[v + 1] - p.rowptr[v]);
+            }
+            act_cnt += act;
+            if (p.labels) {  // worklist_1 = worklist_2 = the active rows
+                const unsigned ball = __ballot_sync(kFull, act);
+                if (ball) {
+                    const int lane = t & 31, leader = __ffs(ball) - 1;
+                    int pos = 0;
+                    if (lane == leader) pos = atomicAdd(&sm.cnt, __popc(ball));
+                    pos = __shfl_sync(kFull, pos, leader);
+                    if (act) {
+                        const int64_t at = blo + pos + __popc(ball & lanemask_lt());
+                        p.L1[0][at] = (int32_t)v;
+                        p.L2[0][at] = (int32_t)v;
+                    }
+                }
+            }
+        }
+        const long long s = block_sum_int(sm, act_cnt);
+        act_block = (int)s;
+        if (t == 0 && s) atomicAdd(&p.ctrl[7], (unsigned long long)s);
+        if (p.K && !p.keys_mode) {
+            const uint64_t bm = ~block_min_u64(sm, ~(uint64_t)maxdeg);  // block max
+            if (t == 0 && bm) atomicMax(&p.ctrl[8], (unsigned long long)bm);
+        }
+    }
+    grid_barrier(bar);
+    stamp(p, 0);
+    const unsigned long long n_active = ld_acquire_u64(&p.ctrl[7]);
+    // 32-bit column keys for skewed degree distributions: random neighbour
+    // ids gather from all of T, which does not stay in L2 (C4); on meshes the
+    // extra key arithmetic costs more than the halved bytes save
+    if (t == 0) {
+        int use = 0;
+        if (p.K) use = p.keys_mode ? 1 : (double)ld_acquire_u64(&p.ctrl[8]) > 16.0 * (double)p.nnz / (double)p.n;
+        s_use_keys = use;
+    }
+    __syncthreads();
+
+    int it = 0;
+    int status = MIS2_OK;
+    const int64_t range = bhi - blo;
+    // this block's worklist segment sizes (a masked call starts from its lists)
+    int cnt1 = p.labels ? act_block : (int)range, cnt2 = cnt1;
+    while (n_active > 0) {  // while worklist_1 != {}
+        const int cur = it & 1;
+        // ---- Refresh Column over worklist_2
+        const bool push = PUSH && it < p.push_iters;
+        const bool dense2 = (it == 0 && !p.labels) || (int64_t)cnt2 * kDenseDen >= range * kDenseNum;
+        if (push) {
+            cnt2 = dense2 ? dense_phase<G, STATS, 0, PUSH>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0)
+                          : sparse_phase<G, STATS, 0, PUSH>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
+        } else {
+            cnt2 = dense2 ? dense_phase<G, STATS, 0, false>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0)
+                          : sparse_phase<G, STATS, 0, false>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
+        }
+        grid_barrier(bar);
+        stamp(p, 1 + 2 * it);
+        // ---- Decide over worklist_1 + fused refresh of iteration it+1
+        const uint64_t fi_next = p.prio.iter_term(it + 1);
+        const bool dense1 = (it == 0 && !p.labels) || (int64_t)cnt1 * kDenseDen >= range * kDenseNum;
+        if (push) cnt1 = decide_push<STATS>(sm, p, it, blo, bhi, p.L1[cur], cnt1, dense1, p.L1[cur ^ 1], fi_next);
+        else if (dense1) cnt1 = dense_phase<G, STATS, 1>(sm, p, it, blo, bhi, p.L1[cur ^ 1], ph, fi_next);
+        else cnt1 = sparse_phase<G, STATS, 1>(sm, p, it, blo, p.L1[cur], cnt1, p.L1[cur ^ 1], ph, fi_next);
+        if (t == 0) {
+            if (cnt1) atomicAdd(&ring[it & 3], (unsigned long long)cnt1);
+            if (blockIdx.x == 0) ring[(it + 2) & 3] = 0;  // slot last read two barriers ago
+        }
+        grid_barrier(bar);
+        stamp(p, 2 + 2 * it);
+        const unsigned long long remaining = ld_acquire_u64(&ring[it & 3]);
+        it++;
+        if (remaining == 0) break;
+        if (it >= p.max_iters) {  // reading Q12
+            status = MIS2_ENOTCONVERGED;
+            break;
+        }
+    }
+
+    // return {v : T_v = IN}
+    l2_release(p, blo, bhi);
+    int cnt = 0;
+    for (int64_t v = blo + t; v < bhi; v += kMB) {
+        const uint8_t in = (p.T[v] == kIN);
+        p.in_set[v] = in;
+        cnt += in;
+    }
+    const long long bc = block_sum_int(sm, cnt);
+    if (t == 0) {
+        atomicAdd(&p.ctrl[5], (unsigned long long)bc);
+        __threadfence();
+        const unsigned long long ticket = atomicAdd(&p.ctrl[6], 1ull);
+        if (ticket == gridDim.x - 1) {  // last block publishes the scalars
+            __threadfence();
+            *p.d_count = (int64_t)ld_acquire_u64(&p.ctrl[5]);
+            *p.d_iters = it;
+            *p.d_status = status;
+        }
+    }
+}
+
+// ------------------------------------------------------------ per-phase kernels
+// The same phases as one launch each, for the partitioned driver (dist.cu),
+// which exchanges ghost T / M between them.  Block worklist segment sizes
+// live in cnts[0..B) (worklist_1) and cnts[B..2B) (worklist_2).
+__device__ __forceinline__ void init_mbars(TileSmem& sm, const MisParams& p, int G2) {
+    if (threadIdx.x == 0) {
+        const int64_t B = gridDim.x;
+        sm.pol = l2_policy(p, p.n * blockIdx.x / B, p.n * (blockIdx.x + 1) / B);
+        mbar_init(&sm.mbar[0], 1);
+        mbar_init(&sm.mbar[1], 1);
+        mbar_init(&sm.mbarS[0], kMB / G2);
+        mbar_init(&sm.mbarS[1], kMB / G2);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+}
+
+template <int G, int PH>
+__global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_part_phase(MisParams p, int it, int* cnts,
+                                                              unsigned long long* wl1_total) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+    init_mbars(sm, p, G * 2 <= 32 ? G * 2 : 32);
+    uint32_t ph = 0u;
+    const int64_t B = gridDim.x;
+    const int64_t blo = p.n * blockIdx.x / B, bhi = p.n * (blockIdx.x + 1) / B;
+    const int64_t range = bhi - blo;
+    const int cur = it & 1;
+    int* cnt = &cnts[(PH == 0 ? B : 0) + blockIdx.x];
+    const int c = *cnt;
+    const bool dense = (it == 0) || (int64_t)c * kDenseDen >= range * kDenseNum;
+    int out;
+    if (PH == 0) {
+        out = dense ? dense_phase<G, false, 0>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0)
+                    : sparse_phase<G, false, 0>(sm, p, it, blo, p.L2[cur], c, p.L2[cur ^ 1], ph, 0);
+    } else {
+        const uint64_t fi_next = p.prio.iter_term(it + 1);
+        out = dense ? dense_phase<G, false, 1>(sm, p, it, blo, bhi, p.L1[cur ^ 1], ph, fi_next)
+                    : sparse_phase<G, false, 1>(sm, p, it, blo, p.L1[cur], c, p.L1[cur ^ 1], ph, fi_next);
+    }
+    if (threadIdx.x == 0) {
+        *cnt = out;
+        if (PH == 1 && out) atomicAdd(wl1_total, (unsigned long long)out);
+    }
+}
+
+}  // namespace mis2k
