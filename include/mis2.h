@@ -6,8 +6,9 @@
  *
  * Conventions (all entry points)
  * ------------------------------
- *  - Graphs are CSR in DEVICE memory: rowptr int64[n+1] (rowptr[0] = 0,
- *    nondecreasing), colinds int32[nnz].  The graph must be symmetric, in
+ *  - Graphs are CSR in DEVICE memory: rowptr int64[n+1] -- or int32[n+1]
+ *    with rowptr_bits = 32 -- (rowptr[0] = 0, nondecreasing), colinds
+ *    int32[nnz].  The graph must be symmetric, in
  *    range and duplicate free; a stored diagonal is allowed and ignored
  *    ("CRS"; reading Q23).  Row order inside a row is free
  *    except for mis2_validate_graph, which also requires sorted rows.
@@ -58,6 +59,7 @@ extern "C" {
 #define MIS2_OP_COARSEN 2   /* mis2_coarsen                                 */
 #define MIS2_OP_MIS2_HOST 3 /* mis2_host (graph staged through the workspace) */
 #define MIS2_OP_VALIDATE 4  /* mis2_validate_graph                          */
+#define MIS2_OP_COLOR 5     /* mis2_color                                   */
 
 /* ------------------------------------------------------------------- flags */
 #define MIS2_FLAG_VALIDATE 0x1u  /* run mis2_validate_graph first (EGRAPH on failure) */
@@ -92,8 +94,18 @@ extern "C" {
 typedef struct {
     int64_t n;              /* |V|                                         */
     int64_t nnz;            /* stored entries = rowptr[n]                  */
-    const int64_t* rowptr;  /* device int64[n+1]                           */
+    union {
+        const int64_t* rowptr;    /* device int64[n+1] (rowptr_bits 0 or 64) */
+        const int32_t* rowptr32;  /* device int32[n+1] (rowptr_bits 32)      */
+    };
     const int32_t* colinds; /* device int32[nnz]                           */
+    int32_t rowptr_bits;    /* 0 or 64: int64 row pointers; 32: int32 row pointers
+                               (nnz < 2^31), widened into the workspace on entry by
+                               mis2 / mis2_async / mis2_aggregate / mis2_coarsen /
+                               mis2_validate_graph (the workspace sizes include it);
+                               other entry points: MIS2_EINVAL.  Anything else:
+                               MIS2_EINVAL. */
+    int32_t reserved;       /* 0 */
 } mis2_graph;
 
 typedef struct {
@@ -262,7 +274,8 @@ int mis2_plan_part(int64_t n_global, int nparts, int part, const int64_t* rowptr
  * Jones-Plassmann rounds, priorities = the MIS-2 status words of iteration 0
  * with `seed`; every vertex takes the smallest colour none of its
  * earlier-coloured neighbours has).  color: device int32[n]; *ncolors on
- * return (synchronises the stream).  Scratch is allocated internally.
+ * return (synchronises the stream).  Scratch from the caller's workspace
+ * ws (>= mis2_workspace_size(n, nnz, MIS2_OP_COLOR) bytes).
  *
  * mis2_cgs_setup: Alg. 4's setup.  labels (device int32[n]) and
  * num_aggs give the clusters (e.g. mis2_aggregate), `coarse` their coarse
@@ -271,7 +284,8 @@ int mis2_plan_part(int64_t n_global, int nparts, int part, const int64_t* rowptr
  * its own cluster, the graph itself coloured).  vals: device f64[nnz], A_ii
  * must be stored and nonzero (MIS2_EINVAL otherwise).  g, vals must stay
  * valid while the handle is used; the handle owns its cluster / colour-set
- * arrays (freed by mis2_cgs_destroy).
+ * arrays and the setup scratch -- one device allocation made by the setup
+ * call, freed by mis2_cgs_destroy (the apply calls allocate nothing).
  *
  * mis2_cgs_apply: `sweeps` sweeps on x (device f64[n], in place) for the
  * right-hand side b (device f64[n]): direction 1 forward (colours and rows
@@ -280,7 +294,8 @@ int mis2_plan_part(int64_t n_global, int nparts, int part, const int64_t* rowptr
  * of one colour are updated concurrently; enqueued on `stream`.
  * ---------------------------------------------------------------------- */
 typedef struct mis2_cgs mis2_cgs;
-int mis2_color(const mis2_graph* g, uint64_t seed, int32_t* color, int32_t* ncolors, void* stream);
+int mis2_color(const mis2_graph* g, uint64_t seed, int32_t* color, int32_t* ncolors, void* ws, size_t ws_bytes,
+               void* stream);
 int mis2_cgs_setup(const mis2_graph* g, const double* vals, const int32_t* labels, int64_t num_aggs,
                    const mis2_graph* coarse, uint64_t seed, mis2_cgs** out, void* stream);
 int mis2_cgs_ncolors(const mis2_cgs* h);

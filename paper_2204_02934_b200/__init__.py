@@ -20,7 +20,7 @@ __all__ = ["mis2", "mis2_async", "mis2_host", "aggregate", "coarsen", "validate_
            "Mis2Error", "lib", "SCHEMES", "EXPORTS", "workspace"]
 
 SCHEMES = {"xorstar": 0, "fixed": 1, "xor": 2}
-OP_MIS2, OP_AGGREGATE, OP_COARSEN, OP_MIS2_HOST, OP_VALIDATE = 0, 1, 2, 3, 4
+OP_MIS2, OP_AGGREGATE, OP_COARSEN, OP_MIS2_HOST, OP_VALIDATE, OP_COLOR = 0, 1, 2, 3, 4, 5
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, EGRAPH, ENOTCONVERGED, ERANGE, EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7, -9
 FLAG_VALIDATE = 1
 FLAG_TIMELINE = 2
@@ -49,8 +49,9 @@ class Mis2Error(RuntimeError):
 
 
 class _Graph(ctypes.Structure):
+    # the C struct's rowptr / rowptr32 union is one pointer; rowptr_bits says which
     _fields_ = [("n", ctypes.c_int64), ("nnz", ctypes.c_int64), ("rowptr", ctypes.c_void_p),
-                ("colinds", ctypes.c_void_p)]
+                ("colinds", ctypes.c_void_p), ("rowptr_bits", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class _Opts(ctypes.Structure):
@@ -84,7 +85,7 @@ def lib():
         L.mis2_validate_graph.argtypes = [P, P, SZ, P]
         L.mis2_dist_aggregate.argtypes = [P, P, P, P, P, P]
         L.mis2_dist_coarsen.argtypes = [P, P, I64, P, P, I64, P, P]
-        L.mis2_color.argtypes = [P, ctypes.c_uint64, P, P, P]
+        L.mis2_color.argtypes = [P, ctypes.c_uint64, P, P, P, SZ, P]
         L.mis2_cgs_setup.argtypes = [P, P, P, I64, P, ctypes.c_uint64, P, P]
         L.mis2_cgs_ncolors.argtypes = [P]
         L.mis2_cgs_apply.argtypes = [P, P, P, I32, I32, P]
@@ -148,13 +149,15 @@ def workspace(op: int, n: int, nnz: int):
 
 
 def _graph(rowptr, colinds):
+    """CSR tensors -> the C struct: rowptr int64 or int32 (rowptr_bits 32), colinds int32."""
     torch = _torch()
     assert rowptr.is_cuda and colinds.is_cuda, "rowptr/colinds must be CUDA tensors"
-    assert rowptr.dtype == torch.int64 and colinds.dtype == torch.int32
+    assert rowptr.dtype in (torch.int64, torch.int32) and colinds.dtype == torch.int32
     assert rowptr.is_contiguous() and colinds.is_contiguous()
     n = rowptr.numel() - 1
     nnz = colinds.numel()
-    return _Graph(n, nnz, rowptr.data_ptr(), colinds.data_ptr() if nnz else None), n, nnz
+    bits = 32 if rowptr.dtype == torch.int32 else 64
+    return _Graph(n, nnz, rowptr.data_ptr(), colinds.data_ptr() if nnz else None, bits, 0), n, nnz
 
 
 def _opts(seed=0, scheme="xorstar", max_iters=0, group=0, validate=False, prio_override=None, decide="auto",
@@ -466,8 +469,9 @@ def color(rowptr, colinds, seed: int = 0):
     g, n, nnz = _graph(rowptr, colinds)
     out = torch.empty(max(n, 1), dtype=torch.int32, device=rowptr.device)
     nc = ctypes.c_int32(0)
-    _check(lib().mis2_color(ctypes.byref(g), seed & ((1 << 64) - 1), out.data_ptr(), ctypes.byref(nc), _stream()),
-           "mis2_color")
+    ws, wsb = workspace(OP_COLOR, n, nnz)
+    _check(lib().mis2_color(ctypes.byref(g), seed & ((1 << 64) - 1), out.data_ptr(), ctypes.byref(nc),
+                            ws.data_ptr(), wsb, _stream()), "mis2_color")
     return out[:n], int(nc.value)
 
 

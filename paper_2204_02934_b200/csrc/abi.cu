@@ -5,6 +5,8 @@
 #include <cstdio>
 #include <cstring>
 
+#include <algorithm>
+
 #include "internal.h"
 
 namespace mis2h {
@@ -39,8 +41,13 @@ int device_info(DeviceInfo* out) {
     return MIS2_OK;
 }
 
-static int check_graph(const mis2_graph* g) {
+static int check_graph(const mis2_graph* g, bool rowptr32_ok = false) {
     if (!g) { set_error("graph is NULL"); return MIS2_EINVAL; }
+    if (g->rowptr_bits != 0 && g->rowptr_bits != 64 && !(g->rowptr_bits == 32 && rowptr32_ok)) {
+        set_error("rowptr_bits %d not supported here (0/64%s)", g->rowptr_bits, rowptr32_ok ? " or 32" : "");
+        return MIS2_EINVAL;
+    }
+    if (g->rowptr_bits == 32 && g->nnz > 2147483647LL) { set_error("rowptr_bits 32 needs nnz < 2^31"); return MIS2_EINVAL; }
     if (g->n < 0 || g->n > 2147483645LL) { set_error("n out of range [0, 2^31-3]: %lld", (long long)g->n); return MIS2_EINVAL; }
     if (g->nnz < 0) { set_error("nnz < 0"); return MIS2_EINVAL; }
     if (g->n > 0 && (!g->rowptr || (g->nnz > 0 && !g->colinds))) { set_error("null rowptr/colinds"); return MIS2_EINVAL; }
@@ -72,9 +79,39 @@ static size_t mis2_bytes(int64_t n, int64_t nnz) {
     return c.off;
 }
 
+// int32 row pointers (rowptr_bits = 32): widened to int64 into the last
+// 8(n+1) bytes (256-aligned) of the workspace, which the op then does not
+// use (mis2_workspace_size includes them for every op).
+__global__ void k_widen_rowptr(int64_t cnt, const int32_t* __restrict__ src, int64_t* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+static size_t widen_bytes(int64_t n) { return ((sizeof(int64_t) * ((size_t)n + 1) + 255) & ~size_t(255)) + 256; }
+static int widen_graph(const mis2_graph* g, void* ws, size_t* ws_bytes, mis2_graph* out, cudaStream_t s) {
+    *out = *g;
+    out->rowptr_bits = 64;
+    if (g->rowptr_bits != 32 || g->n == 0) return MIS2_OK;
+    const size_t need = widen_bytes(g->n);
+    if (*ws_bytes < need) { set_error("workspace too small for the widened int32 rowptr"); return MIS2_ENOMEM; }
+    const size_t at = (*ws_bytes - need + 255) & ~size_t(255);
+    int64_t* dst = (int64_t*)((char*)ws + at);
+    const int64_t cnt = g->n + 1;
+    DeviceInfo di;
+    MIS2_TRY(device_info(&di));
+    const int64_t blocks = std::min<int64_t>((cnt + 255) / 256, (int64_t)di.sms * 8);
+    k_widen_rowptr<<<(unsigned)blocks, 256, 0, s>>>(cnt, g->rowptr32, dst);
+    count_launch();
+    MIS2_CUDA_TRY(cudaGetLastError());
+    out->rowptr = dst;
+    *ws_bytes = *ws_bytes - need;
+    return MIS2_OK;
+}
+
 }  // namespace mis2h
 
 using namespace mis2h;
+
+static int workspace_size_op(int64_t n, int64_t nnz, int32_t op, size_t* bytes);
 
 extern "C" {
 
@@ -87,7 +124,24 @@ void mis2_opts_default(mis2_opts* o) {
 int mis2_workspace_size(int64_t n, int64_t nnz, int32_t op, size_t* bytes) {
     if (!bytes || n < 0 || nnz < 0) { set_error("bad arguments"); return MIS2_EINVAL; }
     reset_launches();
-    mis2_graph g{n, nnz, nullptr, nullptr};
+    const int rc = workspace_size_op(n, nnz, op, bytes);
+    if (rc == MIS2_OK) *bytes += widen_bytes(n);
+    return rc;
+}
+
+int mis2_validate_graph(const mis2_graph* g, void* ws, size_t ws_bytes, void* stream) {
+    reset_launches();
+    MIS2_TRY(check_graph(g, true));
+    if (!ws) { set_error("workspace is NULL"); return MIS2_EINVAL; }
+    mis2_graph gw;
+    MIS2_TRY(widen_graph(g, ws, &ws_bytes, &gw, (cudaStream_t)stream));
+    return run_validate(gw, ws, ws_bytes, (cudaStream_t)stream, nullptr);
+}
+
+}  // extern "C"
+
+static int workspace_size_op(int64_t n, int64_t nnz, int32_t op, size_t* bytes) {
+    mis2_graph g{n, nnz, {nullptr}, nullptr, 0, 0};
     switch (op) {
         case MIS2_OP_MIS2: *bytes = mis2_bytes(n, nnz); return MIS2_OK;
         case MIS2_OP_MIS2_HOST: {
@@ -105,22 +159,18 @@ int mis2_workspace_size(int64_t n, int64_t nnz, int32_t op, size_t* bytes) {
         case MIS2_OP_AGGREGATE: return run_aggregate(g, mis2_opts{}, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, bytes);
         case MIS2_OP_COARSEN: return run_coarsen(g, nullptr, 0, nullptr, nullptr, 0, nullptr, nullptr, 0, 0, bytes);
         case MIS2_OP_VALIDATE: return run_validate(g, nullptr, 0, 0, bytes);
+        case MIS2_OP_COLOR: return color_graph(g, 0, nullptr, nullptr, nullptr, 0, 0, bytes);
     }
     set_error("unknown op %d", op);
     return MIS2_EINVAL;
 }
 
-int mis2_validate_graph(const mis2_graph* g, void* ws, size_t ws_bytes, void* stream) {
-    reset_launches();
-    MIS2_TRY(check_graph(g));
-    if (!ws) { set_error("workspace is NULL"); return MIS2_EINVAL; }
-    return run_validate(*g, ws, ws_bytes, (cudaStream_t)stream, nullptr);
-}
+extern "C" {
 
 int mis2_async(const mis2_graph* g, const mis2_opts* o, uint8_t* in_set, int64_t* d_count, int32_t* d_iters,
                int32_t* d_status, void* ws, size_t ws_bytes, void* stream) {
     reset_launches();
-    MIS2_TRY(check_graph(g));
+    MIS2_TRY(check_graph(g, true));
     MIS2_TRY(check_opts(o, g->n));
     if (!d_count || !d_iters || !d_status || (g->n > 0 && !in_set) || !ws) {
         set_error("null output or workspace");
@@ -130,6 +180,9 @@ int mis2_async(const mis2_graph* g, const mis2_opts* o, uint8_t* in_set, int64_t
     mis2_opts_default(&def);
     const mis2_opts& opt = o ? *o : def;
     cudaStream_t s = (cudaStream_t)stream;
+    mis2_graph gw;
+    MIS2_TRY(widen_graph(g, ws, &ws_bytes, &gw, s));
+    g = &gw;
     if (opt.flags & MIS2_FLAG_VALIDATE) MIS2_TRY(run_validate(*g, ws, ws_bytes, s, nullptr));
     Carve c(ws, ws_bytes);
     Mis2Ws w;
@@ -143,13 +196,16 @@ int mis2_async(const mis2_graph* g, const mis2_opts* o, uint8_t* in_set, int64_t
 int mis2(const mis2_graph* g, const mis2_opts* o, uint8_t* in_set, int64_t* count, int32_t* iters,
          int64_t* stats, void* ws, size_t ws_bytes, void* stream) {
     reset_launches();
-    MIS2_TRY(check_graph(g));
+    MIS2_TRY(check_graph(g, true));
     MIS2_TRY(check_opts(o, g->n));
     if (!count || !iters || (g->n > 0 && !in_set) || !ws) { set_error("null output or workspace"); return MIS2_EINVAL; }
     mis2_opts def;
     mis2_opts_default(&def);
     const mis2_opts& opt = o ? *o : def;
     cudaStream_t s = (cudaStream_t)stream;
+    mis2_graph gw;
+    MIS2_TRY(widen_graph(g, ws, &ws_bytes, &gw, s));
+    g = &gw;
     if (opt.flags & MIS2_FLAG_VALIDATE) MIS2_TRY(run_validate(*g, ws, ws_bytes, s, nullptr));
     Carve c(ws, ws_bytes);
     Mis2Ws w;
@@ -213,13 +269,16 @@ int mis2_host(int64_t n, int64_t nnz, const int64_t* rowptr_h, const int32_t* co
 int mis2_aggregate(const mis2_graph* g, const mis2_opts* o, int32_t* labels, int64_t* num_aggs, int32_t* roots,
                    int64_t* stats, void* ws, size_t ws_bytes, void* stream) {
     reset_launches();
-    MIS2_TRY(check_graph(g));
+    MIS2_TRY(check_graph(g, true));
     MIS2_TRY(check_opts(o, g->n));
     if (!num_aggs || (g->n > 0 && !labels) || !ws) { set_error("null output or workspace"); return MIS2_EINVAL; }
     mis2_opts def;
     mis2_opts_default(&def);
     const mis2_opts& opt = o ? *o : def;
     cudaStream_t s = (cudaStream_t)stream;
+    mis2_graph gw;
+    MIS2_TRY(widen_graph(g, ws, &ws_bytes, &gw, s));
+    g = &gw;
     if (opt.flags & MIS2_FLAG_VALIDATE) MIS2_TRY(run_validate(*g, ws, ws_bytes, s, nullptr));
     if (opt.prio_override) { set_error("prio_override is only supported by mis2()"); return MIS2_EINVAL; }
     return run_aggregate(*g, opt, labels, num_aggs, roots, stats, ws, ws_bytes, s, nullptr);
@@ -228,8 +287,11 @@ int mis2_aggregate(const mis2_graph* g, const mis2_opts* o, int32_t* labels, int
 int mis2_coarsen(const mis2_graph* g, const int32_t* labels, int64_t num_aggs, int64_t* c_rowptr, int32_t* c_colinds,
                  int64_t cap, int64_t* c_nnz, void* ws, size_t ws_bytes, void* stream) {
     reset_launches();
-    MIS2_TRY(check_graph(g));
+    MIS2_TRY(check_graph(g, true));
     if (!c_nnz || !c_rowptr || (g->n > 0 && !labels) || !ws || cap < 0) { set_error("bad arguments"); return MIS2_EINVAL; }
+    mis2_graph gw;
+    MIS2_TRY(widen_graph(g, ws, &ws_bytes, &gw, (cudaStream_t)stream));
+    g = &gw;
     return run_coarsen(*g, labels, num_aggs, c_rowptr, c_colinds, cap, c_nnz, ws, ws_bytes, (cudaStream_t)stream,
                        nullptr);
 }

@@ -365,22 +365,34 @@ unsigned grid_for(int64_t n, int sms) {
     return (unsigned)(b < 1 ? 1 : b);
 }
 
-// the colouring (reading Q30) with internally allocated scratch
-int color_graph(const mis2_graph& g, uint64_t seed, int32_t* color, int32_t* ncolors, cudaStream_t s) {
+}  // namespace
+
+// the colouring (reading Q30); scratch carved from the caller's workspace
+// (bytes_needed != NULL: sizing pass only)
+int mis2h::color_graph(const mis2_graph& g, uint64_t seed, int32_t* color, int32_t* ncolors, void* ws, size_t ws_bytes,
+                cudaStream_t s, size_t* bytes_needed) {
+    const int64_t n = g.n;
+    ColorState st;
+    Carve c(ws, ws_bytes);
+    st.W = c.take<uint64_t>((size_t)n + 1);
+    st.cround = c.take<int32_t>((size_t)n + 1);
+    st.wl[0] = c.take<int32_t>((size_t)n + 1);
+    st.wl[1] = c.take<int32_t>((size_t)n + 1);
+    char* ctr = c.take<char>(256);
+    if (bytes_needed) {
+        *bytes_needed = c.off;
+        return MIS2_OK;
+    }
+    if (!c.ok()) {
+        set_error("workspace too small: need %zu bytes, got %zu", c.off, ws_bytes);
+        return MIS2_ENOMEM;
+    }
     DeviceInfo di;
     MIS2_TRY(device_info(&di));
-    const int64_t n = g.n;
     if (n == 0) {
         *ncolors = 0;
         return MIS2_OK;
     }
-    ColorState st;
-    char* ctr;
-    MIS2_CUDA_TRY(cudaMallocAsync((void**)&st.W, sizeof(uint64_t) * n, s));
-    MIS2_CUDA_TRY(cudaMallocAsync((void**)&st.cround, sizeof(int32_t) * n, s));
-    MIS2_CUDA_TRY(cudaMallocAsync((void**)&st.wl[0], sizeof(int32_t) * n, s));
-    MIS2_CUDA_TRY(cudaMallocAsync((void**)&st.wl[1], sizeof(int32_t) * n, s));
-    MIS2_CUDA_TRY(cudaMallocAsync((void**)&ctr, 256, s));
     MIS2_CUDA_TRY(cudaMemsetAsync(ctr, 0, 256, s));
     st.color = color;
     st.bar = (unsigned int*)ctr;
@@ -425,32 +437,29 @@ int color_graph(const mis2_graph& g, uint64_t seed, int32_t* color, int32_t* nco
     } else {
         *ncolors = hv[0] + 1;
     }
-    cudaFreeAsync(st.W, s);
-    cudaFreeAsync(st.cround, s);
-    cudaFreeAsync(st.wl[0], s);
-    cudaFreeAsync(st.wl[1], s);
-    cudaFreeAsync(ctr, s);
     return rc;
 }
 
-}  // namespace
 
 extern "C" {
 
-int mis2_color(const mis2_graph* g, uint64_t seed, int32_t* color, int32_t* ncolors, void* stream) {
+int mis2_color(const mis2_graph* g, uint64_t seed, int32_t* color, int32_t* ncolors, void* ws, size_t ws_bytes,
+               void* stream) {
     reset_launches();
-    if (!g || !ncolors || g->n < 0 || (g->n > 0 && (!color || !g->rowptr)) || g->n > 2147483645LL) {
+    if (!g || !ncolors || g->n < 0 || (g->n > 0 && (!color || !g->rowptr || !ws)) || g->n > 2147483645LL ||
+        (g->rowptr_bits != 0 && g->rowptr_bits != 64)) {
         set_error("bad arguments");
         return MIS2_EINVAL;
     }
-    return color_graph(*g, seed, color, ncolors, (cudaStream_t)stream);
+    return color_graph(*g, seed, color, ncolors, ws, ws_bytes, (cudaStream_t)stream, nullptr);
 }
 
 int mis2_cgs_setup(const mis2_graph* g, const double* vals, const int32_t* labels, int64_t num_aggs,
                    const mis2_graph* coarse, uint64_t seed, mis2_cgs** out, void* stream) {
     reset_launches();
     if (!g || !out || g->n < 0 || (g->n > 0 && (!vals || !g->rowptr || !g->colinds)) ||
-        (labels && (!coarse || num_aggs < 1 || coarse->n != num_aggs)) || g->n > 2147483645LL) {
+        (labels && (!coarse || num_aggs < 1 || coarse->n != num_aggs)) || g->n > 2147483645LL ||
+        (g->rowptr_bits != 0 && g->rowptr_bits != 64) || (coarse && coarse->rowptr_bits != 0 && coarse->rowptr_bits != 64)) {
         set_error("bad arguments");
         return MIS2_EINVAL;
     }
@@ -475,9 +484,15 @@ int mis2_cgs_setup(const mis2_graph* g, const double* vals, const int32_t* label
     int32_t* ccolor;
     unsigned long long* cnt;
     void* tmp;
+    void* cws;
+    size_t cws_bytes = 0;
     const int64_t nk = std::max<int64_t>(na, 64) + 2;
-    // one allocation for the handle's arrays and the setup scratch
+    const mis2_graph& cg = point ? *g : *coarse;
+    if ((rc = color_graph(cg, seed, nullptr, nullptr, nullptr, 0, s, &cws_bytes)) != MIS2_OK) return fail(rc);
+    // one allocation (owned by the handle) for its arrays and the setup
+    // scratch, including the colouring's
     auto layout = [&](Carve& c) {
+        cws = c.take<char>(cws_bytes);
         h->diag = c.take<double>((size_t)n + 1);
         h->cptr = c.take<int64_t>((size_t)na + 2);
         h->crows = c.take<int32_t>((size_t)n + 1);
@@ -498,7 +513,7 @@ int mis2_cgs_setup(const mis2_graph* g, const double* vals, const int32_t* label
         count_launch();
     }
     // colour the coarse graph (point: the graph itself)
-    if ((rc = color_graph(point ? *g : *coarse, seed, ccolor, &h->ncolors, s)) != MIS2_OK) return fail(rc);
+    if ((rc = color_graph(cg, seed, ccolor, &h->ncolors, cws, cws_bytes, s, nullptr)) != MIS2_OK) return fail(rc);
     // rows of each cluster, ascending
     if (point) {
         k_iota<<<grid_for(n + 1, di.sms), 256, 0, s>>>(n, h->crows, h->cptr);

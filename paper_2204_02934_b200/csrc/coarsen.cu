@@ -28,10 +28,14 @@ __global__ void k_check_labels(int64_t n, const int32_t* __restrict__ labels, in
 }
 
 __global__ void k_seglen(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ labels,
-                         unsigned long long* __restrict__ seglen) {
+                         int64_t na, unsigned long long* __restrict__ seglen) {
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
         const int64_t d = rowptr[v + 1] - rowptr[v];
-        if (d) atomicAdd(&seglen[labels[v]], (unsigned long long)d);
+        const int32_t a = labels[v];
+        // out-of-range labels are skipped here and in k_fill (k_check_labels
+        // flags them; the call returns MIS2_EINVAL without touching memory
+        // outside the workspace)
+        if (d && a >= 0 && a < na) atomicAdd(&seglen[a], (unsigned long long)d);
     }
 }
 
@@ -49,7 +53,7 @@ __global__ void k_seglen(int64_t n, const int64_t* __restrict__ rowptr, const in
 constexpr int kFillList = MIS2_FILL_LIST;
 template <int G>
 __global__ void k_fill(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colinds,
-                       const int32_t* __restrict__ labels, unsigned long long* __restrict__ cursor,
+                       const int32_t* __restrict__ labels, int64_t na, unsigned long long* __restrict__ cursor,
                        int32_t* __restrict__ buf) {
     constexpr int RPW = 32 / G;
     const int lane = threadIdx.x & 31, grp = lane / G, sub = lane % G;
@@ -61,11 +65,11 @@ __global__ void k_fill(int64_t n, const int64_t* __restrict__ rowptr, const int3
         int32_t lst[kFillList];
         int cnt = 0;
         int32_t a = 0;
-        if (valid) {
+        if (valid) a = labels[v];
+        if (valid && a >= 0 && a < na) {
             const int64_t s = rowptr[v], e = rowptr[v + 1];
-            a = labels[v];
             row_batched<G, 8>(s, e, sub, colinds, [&](int32_t w) { return labels[w]; }, [&](int32_t, int32_t b) {
-                if (b == a) return;
+                if (b == a || b < 0 || b >= na) return;
                 bool found = false;
 #pragma unroll
                 for (int k = 0; k < kFillList; k++) found |= (k < cnt) && lst[k] == b;
@@ -329,7 +333,7 @@ int run_coarsen(const mis2_graph& g, const int32_t* labels, int64_t na, int64_t*
     MIS2_CUDA_TRY(cudaMemsetAsync(seglen, 0, sizeof(unsigned long long) * ((size_t)na + 1), s));
     count_launch(2);
     k_check_labels<<<(unsigned)blocks, kBlock, 0, s>>>(n, labels, na, &scal[0]);
-    k_seglen<<<(unsigned)blocks, kBlock, 0, s>>>(n, g.rowptr, labels, seglen);
+    k_seglen<<<(unsigned)blocks, kBlock, 0, s>>>(n, g.rowptr, labels, na, seglen);
     count_launch(2);
     MIS2_TRY(scan_counts64((const int64_t*)seglen, na, sptr, tmp, s));
     MIS2_CUDA_TRY(cudaMemcpyAsync(cursor, sptr, sizeof(int64_t) * (size_t)na, cudaMemcpyDeviceToDevice, s));
@@ -339,12 +343,12 @@ int run_coarsen(const mis2_graph& g, const int32_t* labels, int64_t na, int64_t*
         if (fb > (int64_t)di.sms * 16) fb = (int64_t)di.sms * 16;
         if (fb < 1) fb = 1;
         switch (G) {
-            case 1: k_fill<1><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, cursor, buf); break;
-            case 2: k_fill<2><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, cursor, buf); break;
-            case 4: k_fill<4><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, cursor, buf); break;
-            case 8: k_fill<8><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, cursor, buf); break;
-            case 16: k_fill<16><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, cursor, buf); break;
-            default: k_fill<32><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, cursor, buf); break;
+            case 1: k_fill<1><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, na, cursor, buf); break;
+            case 2: k_fill<2><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, na, cursor, buf); break;
+            case 4: k_fill<4><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, na, cursor, buf); break;
+            case 8: k_fill<8><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, na, cursor, buf); break;
+            case 16: k_fill<16><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, na, cursor, buf); break;
+            default: k_fill<32><<<(unsigned)fb, kBlock, 0, s>>>(n, g.rowptr, g.colinds, labels, na, cursor, buf); break;
         }
         count_launch();
     }

@@ -868,46 +868,52 @@ static int dist_coarsen_run(mis2_comm* c, const std::vector<const int32_t*>& lab
         mx = std::max(mx, x);
     }
     const int64_t ns = (int64_t)P * na;
-    DevBuf srow, scol, slab;
+    DevBuf srow, scol, slab, arow, pcol, acol;
     MIS2_TRY(srow.alloc(sizeof(int64_t) * (ns + 1)));
     MIS2_TRY(slab.alloc(sizeof(int32_t) * (ns + 1)));
+    MIS2_TRY(scol.alloc(sizeof(int32_t) * (tot + 1)));
     int64_t* sr = (int64_t*)srow.p;
     const unsigned gb = (unsigned)std::min<int64_t>((na + 256) / 256 + 1, 4096);
+    // the coarse CSR of every part: on the device already (LOCAL) or
+    // allgathered (NCCL: row pointers, and the columns padded to the largest
+    // part's count -- only the first all_nnz[p] entries of a part are used)
+    std::vector<const int64_t*> prow(P);
+    std::vector<const int32_t*> pcolp(P);
     if (c->local) {
-        MIS2_TRY(scol.alloc(sizeof(int32_t) * (tot + 1)));
-        int64_t off = 0;
         for (int p = 0; p < P; p++) {
-            k_shift_i64<<<gb, 256, 0, s>>>((const int64_t*)crow[p].p, na, off, sr + (int64_t)p * na);
-            count_launch();
-            if (nnz[p])
-                MIS2_CUDA_TRY(cudaMemcpyAsync((int32_t*)scol.p + off, ccol[p].p, sizeof(int32_t) * nnz[p],
-                                              cudaMemcpyDeviceToDevice, s));
-            off += nnz[p];
+            prow[p] = (const int64_t*)crow[p].p;
+            pcolp[p] = (const int32_t*)ccol[p].p;
         }
-        MIS2_CUDA_TRY(cudaMemcpyAsync(sr + ns, &tot, sizeof(int64_t), cudaMemcpyHostToDevice, s));
     } else {
-        // allgather of the row pointers and of the (padded) coarse columns
-        DevBuf arow, pcol;
         MIS2_TRY(arow.alloc(sizeof(int64_t) * (na + 1) * P));
         MIS2_TRY(pcol.alloc(sizeof(int32_t) * (mx + 1)));
-        MIS2_TRY(scol.alloc(sizeof(int32_t) * ((mx + 1) * P)));
+        MIS2_TRY(acol.alloc(sizeof(int32_t) * ((mx + 1) * P)));
         if (nnz[0]) MIS2_CUDA_TRY(cudaMemcpyAsync(pcol.p, ccol[0].p, sizeof(int32_t) * nnz[0], cudaMemcpyDeviceToDevice, s));
         NCCL_TRY(c->api, c->api->AllGather(crow[0].p, arow.p, (size_t)(na + 1), ncclInt64, c->nccl, s));
-        NCCL_TRY(c->api, c->api->AllGather(pcol.p, scol.p, (size_t)(mx + 1), ncclInt32, c->nccl, s));
+        NCCL_TRY(c->api, c->api->AllGather(pcol.p, acol.p, (size_t)(mx + 1), ncclInt32, c->nccl, s));
         for (int p = 0; p < P; p++) {
-            k_shift_i64<<<gb, 256, 0, s>>>((const int64_t*)arow.p + (int64_t)p * (na + 1), na, (int64_t)p * (mx + 1),
-                                           sr + (int64_t)p * na);
-            count_launch();
+            prow[p] = (const int64_t*)arow.p + (int64_t)p * (na + 1);
+            pcolp[p] = (const int32_t*)acol.p + (int64_t)p * (mx + 1);
         }
-        const int64_t last = (int64_t)(P - 1) * (mx + 1) + all_nnz[P - 1];
-        MIS2_CUDA_TRY(cudaMemcpyAsync(sr + ns, &last, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-        MIS2_CUDA_TRY(cudaStreamSynchronize(s));  // `last` is a host stack value
     }
+    // stacked graph: part p's coarse rows are rows [p*na, (p+1)*na), its
+    // columns the contiguous range [off_p, off_p + all_nnz[p]) -- every row
+    // ends where the next begins, the last at tot
+    int64_t off = 0;
+    for (int p = 0; p < P; p++) {
+        k_shift_i64<<<gb, 256, 0, s>>>(prow[p], na, off, sr + (int64_t)p * na);
+        count_launch();
+        if (all_nnz[p])
+            MIS2_CUDA_TRY(cudaMemcpyAsync((int32_t*)scol.p + off, pcolp[p], sizeof(int32_t) * all_nnz[p],
+                                          cudaMemcpyDeviceToDevice, s));
+        off += all_nnz[p];
+    }
+    MIS2_CUDA_TRY(cudaMemcpyAsync(sr + ns, &tot, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    MIS2_CUDA_TRY(cudaStreamSynchronize(s));  // `tot` is a host stack value
     k_mod_labels<<<(unsigned)std::min<int64_t>((ns + 255) / 256 + 1, 4096), 256, 0, s>>>((int32_t*)slab.p, ns, na);
     count_launch();
     MIS2_CUDA_TRY(cudaStreamSynchronize(s));
-    const int64_t snnz = c->local ? tot : (int64_t)P * (mx + 1);
-    mis2_graph gm{ns, snnz, sr, (const int32_t*)scol.p};
+    mis2_graph gm{ns, tot, sr, (const int32_t*)scol.p};
     size_t wsb = 0;
     MIS2_TRY(run_coarsen(gm, nullptr, 0, nullptr, nullptr, 0, nullptr, nullptr, 0, s, &wsb));
     DevBuf ws;

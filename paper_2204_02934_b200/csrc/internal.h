@@ -55,6 +55,7 @@ struct DeviceInfo {
 int device_info(DeviceInfo* out);
 
 constexpr int kStatsMaxIters = 400;
+constexpr int kIterRing = 1024;  // dataflow sync supports max_iters <= kIterRing (else grid barriers)
 
 // MIS-2 state carved from the workspace
 struct Mis2Ws {
@@ -68,7 +69,10 @@ struct Mis2Ws {
     uint32_t* cnt;
     uint32_t* degc;
     uint32_t* K;        // 32-bit column keys (mis2_core.cu kkey)
-    unsigned long long* ctrl;  // [0]=barrier, [1..4]=ring of |wl1| sums, [5]=count, [6]=ticket
+    unsigned long long* ctrl;  // [0]=barrier, [1..4]=ring of |wl1| sums, [5]=count, [6]=ticket,
+                               // [7]=active, [8]=max degree, [9]=published iteration count (dataflow)
+    unsigned long long* iter_ring;  // [kIterRing] dataflow: per-iteration (arrivals << 44 | sum |wl1|)
+    unsigned int* prog;             // [max blocks] dataflow: phases completed per block
     long long* dstats;         // [kStatsMaxIters * 6]
     long long* scal;           // [8] host-visible scalars of mis2()/mis2_host()
 };
@@ -116,6 +120,9 @@ int run_coarsen(const mis2_graph& g, const int32_t* labels, int64_t na, int64_t*
                 int32_t* c_colinds, int64_t cap, int64_t* c_nnz, void* ws, size_t ws_bytes,
                 cudaStream_t s, size_t* bytes_needed);
 int run_validate(const mis2_graph& g, void* ws, size_t ws_bytes, cudaStream_t s, size_t* bytes_needed);
+// Alg. 4 setup colouring (cgs.cu, reading Q30)
+int color_graph(const mis2_graph& g, uint64_t seed, int32_t* color, int32_t* ncolors, void* ws, size_t ws_bytes,
+                cudaStream_t s, size_t* bytes_needed);
 
 // aggregation row kernels on raw arrays (aggregate.cu), for the partitioned driver
 void agg_phase1(int G, int64_t n, const int64_t* rowptr, const int32_t* colinds, const uint8_t* in1,

@@ -99,6 +99,11 @@ struct MisParams {
     int32_t* L1[2];                      // worklist_1, double buffered, per-block segments
     int32_t* L2[2];                      // worklist_2
     unsigned long long* ctrl;
+    // dataflow synchronisation (see df_sync): per-block completed-phase
+    // counters and per-iteration (arrivals << 44 | sum of |worklist_1|) words
+    unsigned int* prog;
+    unsigned long long* iter_ring;
+    int dataflow;                        // 1: neighbour waits instead of grid barriers
     int32_t* heavy;       // [n] deferred long rows, per-block segments at blo
     uint8_t* oflag;       // push-form Decide: some w in N[v] got M_w = OUT this iteration
     uint32_t* cnt;        // push-form Decide: |{w in N[v] : M_w = T_v}| this iteration
@@ -132,9 +137,30 @@ struct __align__(16) TileSmem {
     int hcount;
     int hnext;       // deferred rows: next row for a warp
     int nhuge;       // deferred rows too long for a warp
+    int cmin, cmax;  // dataflow: least / greatest column read by this block (iteration 0)
+    int dlo, dhi;    // dataflow: blocks whose rows this block reads (and which read its rows)
+    int done;        // dataflow: iteration count published by the last block of the final iteration
     uint64_t red64[kMW];
     int wred[kMW];
 };
+
+__device__ __forceinline__ TileSmem& tile_smem() {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    return *reinterpret_cast<TileSmem*>(smem_raw);
+}
+
+// Dataflow synchronisation: the least and greatest column the block reads in
+// iteration 0 (every active row is in worklist_2 then), reduced per warp into
+// the block's shared pair.  Called by all 32 lanes of a warp.
+__device__ __forceinline__ void track_cols_flush(int lo, int hi) {
+    lo = __reduce_min_sync(kFull, lo);
+    hi = __reduce_max_sync(kFull, hi);
+    if ((threadIdx.x & 31) == 0 && hi >= 0) {
+        TileSmem& sm = tile_smem();
+        atomicMin(&sm.cmin, lo);
+        atomicMax(&sm.cmax, hi);
+    }
+}
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -443,6 +469,16 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
                                             int len, uint64_t tv, int it, uint64_t fi_next) {
     bool keep = false;
     if (PH == 0) {
+        if (it == 0 && p.dataflow) {
+            int lo = 0x7fffffff, hi = -1;
+            if (act)
+                for (int j = sub; j < len; j += GG) {
+                    const int c = x[j];
+                    lo = min(lo, c);
+                    hi = max(hi, c);
+                }
+            track_cols_flush(lo, hi);
+        }
         uint32_t mf;
         int dc = 0;
         if (p.K && s_use_keys && !(PUSH && it == 0 && p.labels)) {
@@ -565,6 +601,15 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
         stat_nbrs<STATS>(p, tag, x, len, tid, NT, st);
     }
     if (PH == 0) {
+        if (it == 0 && p.dataflow) {
+            int lo = 0x7fffffff, hi = -1;
+            for (int64_t j = tid; j < len; j += NT) {
+                const int c = x[j];
+                lo = min(lo, c);
+                hi = max(hi, c);
+            }
+            track_cols_flush(lo, hi);
+        }
         const uint64_t tv = p.T[v];
         const bool count_deg = PUSH && it == 0 && p.labels;
         const bool keys = p.K && s_use_keys && !count_deg;
@@ -823,7 +868,6 @@ struct __align__(16) SMeta {
     int32_t v;    // vertex (-1: no row)
     int32_t len;  // row length; bit 30 set: staged in the slot
 };
-constexpr int kMaxDbgBlocks = 1184;
 // sparse step layout of a staging buffer: row slots | SMeta per row | T_v per row
 constexpr int kMaxRowsS = kMB / 2;                    // rows per sparse step (GS >= 2)
 constexpr int kTvOff = kTileCap - 2 * kMaxRowsS;      // uint64 T_v per row
@@ -1099,6 +1143,68 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, int64_t blo
     return out;
 }
 
+// ------------------------------------------------------------ dataflow sync
+// Instead of a grid-wide barrier between phases, a block waits only for the
+// blocks whose rows it reads.  Every phase reads the previous phase's values
+// of the rows in N[own rows] and writes only its own rows (push form: rows
+// within distance 1 of its own), so block b may start phase k once every
+// block d in D_b has completed phase k - 1, where D_b = the blocks whose
+// row ranges meet [least, greatest] column read by b in iteration 0, plus
+// b.  For a symmetric graph the relation covers both directions of every
+// conflict: an edge (u in b, w in d) puts d in D_b (b reads w) and b in D_d
+// (d reads u), so no block overwrites a value a neighbour has still to read
+// and no block reads a value before its writer has produced it.  Blocks of a
+// banded graph (the stencils: D_b ~ 13 of 592 blocks on C2) run ahead of
+// distant slow blocks instead of idling at a barrier; an unbanded graph
+// (Kronecker) has D_b = all blocks, i.e. a barrier.  The loop condition
+// |worklist_1| = 0 is a global sum: each block adds its count to the
+// word of its iteration; the last arrival of an iteration with a zero sum
+// publishes the iteration count (`done`).  Blocks that have not seen it yet
+// may start the next iteration's Refresh Column -- it writes only M of rows
+// whose neighbours are all decided, which no later phase reads -- and stop
+// at their next wait.
+__device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* a) {
+    unsigned int v;
+    asm volatile("ld.relaxed.gpu.u32 %0,[%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+// owner block of row r under the static ranges [n*b/B, n*(b+1)/B)
+__device__ __forceinline__ int owner_block(int64_t n, int64_t B, int64_t r) {
+    int64_t b = n > 0 ? (r * B) / n : 0;
+    if (b >= B) b = B - 1;
+    while (b + 1 < B && n * (b + 1) / B <= r) b++;
+    while (b > 0 && n * b / B > r) b--;
+    return (int)b;
+}
+// completes phase k of this block and waits for D_b to complete it; returns
+// the published iteration count (0 = not finished).  All threads call it.
+__device__ __forceinline__ int df_sync(TileSmem& sm, const MisParams& p, unsigned int k) {
+    __syncthreads();  // the block's writes of phase k are done
+    const int t = threadIdx.x;
+    if (t == 0) asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(p.prog + blockIdx.x), "r"(k) : "memory");
+    if (t < 32) {
+        const int dlo = sm.dlo, nd = sm.dhi - sm.dlo + 1;
+        int done = 0;
+        for (;;) {
+            bool ok = true;
+            for (int i = t; i < nd; i += 32) ok &= ld_relaxed_u32(p.prog + dlo + i) >= k;
+            if (__all_sync(kFull, ok)) break;
+            int d = 0;
+            if (t == 0) d = (int)ld_relaxed_u32(reinterpret_cast<const unsigned int*>(&p.ctrl[9]));
+            done = __shfl_sync(kFull, d, 0);
+            if (done) break;  // warp-uniform
+            __nanosleep(20);
+        }
+        if (t == 0) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            if (!done) done = (int)ld_relaxed_u32(reinterpret_cast<const unsigned int*>(&p.ctrl[9]));
+            sm.done = done;
+        }
+    }
+    __syncthreads();
+    return sm.done;
+}
+
 __device__ __forceinline__ void stamp(const MisParams& p, int slot) {
     if (p.timeline && blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long ns;
@@ -1131,7 +1237,15 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         mbar_init(&sm.mbarS[1], kRowGroups);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         sm.pol = l2_policy(p, blo, bhi);
+        sm.cmin = 0x7fffffff;
+        sm.cmax = -1;
+        sm.dlo = 0;  // until iteration 0's columns are known: every block
+        sm.dhi = (int)B - 1;
+        sm.done = 0;
+        if (p.dataflow) p.prog[blockIdx.x] = 0u;
     }
+    if (p.dataflow)  // ordered before any use by the grid barrier after the init phase
+        for (int i = (int)blockIdx.x * kMB + t; i < p.max_iters; i += (int)B * kMB) p.iter_ring[i] = 0ull;
     uint32_t ph = 0u;  // mbarrier phase bits: 0,1 dense buffers; 2,3 sparse buffers
 
     // worklists <- 0..|V|; Refresh Row of iteration 0.
@@ -1197,6 +1311,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
     const int64_t range = bhi - blo;
     // this block's worklist segment sizes (a masked call starts from its lists)
     int cnt1 = p.labels ? act_block : (int)range, cnt2 = cnt1;
+    unsigned int kph = 0;  // dataflow: phases completed by this block
     while (n_active > 0) {  // while worklist_1 != {}
         const int cur = it & 1;
         // ---- Refresh Column over worklist_2
@@ -1209,7 +1324,18 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
             cnt2 = dense2 ? dense_phase<G, STATS, 0, false>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0)
                           : sparse_phase<G, STATS, 0, false>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
         }
-        grid_barrier(bar);
+        if (p.dataflow) {
+            if (it == 0 && t == 0) {  // D_b from the columns read in iteration 0 (and the own rows)
+                const int64_t lo = min((int64_t)sm.cmin, blo), hi = max((int64_t)sm.cmax, bhi - 1);
+                sm.dlo = range > 0 ? owner_block(p.n, B, lo) : (int)blockIdx.x;
+                sm.dhi = range > 0 ? owner_block(p.n, B, hi) : (int)blockIdx.x;
+                if (sm.dlo > (int)blockIdx.x) sm.dlo = (int)blockIdx.x;
+                if (sm.dhi < (int)blockIdx.x) sm.dhi = (int)blockIdx.x;
+            }
+            if (df_sync(sm, p, ++kph)) break;
+        } else {
+            grid_barrier(bar);
+        }
         stamp(p, 1 + 2 * it);
         // ---- Decide over worklist_1 + fused refresh of iteration it+1
         const uint64_t fi_next = p.prio.iter_term(it + 1);
@@ -1217,6 +1343,23 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         if (push) cnt1 = decide_push<STATS>(sm, p, it, blo, bhi, p.L1[cur], cnt1, dense1, p.L1[cur ^ 1], fi_next);
         else if (dense1) cnt1 = dense_phase<G, STATS, 1>(sm, p, it, blo, bhi, p.L1[cur ^ 1], ph, fi_next);
         else cnt1 = sparse_phase<G, STATS, 1>(sm, p, it, blo, p.L1[cur], cnt1, p.L1[cur ^ 1], ph, fi_next);
+        if (p.dataflow) {
+            if (t == 0) {  // arrival at iteration it: (1 << 44) | |worklist_1 segment|
+                unsigned long long old;
+                asm volatile("atom.add.acq_rel.gpu.u64 %0,[%1],%2;"
+                             : "=l"(old)
+                             : "l"(p.iter_ring + it), "l"((1ull << 44) | (unsigned long long)cnt1)
+                             : "memory");
+                if ((old >> 44) == (unsigned long long)(B - 1) && (old & ((1ull << 44) - 1)) + cnt1 == 0)
+                    asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&p.ctrl[9]), "r"(it + 1) : "memory");
+            }
+            const int done = df_sync(sm, p, ++kph);
+            stamp(p, 2 + 2 * it);
+            it++;
+            if (done) break;
+            if (it >= p.max_iters) break;  // status from the published count (below)
+            continue;
+        }
         if (t == 0) {
             if (cnt1) atomicAdd(&ring[it & 3], (unsigned long long)cnt1);
             if (blockIdx.x == 0) ring[(it + 2) & 3] = 0;  // slot last read two barriers ago
@@ -1248,6 +1391,11 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         if (ticket == gridDim.x - 1) {  // last block publishes the scalars
             __threadfence();
             *p.d_count = (int64_t)ld_acquire_u64(&p.ctrl[5]);
+            if (p.dataflow && n_active > 0) {  // every block has left the loop: the count is final
+                const int done = (int)ld_relaxed_u32(reinterpret_cast<const unsigned int*>(&p.ctrl[9]));
+                it = done ? done : p.max_iters;
+                status = done ? MIS2_OK : MIS2_ENOTCONVERGED;
+            }
             *p.d_iters = it;
             *p.d_status = status;
         }

@@ -8,15 +8,22 @@ namespace mis2k {
 
 enum { kBadRowptr = 1, kBadRange = 2, kBadOrder = 4, kBadSym = 8 };
 
-__global__ void k_validate(int64_t n, int64_t nnz, const int64_t* __restrict__ rowptr,
-                           const int32_t* __restrict__ colinds, int* err) {
+// pass 1: rowptr[0] = 0, nondecreasing, rowptr[n] = nnz, within [0, nnz]
+__global__ void k_validate_rowptr(int64_t n, int64_t nnz, const int64_t* __restrict__ rowptr, int* err) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
         const int64_t s = rowptr[v], e = rowptr[v + 1];
-        if ((v == 0 && s != 0) || e < s || (v == n - 1 && e != nnz) || s < 0 || e > nnz) {
-            atomicOr(err, kBadRowptr);
-            continue;
-        }
+        if ((v == 0 && s != 0) || e < s || (v == n - 1 && e != nnz) || s < 0 || e > nnz) atomicOr(err, kBadRowptr);
+    }
+}
+// pass 2 (skipped when pass 1 failed, so every row bound it reads is sound):
+// colinds in range, rows strictly increasing, pattern symmetric
+__global__ void k_validate(int64_t n, int64_t nnz, const int64_t* __restrict__ rowptr,
+                           const int32_t* __restrict__ colinds, int* err) {
+    if (*(volatile int*)err & kBadRowptr) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+        const int64_t s = rowptr[v], e = rowptr[v + 1];
         int32_t prev = -1;
         for (int64_t j = s; j < e; j++) {
             const int32_t w = colinds[j];
@@ -54,6 +61,7 @@ int run_validate(const mis2_graph& g, void* ws, size_t ws_bytes, cudaStream_t s,
     MIS2_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int), s));
     int64_t blocks = (g.n + kBlock - 1) / kBlock;
     if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
+    k_validate_rowptr<<<(unsigned)blocks, kBlock, 0, s>>>(g.n, g.nnz, g.rowptr, err);
     k_validate<<<(unsigned)blocks, kBlock, 0, s>>>(g.n, g.nnz, g.rowptr, g.colinds, err);
     count_launch(2);
     MIS2_CUDA_TRY(cudaGetLastError());

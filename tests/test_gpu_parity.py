@@ -218,10 +218,11 @@ def test_mis2_host_e2e():
 
 
 # ----------------------------------------------------------------- aggregation
-def check_agg(g, seed=0, decide="auto", word_bits=64):
+def check_agg(g, seed=0, decide="auto", word_bits=64, keys="auto", o=None):
     rp, ci = dev(g)
-    a = M().aggregate(rp, ci, seed=seed, decide=decide, word_bits=word_bits)
-    o = O.aggregate(g.rowptr, g.colinds, seed=seed, word_bits=word_bits)
+    a = M().aggregate(rp, ci, seed=seed, decide=decide, word_bits=word_bits, keys=keys)
+    if o is None:
+        o = O.aggregate(g.rowptr, g.colinds, seed=seed, word_bits=word_bits)
     assert a.num_aggs == o.num_aggs, g.name
     assert np.array_equal(a.labels.cpu().numpy(), o.labels), g.name
     assert np.array_equal(a.roots.cpu().numpy(), o.roots), g.name
@@ -252,6 +253,24 @@ def test_aggregate_configs():
 @pytest.mark.slow
 def test_aggregate_config3():
     check_agg(G.config_graph(2))
+
+
+@pytest.mark.slow
+def test_aggregate_config4():
+    """Alg. 3 on the Kronecker scale-24 graph (configs[3]): labels, roots and
+    all 8 statistics bit-exact.  The default launch picks the 32-bit column
+    keys for this skewed graph, so the masked phase-2 MIS-2 runs with them."""
+    check_agg(G.config_graph(3))
+
+
+@pytest.mark.parametrize("decide", ["pull", "push"])
+def test_aggregate_masked_keys(decide):
+    """The masked (phase-2) MIS-2 with the 32-bit column keys forced on:
+    small random / power-law / stencil graphs and skewed Kronecker graphs."""
+    gs = small_graphs(40, 2500) + [G.kronecker(12), G.random_powerlaw_graph(4000, 20, 3), G.laplace3d_27pt(20)]
+    for g in gs:
+        check_agg(g, decide=decide, keys="on")
+        check_agg(g, seed=5, decide=decide, keys="on")
 
 
 # ----------------------------------------------------------------- coarsening
@@ -309,11 +328,20 @@ def test_multilevel_elasticity():
 
 @pytest.mark.slow
 def test_multilevel_config5():
+    """configs[4] (3-dof 27-pt 150^3): level-0 labels, roots, statistics and
+    coarse CSR element-wise against the oracle, then every level size and
+    the final coarse CSR of the multilevel run."""
     g = G.config_graph(4)
+    oa = O.aggregate(g.rowptr, g.colinds)
+    a = check_agg(g, o=oa)
     rp, ci = dev(g)
-    levels, _, _ = M().multilevel(rp, ci, threshold=1000)
-    olevels, _ = O.multilevel(g.rowptr, g.colinds, threshold=1000)
-    assert levels == olevels
+    crow, ccol = M().coarsen(rp, ci, a.labels, a.num_aggs)
+    orow, ocol = O.coarsen(g.rowptr, g.colinds, oa.labels, oa.num_aggs)
+    assert np.array_equal(crow.cpu().numpy(), orow) and np.array_equal(ccol.cpu().numpy(), ocol)
+    levels, (frp, fci), _ = M().multilevel(rp, ci, threshold=1000)
+    olevels_rest, (orp, oci) = O.multilevel(orow, ocol, threshold=1000)
+    assert levels == [(g.n, int(g.rowptr[-1]), oa.num_aggs)] + olevels_rest
+    assert np.array_equal(frp.cpu().numpy(), orp) and np.array_equal(fci.cpu().numpy(), oci)
 
 
 # ----------------------------------------------------------------- Alg. 2 (NEXT-1)
@@ -405,6 +433,22 @@ def test_partitioned_coarsen_and_multilevel(nparts):
         assert [l[0] for l in lv] == [l[0] for l in lv1] and [l[2] for l in lv] == [l[2] for l in lv1], g.name
         if fin is not None:
             assert torch.equal(fin[0], fin1[0]) and torch.equal(fin[1], fin1[1])
+
+
+@pytest.mark.slow
+def test_partitioned_aggregate_config3():
+    """configs[3]'s workload: Alg. 3 of the 7-pt 300^3 graph row-partitioned
+    over 2, 4 and 8 parts (local transport) -- labels and statistics
+    bit-exact against the oracle."""
+    g = G.config_graph(2)
+    o = O.aggregate(g.rowptr, g.colinds)
+    lab = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    for nparts in (2, 4, 8):
+        c = M().Comm.local_parts(nparts).set_graph(g.n, g.rowptr, g.colinds)
+        na, st = c.aggregate(lab)
+        c.close()
+        assert na == o.num_aggs and st == o.stats, nparts
+        assert np.array_equal(lab.cpu().numpy(), o.labels), nparts
 
 
 @pytest.mark.slow
@@ -543,3 +587,91 @@ def test_word32_aggregate_and_partitioned():
             assert np.array_equal(out[: g.n].cpu().numpy().astype(bool), o.in_set) and (cnt, its) == (o.count, o.iterations)
             oa = O.aggregate(g.rowptr, g.colinds, word_bits=32)
             assert na == oa.num_aggs and np.array_equal(lab[: g.n].cpu().numpy(), oa.labels) and st == oa.stats
+
+
+# ----------------------------------------------------------------- boundary (include/mis2.h)
+def test_int32_rowptr():
+    """rowptr_bits = 32: int32 row pointers give the same MIS-2, aggregation,
+    coarse graph and validation as int64 ones."""
+    for g in [G.config_graph(0), G.laplace3d_27pt(20), G.kronecker(10), G.random_graph(300, 0.05, 1)]:
+        rp, ci = dev(g)
+        rp32 = rp.to(torch.int32)
+        r64, r32 = M().mis2(rp, ci), M().mis2(rp32, ci)
+        assert torch.equal(r64.in_set, r32.in_set) and (r64.count, r64.iterations) == (r32.count, r32.iterations)
+        a64, a32 = M().aggregate(rp, ci), M().aggregate(rp32, ci)
+        assert torch.equal(a64.labels, a32.labels) and a64.stats == a32.stats
+        c64, c32 = M().coarsen(rp, ci, a64.labels, a64.num_aggs), M().coarsen(rp32, ci, a64.labels, a64.num_aggs)
+        assert torch.equal(c64[0], c32[0]) and torch.equal(c64[1], c32[1])
+        M().validate_graph(rp32, ci)
+        o = O.mis2(g.rowptr, g.colinds)
+        assert np.array_equal(r32.in_set.cpu().numpy().astype(bool), o.in_set)
+
+
+def test_validate_malformed_rowptr():
+    """A malformed rowptr is EGRAPH (not a device fault): the symmetry pass
+    only runs on a sound rowptr."""
+    g = G.laplace3d_7pt(8)
+    rp, ci = dev(g)
+    for bad in ([(3, -5)], [(4, g.rowptr[-1] * 4)], [(5, 2), (6, 1)], [(g.n, g.rowptr[-1] + 7)]):
+        b = rp.clone()
+        for i, v in bad:
+            b[i] = int(v)
+        with pytest.raises(M().Mis2Error) as e:
+            M().validate_graph(b, ci)
+        assert e.value.rc == M().EGRAPH
+    r = M().mis2(rp, ci)  # the context is still usable
+    assert r.count == O.mis2(g.rowptr, g.colinds).count
+
+
+def test_coarsen_labels_out_of_range():
+    """Labels outside [0, num_aggs) are rejected with EINVAL before any kernel
+    indexes with them; the device context stays usable."""
+    g = G.laplace3d_7pt(10)
+    rp, ci = dev(g)
+    a = M().aggregate(rp, ci)
+    for bad_val in (-7, a.num_aggs, 1 << 30):
+        lab = a.labels.clone()
+        lab[17] = bad_val
+        with pytest.raises(M().Mis2Error) as e:
+            M().coarsen(rp, ci, lab, a.num_aggs)
+        assert e.value.rc == M().EINVAL
+    torch.cuda.synchronize()
+    check_coarsen(g)
+
+
+def test_empty_graph_null_rowptr():
+    """n = 0 with NULL rowptr / colinds: empty set, 0 iterations, no kernel."""
+    import ctypes
+    m = M()
+    g = m._Graph(0, 0, None, None, 64, 0)
+    o = m._opts()
+    ws, wsb = m.workspace(m.OP_MIS2, 0, 0)
+    cnt, its = ctypes.c_int64(-1), ctypes.c_int32(-1)
+    out = torch.empty(1, dtype=torch.uint8, device="cuda")
+    rc = m.lib().mis2(ctypes.byref(g), ctypes.byref(o), out.data_ptr(), ctypes.byref(cnt), ctypes.byref(its), None,
+                      ws.data_ptr(), wsb, m._stream())
+    assert rc == 0 and cnt.value == 0 and its.value == 0
+    torch.cuda.synchronize()
+
+
+def test_nccl_transport_world1():
+    """The NCCL transport (one process per GPU) on the single GPU of this box,
+    world size 1: ncclCommInitRank, the request-count allgather of
+    set_graph, the per-iteration allreduce of |worklist_1|, the root-count
+    allgather of the aggregation and the coarse-CSR allgather of
+    mis2_dist_coarsen all run; results bit-identical to the oracle."""
+    m = M()
+    for g in [G.config_graph(0), G.laplace3d_27pt(20), G.kronecker(10)]:
+        c = m.Comm.nccl(m.comm_unique_id(), 1, 0).set_graph(g.n, g.rowptr, g.colinds)
+        out = torch.empty(g.n, dtype=torch.uint8, device="cuda")
+        cnt, its = c.mis2(out)
+        o = O.mis2(g.rowptr, g.colinds)
+        assert np.array_equal(out.cpu().numpy().astype(bool), o.in_set) and (cnt, its) == (o.count, o.iterations)
+        lab = torch.empty(g.n, dtype=torch.int32, device="cuda")
+        na, st = c.aggregate(lab)
+        oa = O.aggregate(g.rowptr, g.colinds)
+        assert na == oa.num_aggs and st == oa.stats and np.array_equal(lab.cpu().numpy(), oa.labels)
+        crow, ccol = c.coarsen(lab, na)
+        orow, ocol = O.coarsen(g.rowptr, g.colinds, oa.labels, oa.num_aggs)
+        assert np.array_equal(crow.cpu().numpy(), orow) and np.array_equal(ccol.cpu().numpy(), ocol)
+        c.close()

@@ -117,3 +117,39 @@ def test_symmetric_sweep_is_a_symmetric_operator_and_converges():
         x = O.cluster_sgs(g.rowptr, g.colinds, vals, labels, na, ccolor, nc, b, x, 1)
         err.append(np.sqrt((x - xs) @ A @ (x - xs)))
     assert all(e2 < e1 for e1, e2 in zip(err, err[1:]))
+
+
+def greedy_in_priority_order(g, seed, ascending=True):
+    """Independent formulation of reading Q30: sequential greedy colouring that
+    visits the vertices in ascending order of their iteration-0 MIS-2 word
+    (Eq. 1 via tests/pins.py's big-int hash).  Jones-Plassmann colours a vertex
+    once it is the least uncoloured word among its neighbours, so exactly its
+    smaller-word neighbours are coloured then: the same colours as this
+    sequential sweep."""
+    from pins import adjacency_sets, py_word
+    adj = adjacency_sets(g.rowptr, g.colinds)
+    order = sorted(range(g.n), key=lambda v: py_word(0, v, g.n, seed), reverse=not ascending)
+    color = [-1] * g.n
+    for v in order:
+        used = {color[u] for u in adj[v] if color[u] >= 0}
+        c = 0
+        while c in used:
+            c += 1
+        color[v] = c
+    return np.array(color, dtype=np.int32)
+
+
+@pytest.mark.parametrize("seed", [0, 31, 12345])
+def test_coloring_equals_sequential_greedy_by_priority(seed):
+    """Pins the exact colouring of reading Q30 (P:339, P:683 'greedy graph
+    coloring'): the oracle's Jones-Plassmann rounds equal a sequential greedy
+    sweep in ascending priority order, independently written; a max-priority
+    reading (descending order) gives a different colouring on these graphs."""
+    differs = 0
+    for g in graphs() + [G.kronecker(8), G.random_graph(150, 0.1, 7), G.from_edges(9, [])]:
+        color, nc = O.color_jp(g.rowptr, g.colinds, seed=seed)
+        ref = greedy_in_priority_order(g, seed)
+        assert np.array_equal(color, ref), g.name
+        assert nc == (int(ref.max()) + 1 if g.n else 0)
+        differs += not np.array_equal(color, greedy_in_priority_order(g, seed, ascending=False))
+    assert differs > 0

@@ -401,3 +401,53 @@ def test_multilevel_reaches_threshold():
     assert len(levels) >= 1 and rp.shape[0] - 1 < 1000
     for (n0, _, na), (n1, _, _) in zip(levels, levels[1:]):
         assert n1 == na < n0
+
+
+def basic_coarsening_reference(g, seed=0):
+    """Independent formulation of Alg. 2 with reading Q28, from the
+    MIS-2 set alone: roots numbered in ascending vertex order (Q18); each root
+    and its neighbours form its aggregate (the neighbours of one
+    root are adjacent to no other root, since roots are 3 apart); every other
+    vertex joins the aggregate of its smallest-id aggregated neighbour
+    (P:280 'any neighbor', Q28)."""
+    from pins import adjacency_sets
+    adj = adjacency_sets(g.rowptr, g.colinds)
+    S = O.mis2(g.rowptr, g.colinds, seed=seed).in_set
+    roots = [v for v in range(g.n) if S[v]]
+    label = [-1] * g.n
+    for a, r in enumerate(roots):
+        label[r] = a
+        for w in adj[r]:
+            assert label[w] in (-1, a)
+            label[w] = a
+    tent = list(label)
+    for v in range(g.n):
+        if tent[v] < 0:
+            cand = sorted(u for u in adj[v] if tent[u] >= 0)
+            label[v] = tent[cand[0]]
+    return np.array(label, dtype=np.int32), len(roots)
+
+
+@pytest.mark.parametrize("seed", [0, 3])
+def test_basic_coarsening_join_rule(seed):
+    """Pins the exact labels of Alg. 2 (reading Q28) against the independent
+    formulation above; a largest-id join would differ on these graphs."""
+    gs = [G.grid2d_5pt(10, 10), G.laplace3d_7pt(8), G.laplace3d_27pt(6), G.random_graph(300, 0.02, 5),
+          G.random_powerlaw_graph(400, 4, 2), G.elasticity3d(4), G.kronecker(9)]
+    for g in gs:
+        labels, na = O.coarsen_basic(g.rowptr, g.colinds, seed=seed)
+        ref, rna = basic_coarsening_reference(g, seed)
+        assert na == rna and np.array_equal(labels, ref), g.name
+    # the rule matters: joining the LARGEST-id aggregated neighbour changes some label
+    from pins import adjacency_sets
+    g = G.laplace3d_7pt(8)
+    labels, _ = O.coarsen_basic(g.rowptr, g.colinds, seed=seed)
+    ref, _ = basic_coarsening_reference(g, seed)
+    adj = adjacency_sets(g.rowptr, g.colinds)
+    S = O.mis2(g.rowptr, g.colinds, seed=seed).in_set
+    phase1 = {v for v in range(g.n) if S[v] or any(S[u] for u in adj[v])}
+    alt = ref.copy()
+    for v in range(g.n):
+        if v not in phase1:
+            alt[v] = ref[max(u for u in adj[v] if u in phase1)]
+    assert not np.array_equal(alt, labels)
