@@ -55,7 +55,6 @@ struct DeviceInfo {
 int device_info(DeviceInfo* out);
 
 constexpr int kStatsMaxIters = 400;
-constexpr int kIterRing = 1024;  // dataflow sync supports max_iters <= kIterRing (else grid barriers)
 
 // MIS-2 state carved from the workspace
 struct Mis2Ws {
@@ -70,9 +69,7 @@ struct Mis2Ws {
     uint32_t* degc;
     uint32_t* K;        // 32-bit column keys (mis2_core.cu kkey)
     unsigned long long* ctrl;  // [0]=barrier, [1..4]=ring of |wl1| sums, [5]=count, [6]=ticket,
-                               // [7]=active, [8]=max degree, [9]=published iteration count (dataflow)
-    unsigned long long* iter_ring;  // [kIterRing] dataflow: per-iteration (arrivals << 44 | sum |wl1|)
-    unsigned int* prog;             // [max blocks] dataflow: phases completed per block
+                               // [7]=active, [8]=max degree
     long long* dstats;         // [kStatsMaxIters * 6]
     long long* scal;           // [8] host-visible scalars of mis2()/mis2_host()
 };

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(kMB) mis2_part_init(MisParams p, int* cnts, un
 __global__ void mis2_part_final(MisParams p, unsigned long long* count) {
     {
         const int64_t B = gridDim.x;
-        l2_release(p, p.n * blockIdx.x / B, p.n * (blockIdx.x + 1) / B);
+        l2_release(p, make_rows(p.n, B, blockIdx.x, kMB, false));
     }
     int c = 0;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < p.n; v += (int64_t)gridDim.x * blockDim.x) {
@@ -120,9 +120,8 @@ static void* pick_kernel(int G, bool stats, bool push) {
 int max_coop_warps(const DeviceInfo& d) { return d.sms * 64; }
 
 void carve_mis2(Carve& c, int64_t n, int64_t nnz, int max_warps, Mis2Ws* w) {
+    (void)max_warps;
     w->ctrl = c.take<unsigned long long>(16);
-    w->iter_ring = c.take<unsigned long long>(kIterRing);
-    w->prog = c.take<unsigned int>((size_t)max_warps);  // >= blocks of any cooperative grid
     w->T = c.take<uint64_t>((size_t)n + 1);
     w->M = c.take<uint32_t>((size_t)n + 1);
     for (int i = 0; i < 2; i++) {
@@ -320,18 +319,6 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
         p.L2[i] = w.L2[i];
     }
     p.ctrl = w.ctrl;
-    p.iter_ring = w.iter_ring;
-    p.prog = w.prog;
-    // dataflow sync (mis2_kernel.cuh df_sync): neighbour waits instead of grid
-    // barriers.  Opt-in measurement mode (MIS2_DATAFLOW=1, results identical):
-    // measured C2 391 -> 457 us (blocks favoured by the warp scheduler run
-    // ahead and the starved ones finish later), C3 5.59 -> 5.49 ms, C5 8.34 ->
-    // 8.32 ms, C4 74.7 -> 75.5 ms.  Never with the per-iteration statistics (a
-    // block may start an iteration past the last one) or beyond the
-    // iteration-word capacity.
-    p.dataflow = 0;
-    if (const char* e = getenv("MIS2_DATAFLOW"))
-        p.dataflow = atoi(e) != 0 && !stats && max_iters <= kIterRing && grid <= max_coop_warps(di);
     p.heavy = w.heavy;
     p.mark = w.mark;
     p.oflag = w.oflag;
@@ -357,6 +344,10 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     p.id_mask = (uint32_t)((1ull << p.prio.b) - 1ull);
     p.prio.n = g.n;
     p.l2_keep = l2_keep_for(g.nnz);
+    // cyclic row ownership (mis2_kernel.cuh Rows); MIS2_CYCLIC=0: contiguous
+    // ranges (measurement knob, results identical)
+    p.cyclic = 1;
+    if (const char* e = getenv("MIS2_CYCLIC")) p.cyclic = atoi(e) != 0;
     p.push_iters = push_iters;
     p.prio.override_ = o.prio_override;
     p.prio.override_iters = o.prio_override ? o.prio_iters : 0;

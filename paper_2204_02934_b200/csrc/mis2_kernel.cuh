@@ -71,7 +71,16 @@ template <int G>
 __host__ __device__ constexpr int heavy_len() {
     return MIS2_HEAVY_BATCHES * G * gather_batch<G>();
 }
-constexpr int kDenseNum = 3, kDenseDen = 8;  // dense if |worklist segment| >= 3/8 of the range (pull phases)
+constexpr int kDenseNum = 3, kDenseDen = 8;
+// lanes per row of the sparse (worklist) phases: GS = min(G * kSparseMul, 32)
+#ifndef MIS2_SPARSE_MUL
+#define MIS2_SPARSE_MUL 2
+#endif
+constexpr int kSparseMul = MIS2_SPARSE_MUL;
+template <int G>
+__host__ __device__ constexpr int sparse_group() {
+    return G * kSparseMul <= 32 ? G * kSparseMul : 32;
+}  // dense if |worklist segment| >= 3/8 of the range (pull phases)
 // M_v is only ever compared against T_v (Decide: "M_w = T_v", "M_w = OUT").
 // By Eq. 1 the low b bits of an undecided word are id+1, unique per vertex,
 // never 0 and never all ones (2^b - 1 > |V|), and M_w is always a
@@ -99,12 +108,7 @@ struct MisParams {
     int32_t* L1[2];                      // worklist_1, double buffered, per-block segments
     int32_t* L2[2];                      // worklist_2
     unsigned long long* ctrl;
-    // dataflow synchronisation (see df_sync): per-block completed-phase
-    // counters and per-iteration (arrivals << 44 | sum of |worklist_1|) words
-    unsigned int* prog;
-    unsigned long long* iter_ring;
-    int dataflow;                        // 1: neighbour waits instead of grid barriers
-    int32_t* heavy;       // [n] deferred long rows, per-block segments at blo
+    int32_t* heavy;       // [n] deferred long rows, per-block segments at Rows::seg
     uint8_t* oflag;       // push-form Decide: some w in N[v] got M_w = OUT this iteration
     uint32_t* cnt;        // push-form Decide: |{w in N[v] : M_w = T_v}| this iteration
     uint32_t* degc;       // |N[v] ∩ active| (closed), written by the column pass of iteration 0
@@ -112,6 +116,7 @@ struct MisParams {
     long long* dstats;    // stats only
     long long* timeline;  // MIS2_FLAG_TIMELINE only
     float l2_keep;        // fraction of each block's colinds span kept in L2 (evict_last)
+    int cyclic;           // row ownership: 0 = one contiguous range per block, 1 = cyclic chunks (Rows)
     int push_iters;       // PUSH kernels: iterations it < push_iters use the push-form Decide
     int dbg_it, dbg_ph;   // MIS2_FLAG_TIMELINE: sparse phase instrumented into `mark`
     Prio prio;
@@ -121,6 +126,57 @@ struct MisParams {
     int32_t* d_iters;
     int32_t* d_status;
 };
+
+// ------------------------------------------------------------ row ownership
+// The rows of block b as "runs" of at most rpb consecutive rows (rpb = the
+// rows of one dense step, kMB / G).
+//  * contiguous (partitioned driver): the range [n*b/B, n*(b+1)/B) cut into
+//    runs of rpb rows;
+//  * cyclic (single GPU): the graph's rpb-row chunks c = b, b + B, b + 2B, ...
+//    Vertices still undecided late in the loop cluster in space, so a block
+//    owning one contiguous range can hold several times the mean worklist
+//    of a phase (C2 iteration 5: 483 rows on average, 1689 on the largest)
+//    and the grid barrier waits for it; chunks dealt round-robin give every
+//    block a sample of the whole graph.
+// The block's worklist / deferred-row segment is [seg, seg + count) of the
+// int32[n] list arrays (segments of different blocks are disjoint).
+struct Rows {
+    int64_t n, B, b, rpb;
+    bool cyclic;
+    int64_t lo, hi;  // contiguous range (cyclic: unused)
+    int64_t nruns, count, seg;
+    __device__ __forceinline__ int64_t run_lo(int64_t k) const { return cyclic ? (b + k * B) * rpb : lo + k * rpb; }
+    __device__ __forceinline__ int64_t run_hi(int64_t k) const {
+        const int64_t e = run_lo(k) + rpb, lim = cyclic ? n : hi;
+        return e < lim ? e : lim;
+    }
+    __device__ __forceinline__ int64_t row_at(int64_t i) const { return run_lo(i / rpb) + i % rpb; }
+};
+__device__ __forceinline__ Rows make_rows(int64_t n, int64_t B, int64_t b, int64_t rpb, bool cyclic) {
+    Rows r;
+    r.n = n;
+    r.B = B;
+    r.b = b;
+    r.rpb = rpb;
+    r.cyclic = cyclic;
+    if (!cyclic) {
+        r.lo = n * b / B;
+        r.hi = n * (b + 1) / B;
+        r.count = r.hi - r.lo;
+        r.nruns = (r.count + rpb - 1) / rpb;
+        r.seg = r.lo;
+        return r;
+    }
+    r.lo = r.hi = 0;
+    const int64_t nch = (n + rpb - 1) / rpb;         // chunks of the graph; chunk c -> block c mod B
+    const int64_t tail = nch * rpb - n;              // rows missing from the last chunk
+    const int64_t last_owner = nch > 0 ? (nch - 1) % B : -1;
+    r.nruns = b < nch ? (nch - b + B - 1) / B : 0;
+    r.count = r.nruns * rpb - (b == last_owner ? tail : 0);
+    const int64_t before = (nch / B) * b + (b < nch % B ? b : nch % B);  // chunks of blocks < b
+    r.seg = before * rpb - (last_owner >= 0 && last_owner < b ? tail : 0);
+    return r;
+}
 
 // per block: the column passes use the 32-bit keys (decided once per call,
 // after the init phase; see the kernel)
@@ -137,30 +193,9 @@ struct __align__(16) TileSmem {
     int hcount;
     int hnext;       // deferred rows: next row for a warp
     int nhuge;       // deferred rows too long for a warp
-    int cmin, cmax;  // dataflow: least / greatest column read by this block (iteration 0)
-    int dlo, dhi;    // dataflow: blocks whose rows this block reads (and which read its rows)
-    int done;        // dataflow: iteration count published by the last block of the final iteration
     uint64_t red64[kMW];
     int wred[kMW];
 };
-
-__device__ __forceinline__ TileSmem& tile_smem() {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    return *reinterpret_cast<TileSmem*>(smem_raw);
-}
-
-// Dataflow synchronisation: the least and greatest column the block reads in
-// iteration 0 (every active row is in worklist_2 then), reduced per warp into
-// the block's shared pair.  Called by all 32 lanes of a warp.
-__device__ __forceinline__ void track_cols_flush(int lo, int hi) {
-    lo = __reduce_min_sync(kFull, lo);
-    hi = __reduce_max_sync(kFull, hi);
-    if ((threadIdx.x & 31) == 0 && hi >= 0) {
-        TileSmem& sm = tile_smem();
-        atomicMin(&sm.cmin, lo);
-        atomicMax(&sm.cmax, hi);
-    }
-}
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -200,8 +235,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // evict_first, so a fixed, evenly spread part of the stream stays resident
 // from phase to phase (all blocks see the same hit rate).  The span is
 // demoted back to evict_normal when the call ends (l2_release).
-__device__ __forceinline__ uint64_t l2_policy(const MisParams& p, int64_t blo, int64_t bhi) {
-    const int64_t s0 = p.rowptr[blo] & ~(int64_t)31, s1 = p.rowptr[bhi];
+__device__ __forceinline__ uint64_t l2_policy_range(const MisParams& p, int64_t s0, int64_t s1) {
     const char* base = reinterpret_cast<const char*>(p.colinds + s0);
     int64_t tot = (s1 - s0) * 4 + 128;
     if (tot > 0x7fffff00ll) tot = 0x7fffff00ll;
@@ -216,13 +250,25 @@ __device__ __forceinline__ uint64_t l2_policy(const MisParams& p, int64_t blo, i
                  : "l"(base), "r"((uint32_t)prim), "r"((uint32_t)tot));
     return pol;
 }
-__device__ __forceinline__ void l2_release(const MisParams& p, int64_t blo, int64_t bhi) {
+// contiguous ownership: the first l2_keep of the block's own colinds span;
+// cyclic ownership: the first l2_keep of the whole colinds array (= the first
+// l2_keep of every block's chunks, since chunk c belongs to block c mod B)
+__device__ __forceinline__ uint64_t l2_policy(const MisParams& p, const Rows& r) {
+    if (r.cyclic) return l2_policy_range(p, 0, p.nnz);
+    return l2_policy_range(p, p.rowptr[r.lo] & ~(int64_t)31, p.rowptr[r.hi]);
+}
+__device__ __forceinline__ void l2_release(const MisParams& p, const Rows& r) {
     if (p.l2_keep <= 0.f) return;
-    const int64_t s0 = p.rowptr[blo] & ~(int64_t)31, s1 = p.rowptr[bhi];
-    const int64_t prim = (int64_t)((double)((s1 - s0) * 4 + 128) * (double)p.l2_keep);
+    const int64_t s0 = r.cyclic ? 0 : (p.rowptr[r.lo] & ~(int64_t)31), s1 = r.cyclic ? p.nnz : p.rowptr[r.hi];
+    int64_t tot = (s1 - s0) * 4 + 128;
+    if (tot > 0x7fffff00ll) tot = 0x7fffff00ll;
+    const int64_t prim = (int64_t)((double)tot * (double)p.l2_keep);
     const char* base = reinterpret_cast<const char*>(p.colinds + s0);
-    for (int64_t o = (int64_t)threadIdx.x * 128; o < prim; o += (int64_t)blockDim.x * 128)
-        asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(base + o) : "memory");
+    // cyclic: the blocks split the kept range; contiguous: each block its own
+    const int64_t lines = (prim + 127) / 128;
+    const int64_t l0 = r.cyclic ? lines * r.b / r.B : 0, l1 = r.cyclic ? lines * (r.b + 1) / r.B : lines;
+    for (int64_t l = l0 + threadIdx.x; l < l1; l += blockDim.x)
+        asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(base + l * 128) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -469,16 +515,6 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
                                             int len, uint64_t tv, int it, uint64_t fi_next) {
     bool keep = false;
     if (PH == 0) {
-        if (it == 0 && p.dataflow) {
-            int lo = 0x7fffffff, hi = -1;
-            if (act)
-                for (int j = sub; j < len; j += GG) {
-                    const int c = x[j];
-                    lo = min(lo, c);
-                    hi = max(hi, c);
-                }
-            track_cols_flush(lo, hi);
-        }
         uint32_t mf;
         int dc = 0;
         if (p.K && s_use_keys && !(PUSH && it == 0 && p.labels)) {
@@ -556,12 +592,12 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
 
 // defer a long row to whole-block processing (group leader decides, group agrees)
 template <int GG>
-__device__ __forceinline__ bool defer_long(TileSmem& sm, const MisParams& p, int64_t blo, bool act, int sub,
+__device__ __forceinline__ bool defer_long(TileSmem& sm, const MisParams& p, int64_t seg, bool act, int sub,
                                            int64_t v, int64_t len) {
     bool defer = false;
     if (act && sub == 0 && len > heavy_len<GG>()) {
         const int h = atomicAdd(&sm.hcount, 1);
-        p.heavy[blo + h] = (int32_t)v;  // at most one entry per row of the block's range
+        p.heavy[seg + h] = (int32_t)v;  // at most one entry per row of the block's segment
         defer = true;
     }
     return __shfl_sync(kFull, defer, (threadIdx.x & 31) & ~(GG - 1));
@@ -601,15 +637,6 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
         stat_nbrs<STATS>(p, tag, x, len, tid, NT, st);
     }
     if (PH == 0) {
-        if (it == 0 && p.dataflow) {
-            int lo = 0x7fffffff, hi = -1;
-            for (int64_t j = tid; j < len; j += NT) {
-                const int c = x[j];
-                lo = min(lo, c);
-                hi = max(hi, c);
-            }
-            track_cols_flush(lo, hi);
-        }
         const uint64_t tv = p.T[v];
         const bool count_deg = PUSH && it == 0 && p.labels;
         const bool keys = p.K && s_use_keys && !count_deg;
@@ -695,7 +722,7 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
 // kHugeRow are reduced afterwards by the whole block, one at a time.
 constexpr int kHugeRow = 32768;
 template <bool STATS, int PH, bool PUSH>
-__device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, int32_t* lout, uint64_t fi_next,
+__device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t seg, int32_t* lout, uint64_t fi_next,
                             Stat& st) {
     const int t = threadIdx.x, lane = t & 31;
     const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
@@ -721,21 +748,21 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
             if (lane == 0) i = atomicAdd(&sm.hnext, 1);
             i = __shfl_sync(kFull, i, 0);
             if (i >= nh) break;
-            const int64_t v = p.heavy[blo + i];
+            const int64_t v = p.heavy[seg + i];
             const int64_t len = p.rowptr[v + 1] - p.rowptr[v];
             if (len > kHugeRow && nh <= 2 * kTileCap) {
                 if (lane == 0) huge[atomicAdd(&sm.nhuge, 1)] = (int32_t)v;
                 continue;
             }
             const bool keep = heavy_row<32, STATS, PH, PUSH>(sm, p, it, fi_next, v, st, tag);
-            append(sm, keep && lane == 0, (int32_t)v, lout, blo);
+            append(sm, keep && lane == 0, (int32_t)v, lout, seg);
         }
         __syncthreads();
         const int nb = sm.nhuge;
         for (int k = 0; k < nb; k++) {
             const int64_t v = huge[k];
             const bool keep = heavy_row<kMB, STATS, PH, PUSH>(sm, p, it, fi_next, v, st, tag);
-            append(sm, keep && t == 0, (int32_t)v, lout, blo);
+            append(sm, keep && t == 0, (int32_t)v, lout, seg);
         }
     }
     stats_flush<STATS>(p, it, PH == 0 ? 1 : 0, st);
@@ -745,7 +772,7 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         dbuf[62] = (long long)ns;
         long long e = 0;
         for (int i = 0; i < nh; i++) {
-            const int64_t v = p.heavy[blo + i];
+            const int64_t v = p.heavy[seg + i];
             e += p.rowptr[v + 1] - p.rowptr[v];
         }
         dbuf[63] = e;
@@ -762,9 +789,8 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
 // PH = 0: Refresh Column over worklist_2 (M_v != OUT, active)
 // PH = 1: Decide over worklist_1 (T_v undecided)
 template <int G, bool STATS, int PH, bool PUSH = false>
-__device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, int64_t bhi, int32_t* lout,
+__device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, const Rows& rows, int32_t* lout,
                            uint32_t& ph, uint64_t fi_next) {
-    constexpr int RPB = kMB / G;
     const int t = threadIdx.x, g = t / G, sub = t % G;
     const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
     Stat st;
@@ -772,14 +798,14 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
         sm.cnt = 0;
         sm.hcount = 0;
     }
-    const int64_t nsteps = (bhi - blo + RPB - 1) / RPB;
+    const int64_t nsteps = rows.nruns;  // step k = run k of the block's rows (<= kMB / G rows)
     int64_t nx_s = 0, nx_e = 0;  // bounds of the next tile (thread 0), prefetched a step ahead
     if (t == 0 && nsteps > 0) {
-        const int64_t r1 = blo + RPB < bhi ? blo + RPB : bhi;
-        const int64_t r2 = r1 + RPB < bhi ? r1 + RPB : bhi;
-        nx_s = p.rowptr[r1];
-        nx_e = p.rowptr[r2];
-        stage_tile(sm, p, 0, p.rowptr[blo], nx_s);
+        if (nsteps > 1) {
+            nx_s = p.rowptr[rows.run_lo(1)];
+            nx_e = p.rowptr[rows.run_hi(1)];
+        }
+        stage_tile(sm, p, 0, p.rowptr[rows.run_lo(0)], p.rowptr[rows.run_hi(0)]);
     }
     const bool dbg = p.timeline && it == p.dbg_it && PH == p.dbg_ph && threadIdx.x == 0;
     long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
@@ -791,7 +817,7 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
     if (dbg) {
         dbuf[0] = gt();
         dbuf[1] = nsteps;
-        dbuf[2] = bhi - blo;
+        dbuf[2] = rows.count;
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         dbuf[59] = smid;
@@ -800,11 +826,12 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
     int64_t ns0 = 0, ne0 = 0;
     uint64_t ntv = kOUT;
     uint32_t nmv = kM_OUT;
-    if (blo + g < bhi) {
-        ns0 = p.rowptr[blo + g];
-        ne0 = p.rowptr[blo + g + 1];
-        ntv = p.T[blo + g];
-        if (PH == 0) nmv = p.M[blo + g];
+    if (nsteps > 0 && rows.run_lo(0) + g < rows.run_hi(0)) {
+        const int64_t v0 = rows.run_lo(0) + g;
+        ns0 = p.rowptr[v0];
+        ne0 = p.rowptr[v0 + 1];
+        ntv = p.T[v0];
+        if (PH == 0) nmv = p.M[v0];
     }
     for (int64_t k = 0; k < nsteps; k++) {
         const int slot = (int)(k & 1);
@@ -813,26 +840,24 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
         if (dbg && k < 12) dbuf[4 + 5 * k + 1] = gt();
         if (t == 0 && k + 1 < nsteps) {
             const int64_t s1 = nx_s, e1 = nx_e;
-            const int64_t r2 = blo + (k + 2) * RPB;
-            if (r2 < bhi) {
-                const int64_t r3 = r2 + RPB < bhi ? r2 + RPB : bhi;
-                nx_s = p.rowptr[r2];
-                nx_e = p.rowptr[r3];
+            if (k + 2 < nsteps) {
+                nx_s = p.rowptr[rows.run_lo(k + 2)];
+                nx_e = p.rowptr[rows.run_hi(k + 2)];
             }
             stage_tile(sm, p, slot ^ 1, s1, e1);
         }
         // this tile's row bounds and status were loaded one step ahead; load
         // the next tile's now (a phase writes only rows of the tile it is
         // processing, so the prefetched words are current)
-        const int64_t v = blo + k * RPB + g;
-        const bool valid = v < bhi;
+        const int64_t v = rows.run_lo(k) + g;
+        const bool valid = v < rows.run_hi(k);
         const int64_t s = ns0, e = ne0;
         const uint64_t tv = ntv;
         bool act = false;
         if (valid) act = PH == 0 ? (nmv != kM_OUT && nmv != 0u) : (tv != kIN && tv != kOUT);
-        {
-            const int64_t vn = v + RPB;
-            if (vn < bhi) {
+        if (k + 1 < nsteps) {
+            const int64_t vn = rows.run_lo(k + 1) + g;
+            if (vn < rows.run_hi(k + 1)) {
                 ns0 = p.rowptr[vn];
                 ne0 = p.rowptr[vn + 1];
                 ntv = p.T[vn];
@@ -840,7 +865,7 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
             }
         }
         const int64_t len = e - s;
-        if (defer_long<G>(sm, p, blo, act, sub, v, len)) act = false;
+        if (defer_long<G>(sm, p, rows.seg, act, sub, v, len)) act = false;
         if (dbg && k < 12) dbuf[4 + 5 * k + 2] = gt();
         mbar_wait(&sm.mbar[slot], (ph >> slot) & 1u);
         ph ^= 1u << slot;
@@ -852,10 +877,10 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo
             stat_row<STATS>(p, tag, v, sub == 0, len, st);
             stat_nbrs<STATS>(p, tag, x, len, sub, G, st);
         }
-        append(sm, keep, (int32_t)v, lout, blo);
+        append(sm, keep, (int32_t)v, lout, rows.seg);
     }
     if (dbg) dbuf[3] = gt();
-    return finish_phase<STATS, PH, PUSH>(sm, p, it, blo, lout, fi_next, st);
+    return finish_phase<STATS, PH, PUSH>(sm, p, it, rows.seg, lout, fi_next, st);
 }
 
 // ------------------------------------------------------------ sparse phase
@@ -875,9 +900,9 @@ constexpr int kSlotRegion = kTvOff - 4 * kMaxRowsS;   // entries used for row sl
 static_assert(kSlotRegion > 0 && (kSlotRegion % 4) == 0, "sparse layout");
 
 template <int G, bool STATS, int PH, bool PUSH = false>
-__device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t blo, const int32_t* lin, int nin,
+__device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t seg, const int32_t* lin, int nin,
                             int32_t* lout, uint32_t& ph, uint64_t fi_next) {
-    constexpr int GS = G * 2 <= 32 ? G * 2 : 32;
+    constexpr int GS = sparse_group<G>();
     constexpr int RPBS = kMB / GS;
     constexpr int SLOT = (kSlotRegion / RPBS) & ~3;
     static_assert(RPBS * sizeof(SMeta) <= (kTileCap - kSlotRegion) * 4, "SMeta region too small");
@@ -897,7 +922,7 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
     // processed, so the copy of tile j+1 is issued without waiting on loads.
     auto row_of = [&](int j) -> int64_t {
         const int idx = j * RPBS + gs;
-        return (sub == 0 && j < nsteps && idx < nin) ? (int64_t)lin[blo + idx] : -1;
+        return (sub == 0 && j < nsteps && idx < nin) ? (int64_t)lin[seg + idx] : -1;
     };
     auto issue = [&](int slot, int64_t v, int64_t s, int64_t e, uint64_t tv) {
         if (sub != 0) return;
@@ -972,7 +997,7 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         const int len = m.len & ~kStaged;
         const uint64_t tv = reinterpret_cast<const uint64_t*>(sm.buf[slot] + kTvOff)[gs];
         bool act = valid;
-        if (defer_long<GS>(sm, p, blo, act, sub, v, len)) act = false;
+        if (defer_long<GS>(sm, p, seg, act, sub, v, len)) act = false;
         if (dbg && k < 12) dbuf[4 + 5 * k + 2] = gt();
         mbar_wait(&sm.mbarS[slot], (ph >> (2 + slot)) & 1u);
         ph ^= 1u << (2 + slot);
@@ -985,7 +1010,7 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
             stat_row<STATS>(p, tag, v, sub == 0, len, st);
             stat_nbrs<STATS>(p, tag, x, len, sub, GS, st);
         }
-        append(sm, keep, (int32_t)v, lout, blo);
+        append(sm, keep, (int32_t)v, lout, seg);
         v1 = v2;
         s1 = s2;
         e1 = e2;
@@ -993,7 +1018,7 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t bl
         v2 = v3;
     }
     if (dbg) dbuf[3] = gt();
-    return finish_phase<STATS, PH, PUSH>(sm, p, it, blo, lout, fi_next, st);
+    return finish_phase<STATS, PH, PUSH>(sm, p, it, seg, lout, fi_next, st);
 }
 
 // ------------------------------------------------------------ push-form Decide
@@ -1009,7 +1034,7 @@ __device__ __forceinline__ bool row_has(const int32_t* x, int64_t len, int32_t v
     return false;
 }
 template <bool STATS>
-__device__ int decide_push(TileSmem& sm, const MisParams& p, int it, int64_t blo, int64_t bhi, const int32_t* lin,
+__device__ int decide_push(TileSmem& sm, const MisParams& p, int it, const Rows& rows, const int32_t* lin,
                            int nin, bool dense, int32_t* lout, uint64_t fi_next) {
     const int t = threadIdx.x;
     const unsigned tag = 2u * (unsigned)it + 2u;
@@ -1024,7 +1049,7 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, int64_t blo
         sm.hcount = 0;
     }
     __syncthreads();
-    const int64_t total = dense ? bhi - blo : (int64_t)nin;
+    const int64_t total = dense ? rows.count : (int64_t)nin;
     const bool dbg = p.timeline && it == p.dbg_it && 1 == p.dbg_ph && t == 0;
     long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
     auto gt = []() {
@@ -1047,7 +1072,7 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, int64_t blo
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int64_t idx = base + u * kMB + t;
-            vv[u] = idx < total ? (dense ? blo + idx : (int64_t)lin[blo + idx]) : -1;
+            vv[u] = idx < total ? (dense ? rows.row_at(idx) : (int64_t)lin[rows.seg + idx]) : -1;
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -1108,7 +1133,7 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, int64_t blo
                     stat_nbrs<STATS>(p, tag, p.colinds + s, e - s, 0, 1, st);
                 }
             }
-            append(sm, keep, (int32_t)(v < 0 ? 0 : v), lout, blo);
+            append(sm, keep, (int32_t)(v < 0 ? 0 : v), lout, rows.seg);
         }
     }
     if (dbg) dbuf[2] = gt();
@@ -1132,7 +1157,7 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, int64_t blo
                     keep = true;
                 }
             }
-            append(sm, keep, v, lout, blo);
+            append(sm, keep, v, lout, rows.seg);
         }
     }
     if (dbg) dbuf[3] = gt();
@@ -1141,68 +1166,6 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, int64_t blo
     const int out = sm.cnt;
     __syncthreads();
     return out;
-}
-
-// ------------------------------------------------------------ dataflow sync
-// Instead of a grid-wide barrier between phases, a block waits only for the
-// blocks whose rows it reads.  Every phase reads the previous phase's values
-// of the rows in N[own rows] and writes only its own rows (push form: rows
-// within distance 1 of its own), so block b may start phase k once every
-// block d in D_b has completed phase k - 1, where D_b = the blocks whose
-// row ranges meet [least, greatest] column read by b in iteration 0, plus
-// b.  For a symmetric graph the relation covers both directions of every
-// conflict: an edge (u in b, w in d) puts d in D_b (b reads w) and b in D_d
-// (d reads u), so no block overwrites a value a neighbour has still to read
-// and no block reads a value before its writer has produced it.  Blocks of a
-// banded graph (the stencils: D_b ~ 13 of 592 blocks on C2) run ahead of
-// distant slow blocks instead of idling at a barrier; an unbanded graph
-// (Kronecker) has D_b = all blocks, i.e. a barrier.  The loop condition
-// |worklist_1| = 0 is a global sum: each block adds its count to the
-// word of its iteration; the last arrival of an iteration with a zero sum
-// publishes the iteration count (`done`).  Blocks that have not seen it yet
-// may start the next iteration's Refresh Column -- it writes only M of rows
-// whose neighbours are all decided, which no later phase reads -- and stop
-// at their next wait.
-__device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* a) {
-    unsigned int v;
-    asm volatile("ld.relaxed.gpu.u32 %0,[%1];" : "=r"(v) : "l"(a) : "memory");
-    return v;
-}
-// owner block of row r under the static ranges [n*b/B, n*(b+1)/B)
-__device__ __forceinline__ int owner_block(int64_t n, int64_t B, int64_t r) {
-    int64_t b = n > 0 ? (r * B) / n : 0;
-    if (b >= B) b = B - 1;
-    while (b + 1 < B && n * (b + 1) / B <= r) b++;
-    while (b > 0 && n * b / B > r) b--;
-    return (int)b;
-}
-// completes phase k of this block and waits for D_b to complete it; returns
-// the published iteration count (0 = not finished).  All threads call it.
-__device__ __forceinline__ int df_sync(TileSmem& sm, const MisParams& p, unsigned int k) {
-    __syncthreads();  // the block's writes of phase k are done
-    const int t = threadIdx.x;
-    if (t == 0) asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(p.prog + blockIdx.x), "r"(k) : "memory");
-    if (t < 32) {
-        const int dlo = sm.dlo, nd = sm.dhi - sm.dlo + 1;
-        int done = 0;
-        for (;;) {
-            bool ok = true;
-            for (int i = t; i < nd; i += 32) ok &= ld_relaxed_u32(p.prog + dlo + i) >= k;
-            if (__all_sync(kFull, ok)) break;
-            int d = 0;
-            if (t == 0) d = (int)ld_relaxed_u32(reinterpret_cast<const unsigned int*>(&p.ctrl[9]));
-            done = __shfl_sync(kFull, d, 0);
-            if (done) break;  // warp-uniform
-            __nanosleep(20);
-        }
-        if (t == 0) {
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-            if (!done) done = (int)ld_relaxed_u32(reinterpret_cast<const unsigned int*>(&p.ctrl[9]));
-            sm.done = done;
-        }
-    }
-    __syncthreads();
-    return sm.done;
 }
 
 __device__ __forceinline__ void stamp(const MisParams& p, int slot) {
@@ -1225,27 +1188,19 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
     TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
     const int t = threadIdx.x;
     const int64_t B = gridDim.x;
-    const int64_t blo = p.n * blockIdx.x / B, bhi = p.n * (blockIdx.x + 1) / B;
+    const Rows rows = make_rows(p.n, B, blockIdx.x, kMB / G, p.cyclic != 0);
     unsigned int* bar = (unsigned int*)&p.ctrl[0];
     unsigned long long* ring = &p.ctrl[1];
 
     if (t == 0) {
         mbar_init(&sm.mbar[0], 1);
         mbar_init(&sm.mbar[1], 1);
-        constexpr int kRowGroups = kMB / (G * 2 <= 32 ? G * 2 : 32);
+        constexpr int kRowGroups = kMB / sparse_group<G>();
         mbar_init(&sm.mbarS[0], kRowGroups);
         mbar_init(&sm.mbarS[1], kRowGroups);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        sm.pol = l2_policy(p, blo, bhi);
-        sm.cmin = 0x7fffffff;
-        sm.cmax = -1;
-        sm.dlo = 0;  // until iteration 0's columns are known: every block
-        sm.dhi = (int)B - 1;
-        sm.done = 0;
-        if (p.dataflow) p.prog[blockIdx.x] = 0u;
+        sm.pol = l2_policy(p, rows);
     }
-    if (p.dataflow)  // ordered before any use by the grid barrier after the init phase
-        for (int i = (int)blockIdx.x * kMB + t; i < p.max_iters; i += (int)B * kMB) p.iter_ring[i] = 0ull;
     uint32_t ph = 0u;  // mbarrier phase bits: 0,1 dense buffers; 2,3 sparse buffers
 
     // worklists <- 0..|V|; Refresh Row of iteration 0.
@@ -1258,9 +1213,9 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         int64_t maxdeg = 0;
         if (t == 0) sm.cnt = 0;
         __syncthreads();
-        for (int64_t base = blo; base < bhi; base += kMB) {
-            const int64_t v = base + t;
-            const bool in = v < bhi;
+        for (int64_t base = 0; base < rows.count; base += kMB) {
+            const bool in = base + t < rows.count;
+            const int64_t v = in ? rows.row_at(base + t) : 0;
             const bool act = in && (p.labels ? (p.labels[v] < 0) : true);
             if (in) {
                 set_T(p, v, act ? p.prio.word(0, fi0, p.gbase + v) : kOUT);
@@ -1278,7 +1233,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
                     if (lane == leader) pos = atomicAdd(&sm.cnt, __popc(ball));
                     pos = __shfl_sync(kFull, pos, leader);
                     if (act) {
-                        const int64_t at = blo + pos + __popc(ball & lanemask_lt());
+                        const int64_t at = rows.seg + pos + __popc(ball & lanemask_lt());
                         p.L1[0][at] = (int32_t)v;
                         p.L2[0][at] = (int32_t)v;
                     }
@@ -1308,58 +1263,29 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
 
     int it = 0;
     int status = MIS2_OK;
-    const int64_t range = bhi - blo;
+    const int64_t range = rows.count;
     // this block's worklist segment sizes (a masked call starts from its lists)
     int cnt1 = p.labels ? act_block : (int)range, cnt2 = cnt1;
-    unsigned int kph = 0;  // dataflow: phases completed by this block
     while (n_active > 0) {  // while worklist_1 != {}
         const int cur = it & 1;
         // ---- Refresh Column over worklist_2
         const bool push = PUSH && it < p.push_iters;
         const bool dense2 = (it == 0 && !p.labels) || (int64_t)cnt2 * kDenseDen >= range * kDenseNum;
         if (push) {
-            cnt2 = dense2 ? dense_phase<G, STATS, 0, PUSH>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0)
-                          : sparse_phase<G, STATS, 0, PUSH>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
+            cnt2 = dense2 ? dense_phase<G, STATS, 0, PUSH>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0)
+                          : sparse_phase<G, STATS, 0, PUSH>(sm, p, it, rows.seg, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
         } else {
-            cnt2 = dense2 ? dense_phase<G, STATS, 0, false>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0)
-                          : sparse_phase<G, STATS, 0, false>(sm, p, it, blo, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
+            cnt2 = dense2 ? dense_phase<G, STATS, 0, false>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0)
+                          : sparse_phase<G, STATS, 0, false>(sm, p, it, rows.seg, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
         }
-        if (p.dataflow) {
-            if (it == 0 && t == 0) {  // D_b from the columns read in iteration 0 (and the own rows)
-                const int64_t lo = min((int64_t)sm.cmin, blo), hi = max((int64_t)sm.cmax, bhi - 1);
-                sm.dlo = range > 0 ? owner_block(p.n, B, lo) : (int)blockIdx.x;
-                sm.dhi = range > 0 ? owner_block(p.n, B, hi) : (int)blockIdx.x;
-                if (sm.dlo > (int)blockIdx.x) sm.dlo = (int)blockIdx.x;
-                if (sm.dhi < (int)blockIdx.x) sm.dhi = (int)blockIdx.x;
-            }
-            if (df_sync(sm, p, ++kph)) break;
-        } else {
-            grid_barrier(bar);
-        }
+        grid_barrier(bar);
         stamp(p, 1 + 2 * it);
         // ---- Decide over worklist_1 + fused refresh of iteration it+1
         const uint64_t fi_next = p.prio.iter_term(it + 1);
         const bool dense1 = (it == 0 && !p.labels) || (int64_t)cnt1 * kDenseDen >= range * kDenseNum;
-        if (push) cnt1 = decide_push<STATS>(sm, p, it, blo, bhi, p.L1[cur], cnt1, dense1, p.L1[cur ^ 1], fi_next);
-        else if (dense1) cnt1 = dense_phase<G, STATS, 1>(sm, p, it, blo, bhi, p.L1[cur ^ 1], ph, fi_next);
-        else cnt1 = sparse_phase<G, STATS, 1>(sm, p, it, blo, p.L1[cur], cnt1, p.L1[cur ^ 1], ph, fi_next);
-        if (p.dataflow) {
-            if (t == 0) {  // arrival at iteration it: (1 << 44) | |worklist_1 segment|
-                unsigned long long old;
-                asm volatile("atom.add.acq_rel.gpu.u64 %0,[%1],%2;"
-                             : "=l"(old)
-                             : "l"(p.iter_ring + it), "l"((1ull << 44) | (unsigned long long)cnt1)
-                             : "memory");
-                if ((old >> 44) == (unsigned long long)(B - 1) && (old & ((1ull << 44) - 1)) + cnt1 == 0)
-                    asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&p.ctrl[9]), "r"(it + 1) : "memory");
-            }
-            const int done = df_sync(sm, p, ++kph);
-            stamp(p, 2 + 2 * it);
-            it++;
-            if (done) break;
-            if (it >= p.max_iters) break;  // status from the published count (below)
-            continue;
-        }
+        if (push) cnt1 = decide_push<STATS>(sm, p, it, rows, p.L1[cur], cnt1, dense1, p.L1[cur ^ 1], fi_next);
+        else if (dense1) cnt1 = dense_phase<G, STATS, 1>(sm, p, it, rows, p.L1[cur ^ 1], ph, fi_next);
+        else cnt1 = sparse_phase<G, STATS, 1>(sm, p, it, rows.seg, p.L1[cur], cnt1, p.L1[cur ^ 1], ph, fi_next);
         if (t == 0) {
             if (cnt1) atomicAdd(&ring[it & 3], (unsigned long long)cnt1);
             if (blockIdx.x == 0) ring[(it + 2) & 3] = 0;  // slot last read two barriers ago
@@ -1376,9 +1302,10 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
     }
 
     // return {v : T_v = IN}
-    l2_release(p, blo, bhi);
+    l2_release(p, rows);
     int cnt = 0;
-    for (int64_t v = blo + t; v < bhi; v += kMB) {
+    for (int64_t i = t; i < rows.count; i += kMB) {
+        const int64_t v = rows.row_at(i);
         const uint8_t in = (p.T[v] == kIN);
         p.in_set[v] = in;
         cnt += in;
@@ -1391,11 +1318,6 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         if (ticket == gridDim.x - 1) {  // last block publishes the scalars
             __threadfence();
             *p.d_count = (int64_t)ld_acquire_u64(&p.ctrl[5]);
-            if (p.dataflow && n_active > 0) {  // every block has left the loop: the count is final
-                const int done = (int)ld_relaxed_u32(reinterpret_cast<const unsigned int*>(&p.ctrl[9]));
-                it = done ? done : p.max_iters;
-                status = done ? MIS2_OK : MIS2_ENOTCONVERGED;
-            }
             *p.d_iters = it;
             *p.d_status = status;
         }
@@ -1409,7 +1331,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
 __device__ __forceinline__ void init_mbars(TileSmem& sm, const MisParams& p, int G2) {
     if (threadIdx.x == 0) {
         const int64_t B = gridDim.x;
-        sm.pol = l2_policy(p, p.n * blockIdx.x / B, p.n * (blockIdx.x + 1) / B);
+        sm.pol = l2_policy(p, make_rows(p.n, B, blockIdx.x, kMB, false));
         mbar_init(&sm.mbar[0], 1);
         mbar_init(&sm.mbar[1], 1);
         mbar_init(&sm.mbarS[0], kMB / G2);
@@ -1424,23 +1346,23 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_part_phase(MisParam
                                                               unsigned long long* wl1_total) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
-    init_mbars(sm, p, G * 2 <= 32 ? G * 2 : 32);
+    init_mbars(sm, p, sparse_group<G>());
     uint32_t ph = 0u;
     const int64_t B = gridDim.x;
-    const int64_t blo = p.n * blockIdx.x / B, bhi = p.n * (blockIdx.x + 1) / B;
-    const int64_t range = bhi - blo;
+    const Rows rows = make_rows(p.n, B, blockIdx.x, kMB / G, false);  // contiguous: ghosts follow the owned rows
+    const int64_t range = rows.count;
     const int cur = it & 1;
     int* cnt = &cnts[(PH == 0 ? B : 0) + blockIdx.x];
     const int c = *cnt;
     const bool dense = (it == 0) || (int64_t)c * kDenseDen >= range * kDenseNum;
     int out;
     if (PH == 0) {
-        out = dense ? dense_phase<G, false, 0>(sm, p, it, blo, bhi, p.L2[cur ^ 1], ph, 0)
-                    : sparse_phase<G, false, 0>(sm, p, it, blo, p.L2[cur], c, p.L2[cur ^ 1], ph, 0);
+        out = dense ? dense_phase<G, false, 0>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0)
+                    : sparse_phase<G, false, 0>(sm, p, it, rows.seg, p.L2[cur], c, p.L2[cur ^ 1], ph, 0);
     } else {
         const uint64_t fi_next = p.prio.iter_term(it + 1);
-        out = dense ? dense_phase<G, false, 1>(sm, p, it, blo, bhi, p.L1[cur ^ 1], ph, fi_next)
-                    : sparse_phase<G, false, 1>(sm, p, it, blo, p.L1[cur], c, p.L1[cur ^ 1], ph, fi_next);
+        out = dense ? dense_phase<G, false, 1>(sm, p, it, rows, p.L1[cur ^ 1], ph, fi_next)
+                    : sparse_phase<G, false, 1>(sm, p, it, rows.seg, p.L1[cur], c, p.L1[cur ^ 1], ph, fi_next);
     }
     if (threadIdx.x == 0) {
         *cnt = out;

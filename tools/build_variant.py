@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2204_02934_b200 import build as B
 
 name, extra = sys.argv[1], sys.argv[2:]
-out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ab", name)
+out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "abv", name)  # shipped by gpurun; delete after use
 os.makedirs(out, exist_ok=True)
 inc = B.nccl_include()
 
