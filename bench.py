@@ -64,6 +64,148 @@ def alg_bytes(stats: np.ndarray, n: int) -> int:
     return total
 
 
+def survey_bytes(stats: np.ndarray) -> int:
+    """Algorithmic bytes of one MIS-2 call by SURVEY.md §8(d).3 (the paper's
+    data structures, 8-byte words, 4-byte colinds and worklist entries,
+    8-byte rowptr; each byte counted once per pass, gathers once per distinct
+    vertex).  stats rows = iterations: |wl1| |wl2| E1 E2 |N[wl1]| |N[wl2]|:
+      B_i = 4 E2 + 8 |N[wl2]| + (4+8+8) |wl2| + 4 |wl2'|        (Refresh Column)
+          + 4 E1 + 8 |N[wl1]| + (4+8+16) |wl1| + 4 |wl1'|       (Decide)"""
+    total = 0
+    it = stats.shape[0]
+    for i in range(it):
+        w1, w2, e1, e2, d1, d2 = (int(x) for x in stats[i])
+        w1n = int(stats[i + 1, 0]) if i + 1 < it else 0
+        w2n = int(stats[i + 1, 1]) if i + 1 < it else 0
+        total += 4 * e2 + 8 * d2 + 20 * w2 + 4 * w2n
+        total += 4 * e1 + 8 * d1 + 28 * w1 + 4 * w1n
+    return total
+
+
+def agg_bytes(iter_stats, n: int, nnz: int) -> int:
+    """Algorithmic bytes of one Alg. 3 call: the two MIS-2 calls
+    by §8(d).3 (the second one masked, from its own worklist statistics) plus
+    one CSR pass per labelling phase (phase 1 pull, phase 2 accept / label,
+    phase 3): 3 x (4 nnz + 8 (n+1) + 4 n)."""
+    return survey_bytes(iter_stats[0]) + survey_bytes(iter_stats[1]) + 3 * (4 * nnz + 8 * (n + 1) + 4 * n)
+
+
+def host_cpu():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+def lib_build_id() -> str:
+    """sha256 (16 hex) of the libmis2.so the bench loads: stamps the ncu numbers."""
+    import hashlib
+    import paper_2204_02934_b200 as m
+    path = os.environ.get("MIS2_LIB_PATH") or m._build.LIB
+    with open(path, "rb") as fh:
+        return hashlib.sha256(fh.read()).hexdigest()[:16]
+
+
+NCU_METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+               "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+               "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"]
+
+
+def ncu_capture(config: int, peak: float, timeout: float = 240.0):
+    """One ncu replay of the persistent MIS-2 kernel of this build on the bench
+    graph (a subprocess after the timed region; its time is never a bench
+    value): DRAM bytes per launch, DRAM GB/s and fraction of the measured
+    peak, sectors per global-load request, L2 hit rate.  ncu flushes the
+    caches before the replay (--cache-control all) and leaves the clocks
+    alone (--clock-control none).  None when ncu is not installed."""
+    import shutil
+    import subprocess
+    exe = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    if exe is None:
+        return None
+    cmd = [exe, "--metrics", ",".join(NCU_METRICS), "--clock-control", "none", "--cache-control", "all",
+           "-k", "regex:mis2_persistent", "-s", "2", "-c", "1", "--csv",
+           sys.executable, os.path.join(ROOT, "tools", "ncu_mis2.py"), str(config)]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout).stdout
+    except (subprocess.SubprocessError, OSError) as e:
+        return {"error": str(e)[:200]}
+    import csv
+    vals = {}
+    for row in csv.reader(line for line in out.splitlines() if line.startswith('"')):
+        if len(row) >= 15 and row[12] in NCU_METRICS:
+            unit, v = row[13], float(row[14].replace(",", ""))
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6,
+                     "nsecond": 1e-9, "msecond": 1e-3, "ms": 1e-3}.get(unit, 1)
+            vals[row[12]] = v * scale
+    if "gpu__time_duration.sum" not in vals or "dram__bytes_read.sum" not in vals:
+        return {"error": "ncu produced no metrics", "tail": out[-300:]}
+    t = vals["gpu__time_duration.sum"]
+    dram = vals["dram__bytes_read.sum"] + vals.get("dram__bytes_write.sum", 0.0)
+    req = vals.get("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", 0.0)
+    return {"kernel": "mis2k::mis2_persistent", "launch_us": t * 1e6, "dram_bytes": dram,
+            "dram_gbs": dram / t / 1e9, "dram_frac": dram / t / 1e9 / peak,
+            "dram_pct_of_peak_sustained": vals.get("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "sectors_per_request": vals.get("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", 0.0) / req if req else None,
+            "l2_hit_pct": vals.get("lts__t_sector_hit_rate.pct"), "build": lib_build_id(),
+            "how": "ncu --cache-control all --clock-control none, one replay (cold caches, serialised)"}
+
+
+def time_calls(fn, steps: int, flush, stream, torch):
+    """median / min ms of `steps` calls, each between CUDA events on `stream`,
+    the L2 flushed before each (outside the event pair)."""
+    per = []
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        per.append(a.elapsed_time(b))
+    return statistics.median(per), min(per)
+
+
+def sub_records(m, torch, flush, stream, peak, steps: int, c2=None):
+    """Secondary configurations, timed like the headline (CUDA events, L2
+    flushed between calls): MIS-2 on configs[2..4] and Alg. 3 on configs[1],
+    each with its algorithmic bytes and fraction of the HBM peak."""
+    import mis2gen as G
+    out = []
+    for cfg, name in ((2, "C3 7-pt 300^3 MIS-2"), (3, "C4 Kronecker scale 24 MIS-2"),
+                      (4, "C5 3-dof 27-pt 150^3 MIS-2")):
+        g = G.config_graph(cfg)
+        rp, ci = torch.from_numpy(g.rowptr).cuda(), torch.from_numpy(g.colinds).cuda()
+        st = m.mis2(rp, ci, stats=True)
+        ref = m.mis2(rp, ci)
+        res = torch.empty(g.n, dtype=torch.uint8, device="cuda")
+        sc = torch.zeros(2, dtype=torch.int64, device="cuda")
+        med, mn = time_calls(lambda: m.mis2_async(rp, ci, res, sc), steps, flush, stream, torch)
+        assert int(sc[0].item()) == ref.count
+        b = survey_bytes(st.stats)
+        out.append({"config": name, "configs_index": cfg, "n": g.n, "nnz": g.nnz, "ms": med, "ms_min": mn,
+                    "gteps": g.nnz / (med / 1e3) / 1e9, "iterations": ref.iterations, "mis2_size": ref.count,
+                    "alg_bytes": b, "achieved_gbs": b / (med / 1e3) / 1e9, "frac": b / (med / 1e3) / 1e9 / peak})
+        del rp, ci, res
+        torch.cuda.empty_cache()
+    if c2 is not None:
+        g, rp, ci = c2
+        a = m.aggregate(rp, ci, iter_stats=True)
+        med, mn = time_calls(lambda: m.aggregate(rp, ci), steps, flush, stream, torch)
+        b = agg_bytes(a.iter_stats, g.n, g.nnz)
+        out.append({"config": "C2 27-pt 100^3 Alg. 3 aggregation", "configs_index": 1, "n": g.n, "nnz": g.nnz,
+                    "ms": med, "ms_min": mn, "gteps": g.nnz / (med / 1e3) / 1e9, "num_aggs": a.num_aggs,
+                    "alg_bytes": b, "achieved_gbs": b / (med / 1e3) / 1e9, "frac": b / (med / 1e3) / 1e9 / peak,
+                    "note": "includes the host reads of the aggregate count (one synchronising ABI call)"})
+    return out
+
+
 class ClockSampler:
     """NVML sampling of SM clock + clock-event reasons during the timed region."""
 
@@ -261,10 +403,11 @@ def run_ours(args):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     stream = torch.cuda.current_stream()
 
-    # instrumented (untimed) call: worklist statistics for the byte model
+    # instrumented (untimed) call: worklist statistics for the byte models
     st = m.mis2(rp, ci, stats=True)
     check = m.mis2(rp, ci)
-    bytes_per_call = alg_bytes(st.stats, g.n)
+    bytes_per_call = survey_bytes(st.stats)
+    bytes_impl = alg_bytes(st.stats, g.n)          # this layout (M as 4-byte id fields)
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -300,13 +443,6 @@ def run_ours(args):
 
     peak, peak_src = peaks()
     achieved = bytes_per_call / (ms / 1e3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as fh:
-            td = json.load(fh)
-        if td.get("n") == g.n and td.get("nnz") == g.nnz:
-            traffic = td.get("dram_bytes_per_launch")
 
     # end-to-end through mis2_host(): pinned host CSR in, in_set out
     e2e = None
@@ -330,12 +466,23 @@ def run_ours(args):
         e2e = {"value": world * g.nnz / (ems / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": int(g.rowptr.nbytes + g.colinds.nbytes), "d2h_bytes_per_step": int(g.n + 16)}
 
+    subs = None
+    if rank == 0 and world == 1 and not args.no_subs:
+        subs = sub_records(m, torch, flush, stream, peak, args.sub_steps, c2=(g, rp, ci))
+
+    # ncu (a subprocess, after every timed region): DRAM traffic of one
+    # launch of this build's kernel, sectors per request
+    ncu = None
+    if rank == 0 and world == 1 and not args.no_ncu:
+        ncu = ncu_capture(args.config, peak)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, runs, el, _ = cpu_oracle_rate(g, args.cpu_seconds)
+        model, nproc = host_cpu()
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{runs} full serial MIS-2 calls of the oracle (oracle/oracle.c, 1 thread) on the same "
-                         f"graph, {el:.1f} s"}
+                         f"graph, {el:.1f} s", "cpu_model": model, "nproc": nproc}
 
     if rank == 0:
         line = {
@@ -348,8 +495,12 @@ def run_ours(args):
                        "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
                        "ms_min": min(per), "ms_median": statistics.median(per), "wall_s": wall},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "mis2k::mis2_persistent",
-                         "alg_bytes_per_launch": bytes_per_call, "peak_source": peak_src},
+                         "frac": achieved / peak,
+                         "traffic": ncu.get("dram_bytes") if isinstance(ncu, dict) else None,
+                         "kernel": "mis2k::mis2_persistent",
+                         "alg_bytes_per_launch": bytes_per_call, "alg_bytes_model": "SURVEY.md 8(d).3",
+                         "alg_bytes_impl_layout": bytes_impl, "peak_source": peak_src, "ncu": ncu},
+            "configs": subs,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -370,6 +521,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-ncu", action="store_true", help="skip the ncu DRAM-traffic capture")
+    ap.add_argument("--no-subs", action="store_true", help="skip the secondary configuration records")
+    ap.add_argument("--sub-steps", type=int, default=5)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

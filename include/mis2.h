@@ -85,6 +85,10 @@ extern "C" {
                                     zero-extended in the 64-bit arrays, which orders every word
                                     exactly as 32-bit storage would (results identical to a
                                     32-bit implementation).  MIS-2 / aggregation / partitioned. */
+#define MIS2_FLAG_ITER_STATS 0x100u /* mis2_aggregate: `stats` holds 8 + 12 * max_iters int64: after the
+                                       8 summary entries, the per-iteration worklist statistics (as
+                                       mis2()'s `stats`, max_iters rows of 6) of the phase-1 MIS-2, then of
+                                       the masked phase-2 MIS-2 (instrumented, slower runs; measurement) */
 #define MIS2_FLAG_TIMELINE 0x2u  /* measurement aid: mis2()'s `stats` receives int64 device
                                     timestamps (ns, %globaltimer) taken by block 0 after
                                     the init phase and after every grid barrier:

@@ -32,6 +32,7 @@ FLAG_KEYS = 32
 FLAG_NO_KEYS = 64
 KEYS = {"auto": 0, "on": FLAG_KEYS, "off": FLAG_NO_KEYS}
 FLAG_WORD32 = 128
+FLAG_ITER_STATS = 256
 WORD_BITS = {64: 0, 32: FLAG_WORD32}
 
 # every symbol include/mis2.h declares
@@ -258,11 +259,12 @@ class AggResult:
     num_aggs: int
     roots: "object"    # torch.int32 CUDA [num_aggs]
     stats: dict
+    iter_stats: tuple | None = None  # (phase-1 MIS-2, masked phase-2 MIS-2) worklist statistics
 
 
 def aggregate(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
               validate: bool = False, basic: bool = False, decide: str = "auto", keys: str = "auto",
-              word_bits: int = 64) -> AggResult:
+              word_bits: int = 64, iter_stats: bool = False) -> AggResult:
     """Alg. 3, or Alg. 2 with basic=True,
     through ``mis2_aggregate()``."""
     torch = _torch()
@@ -270,16 +272,25 @@ def aggregate(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters
     o = _opts(seed, scheme, max_iters, group, validate, decide=decide, keys=keys, word_bits=word_bits)
     if basic:
         o.flags |= FLAG_BASIC
+    mi = max_iters if max_iters > 0 else 10 * (n + 1).bit_length() + 20
+    if iter_stats:
+        o.flags |= FLAG_ITER_STATS
     ws, wsb = workspace(OP_AGGREGATE, n, nnz)
     labels = torch.empty(max(n, 1), dtype=torch.int32, device=rowptr.device)
     roots = torch.empty(max(n, 1), dtype=torch.int32, device=rowptr.device)
     na = ctypes.c_int64(0)
-    st = np.zeros(8, dtype=np.int64)
+    st = np.zeros(8 + (12 * mi if iter_stats else 0), dtype=np.int64)
     rc = lib().mis2_aggregate(ctypes.byref(g), ctypes.byref(o), labels.data_ptr(), ctypes.byref(na),
                               roots.data_ptr(), st.ctypes.data, ws.data_ptr(), wsb, _stream())
     _check(rc, "mis2_aggregate")
     keys = ["mis1", "iters1", "mis2", "iters2", "accepted2", "leftovers", "n1", "num_aggs"]
-    return AggResult(labels[:n], int(na.value), roots[: na.value], dict(zip(keys, map(int, st))))
+    summary = dict(zip(keys, map(int, st[:8])))
+    its = None
+    if iter_stats:
+        a = st[8:8 + 6 * mi].reshape(mi, 6)[: summary["iters1"]].copy()
+        b = st[8 + 6 * mi:].reshape(mi, 6)[: summary["iters2"]].copy()
+        its = (a, b)
+    return AggResult(labels[:n], int(na.value), roots[: na.value], summary, its)
 
 
 def coarsen(rowptr, colinds, labels, num_aggs: int):

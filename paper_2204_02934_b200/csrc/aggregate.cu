@@ -3,6 +3,8 @@
 // the phase bookkeeping is a handful of row-parallel kernels (G lanes per
 // CSR row, as in the MIS-2 passes) plus two exclusive scans that number the
 // aggregates in ascending root order (reading Q18).
+#include <cstring>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -510,9 +512,16 @@ int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int6
     int32_t* s32 = (int32_t*)w.scal;
     MIS2_CUDA_TRY(cudaMemsetAsync(w.scal, 0, 32 * sizeof(long long), s));
 
+    // per-iteration worklist statistics of both MIS-2 calls (MIS2_FLAG_ITER_STATS)
+    const bool iter_stats = stats && (o.flags & MIS2_FLAG_ITER_STATS) && !(o.flags & MIS2_FLAG_TIMELINE);
+    const int64_t mi = max_iters_for(n, o.max_iters);
+    int64_t* ist1 = iter_stats ? stats + 8 : nullptr;
+    int64_t* ist2 = iter_stats ? stats + 8 + 6 * mi : nullptr;
+    if (iter_stats) memset(stats + 8, 0, sizeof(int64_t) * 12 * (size_t)mi);
+
     // ---- phase 1: M1 = MIS2(G)
     MIS2_TRY(run_mis2(g, o, nullptr, w.in1, (int64_t*)&w.scal[kCount1], &s32[2 * kIters1],
-                      &s32[2 * kStatus1], nullptr, w.mis, s));
+                      &s32[2 * kStatus1], ist1, w.mis, s));
     MIS2_TRY(scan_flags(w.in1, n, w.rid, &s32[2 * kN1], w.scan_tmp, s));
     rows(G, n, di.sms, s, 1, g, w, labels, roots);
 
@@ -533,7 +542,7 @@ int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int6
 
     // ---- phase 2: M2 = MIS2(G \ aggregated) on the same ids / seed (Q15)
     MIS2_TRY(run_mis2(g, o, labels, w.in2, (int64_t*)&w.scal[kCount2], &s32[2 * kIters2],
-                      &s32[2 * kStatus2], nullptr, w.mis, s));
+                      &s32[2 * kStatus2], ist2, w.mis, s));
     rows(G, n, di.sms, s, 2, g, w, labels, roots);
     MIS2_TRY(scan_flags(w.acc, n, w.aid, &s32[2 * kN2], w.scan_tmp, s));
     rows(G, n, di.sms, s, 3, g, w, labels, roots);
