@@ -50,7 +50,10 @@ constexpr int kMW = MIS2_WARPS;
 constexpr int kMB = 32 * kMW;
 constexpr int kMinBlocksPerSM = kMW >= 16 ? 1 : 4;
 // int32 colinds per staging buffer: a dense step of 27-entry rows
-constexpr int kTileCap = (kMB >= 512 ? kMB / 2 : kMB) * 27;
+#ifndef MIS2_TILE_ROWS
+#define MIS2_TILE_ROWS (kMB >= 512 ? kMB / 2 : kMB)
+#endif
+constexpr int kTileCap = (MIS2_TILE_ROWS) * 27;
 // rows longer than 8 gather batches of their lane group are deferred and
 // reduced by the whole block (flattened over all deferred rows of the block)
 // independent gathers per lane per batch of the row loops

@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, mis2gen as G, paper_2204_02934_b200 as m
 it, ph = int(sys.argv[1]), int(sys.argv[2])
 os.environ["MIS2_DBG_IT"], os.environ["MIS2_DBG_PH"] = str(it), str(ph)
-g = G.config_graph(1)
+g = G.config_graph(int(os.environ.get("CFG", "1")))
 rp = torch.from_numpy(g.rowptr).cuda(); ci = torch.from_numpy(g.colinds).cuda()
 m.mis2(rp, ci)
 r = m.mis2(rp, ci, timeline=True)
@@ -24,3 +24,11 @@ for k in range(min(8, int(d[:, 1].max()))):
     st = d[sel, 4 + 5 * k: 9 + 5 * k].astype(np.float64)
     dt = np.diff(st, axis=1) / 1e3
     print(f"step {k}: n={sel.sum():4d} sync {np.median(dt[:,0]):6.2f} plan {np.median(dt[:,1]):6.2f} wait {np.median(dt[:,2]):6.2f} process {np.median(dt[:,3]):6.2f}   (max {dt.max(0).round(2).tolist()})  start@{np.median(st[:,0]-t0)/1e3:.2f}")
+# per-SM view: blocks grouped by SM id (dbuf[59], dense phases only), end times
+if (d[:, 59] > 0).any():
+    ends = (d[:, 3] - t0) / 1e3
+    sm = d[:, 59]
+    per_sm_last = np.array([ends[sm == s].max() for s in np.unique(sm)])
+    per_sm_first = np.array([ends[sm == s].min() for s in np.unique(sm)])
+    print(f"SMs {len(per_sm_last)}: last block end median {np.median(per_sm_last):.2f} max {per_sm_last.max():.2f}; "
+          f"first block end median {np.median(per_sm_first):.2f}")
