@@ -200,11 +200,19 @@ struct mis2_comm {
     std::vector<HostPart> hp;   // local: P parts; NCCL: 1 (this rank)
     std::vector<PartDev> dev;   // same
     std::vector<void*> allocs;
-    std::vector<uint64_t*> sendT;
-    std::vector<uint32_t*> sendM;
+    std::vector<uint64_t*> sendT;          // packed-halo scratch of exchange_arr (aggregation passes)
     std::vector<int32_t*> send_idx_d;
-    unsigned long long* d_sum = nullptr;  // NCCL allreduce buffer
     std::vector<AggPart> agg;              // partitioned aggregation state
+    // the partitioned MIS-2 kernel's view of every partition (P entries):
+    // local transport -> the other parts' device buffers; NCCL -> the other
+    // ranks' buffers mapped over NVLink (CUDA IPC)
+    std::vector<uint64_t*> peer_T;
+    std::vector<uint32_t*> peer_M;
+    std::vector<unsigned long long*> peer_box;
+    std::vector<void*> ipc_opened;
+    unsigned int epoch = 0;                // last partition-barrier epoch (advances identically on every rank)
+    void* dscratch = nullptr;              // kernel parameter block + results
+    int64_t* d_counts = nullptr;           // [2 * (P + 1)] allgather buffers of gather_counts
 };
 
 static int dev_alloc(mis2_comm* c, void** p, size_t bytes) {
@@ -214,15 +222,21 @@ static int dev_alloc(mis2_comm* c, void** p, size_t bytes) {
 }
 
 static void free_parts(mis2_comm* c) {
+    if (!c->ipc_opened.empty()) cudaDeviceSynchronize();  // peers' kernels may still reference the mappings
+    for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+    c->ipc_opened.clear();
     for (void* p : c->allocs) cudaFree(p);
     c->allocs.clear();
     c->hp.clear();
     c->dev.clear();
     c->sendT.clear();
-    c->sendM.clear();
     c->send_idx_d.clear();
-    c->d_sum = nullptr;
     c->agg.clear();
+    c->peer_T.clear();
+    c->peer_M.clear();
+    c->peer_box.clear();
+    c->dscratch = nullptr;
+    c->d_counts = nullptr;
 }
 
 // upload one planned part
@@ -234,7 +248,6 @@ static int upload_part(mis2_comm* c, const HostPart& h, PartDev& d, cudaStream_t
     d.gbase = h.lo;
     d.nnz = h.nnz;
     d.G = choose_group(h.n_own, h.nnz, 0);
-    d.grid = part_grid(h.n_own, d.G);
     const int64_t nt = d.n_own + d.n_ghost + 1;
     void* p;
     MIS2_TRY(dev_alloc(c, &p, sizeof(int64_t) * (d.n_own + 1)));
@@ -253,10 +266,16 @@ static int upload_part(mis2_comm* c, const HostPart& h, PartDev& d, cudaStream_t
         MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * (d.n_own + 1)));
         d.L2[i] = (int32_t*)p;
     }
-    MIS2_TRY(dev_alloc(c, &p, sizeof(int) * 2 * (d.grid + 1)));
-    d.cnts = (int*)p;
-    MIS2_TRY(dev_alloc(c, &p, sizeof(unsigned long long) * 8));
-    d.ctr = (unsigned long long*)p;
+    // partition barrier state (mis2_kernel.cuh part_sync); the mailboxes get
+    // their own allocation (other ranks map it over NVLink)
+    MIS2_TRY(dev_alloc(c, &p, 256 + sizeof(unsigned long long) * 4));
+    MIS2_CUDA_TRY(cudaMemsetAsync(p, 0, 256 + sizeof(unsigned long long) * 4, s));
+    d.bar = (unsigned int*)p;
+    d.acc = (unsigned long long*)((char*)p + 256);
+    d.rel = d.acc + 2;
+    MIS2_TRY(dev_alloc(c, &p, sizeof(unsigned long long) * 2 * c->nparts));
+    MIS2_CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(unsigned long long) * 2 * c->nparts, s));
+    d.box = (unsigned long long*)p;
     MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * (d.n_own + 1)));
     d.heavy = (int32_t*)p;
     const int64_t ns = (int64_t)h.send_idx.size();
@@ -265,56 +284,58 @@ static int upload_part(mis2_comm* c, const HostPart& h, PartDev& d, cudaStream_t
     if (ns) MIS2_CUDA_TRY(cudaMemcpyAsync(p, h.send_idx.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, s));
     MIS2_TRY(dev_alloc(c, &p, sizeof(uint64_t) * (ns + 1)));
     c->sendT.push_back((uint64_t*)p);
-    MIS2_TRY(dev_alloc(c, &p, sizeof(uint32_t) * (ns + 1)));
-    c->sendM.push_back((uint32_t*)p);
+    return MIS2_OK;
+}
+
+// halo pushes of part `me` (owned row -> peer, index in the peer's T / M):
+// its send list to peer q lands at q's ghost slots n_own_q + recv_off_q[me] + k
+static int upload_sends(mis2_comm* c, const HostPart& h, PartDev& d, int me, const std::vector<int64_t>& n_own_of,
+                        const std::vector<int64_t>& recv_off_me_of, cudaStream_t s) {
+    const int P = c->nparts;
+    const int64_t ns = (int64_t)h.send_idx.size();
+    struct E {
+        int32_t src, peer;
+        int64_t dst;
+    };
+    std::vector<E> ent(ns);
+    for (int q = 0; q < P; q++)
+        for (int64_t k = 0; k < h.send_cnt[q]; k++) {
+            const int64_t i = h.send_off[q] + k;
+            ent[i] = E{h.send_idx[i], q, n_own_of[q] + recv_off_me_of[q] + k};
+        }
+    (void)me;
+    // sorted by owned row: a block pushes the entries of the rows it owns
+    std::stable_sort(ent.begin(), ent.end(), [](const E& a, const E& b) { return a.src < b.src; });
+    std::vector<int32_t> src(ns), peer(ns);
+    std::vector<int64_t> dst(ns);
+    for (int64_t i = 0; i < ns; i++) {
+        src[i] = ent[i].src;
+        peer[i] = ent[i].peer;
+        dst[i] = ent[i].dst;
+    }
+    const int64_t ngrp = d.n_own / 8 + 2;
+    std::vector<int64_t> csp(ngrp + 1, 0);
+    for (int64_t i = 0; i < ns; i++) csp[src[i] / 8 + 1]++;
+    for (int64_t g = 0; g < ngrp; g++) csp[g + 1] += csp[g];
+    void* p;
+    MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * (ns + 1)));
+    d.send_src = (const int32_t*)p;
+    if (ns) MIS2_CUDA_TRY(cudaMemcpyAsync(p, src.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, s));
+    MIS2_TRY(dev_alloc(c, &p, sizeof(int32_t) * (ns + 1)));
+    d.send_peer = (const int32_t*)p;
+    if (ns) MIS2_CUDA_TRY(cudaMemcpyAsync(p, peer.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, s));
+    MIS2_TRY(dev_alloc(c, &p, sizeof(int64_t) * (ns + 1)));
+    d.send_dst = (const int64_t*)p;
+    if (ns) MIS2_CUDA_TRY(cudaMemcpyAsync(p, dst.data(), sizeof(int64_t) * ns, cudaMemcpyHostToDevice, s));
+    MIS2_TRY(dev_alloc(c, &p, sizeof(int64_t) * (ngrp + 1)));
+    d.send_csp = (const int64_t*)p;
+    MIS2_CUDA_TRY(cudaMemcpyAsync(p, csp.data(), sizeof(int64_t) * (ngrp + 1), cudaMemcpyHostToDevice, s));
+    d.nsend = ns;
+    MIS2_CUDA_TRY(cudaStreamSynchronize(s));  // the host vectors go out of scope
     return MIS2_OK;
 }
 
 // ------------------------------------------------------------------ halo exchange
-// which = 0: T (uint64), 1: M (uint32)
-static int exchange(mis2_comm* c, int which, cudaStream_t s) {
-    const int P = c->nparts;
-    const int L = (int)c->dev.size();
-    for (int i = 0; i < L; i++) {  // pack
-        const int64_t ns = (int64_t)c->hp[i].send_idx.size();
-        if (!ns) continue;
-        const int blocks = (int)std::min<int64_t>((ns + 255) / 256, 1024);
-        if (which == 0) k_pack_u64<<<blocks, 256, 0, s>>>(c->dev[i].T, c->send_idx_d[i], ns, c->sendT[i]);
-        else k_pack_u32<<<blocks, 256, 0, s>>>(c->dev[i].M, c->send_idx_d[i], ns, c->sendM[i]);
-        count_launch();
-    }
-    MIS2_CUDA_TRY(cudaGetLastError());
-    const size_t es = which == 0 ? sizeof(uint64_t) : sizeof(uint32_t);
-    if (c->local) {
-        for (int p = 0; p < P; p++) {
-            char* dst = which == 0 ? (char*)c->dev[p].T : (char*)c->dev[p].M;
-            for (int q = 0; q < P; q++) {
-                const int64_t cnt = c->hp[p].recv_cnt[q];
-                if (!cnt || q == p) continue;
-                const char* src = (which == 0 ? (const char*)c->sendT[q] : (const char*)c->sendM[q]) +
-                                  es * c->hp[q].send_off[p];
-                MIS2_CUDA_TRY(cudaMemcpyAsync(dst + es * (c->dev[p].n_own + c->hp[p].recv_off[q]), src, es * cnt,
-                                              cudaMemcpyDeviceToDevice, s));
-            }
-        }
-        return MIS2_OK;
-    }
-    const HostPart& h = c->hp[0];
-    const PartDev& d = c->dev[0];
-    const ncclDataType_t ty = which == 0 ? ncclUint64 : ncclUint32;
-    char* dst = which == 0 ? (char*)d.T : (char*)d.M;
-    const char* sb = which == 0 ? (const char*)c->sendT[0] : (const char*)c->sendM[0];
-    NCCL_TRY(c->api, c->api->GroupStart());
-    for (int q = 0; q < P; q++) {
-        if (q == c->rank) continue;
-        if (h.send_cnt[q]) NCCL_TRY(c->api, c->api->Send(sb + es * h.send_off[q], h.send_cnt[q], ty, q, c->nccl, s));
-        if (h.recv_cnt[q])
-            NCCL_TRY(c->api, c->api->Recv(dst + es * (d.n_own + h.recv_off[q]), h.recv_cnt[q], ty, q, c->nccl, s));
-    }
-    NCCL_TRY(c->api, c->api->GroupEnd());
-    return MIS2_OK;
-}
-
 // ghost values of a per-part array of es-byte elements (1 or 4): arr[i] is
 // part i's local array [owned | ghosts]; the send buffers of T are scratch
 static int exchange_arr(mis2_comm* c, const std::vector<void*>& arr, int es, cudaStream_t s) {
@@ -366,33 +387,11 @@ static int gather_counts(mis2_comm* c, const std::vector<int64_t>& mine, std::ve
         for (int p = 0; p < P; p++) all[p] = mine[p];
         return MIS2_OK;
     }
-    int64_t *d_in, *d_all;
-    MIS2_CUDA_TRY(cudaMalloc(&d_in, sizeof(int64_t)));
-    MIS2_CUDA_TRY(cudaMalloc(&d_all, sizeof(int64_t) * P));
+    int64_t* d_in = c->d_counts;  // allocated with the graph: no allocation per call
+    int64_t* d_all = c->d_counts + 1;
     MIS2_CUDA_TRY(cudaMemcpyAsync(d_in, &mine[0], sizeof(int64_t), cudaMemcpyHostToDevice, s));
     NCCL_TRY(c->api, c->api->AllGather(d_in, d_all, 1, ncclInt64, c->nccl, s));
     MIS2_CUDA_TRY(cudaMemcpyAsync(all.data(), d_all, sizeof(int64_t) * P, cudaMemcpyDeviceToHost, s));
-    MIS2_CUDA_TRY(cudaStreamSynchronize(s));
-    cudaFree(d_in);
-    cudaFree(d_all);
-    return MIS2_OK;
-}
-
-// sum of ctr[slot] over all partitions -> host
-static int global_sum(mis2_comm* c, int slot, unsigned long long* out, cudaStream_t s) {
-    if (c->local) {
-        unsigned long long tot = 0;
-        for (auto& d : c->dev) {
-            unsigned long long v = 0;
-            MIS2_CUDA_TRY(cudaMemcpyAsync(&v, d.ctr + slot, sizeof(v), cudaMemcpyDeviceToHost, s));
-            MIS2_CUDA_TRY(cudaStreamSynchronize(s));
-            tot += v;
-        }
-        *out = tot;
-        return MIS2_OK;
-    }
-    NCCL_TRY(c->api, c->api->AllReduce(c->dev[0].ctr + slot, c->d_sum, 1, ncclUint64, ncclSum, c->nccl, s));
-    MIS2_CUDA_TRY(cudaMemcpyAsync(out, c->d_sum, sizeof(*out), cudaMemcpyDeviceToHost, s));
     MIS2_CUDA_TRY(cudaStreamSynchronize(s));
     return MIS2_OK;
 }
@@ -539,62 +538,117 @@ int mis2_comm_set_graph(mis2_comm* c, int64_t n_global, const int64_t* rowptr_h,
         std::vector<std::vector<int64_t>> wanted(P);
         for (int p = 0; p < P; p++) wanted[p].assign(in.begin() + in_off[p], in.begin() + in_off[p + 1]);
         finish_sends(h, wanted, P);
-        void* p;
-        MIS2_TRY(dev_alloc(c, &p, sizeof(unsigned long long) * 2));
-        c->d_sum = (unsigned long long*)p;
     }
     c->dev.resize(c->hp.size());
     for (size_t i = 0; i < c->hp.size(); i++) MIS2_TRY(upload_part(c, c->hp[i], c->dev[i], s));
+    {
+        void* p;
+        MIS2_TRY(dev_alloc(c, &p, dist_scratch_bytes((int)c->dev.size())));
+        c->dscratch = p;
+        MIS2_TRY(dev_alloc(c, &p, sizeof(int64_t) * 2 * (P + 1)));
+        c->d_counts = (int64_t*)p;
+    }
+    c->peer_T.assign(P, nullptr);
+    c->peer_M.assign(P, nullptr);
+    c->peer_box.assign(P, nullptr);
+    if (c->local) {
+        // every part's buffers are on this device: the halo pushes and the
+        // mailbox posts of the partitioned kernel are plain device stores
+        std::vector<int64_t> n_own_of(P);
+        for (int q = 0; q < P; q++) {
+            n_own_of[q] = c->dev[q].n_own;
+            c->peer_T[q] = c->dev[q].T;
+            c->peer_M[q] = c->dev[q].M;
+            c->peer_box[q] = c->dev[q].box;
+            c->dev[q].gpart = q;
+        }
+        for (int q = 0; q < P; q++) {
+            std::vector<int64_t> roff(P);  // where q's sends land in each peer
+            for (int d = 0; d < P; d++) roff[d] = c->hp[d].recv_off[q];
+            MIS2_TRY(upload_sends(c, c->hp[q], c->dev[q], q, n_own_of, roff, s));
+        }
+    } else {
+        // one part per rank: its peers' T / M / mailboxes are mapped over
+        // NVLink (CUDA IPC; handles and ghost layouts allgathered over NCCL)
+        const int me = c->rank;
+        PartDev& d = c->dev[0];
+        d.gpart = me;
+        // layout: [n_own, recv_off[0..P)] of every rank
+        std::vector<int64_t> lay((size_t)(P + 1)), lay_all((size_t)(P + 1) * P);
+        lay[0] = d.n_own;
+        for (int q = 0; q < P; q++) lay[1 + q] = c->hp[0].recv_off[q];
+        cudaIpcMemHandle_t hs[3];
+        MIS2_CUDA_TRY(cudaIpcGetMemHandle(&hs[0], d.T));
+        MIS2_CUDA_TRY(cudaIpcGetMemHandle(&hs[1], d.M));
+        MIS2_CUDA_TRY(cudaIpcGetMemHandle(&hs[2], d.box));
+        const size_t hb = sizeof(hs), lb = sizeof(int64_t) * (P + 1);
+        void* buf;
+        MIS2_CUDA_TRY(cudaMalloc(&buf, (hb + lb) * (P + 1)));
+        char* mine = (char*)buf;
+        char* all = mine + hb + lb;
+        MIS2_CUDA_TRY(cudaMemcpyAsync(mine, hs, hb, cudaMemcpyHostToDevice, s));
+        MIS2_CUDA_TRY(cudaMemcpyAsync(mine + hb, lay.data(), lb, cudaMemcpyHostToDevice, s));
+        NCCL_TRY(c->api, c->api->AllGather(mine, all, hb + lb, ncclUint8, c->nccl, s));
+        std::vector<char> host((hb + lb) * P);
+        MIS2_CUDA_TRY(cudaMemcpyAsync(host.data(), all, (hb + lb) * P, cudaMemcpyDeviceToHost, s));
+        MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+        cudaFree(buf);
+        std::vector<int64_t> n_own_of(P), roff(P);
+        for (int q = 0; q < P; q++) {
+            const char* rec = host.data() + (hb + lb) * q;
+            const int64_t* ql = (const int64_t*)(rec + hb);
+            n_own_of[q] = ql[0];
+            roff[q] = ql[1 + me];  // where my sends land in q
+            if (q == me) {
+                c->peer_T[q] = d.T;
+                c->peer_M[q] = d.M;
+                c->peer_box[q] = d.box;
+                continue;
+            }
+            cudaIpcMemHandle_t qh[3];
+            memcpy(qh, rec, hb);
+            void* ptr[3];
+            for (int k = 0; k < 3; k++) {
+                MIS2_CUDA_TRY(cudaIpcOpenMemHandle(&ptr[k], qh[k], cudaIpcMemLazyEnablePeerAccess));
+                c->ipc_opened.push_back(ptr[k]);
+            }
+            c->peer_T[q] = (uint64_t*)ptr[0];
+            c->peer_M[q] = (uint32_t*)ptr[1];
+            c->peer_box[q] = (unsigned long long*)ptr[2];
+        }
+        MIS2_TRY(upload_sends(c, c->hp[0], d, me, n_own_of, roff, s));
+    }
     MIS2_CUDA_TRY(cudaStreamSynchronize(s));
     return MIS2_OK;
 }
 
 }  // extern "C"
 
-// Alg. 1 over the partition.  in_sets[i] = part i's owned mask; labels[i]
-// (or empty) = part i's phase-2 mask (active iff < 0, owned rows).
+// Alg. 1 over the partition (one launch of the partitioned persistent
+// kernel, mis2_kernel.cuh mis2_dist_persistent).  in_sets[i] = part i's
+// owned mask; labels[i] (or empty) = part i's phase-2 mask (active iff < 0,
+// owned rows).
 static int dist_mis2_run(mis2_comm* c, const mis2_opts& opt, const std::vector<uint8_t*>& in_sets,
                          const std::vector<const int32_t*>& labels, int64_t* count, int32_t* iters, cudaStream_t s) {
     const int max_iters = max_iters_for(c->n_global, opt.max_iters);
     const int L = (int)c->dev.size();
+    int64_t n_loc = 0, nnz_loc = 0;
     for (int i = 0; i < L; i++) {
         PartDev& d = c->dev[i];
         d.seed = opt.seed;
         d.scheme = opt.scheme;
         d.hshift = (opt.flags & MIS2_FLAG_WORD32) ? 32 : 0;
-        if (opt.group) d.G = opt.group;
         d.labels = labels.empty() ? nullptr : labels[i];
         d.in_set = in_sets[i];
-        MIS2_CUDA_TRY(cudaMemsetAsync(d.ctr, 0, sizeof(unsigned long long) * 8, s));
-        MIS2_TRY(part_step(d, kPartInit, 0, s));
+        n_loc += d.n_own;
+        nnz_loc += d.nnz;
     }
-    unsigned long long active = 0;
-    MIS2_TRY(global_sum(c, 0, &active, s));
-    int it = 0, status = MIS2_OK;
-    while (active > 0) {  // while worklist_1 != {}
-        MIS2_TRY(exchange(c, 0, s));  // ghost T before Refresh Column
-        for (int i = 0; i < L; i++) MIS2_TRY(part_step(c->dev[i], kPartColumn, it, s));
-        MIS2_TRY(exchange(c, 1, s));  // ghost M before Decide
-        for (int i = 0; i < L; i++) {
-            MIS2_CUDA_TRY(cudaMemsetAsync(c->dev[i].ctr + 1, 0, sizeof(unsigned long long), s));
-            MIS2_TRY(part_step(c->dev[i], kPartDecide, it, s));
-        }
-        unsigned long long rem = 0;
-        MIS2_TRY(global_sum(c, 1, &rem, s));
-        it++;
-        if (rem == 0) break;
-        if (it >= max_iters) {
-            status = MIS2_ENOTCONVERGED;
-            break;
-        }
-    }
-    for (int i = 0; i < L; i++) MIS2_TRY(part_step(c->dev[i], kPartFinal, it, s));
-    unsigned long long cnt = 0;
-    MIS2_TRY(global_sum(c, 2, &cnt, s));
-    *count = (int64_t)cnt;
-    *iters = it;
-    if (status != MIS2_OK) set_error("MIS-2 did not converge within max_iters");
-    return status;
+    // one lane-group width for every local part (the persistent kernel is
+    // one launch); the ranks of the NCCL transport each choose from their
+    // own rows, which only changes the work split, never the result
+    const int G = opt.group ? opt.group : choose_group(n_loc, nnz_loc, 0);
+    return dist_mis2_launch(c->dev, c->peer_T, c->peer_M, c->peer_box, !c->local, G, max_iters, &c->epoch,
+                            c->dscratch, count, iters, s);
 }
 
 static int agg_alloc(mis2_comm* c) {

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "../../include/mis2.h"
@@ -97,16 +98,31 @@ struct PartDev {
     uint32_t* M;             // n_own + n_ghost
     int32_t* L1[2];
     int32_t* L2[2];
-    int* cnts;               // [2 * grid]
-    unsigned long long* ctr; // [0] active, [1] |wl1| this iteration, [2] count
     int32_t* heavy;          // n_own deferred long rows
     uint8_t* in_set;         // n_own
-    int grid, G, scheme, hshift;
+    int G, scheme, hshift;
     uint64_t seed;
+    // halo pushes (mis2_kernel.cuh PartK): owned row send_src[i] -> partition send_peer[i], index send_dst[i]
+    int64_t nsend;
+    const int64_t* send_csp;       // [n_own / 8 + 2] entries per 8-row group (sorted by row)
+    const int32_t* send_src;
+    const int32_t* send_peer;
+    const int64_t* send_dst;
+    unsigned int* bar;             // partition barrier counter
+    unsigned long long* acc;       // [2]
+    unsigned long long* box;       // [2 * P] mailboxes
+    unsigned long long* rel;       // [1]
+    int gpart;                     // global partition id
 };
-enum { kPartInit = 0, kPartColumn = 1, kPartDecide = 2, kPartFinal = 3 };
-int part_step(const PartDev& d, int op, int it, cudaStream_t s);
-int part_grid(int64_t n_own, int G);
+// Alg. 1 over the local partitions parts[0..nl) (one cooperative launch);
+// peer_T / peer_M / peer_box: every partition's arrays as seen from this
+// device (P entries); sys_scope: peers on other GPUs.  epoch: last partition-barrier epoch, updated.
+// Writes *count (global), *iters; returns MIS2_OK / MIS2_ENOTCONVERGED.
+int dist_mis2_launch(const std::vector<PartDev>& parts, const std::vector<uint64_t*>& peer_T,
+                     const std::vector<uint32_t*>& peer_M, const std::vector<unsigned long long*>& peer_box,
+                     bool sys_scope, int G, int max_iters, unsigned int* epoch, void* dev_scratch, int64_t* count,
+                     int32_t* iters, cudaStream_t s);
+size_t dist_scratch_bytes(int nlocal);
 int debug_read(void* ws, size_t ws_bytes, int64_t n, long long* out, int64_t count);
 
 // aggregation / coarsening / validation (aggregate.cu, coarsen.cu)

@@ -9,43 +9,6 @@
 
 namespace mis2k {
 
-__global__ void __launch_bounds__(kMB) mis2_part_init(MisParams p, int* cnts, unsigned long long* n_active) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
-    const int64_t B = gridDim.x;
-    const int64_t blo = p.n * blockIdx.x / B, bhi = p.n * (blockIdx.x + 1) / B;
-    const uint64_t fi0 = p.prio.iter_term(0);
-    int act_cnt = 0;
-    for (int64_t v = blo + threadIdx.x; v < bhi; v += kMB) {
-        const bool act = p.labels ? (p.labels[v] < 0) : true;
-        p.T[v] = act ? p.prio.word(0, fi0, p.gbase + v) : kOUT;
-        p.M[v] = act ? kPending : 0u;
-        act_cnt += act;
-    }
-    const long long s = block_sum_int(sm, act_cnt);
-    if (threadIdx.x == 0) {
-        cnts[blockIdx.x] = (int)(bhi - blo);
-        cnts[B + blockIdx.x] = (int)(bhi - blo);
-        if (s) atomicAdd(n_active, (unsigned long long)s);
-    }
-}
-
-
-__global__ void mis2_part_final(MisParams p, unsigned long long* count) {
-    {
-        const int64_t B = gridDim.x;
-        l2_release(p, make_rows(p.n, B, blockIdx.x, kMB, false));
-    }
-    int c = 0;
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < p.n; v += (int64_t)gridDim.x * blockDim.x) {
-        const uint8_t in = (p.T[v] == kIN);
-        p.in_set[v] = in;
-        c += in;
-    }
-    c = group_sum<32>(c);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
-}
-
 }  // namespace mis2k
 
 namespace mis2h {
@@ -89,14 +52,12 @@ int choose_group(int64_t n, int64_t nnz, int requested) {
 template <int G>
 void* persistent_kernel(bool stats, bool push);
 template <int G>
-cudaError_t launch_part_phase(int ph, const MisParams& p, int it, int grid, int smem, int* cnts,
-                              unsigned long long* wl1, cudaStream_t s);
-#define MIS2_DECLARE_G(G)                                                                            \
-    template <>                                                                                      \
-    void* persistent_kernel<G>(bool, bool);                                                          \
-    template <>                                                                                      \
-    cudaError_t launch_part_phase<G>(int, const MisParams&, int, int, int, int*, unsigned long long*, \
-                                     cudaStream_t);
+void* dist_kernel();
+#define MIS2_DECLARE_G(G)                   \
+    template <>                             \
+    void* persistent_kernel<G>(bool, bool); \
+    template <>                             \
+    void* dist_kernel<G>();
 MIS2_DECLARE_G(1)
 MIS2_DECLARE_G(2)
 MIS2_DECLARE_G(4)
@@ -166,39 +127,125 @@ static MisParams part_params(const PartDev& d) {
     return p;
 }
 
-int part_step(const PartDev& d, int op, int it, cudaStream_t s) {
-    const MisParams p = part_params(d);
+static void* pick_dist_kernel(int G) {
+    switch (G) {
+        case 1: return dist_kernel<1>();
+        case 2: return dist_kernel<2>();
+        case 4: return dist_kernel<4>();
+        case 8: return dist_kernel<8>();
+        case 16: return dist_kernel<16>();
+        case 32: return dist_kernel<32>();
+    }
+    return nullptr;
+}
+
+size_t dist_scratch_bytes(int nlocal) { return sizeof(PartK) * (size_t)(nlocal > 0 ? nlocal : 1) + 256; }
+
+int dist_mis2_launch(const std::vector<PartDev>& parts, const std::vector<uint64_t*>& peer_T,
+                     const std::vector<uint32_t*>& peer_M, const std::vector<unsigned long long*>& peer_box,
+                     bool sys_scope, int G, int max_iters, unsigned int* epoch, void* dev_scratch, int64_t* count,
+                     int32_t* iters, cudaStream_t s) {
+    DeviceInfo di;
+    MIS2_TRY(device_info(&di));
+    const int nl = (int)parts.size();
+    const int P = (int)peer_T.size();
+    if (P > kMaxParts || nl < 1) {
+        set_error("partitions: %d local of %d (at most %d)", nl, P, kMaxParts);
+        return MIS2_EINVAL;
+    }
+    void* fn = pick_dist_kernel(G);
+    if (!fn) {
+        set_error("group must be one of 1,2,4,8,16,32 (got %d)", G);
+        return MIS2_EINVAL;
+    }
     const int smem = (int)sizeof(TileSmem);
-    const int grid = d.grid;
-    if (op == kPartInit) {
-        cudaFuncSetAttribute((const void*)mis2_part_init, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        mis2_part_init<<<grid, kMB, smem, s>>>(p, d.cnts, d.ctr + 0);
-        count_launch();
-        MIS2_CUDA_TRY(cudaGetLastError());
-        return MIS2_OK;
+    static thread_local void* cached_fn = nullptr;  // attribute + occupancy per kernel, once per thread
+    static thread_local int cached_per_sm = 0;
+    if (cached_fn != fn) {
+        MIS2_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        MIS2_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, fn, kMB, smem));
+        cached_fn = fn;
     }
-    if (op == kPartFinal) {
-        mis2_part_final<<<grid, kMB, 0, s>>>(p, d.ctr + 2);
-        count_launch();
-        MIS2_CUDA_TRY(cudaGetLastError());
-        return MIS2_OK;
+    const int per_sm = cached_per_sm;
+    if (per_sm < 1) {
+        set_error("partitioned kernel does not fit on an SM");
+        return MIS2_EINTERNAL;
     }
-    const int ph = op == kPartColumn ? 0 : 1;
-    cudaError_t e;
-    switch (d.G) {
-        case 1: e = launch_part_phase<1>(ph, p, it, grid, smem, d.cnts, d.ctr + 1, s); break;
-        case 2: e = launch_part_phase<2>(ph, p, it, grid, smem, d.cnts, d.ctr + 1, s); break;
-        case 4: e = launch_part_phase<4>(ph, p, it, grid, smem, d.cnts, d.ctr + 1, s); break;
-        case 8: e = launch_part_phase<8>(ph, p, it, grid, smem, d.cnts, d.ctr + 1, s); break;
-        case 16: e = launch_part_phase<16>(ph, p, it, grid, smem, d.cnts, d.ctr + 1, s); break;
-        default: e = launch_part_phase<32>(ph, p, it, grid, smem, d.cnts, d.ctr + 1, s); break;
+    // blocks per local partition: the co-resident maximum split by owned
+    // rows, about two dense steps per block at most, at least one each
+    const int64_t max_grid = (int64_t)per_sm * di.sms;
+    const int64_t rpb = kMB / G;
+    int64_t tot_rows = 0;
+    for (const PartDev& d : parts) tot_rows += d.n_own;
+    std::vector<int> nblk(nl);
+    int64_t grid = 0;
+    for (int i = 0; i < nl; i++) {
+        int64_t want = (parts[i].n_own + 2 * rpb - 1) / (2 * rpb);
+        const int64_t share = tot_rows > 0 ? (max_grid - nl) * parts[i].n_own / tot_rows + 1 : 1;
+        if (want > share) want = share;
+        if (want < 1) want = 1;
+        nblk[i] = (int)want;
+        grid += want;
     }
+    std::vector<PartK> hk(nl);
+    int blk0 = 0;
+    for (int i = 0; i < nl; i++) {
+        const PartDev& d = parts[i];
+        PartK& k = hk[i];
+        memset(&k, 0, sizeof(k));
+        k.mp = part_params(d);
+        k.blk0 = blk0;
+        k.nblk = nblk[i];
+        blk0 += nblk[i];
+        k.gpart = d.gpart;
+        k.nsend = d.nsend;
+        k.send_csp = d.send_csp;
+        k.send_src = d.send_src;
+        k.send_peer = d.send_peer;
+        k.send_dst = d.send_dst;
+        k.bar = d.bar;
+        k.acc = d.acc;
+        k.box = d.box;
+        k.rel = d.rel;
+    }
+    PeerTab peers;
+    memset(&peers, 0, sizeof(peers));
+    peers.P = P;
+    peers.sys = sys_scope ? 1 : 0;
+    for (int q = 0; q < P; q++) {
+        peers.T[q] = peer_T[q];
+        peers.M[q] = peer_M[q];
+        peers.box[q] = peer_box[q];
+    }
+    PartK* dk = (PartK*)dev_scratch;
+    unsigned long long* dout = (unsigned long long*)((char*)dev_scratch + sizeof(PartK) * nl);
+    dout = (unsigned long long*)(((uintptr_t)dout + 15) & ~(uintptr_t)15);
+    // the parameter block changes only with the per-call options (seed,
+    // masks, outputs): upload it when it differs from the last call's
+    static thread_local std::vector<char> last;
+    static thread_local void* last_dst = nullptr;
+    const size_t kb = sizeof(PartK) * nl;
+    if (last_dst != (void*)dk || last.size() != kb || memcmp(last.data(), hk.data(), kb) != 0) {
+        MIS2_CUDA_TRY(cudaMemcpyAsync(dk, hk.data(), kb, cudaMemcpyHostToDevice, s));
+        MIS2_CUDA_TRY(cudaStreamSynchronize(s));  // hk is a host stack vector
+        last.assign((const char*)hk.data(), (const char*)hk.data() + kb);
+        last_dst = (void*)dk;
+    }
+    unsigned int e0 = *epoch;
+    void* args[] = {&dk, (void*)&nl, &peers, &e0, &max_iters, &dout};
+    int nlv = nl;
+    args[1] = &nlv;
+    MIS2_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(kMB), args, smem, s));
     count_launch();
-    if (e != cudaSuccess) {
-        set_error("part phase launch: %s", cudaGetErrorString(e));
-        return MIS2_ECUDA;
-    }
-    return MIS2_OK;
+    unsigned long long h[3];
+    MIS2_CUDA_TRY(cudaMemcpyAsync(h, dout, sizeof(h), cudaMemcpyDeviceToHost, s));
+    MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+    *count = (int64_t)h[0];
+    *iters = (int32_t)(h[1] & 0xffffffffull);
+    *epoch = (unsigned int)h[2];
+    const int st = (int)(int32_t)(h[1] >> 32);
+    if (st != MIS2_OK) set_error("MIS-2 did not converge within max_iters");
+    return st;
 }
 
 int debug_read(void* ws, size_t ws_bytes, int64_t n, long long* out, int64_t count) {
@@ -211,17 +258,6 @@ int debug_read(void* ws, size_t ws_bytes, int64_t n, long long* out, int64_t cou
     if (count > cap) count = cap;
     MIS2_CUDA_TRY(cudaMemcpy(out, w.mark, sizeof(long long) * count, cudaMemcpyDeviceToHost));
     return MIS2_OK;
-}
-
-int part_grid(int64_t n_own, int G) {
-    DeviceInfo di;
-    if (device_info(&di) != MIS2_OK) return 1;
-    const int64_t rpb = kMB / G;
-    int64_t want = (n_own + 2 * rpb - 1) / (2 * rpb);
-    const int64_t cap = (int64_t)kMinBlocksPerSM * di.sms;
-    if (want > cap) want = cap;
-    if (want < 1) want = 1;
-    return (int)want;
 }
 
 int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uint8_t* in_set, int64_t* d_count,

@@ -14,19 +14,10 @@ void* persistent_kernel<2>(bool stats, bool push) {
 }
 
 template <int G>
-cudaError_t launch_part_phase(int ph, const MisParams& p, int it, int grid, int smem, int* cnts,
-                              unsigned long long* wl1, cudaStream_t s);
+void* dist_kernel();
 template <>
-cudaError_t launch_part_phase<2>(int ph, const MisParams& p, int it, int grid, int smem, int* cnts,
-                                 unsigned long long* wl1, cudaStream_t s) {
-    if (ph == 0) {
-        cudaFuncSetAttribute((const void*)mis2_part_phase<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        mis2_part_phase<2, 0><<<grid, kMB, smem, s>>>(p, it, cnts, wl1);
-    } else {
-        cudaFuncSetAttribute((const void*)mis2_part_phase<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        mis2_part_phase<2, 1><<<grid, kMB, smem, s>>>(p, it, cnts, wl1);
-    }
-    return cudaGetLastError();
+void* dist_kernel<2>() {
+    return (void*)&mis2_dist_persistent<2>;
 }
 
 }  // namespace mis2h

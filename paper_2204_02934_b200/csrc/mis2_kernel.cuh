@@ -1327,49 +1327,287 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
     }
 }
 
-// ------------------------------------------------------------ per-phase kernels
-// The same phases as one launch each, for the partitioned driver (dist.cu),
-// which exchanges ghost T / M between them.  Block worklist segment sizes
-// live in cnts[0..B) (worklist_1) and cnts[B..2B) (worklist_2).
-__device__ __forceinline__ void init_mbars(TileSmem& sm, const MisParams& p, int G2) {
+// ------------------------------------------------------------ partitioned kernel
+// Alg. 1 over a 1-D row partition as ONE persistent kernel
+// per GPU: every phase of the single-GPU kernel runs on the partition's own
+// rows, the halo values are pushed by the kernel itself -- after Refresh
+// Column the M words, after Decide the T words of the owned rows other
+// partitions hold as ghosts are stored straight into those partitions' ghost
+// slots (peer memory over NVLink, or another buffer of this GPU for the
+// local transport) -- and partitions meet at a barrier whose mailboxes carry
+// the per-partition counts, so the loop condition |worklist_1| = 0 is
+// evaluated on the device: no host round trip per iteration.  P:117 (each
+// phase reads only the previous phase's arrays) makes any partition
+// bit-identical to one GPU: global ids in the hash, the global n in b.
+//
+// One launch holds one or several local partitions (the local transport
+// runs all P of them in one cooperative grid, so a partition barrier never
+// waits for a partition that is not resident); partition i's blocks are
+// [blk0, blk0 + nblk).
+constexpr int kMaxParts = 64;
+struct PartK {
+    MisParams mp;                     // n = owned rows; T / M over [owned | ghosts]; contiguous Rows
+    int blk0, nblk;                   // this partition's blocks in the grid
+    int gpart;                        // global partition id
+    int64_t nsend;                    // halo entries: owned row send_src[i] -> partition send_peer[i], slot send_dst[i]
+    const int64_t* send_csp;          // entries of owned rows [8c, 8c + 8): [send_csp[c], send_csp[c + 1]) (sorted by row)
+    const int32_t* send_src;
+    const int32_t* send_peer;
+    const int64_t* send_dst;          // index into the peer's T / M arrays (its ghost region)
+    unsigned int* bar;                // sub-grid barrier counter of this partition
+    unsigned long long* acc;          // [2] per-epoch sum of the partition's block contributions
+    unsigned long long* box;          // [2][P] mailbox: box[e & 1][q] = e << 32 | value of partition q
+    unsigned long long* rel;          // leader -> blocks: e << 32 | sum over partitions
+};
+struct PeerTab {
+    int P;                            // partitions in total (all ranks)
+    int sys;                          // peers on other GPUs: system-scope fences / mailbox accesses
+    uint64_t* T[kMaxParts];           // partition q's T (peer / local address)
+    uint32_t* M[kMaxParts];
+    unsigned long long* box[kMaxParts];
+};
+
+// sense-flip barrier over the nblk blocks of one partition (lb = block index in it)
+__device__ __forceinline__ void part_barrier(unsigned int* bar, int lb, int nblk) {
+    __syncthreads();
     if (threadIdx.x == 0) {
-        const int64_t B = gridDim.x;
-        sm.pol = l2_policy(p, make_rows(p.n, B, blockIdx.x, kMB, false));
-        mbar_init(&sm.mbar[0], 1);
-        mbar_init(&sm.mbar[1], 1);
-        mbar_init(&sm.mbarS[0], kMB / G2);
-        mbar_init(&sm.mbarS[1], kMB / G2);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const unsigned int nb = (lb == 0) ? (0x80000000u - (unsigned)(nblk - 1)) : 1u;
+        unsigned int old, cur;
+        asm volatile("atom.add.release.gpu.u32 %0,[%1],%2;" : "=r"(old) : "l"(bar), "r"(nb) : "memory");
+        for (;;) {
+            asm volatile("ld.relaxed.gpu.u32 %0,[%1];" : "=r"(cur) : "l"(bar) : "memory");
+            if ((old ^ cur) & 0x80000000u) break;
+            __nanosleep(32);
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
 }
 
-template <int G, int PH>
-__global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_part_phase(MisParams p, int it, int* cnts,
-                                                              unsigned long long* wl1_total) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
-    init_mbars(sm, p, sparse_group<G>());
-    uint32_t ph = 0u;
-    const int64_t B = gridDim.x;
-    const Rows rows = make_rows(p.n, B, blockIdx.x, kMB / G, false);  // contiguous: ghosts follow the owned rows
-    const int64_t range = rows.count;
-    const int cur = it & 1;
-    int* cnt = &cnts[(PH == 0 ? B : 0) + blockIdx.x];
-    const int c = *cnt;
-    const bool dense = (it == 0) || (int64_t)c * kDenseDen >= range * kDenseNum;
-    int out;
-    if (PH == 0) {
-        out = dense ? dense_phase<G, false, 0>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0)
-                    : sparse_phase<G, false, 0>(sm, p, it, rows.seg, p.L2[cur], c, p.L2[cur ^ 1], ph, 0);
-    } else {
-        const uint64_t fi_next = p.prio.iter_term(it + 1);
-        out = dense ? dense_phase<G, false, 1>(sm, p, it, rows, p.L1[cur ^ 1], ph, fi_next)
-                    : sparse_phase<G, false, 1>(sm, p, it, rows.seg, p.L1[cur], c, p.L1[cur ^ 1], ph, fi_next);
+// Partition barrier number e (1, 2, ...): every block adds `value` for its
+// partition, the partition's leader (block 0 of it) posts the partition sum
+// in every partition's mailbox (system-scope release: the halo stores of all
+// its blocks come first) and sums all partitions' posts of epoch e; returns
+// that global sum to every block.  Mailboxes are double buffered by epoch
+// parity: a partition can post e + 2 only after every partition has posted
+// e + 1, i.e. after every leader has read the posts of e.
+static __device__ unsigned long long part_sync(const PartK& pk, const PeerTab& peers, int lb, unsigned int e,
+                                        unsigned long long value) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (value) atomicAdd(&pk.acc[e & 1], value);
+        // this block's halo stores before the post
+        if (peers.P > 1 && peers.sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    }
+    part_barrier(pk.bar, lb, pk.nblk);
+    __shared__ unsigned long long s_sum;
+    if (peers.P == 1) {  // one partition: the sum is complete after the barrier
+        if (threadIdx.x == 0) {
+            s_sum = *(volatile unsigned long long*)&pk.acc[e & 1];
+            if (lb == 0) pk.acc[(e + 1) & 1] = 0ull;  // last read at epoch e - 1
+        }
+        __syncthreads();
+        return s_sum;
     }
     if (threadIdx.x == 0) {
-        *cnt = out;
-        if (PH == 1 && out) atomicAdd(wl1_total, (unsigned long long)out);
+        if (lb == 0) {
+            const unsigned long long mine = *(volatile unsigned long long*)&pk.acc[e & 1];
+            pk.acc[(e + 1) & 1] = 0ull;  // last read at epoch e - 1
+            const unsigned long long post = ((unsigned long long)e << 32) | (mine & 0xffffffffull);
+            for (int q = 0; q < peers.P; q++) {
+                unsigned long long* dst = peers.box[q] + (e & 1) * peers.P + pk.gpart;
+                if (peers.sys) asm volatile("st.release.sys.u64 [%0], %1;" ::"l"(dst), "l"(post) : "memory");
+                else asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(dst), "l"(post) : "memory");
+            }
+            unsigned long long sum = 0;
+            for (int q = 0; q < peers.P; q++) {
+                unsigned long long v;
+                const unsigned long long* src = pk.box + (e & 1) * peers.P + q;
+                for (;;) {
+                    if (peers.sys) asm volatile("ld.acquire.sys.u64 %0,[%1];" : "=l"(v) : "l"(src) : "memory");
+                    else asm volatile("ld.acquire.gpu.u64 %0,[%1];" : "=l"(v) : "l"(src) : "memory");
+                    if ((unsigned int)(v >> 32) == e) break;
+                    __nanosleep(64);
+                }
+                sum += v & 0xffffffffull;
+            }
+            asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(pk.rel), "l"(((unsigned long long)e << 32) | sum)
+                         : "memory");
+            s_sum = sum;
+        } else {
+            unsigned long long v;
+            for (;;) {
+                asm volatile("ld.relaxed.gpu.u64 %0,[%1];" : "=l"(v) : "l"(pk.rel) : "memory");
+                if ((unsigned int)(v >> 32) == e) break;
+                __nanosleep(32);
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            s_sum = v & 0xffffffffull;
+        }
+    }
+    __syncthreads();
+    return s_sum;
+}
+
+// halo entries of the rows this block owns, pushed right after the block
+// computed them (its own __syncthreads ends the phase): peer[X][dst] = X[src].
+// No partition-wide barrier before the pushes -- the values are this block's.
+// The entries of run k are [send_csp[lo_k / 8], send_csp[ceil(hi_k / 8)]);
+// every thread takes a contiguous group of runs, the groups' entry counts
+// are scanned in shared memory (the staging buffers are idle between
+// phases) and the entries are then pushed by all threads at once.
+template <typename W>
+__device__ __forceinline__ void push_halo(TileSmem& sm, const PartK& pk, const Rows& rows, const W* src_arr,
+                                          W* const* peer_arr) {
+    if (pk.nsend == 0) return;
+    __syncthreads();
+    const int t = threadIdx.x;
+    const int64_t per = (rows.nruns + kMB - 1) / kMB;  // runs of this thread: [t * per, t * per + per)
+    int64_t* pre = reinterpret_cast<int64_t*>(sm.buf[0]);  // [kMB + 1] exclusive prefix of the groups' counts
+    int64_t cnt = 0;
+    for (int64_t k = t * per; k < rows.nruns && k < (t + 1) * per; k++)
+        cnt += pk.send_csp[(rows.run_hi(k) + 7) >> 3] - pk.send_csp[rows.run_lo(k) >> 3];
+    // block exclusive scan of cnt
+    int64_t x = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int64_t y = __shfl_up_sync(kFull, x, off);
+        if ((t & 31) >= off) x += y;
+    }
+    if ((t & 31) == 31) sm.red64[t >> 5] = (uint64_t)x;
+    __syncthreads();
+    int64_t wbase = 0;
+    for (int w = 0; w < (t >> 5); w++) wbase += (int64_t)sm.red64[w];
+    pre[t] = wbase + x - cnt;
+    if (t == kMB - 1) pre[kMB] = wbase + x;
+    __syncthreads();
+    const int64_t total = pre[kMB];
+    for (int64_t j = t; j < total; j += kMB) {
+        int lo = 0, hi = kMB;  // the group holding entry j: pre[g] <= j < pre[g + 1]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pre[mid] <= j) lo = mid;
+            else hi = mid;
+        }
+        // walk the group's runs to the one holding entry j
+        int64_t r = j - pre[lo];
+        int64_t k = (int64_t)lo * per;
+        for (;; k++) {
+            const int64_t a = pk.send_csp[rows.run_lo(k) >> 3], b = pk.send_csp[(rows.run_hi(k) + 7) >> 3];
+            if (r < b - a) {
+                const int64_t i = a + r;
+                peer_arr[pk.send_peer[i]][pk.send_dst[i]] = src_arr[pk.send_src[i]];
+                break;
+            }
+            r -= b - a;
+        }
+    }
+    __syncthreads();
+}
+
+template <int G>
+__global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_dist_persistent(const PartK* __restrict__ parts,
+                                                                            int nlocal, PeerTab peers,
+                                                                            unsigned int epoch0, int max_iters,
+                                                                            unsigned long long* out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+    const int t = threadIdx.x;
+    int pid = 0;
+    while (pid + 1 < nlocal && (int)blockIdx.x >= parts[pid + 1].blk0) pid++;
+    const PartK& pk = parts[pid];
+    const MisParams& p = pk.mp;  // read through the (restrict) parameter block: no local copy
+    const int lb = (int)blockIdx.x - pk.blk0;
+    // cyclic chunks of the partition's own rows (ghost indices follow them
+    // and are never owned)
+    const Rows rows = make_rows(p.n, pk.nblk, lb, kMB / G, true);
+    unsigned int e = epoch0;
+    if (t == 0) {
+        mbar_init(&sm.mbar[0], 1);
+        mbar_init(&sm.mbar[1], 1);
+        mbar_init(&sm.mbarS[0], kMB / sparse_group<G>());
+        mbar_init(&sm.mbarS[1], kMB / sparse_group<G>());
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        sm.pol = l2_policy(p, rows);
+        s_use_keys = 0;
+    }
+    uint32_t ph = 0u;
+    // worklists <- the active owned rows; Refresh Row of iteration 0
+    int act_block = 0;
+    {
+        const uint64_t fi0 = p.prio.iter_term(0);
+        if (t == 0) sm.cnt = 0;
+        __syncthreads();
+        for (int64_t base = 0; base < rows.count; base += kMB) {
+            const bool in = base + t < rows.count;
+            const int64_t v = in ? rows.row_at(base + t) : 0;
+            const bool act = in && (p.labels ? (p.labels[v] < 0) : true);
+            if (in) {
+                p.T[v] = act ? p.prio.word(0, fi0, p.gbase + v) : kOUT;
+                p.M[v] = act ? kPending : 0u;  // 0 = inactive sentinel (reading Q15)
+            }
+            const unsigned ball = __ballot_sync(kFull, act);
+            if (ball) {
+                const int lane = t & 31, leader = __ffs(ball) - 1;
+                int pos = 0;
+                if (lane == leader) pos = atomicAdd(&sm.cnt, __popc(ball));
+                pos = __shfl_sync(kFull, pos, leader);
+                if (act) {
+                    const int64_t at = rows.seg + pos + __popc(ball & lanemask_lt());
+                    p.L1[0][at] = (int32_t)v;
+                    p.L2[0][at] = (int32_t)v;
+                }
+            }
+        }
+        __syncthreads();
+        act_block = sm.cnt;
+        __syncthreads();
+    }
+    // ghost T / M of iteration 0 (inactive ghosts: T = OUT, M = 0)
+    push_halo<uint64_t>(sm, pk, rows, p.T, peers.T);
+    push_halo<uint32_t>(sm, pk, rows, p.M, peers.M);
+    const unsigned long long n_active = part_sync(pk, peers, lb, ++e, (unsigned long long)act_block);
+
+    int it = 0, status = MIS2_OK;
+    const int64_t range = rows.count;
+    int cnt1 = act_block, cnt2 = act_block;
+    while (n_active > 0) {  // while worklist_1 != {}
+        const int cur = it & 1;
+        // ---- Refresh Column over worklist_2; ghost M pushed to the peers
+        const bool dense2 = (int64_t)cnt2 * kDenseDen >= range * kDenseNum;
+        cnt2 = dense2 ? dense_phase<G, false, 0>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0)
+                      : sparse_phase<G, false, 0>(sm, p, it, rows.seg, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
+        push_halo<uint32_t>(sm, pk, rows, p.M, peers.M);
+        part_sync(pk, peers, lb, ++e, 0ull);
+        // ---- Decide over worklist_1 + fused refresh; ghost T pushed
+        const uint64_t fi_next = p.prio.iter_term(it + 1);
+        const bool dense1 = (int64_t)cnt1 * kDenseDen >= range * kDenseNum;
+        cnt1 = dense1 ? dense_phase<G, false, 1>(sm, p, it, rows, p.L1[cur ^ 1], ph, fi_next)
+                      : sparse_phase<G, false, 1>(sm, p, it, rows.seg, p.L1[cur], cnt1, p.L1[cur ^ 1], ph, fi_next);
+        push_halo<uint64_t>(sm, pk, rows, p.T, peers.T);
+        const unsigned long long remaining = part_sync(pk, peers, lb, ++e, (unsigned long long)cnt1);
+        it++;
+        if (remaining == 0) break;
+        if (it >= max_iters) {  // reading Q12
+            status = MIS2_ENOTCONVERGED;
+            break;
+        }
+    }
+    // return {v : T_v = IN}; the global count through one more barrier
+    l2_release(p, rows);
+    int cnt = 0;
+    for (int64_t i = t; i < rows.count; i += kMB) {
+        const int64_t v = rows.row_at(i);
+        const uint8_t in = (p.T[v] == kIN);
+        p.in_set[v] = in;
+        cnt += in;
+    }
+    const long long bc = block_sum_int(sm, cnt);
+    const unsigned long long total = part_sync(pk, peers, lb, ++e, (unsigned long long)bc);
+    if (blockIdx.x == 0 && t == 0) {
+        out[0] = total;
+        out[1] = (unsigned long long)(unsigned)it | ((unsigned long long)(unsigned)status << 32);
+        out[2] = e;  // the last epoch used
     }
 }
 
