@@ -1,30 +1,33 @@
 // mis2_kernel.cuh -- device code of Alg. 1 (MIS-2, §III-A): the
-// persistent kernel template and the per-phase kernel template of the
-// partitioned driver.  Included by mis2_core.cu (host side, types only) and
-// instantiated per lane-group width G in mis2_g<G>.cu (parallel build).
+// single-GPU persistent kernel and the partitioned persistent kernel (one
+// per GPU), both cooperatively launched sm_100a kernels.  Included by
+// mis2_core.cu (host side, types only) and instantiated per lane-group width
+// G in mis2_g<G>.cu (parallel build).
 #pragma once
-// cooperatively launched sm_100a kernel.
 //
 // Design:
-//  * Each thread block owns a contiguous vertex range [blo, bhi) and works
-//    through it in steps of RPB = 256/G rows, G lanes per CSR row
-//    (§V-D "SIMD parallelism", with a tunable group width).
-//  * worklist_1 / worklist_2 (§V-B) live in the block's slice of
+//  * Each thread block owns runs of at most 256/G consecutive rows (Rows:
+//    cyclic 256/G-row chunks b, b + B, ... on one GPU) and works through them
+//    in steps of one run, G lanes per CSR row (§V-D "SIMD parallelism",
+//    P:452-457, with a tunable group width).
+//  * worklist_1 / worklist_2 (§V-B) live in the block's segment of
 //    int32[n] arrays, double buffered (in -> out) and compacted with warp
 //    ballots + one shared-memory atomic per warp: no global scan, no global
 //    atomics, no block barrier per step.  The order inside a segment is
 //    free (reading Q11): every phase is a per-vertex function of the
 //    previous phase's arrays.
 //  * Dense phases (iteration 0, and any block whose worklist still covers
-//    >= 3/8 of its range) walk consecutive rows; the colinds of the next
-//    tile are streamed into shared memory by the Blackwell bulk-copy engine
+//    >= 3/8 of its rows) walk its runs; the colinds of the next run are
+//    streamed into shared memory by the Blackwell bulk-copy engine
 //    (cp.async.bulk + mbarrier complete_tx), double buffered, while the
-//    current tile gathers T / M.  Worklist membership is read from the
+//    current run gathers T / M.  Worklist membership is read from the
 //    status words (M_v != OUT for worklist_2, T_v undecided for worklist_1).
-//  * Sparse phases read the block's compacted worklist and process rows
-//    straight from global memory.  Rows longer than kHeavyDirect are
-//    deferred and reduced by the whole block.
-//  * Neighbour loops issue predicated batches of independent gathers.
+//  * Sparse phases read the block's compacted worklist; each row group
+//    leader bulk-copies its row into a shared-memory slot one step ahead.
+//    Rows longer than heavy_len<G>() are deferred to warps, rows longer than
+//    kHugeRow to the whole block.
+//  * Neighbour loops issue batches of independent gathers (indices clamped
+//    to the row's last entry: min / exists / forall are idempotent).
 //  * Phases are separated by a grid-wide barrier; |worklist_1| == 0
 //    is tested on the device, so one call is 1 memset + 1 kernel launch.
 //  * Refresh Row of iteration i+1 is fused into Decide of
@@ -39,10 +42,11 @@
 
 namespace mis2k {
 
-// One block per SM (MIS2_WARPS = 32, the default): co-resident blocks of one
-// SM are not scheduled fairly (the youngest block of an SM finishes a phase
-// ~9 us after the oldest on C2, measured), and a grid barrier over 148
-// blocks costs about half of one over 592.
+// Warps per block: 8, four co-resident blocks per SM (shared memory and
+// registers limit it to four).  Measured against 2 x 16 and 1 x 32 warps per
+// SM with full-size tiles (C2 440 / 399 us against 371, profiles/
+// r02a_experiments.md): the co-resident blocks of one SM are not scheduled
+// fairly, but one large block synchronises more warps per step.
 #ifndef MIS2_WARPS
 #define MIS2_WARPS 8
 #endif
