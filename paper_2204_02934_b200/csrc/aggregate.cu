@@ -3,6 +3,8 @@
 // the phase bookkeeping is a handful of row-parallel kernels (G lanes per
 // CSR row, as in the MIS-2 passes) plus two exclusive scans that number the
 // aggregates in ascending root order (reading Q18).
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -286,16 +288,19 @@ __global__ void k_phase3(int64_t n, const int64_t* __restrict__ rowptr, const in
 // shared-memory hash table; labels are split into hash passes so any number
 // of distinct candidates fits.
 constexpr int kHashSlots = 4096;
+// left != NULL (list form): heavy[] holds leftover-list positions, the
+// choice goes to choice[position]; else heavy[] holds vertices -> labels.
 __global__ void k_phase3_heavy(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colinds,
                                const int32_t* __restrict__ tent, const int32_t* __restrict__ size,
                                int32_t* __restrict__ labels, const int32_t* __restrict__ heavy,
-                               const int* heavy_cnt, int* err) {
+                               const int* heavy_cnt, int* err, const int32_t* __restrict__ left = nullptr,
+                               int32_t* __restrict__ choice = nullptr) {
     __shared__ int32_t keys[kHashSlots];
     __shared__ int32_t cnts[kHashSlots];
     __shared__ int s_c[32], s_s[32], s_a[32];
     const int nh = *heavy_cnt;
     for (int h = blockIdx.x; h < nh; h += gridDim.x) {
-        const int64_t v = heavy[h];
+        const int64_t v = left ? left[heavy[h]] : heavy[h];
         const int64_t s = rowptr[v], e = rowptr[v + 1];
         const int64_t d = e - s;
         const int passes = (int)((d + kHashSlots / 2 - 1) / (kHashSlots / 2));
@@ -334,7 +339,8 @@ __global__ void k_phase3_heavy(const int64_t* __restrict__ rowptr, const int32_t
         if (threadIdx.x == 0) {
             for (int w = 1; w < (int)(blockDim.x >> 5); w++)
                 if (better(s_c[w], s_s[w], s_a[w], bc, bs, ba)) { bc = s_c[w]; bs = s_s[w]; ba = s_a[w]; }
-            if (ba < 0) atomicOr(err, kErrNoCandidate);
+            if (left) choice[heavy[h]] = ba;  // checked by k_scatter_choice
+            else if (ba < 0) atomicOr(err, kErrNoCandidate);
             else labels[v] = ba;
         }
         __syncthreads();
@@ -368,6 +374,429 @@ __global__ void k_finish(const int32_t* d_n1, const int32_t* d_n2, int64_t* out_
     *out_na = (int64_t)*d_n1 + (int64_t)*d_n2;
 }
 
+// ---------------------------------------------------------------- list forms
+// Single-GPU Alg. 3 works from ordered lists of roots instead of passes over
+// all n rows: the roots push their aggregate id to their neighbours (roots
+// are >= 3 apart, so no vertex is pushed twice -- checked), only the phase-2
+// roots count their unaggregated neighbours, the aggregate sizes come out of
+// the pushes (no histogram), and phase 3 visits the listed leftovers, whose
+// choices are written by list position and scattered afterwards (so phase 3
+// reads the labels themselves, frozen, and no copy of them is made).  A
+// group of GL lanes takes one list entry at a time (GL from the average
+// degree: short rows fill a warp with several entries); the groups of the
+// grid stride over the list; list lengths are device scalars.
+constexpr int kListWarps = 8;  // warps per block of the list kernels
+
+template <int GL>
+struct ListIdx {
+    int64_t first, stride;
+    int sub;
+    __device__ __forceinline__ ListIdx() {
+        const int64_t gid = (int64_t)blockIdx.x * (kListWarps * 32 / GL) + threadIdx.x / GL;
+        first = gid;
+        stride = (int64_t)gridDim.x * (kListWarps * 32 / GL);
+        sub = threadIdx.x % GL;
+    }
+};
+// every lane of a warp runs the same number of loop trips (the shuffles need
+// the whole warp): the trip bound is the warp's largest group index
+template <int GL>
+__device__ __forceinline__ int64_t warp_trips(const ListIdx<GL>& li, int64_t cnt) {
+    const int64_t wfirst = li.first - (int64_t)((threadIdx.x & 31) / GL);  // group 0 of this warp
+    return cnt > wfirst ? (cnt - wfirst + li.stride - 1) / li.stride : 0;
+}
+
+// Phase 1: root R[i] gets aggregate i (ascending vertex order,
+// Q18) and so do its neighbours; size[i] = 1 + |adj(R[i])|.  labels must be
+// -1 (UNAGG) beforehand.
+template <int GL>
+__global__ void __launch_bounds__(32 * kListWarps) k_push_roots(const int32_t* __restrict__ R, const int32_t* d_cnt,
+                                                                const int64_t* __restrict__ rowptr,
+                                                                const int32_t* __restrict__ colinds,
+                                                                int32_t* __restrict__ labels,
+                                                                int32_t* __restrict__ size, int* err) {
+    const ListIdx<GL> li;
+    const int64_t cnt = *d_cnt, trips = warp_trips(li, cnt);
+    int bad = 0;
+    for (int64_t t = 0; t < trips; t++) {
+        const int64_t i = li.first + t * li.stride;
+        const bool ok = i < cnt;
+        int c = 0;
+        if (ok) {
+            const int32_t r = R[i];
+            if (li.sub == 0) labels[r] = (int32_t)i;
+            const int64_t s = rowptr[r], e = rowptr[r + 1];
+            for (int64_t j = s + li.sub; j < e; j += GL) {
+                const int32_t w = colinds[j];
+                if (w == r) continue;
+                const int32_t old = atomicExch(&labels[w], (int32_t)i);
+                bad |= old >= 0 && old != (int32_t)i;  // two roots within distance 2
+                c++;
+            }
+        }
+        c = group_sum<GL>(c);
+        if (ok && li.sub == 0) size[i] = 1 + c;
+    }
+    if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(err, kErrTwoRoots);
+}
+
+// Phase 2 accept rule (Q16) for the phase-2 roots R2[i]: acc[i] =
+// (>= 2 neighbours w != r unaggregated after phase 1); cnt2[i] = that count
+template <int GL>
+__global__ void __launch_bounds__(32 * kListWarps) k_accept_list(const int32_t* __restrict__ R2, const int32_t* d_cnt,
+                                                                 const int64_t* __restrict__ rowptr,
+                                                                 const int32_t* __restrict__ colinds,
+                                                                 const int32_t* __restrict__ labels,
+                                                                 uint8_t* __restrict__ acc) {
+    const ListIdx<GL> li;
+    const int64_t cnt = *d_cnt, trips = warp_trips(li, cnt);
+    for (int64_t t = 0; t < trips; t++) {
+        const int64_t i = li.first + t * li.stride;
+        int c = 0;
+        if (i < cnt) {
+            const int32_t r = R2[i];
+            const int64_t s = rowptr[r], e = rowptr[r + 1];
+            for (int64_t j = s + li.sub; j < e; j += GL) {
+                const int32_t w = colinds[j];
+                c += (w != r && labels[w] < 0);
+            }
+        }
+        c = group_sum<GL>(c);
+        if (i < cnt && li.sub == 0) acc[i] = c >= 2 ? 1 : 0;
+    }
+}
+
+// Phase 2 labels (Q17): accepted root A[j] gets aggregate n1 + j
+// (ascending vertex order) and so do its unaggregated neighbours (no vertex
+// has two: the phase-2 roots are >= 3 apart in the unaggregated subgraph);
+// size[n1 + j] = 1 + the neighbours it took
+template <int GL>
+__global__ void __launch_bounds__(32 * kListWarps) k_push_accepted(const int32_t* __restrict__ A, const int32_t* d_cnt,
+                                                                   const int32_t* d_n1,
+                                                                   const int64_t* __restrict__ rowptr,
+                                                                   const int32_t* __restrict__ colinds,
+                                                                   int32_t* __restrict__ labels,
+                                                                   int32_t* __restrict__ roots,
+                                                                   int32_t* __restrict__ size, int* err) {
+    const ListIdx<GL> li;
+    const int64_t cnt = *d_cnt, trips = warp_trips(li, cnt);
+    const int32_t n1 = *d_n1;
+    int bad = 0;
+    for (int64_t t = 0; t < trips; t++) {
+        const int64_t i = li.first + t * li.stride;
+        const bool ok = i < cnt;
+        int c = 0;
+        int32_t r = 0;
+        const int32_t id = n1 + (int32_t)i;
+        if (ok) {
+            r = A[i];
+            const int64_t s = rowptr[r], e = rowptr[r + 1];
+            for (int64_t j = s + li.sub; j < e; j += GL) {
+                const int32_t w = colinds[j];
+                if (w == r) continue;
+                const int32_t old = atomicCAS(&labels[w], -1, id);  // phase-1 labels (< n1) stay
+                bad |= old >= n1 && old != id;                      // two accepted roots share a vertex
+                c += old == -1;
+            }
+        }
+        c = group_sum<GL>(c);
+        if (ok && li.sub == 0) {
+            labels[r] = id;
+            roots[id] = r;
+            size[id] = 1 + c;
+        }
+    }
+    if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(err, kErrPhase2Conflict);
+}
+
+// the leftovers (label -1 after phase 2) listed, any order: each one's
+// choice reads only the frozen labels and sizes.  A block takes a
+// contiguous range, counts its leftovers, reserves them with ONE atomic
+// (a warp-aggregated atomic per 32 rows serialises on the counter: C3 0.57
+// ms) and writes them in order.
+__global__ void k_leftovers(int64_t n, const int32_t* __restrict__ labels, int32_t* __restrict__ left,
+                            unsigned long long* nleft) {
+    constexpr int E = 8;  // consecutive vertices per thread per round
+    __shared__ int s_w[33];
+    __shared__ unsigned long long s_base;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+    const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+    int c = 0;
+    for (int64_t v = lo + t; v < hi; v += blockDim.x) c += labels[v] < 0;
+    c = __reduce_add_sync(kFull, c);
+    if (lane == 0) s_w[warp] = c;
+    __syncthreads();
+    if (t == 0) {
+        int tot = 0;
+        for (int w = 0; w < nw; w++) tot += s_w[w];
+        s_base = tot ? atomicAdd(nleft, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+    unsigned long long run = s_base;
+    for (int64_t b0 = lo; b0 < hi; b0 += (int64_t)blockDim.x * E) {
+        const int64_t v0 = b0 + (int64_t)t * E;
+        unsigned bits = 0;
+#pragma unroll
+        for (int k = 0; k < E; k++) bits |= (v0 + k < hi && labels[v0 + k] < 0) ? (1u << k) : 0u;
+        const int mine = __popc(bits);
+        int inc = mine;  // block exclusive scan of the per-thread counts
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(kFull, inc, off);
+            if (lane >= off) inc += y;
+        }
+        __syncthreads();
+        if (lane == 31) s_w[warp] = inc;
+        __syncthreads();
+        int wbase = 0, step = 0;
+        for (int w = 0; w < nw; w++) {
+            if (w < warp) wbase += s_w[w];
+            step += s_w[w];
+        }
+        unsigned long long off = run + wbase + inc - mine;
+#pragma unroll
+        for (int k = 0; k < E; k++)
+            if (bits & (1u << k)) left[off++] = (int32_t)(v0 + k);
+        run += step;
+    }
+}
+
+// Phase 3 (Q19) on the leftover list, a group of GL lanes per row
+// of at most GL entries: lanes holding the same candidate aggregate find each
+// other (__match_any_sync on (group, aggregate)), so every lane knows its
+// candidate's coupling; the group keeps the best (max coupling, min aggsize,
+// min id) and stores it at the row's list position.  Longer rows (<=
+// kHeavyDeg) go to k_phase3_table, longer ones to k_phase3_heavy.
+template <int GL>
+__global__ void __launch_bounds__(32 * kListWarps) k_phase3_list(const int32_t* __restrict__ left,
+                                                                 const unsigned long long* nleft,
+                                                                 const int64_t* __restrict__ rowptr,
+                                                                 const int32_t* __restrict__ colinds,
+                                                                 const int32_t* __restrict__ labels,
+                                                                 const int32_t* __restrict__ size,
+                                                                 int32_t* __restrict__ choice,
+                                                                 int32_t* __restrict__ longq, int* longq_cnt,
+                                                                 int32_t* __restrict__ heavy, int* heavy_cnt) {
+    // U list entries per group per trip, their loads interleaved (the chain
+    // list -> rowptr -> colinds -> labels -> size is latency bound)
+    constexpr int U = 1;  // 2 / 4 measured slower (C3 phase 3: 435 us at 1, 514 us at 4)
+    const ListIdx<GL> li;
+    const int64_t cnt = (int64_t)*nleft;
+    const int64_t wfirst = li.first - (int64_t)((threadIdx.x & 31) / GL);
+    const int64_t trips = cnt > wfirst ? (cnt - wfirst + li.stride * U - 1) / (li.stride * U) : 0;
+    const uint64_t gtag = (uint64_t)(threadIdx.x / GL) << 32;
+    for (int64_t t = 0; t < trips; t++) {
+        int64_t i[U], s[U], e[U];
+        int32_t v[U], a[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            i[u] = li.first + (t * U + u) * li.stride;
+            v[u] = i[u] < cnt ? left[i[u]] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            s[u] = 0;
+            e[u] = 0;
+            if (v[u] >= 0) {
+                s[u] = rowptr[v[u]];
+                e[u] = rowptr[v[u] + 1];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            a[u] = -1;
+            if (v[u] >= 0 && e[u] - s[u] <= GL && s[u] + li.sub < e[u]) {
+                const int32_t w = colinds[s[u] + li.sub];
+                a[u] = (w != v[u]) ? w : -1;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) a[u] = a[u] >= 0 ? labels[a[u]] : -1;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const bool short_row = v[u] >= 0 && e[u] - s[u] <= GL;
+            if (v[u] >= 0 && !short_row && li.sub == 0) {
+                if (e[u] - s[u] > kHeavyDeg) heavy[atomicAdd(heavy_cnt, 1)] = (int32_t)i[u];
+                else longq[atomicAdd(longq_cnt, 1)] = (int32_t)i[u];
+            }
+            const unsigned grp = __match_any_sync(kFull, gtag | (uint32_t)a[u]);
+            int bc = 0, bs = 0, ba = -1;
+            if (a[u] >= 0) {
+                bc = __popc(grp);
+                bs = size[a[u]];
+                ba = a[u];
+            }
+            group_best<GL>(bc, bs, ba);
+            if (short_row && li.sub == 0) choice[i[u]] = ba;  // -1: no candidate (impossible)
+        }
+    }
+}
+
+// Phase 3 for the longer listed rows: a warp per row, the couplings of its
+// candidate aggregates counted in the warp's shared-memory table (match
+// groups of each 32-entry chunk add at once); a table overflow -> heavy.
+constexpr int kP3Slots = 128;
+__global__ void __launch_bounds__(32 * kListWarps) k_phase3_table(const int32_t* __restrict__ left,
+                                                                  const int32_t* __restrict__ longq, const int* longq_cnt,
+                                                                  const int64_t* __restrict__ rowptr,
+                                                                  const int32_t* __restrict__ colinds,
+                                                                  const int32_t* __restrict__ labels,
+                                                                  const int32_t* __restrict__ size,
+                                                                  int32_t* __restrict__ choice,
+                                                                  int32_t* __restrict__ heavy, int* heavy_cnt) {
+    __shared__ int32_t tkey[kListWarps][kP3Slots];
+    __shared__ int32_t tcnt[kListWarps][kP3Slots];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    int32_t* key = tkey[wib];
+    int32_t* cnt = tcnt[wib];
+    const int64_t m = *longq_cnt;
+    for (int64_t q = (int64_t)blockIdx.x * kListWarps + wib; q < m; q += (int64_t)gridDim.x * kListWarps) {
+        const int32_t i = longq[q];
+        const int32_t v = left[i];
+        const int64_t s = rowptr[v], e = rowptr[v + 1];
+#pragma unroll
+        for (int k = 0; k < kP3Slots / 32; k++) {
+            key[lane + 32 * k] = -1;
+            cnt[lane + 32 * k] = 0;
+        }
+        __syncwarp();
+        bool over = false;
+        for (int64_t j0 = s; j0 < e; j0 += 32) {
+            const int64_t j = j0 + lane;
+            int32_t a = -1;
+            if (j < e) {
+                const int32_t w = colinds[j];
+                a = (w != v) ? labels[w] : -1;
+            }
+            const unsigned grp = __match_any_sync(kFull, a);
+            if (a >= 0 && lane == __ffs(grp) - 1) {
+                unsigned h = ((unsigned)a * 2654435761u) % kP3Slots;
+                bool placed = false;
+                for (int probe = 0; probe < kP3Slots; probe++) {
+                    const int32_t k = atomicCAS(&key[h], -1, a);
+                    if (k == -1 || k == a) {
+                        atomicAdd(&cnt[h], __popc(grp));
+                        placed = true;
+                        break;
+                    }
+                    h = (h + 1) % kP3Slots;
+                }
+                over |= !placed;
+            }
+        }
+        __syncwarp();
+        int bc = 0, bs = 0, ba = -1;
+        if (!__any_sync(kFull, over)) {  // (uniform)
+#pragma unroll
+            for (int k = 0; k < kP3Slots / 32; k++) {
+                const int32_t a = key[lane + 32 * k];
+                if (a >= 0) {
+                    const int c = cnt[lane + 32 * k], sz = size[a];
+                    if (better(c, sz, a, bc, bs, ba)) { bc = c; bs = sz; ba = a; }
+                }
+            }
+        }
+        __syncwarp();
+        const bool any_over = __any_sync(kFull, over);
+        group_best<32>(bc, bs, ba);
+        if (lane == 0) {
+            if (any_over) heavy[atomicAdd(heavy_cnt, 1)] = i;
+            else choice[i] = ba;
+        }
+    }
+}
+
+// ---- the induced subgraph of the unaggregated vertices (phase 2, Q15)
+// act[v] = (labels[v] < 0)
+__global__ void k_active_flags(int64_t n, const int32_t* __restrict__ labels, uint8_t* __restrict__ act) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        act[v] = labels[v] < 0;
+}
+// row i of the subgraph = vertex gid[i]: its active neighbours (self included if stored)
+template <int GL>
+__global__ void __launch_bounds__(32 * kListWarps) k_sub_len(const int32_t* __restrict__ gid, const int32_t* d_m,
+                                                             const int64_t* __restrict__ rowptr,
+                                                             const int32_t* __restrict__ colinds,
+                                                             const uint8_t* __restrict__ act,
+                                                             int64_t* __restrict__ len) {
+    const ListIdx<GL> li;
+    const int64_t cnt = *d_m, trips = warp_trips(li, cnt);
+    for (int64_t t = 0; t < trips; t++) {
+        const int64_t i = li.first + t * li.stride;
+        int c = 0;
+        if (i < cnt) {
+            const int32_t v = gid[i];
+            const int64_t s = rowptr[v], e = rowptr[v + 1];
+            for (int64_t j = s + li.sub; j < e; j += GL) c += act[colinds[j]];
+        }
+        c = group_sum<GL>(c);
+        if (i < cnt && li.sub == 0) len[i] = c;
+    }
+}
+// the subgraph's colinds: inv[w] of the active neighbours, in row order
+template <int GL>
+__global__ void __launch_bounds__(32 * kListWarps) k_sub_fill(const int32_t* __restrict__ gid, const int32_t* d_m,
+                                                              const int64_t* __restrict__ rowptr,
+                                                              const int32_t* __restrict__ colinds,
+                                                              const uint8_t* __restrict__ act,
+                                                              const int32_t* __restrict__ inv,
+                                                              const int64_t* __restrict__ srow,
+                                                              int32_t* __restrict__ scol) {
+    const ListIdx<GL> li;
+    const int64_t cnt = *d_m, trips = warp_trips(li, cnt);
+    const int gbase_lane = (threadIdx.x & 31) & ~(GL - 1);
+    const unsigned gmask = (GL == 32 ? kFull : ((1u << GL) - 1u)) << gbase_lane;
+    for (int64_t t = 0; t < trips; t++) {
+        const int64_t i = li.first + t * li.stride;
+        const bool ok = i < cnt;
+        int64_t s = 0, e = 0, o = 0;
+        if (ok) {
+            const int32_t v = gid[i];
+            s = rowptr[v];
+            e = rowptr[v + 1];
+            o = srow[i];
+        }
+        // the group's lanes walk the row in strides of GL; each step's
+        // active entries are placed by their rank among the group's lanes
+        const int64_t steps = (e - s + GL - 1) / GL;
+        int64_t maxsteps = steps;  // warp-wide: the ballots below need every lane
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const int64_t y = __shfl_xor_sync(kFull, maxsteps, off);
+            maxsteps = y > maxsteps ? y : maxsteps;
+        }
+        for (int64_t k = 0; k < maxsteps; k++) {
+            const int64_t j = s + k * GL + li.sub;
+            int32_t w = -1;
+            if (j < e) w = colinds[j];
+            const bool a = w >= 0 && act[w];
+            const unsigned ball = __ballot_sync(kFull, a) & gmask;
+            if (a) scol[o + __popc(ball & lanemask_lt())] = inv[w];
+            o += __popc(ball);
+        }
+    }
+}
+// in_set of the whole graph from the subgraph's (inactive vertices: 0)
+__global__ void k_scatter_in(const int32_t* __restrict__ gid, const int32_t* d_m, const uint8_t* __restrict__ in_sub,
+                             uint8_t* __restrict__ in_full) {
+    const int64_t m = *d_m;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        in_full[gid[i]] = in_sub[i];
+}
+
+// choices -> labels (after every phase-3 read of the frozen labels)
+__global__ void k_scatter_choice(const int32_t* __restrict__ left, const unsigned long long* nleft,
+                                 const int32_t* __restrict__ choice, int32_t* __restrict__ labels, int* err) {
+    const int64_t m = (int64_t)*nleft;
+    int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t a = choice[i];
+        if (a < 0) bad = 1;  // impossible by maximality of M1 (Q20)
+        else labels[left[i]] = a;
+    }
+    if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(err, kErrNoCandidate);
+}
+
 }  // namespace mis2k
 
 namespace mis2h {
@@ -376,7 +805,9 @@ using namespace mis2k;
 struct AggWs {
     Mis2Ws mis;
     uint8_t *in1, *in2, *acc;
-    int32_t *rid, *aid, *tent, *size, *heavy;
+    int32_t *rid, *aid, *tent, *size, *heavy, *left, *longq;
+    int64_t *slen, *srow;  // induced subgraph of phase 2: row lengths, row pointers
+    int32_t* scol;         // its colinds (<= nnz)
     void* scan_tmp;
     long long* scal;  // device scalars
 };
@@ -391,7 +822,12 @@ static void carve_agg(Carve& c, int64_t n, int64_t nnz, int max_warps, AggWs* w)
     w->tent = c.take<int32_t>((size_t)n + 1);
     w->size = c.take<int32_t>((size_t)n + 1);
     w->heavy = c.take<int32_t>((size_t)n + 1);
-    w->scan_tmp = c.take<char>(scan_ws_bytes(n));
+    w->left = c.take<int32_t>((size_t)n + 1);
+    w->longq = c.take<int32_t>((size_t)n + 1);
+    w->slen = c.take<int64_t>((size_t)n + 1);
+    w->srow = c.take<int64_t>((size_t)n + 2);
+    w->scol = c.take<int32_t>((size_t)nnz + 1);
+    w->scan_tmp = c.take<char>(std::max(scan_ws_bytes(n), scan64_ws_bytes(n)));
     w->scal = c.take<long long>(32);
 }
 
@@ -522,10 +958,32 @@ int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int6
     // ---- phase 1: M1 = MIS2(G)
     MIS2_TRY(run_mis2(g, o, nullptr, w.in1, (int64_t*)&w.scal[kCount1], &s32[2 * kIters1],
                       &s32[2 * kStatus1], ist1, w.mis, s));
-    MIS2_TRY(scan_flags(w.in1, n, w.rid, &s32[2 * kN1], w.scan_tmp, s));
-    rows(G, n, di.sms, s, 1, g, w, labels, roots);
-
     const bool basic = (o.flags & MIS2_FLAG_BASIC) != 0;
+    const unsigned lgrid = (unsigned)(di.sms * 8);  // list kernels: 8 warps per block
+    // lanes per list entry: the average row length rounded up to a power of
+    // two in [4, 32] (short rows: several entries per warp)
+    const double avg = n > 0 ? (double)g.nnz / (double)n : 0.0;
+    const int GL = avg <= 4.0 ? 4 : (avg <= 8.0 ? 8 : (avg <= 16.0 ? 16 : 32));
+#define LIST_DISPATCH(gl, CALL)                             \
+    switch (gl) {                                           \
+        case 4: { constexpr int GLL = 4; CALL; } break;     \
+        case 8: { constexpr int GLL = 8; CALL; } break;     \
+        case 16: { constexpr int GLL = 16; CALL; } break;   \
+        default: { constexpr int GLL = 32; CALL; } break;   \
+    }
+    int32_t* rl = roots ? roots : w.rid;            // roots in aggregate order (phase 1, then phase 2)
+    if (basic) {
+        MIS2_TRY(scan_flags(w.in1, n, w.rid, &s32[2 * kN1], w.scan_tmp, s));
+        rows(G, n, di.sms, s, 1, g, w, labels, roots);
+    } else {
+        // roots listed in ascending vertex order = their aggregate ids (Q18); they push them
+        MIS2_TRY(scan_flags_list(w.in1, n, nullptr, nullptr, rl, nullptr, &s32[2 * kN1], w.scan_tmp, s));
+        MIS2_CUDA_TRY(cudaMemsetAsync(labels, 0xff, sizeof(int32_t) * (size_t)n, s));
+        LIST_DISPATCH(GL, (k_push_roots<GLL><<<lgrid, 32 * kListWarps, 0, s>>>(rl, &s32[2 * kN1], g.rowptr, g.colinds,
+                                                                            labels, w.size, &s32[2 * kErr])));
+        count_launch();
+    }
+
     if (basic) {
         // ---- Alg. 2: every leftover joins an adjacent phase-1 aggregate
         MIS2_CUDA_TRY(cudaMemsetAsync(w.size, 0, sizeof(int32_t) * ((size_t)n + 1), s));
@@ -541,26 +999,93 @@ int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int6
     } else {
 
     // ---- phase 2: M2 = MIS2(G \ aggregated) on the same ids / seed (Q15)
-    MIS2_TRY(run_mis2(g, o, labels, w.in2, (int64_t*)&w.scal[kCount2], &s32[2 * kIters2],
-                      &s32[2 * kStatus2], ist2, w.mis, s));
-    rows(G, n, di.sms, s, 2, g, w, labels, roots);
-    MIS2_TRY(scan_flags(w.acc, n, w.aid, &s32[2 * kN2], w.scan_tmp, s));
-    rows(G, n, di.sms, s, 3, g, w, labels, roots);
-
-    // ---- phase 3: frozen tentative labels, max coupling / min size / min id
-    MIS2_CUDA_TRY(cudaMemsetAsync(w.size, 0, sizeof(int32_t) * ((size_t)n + 1), s));
+    // Large graphs: on the induced subgraph of the unaggregated vertices
+    // (below); small ones: the masked call on G (the build's two host reads
+    // of the subgraph's size cost more than the smaller passes save: C2
+    // 0.88 ms masked, 0.97 ms on the subgraph; C3 11.1 -> 10.0 ms, C5 14.8
+    // -> 14.0 ms).  MIS2_AGG_SUB=0/1 forces (measurement knob).
+    bool use_sub = g.nnz >= (int64_t)1 << 26;
+    if (const char* e = getenv("MIS2_AGG_SUB")) use_sub = atoi(e) != 0;
+    if (!use_sub) {
+        MIS2_TRY(run_mis2(g, o, labels, w.in2, (int64_t*)&w.scal[kCount2], &s32[2 * kIters2], &s32[2 * kStatus2],
+                          ist2, w.mis, s));
+    } else {
+    // The induced subgraph of the unaggregated vertices itself: its
+    // rows hold only unaggregated neighbours (C2: 44% of the rows, 17% of
+    // the entries), row i is vertex gid[i] (aid), whose original id the
+    // hash, the packing width b (of the whole graph) and the M id fields use
+    // -- the same iteration as the masked call on G, on less data.
     {
         int64_t blocks = (n + kBlock - 1) / kBlock;
         if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
         if (blocks < 1) blocks = 1;
-        k_tent_size<<<(unsigned)blocks, kBlock, 0, s>>>(n, labels, w.tent, w.size,
-                                                        (unsigned long long*)&w.scal[kLeft]);
+        k_active_flags<<<(unsigned)blocks, kBlock, 0, s>>>(n, labels, w.acc);
         count_launch();
     }
-    rows(G, n, di.sms, s, 4, g, w, labels, roots);
-    k_phase3_heavy<<<di.sms * 4, kBlock, 0, s>>>(g.rowptr, g.colinds, w.tent, w.size, labels, w.heavy,
-                                                &s32[2 * kHeavyCnt], &s32[2 * kErr]);
+    int32_t* gid = w.aid;   // rows of the subgraph -> vertices (ascending)
+    int32_t* inv = w.rid;   // vertices -> rows (active ones); w.rid is free until phase 2's pushes
+    int32_t* d_m = &s32[2 * kN2 + 1];
+    MIS2_TRY(scan_flags_list(w.acc, n, nullptr, inv, gid, nullptr, d_m, w.scan_tmp, s));
+    // the subgraph build is latency bound: several rows per warp (GL <= 8)
+    const int GS = GL < 8 ? GL : 8;
+    LIST_DISPATCH(GS, (k_sub_len<GLL><<<lgrid, 32 * kListWarps, 0, s>>>(gid, d_m, g.rowptr, g.colinds, w.acc,
+                                                                      w.slen)));
     count_launch();
+    int64_t hm[2] = {0, 0};
+    {
+        int32_t m32 = 0;
+        MIS2_CUDA_TRY(cudaMemcpyAsync(&m32, d_m, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        MIS2_CUDA_TRY(cudaStreamSynchronize(s));  // the subgraph's size sizes its launches
+        hm[0] = m32;
+    }
+    MIS2_TRY(scan_counts64(w.slen, hm[0], w.srow, w.scan_tmp, s));
+    LIST_DISPATCH(GS, (k_sub_fill<GLL><<<lgrid, 32 * kListWarps, 0, s>>>(gid, d_m, g.rowptr, g.colinds, w.acc, inv,
+                                                                       w.srow, w.scol)));
+    count_launch();
+    MIS2_CUDA_TRY(cudaMemcpyAsync(&hm[1], w.srow + hm[0], sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+    {
+        mis2_graph gs{hm[0], hm[1], w.srow, w.scol};
+        const SubGraph sub{gid, inv, n};
+        MIS2_TRY(run_mis2(gs, o, nullptr, w.in1, (int64_t*)&w.scal[kCount2], &s32[2 * kIters2], &s32[2 * kStatus2],
+                          ist2, w.mis, s, &sub));
+        MIS2_CUDA_TRY(cudaMemsetAsync(w.in2, 0, (size_t)n, s));
+        k_scatter_in<<<(unsigned)(di.sms * 8), kBlock, 0, s>>>(gid, d_m, w.in1, w.in2);
+        count_launch();
+    }
+    }  // use_sub
+    // the phase-2 roots in vertex order (aid), their acceptance (acc, by
+    // list position), the accepted ones in vertex order (tent) -> aggregates
+    // n1, n1 + 1, ...; their sizes come out of the pushes
+    MIS2_TRY(scan_flags_list(w.in2, n, nullptr, nullptr, w.aid, nullptr, &s32[2 * kN2 + 1], w.scan_tmp, s));
+    LIST_DISPATCH(GL, (k_accept_list<GLL><<<lgrid, 32 * kListWarps, 0, s>>>(w.aid, &s32[2 * kN2 + 1], g.rowptr,
+                                                                          g.colinds, labels, w.acc)));
+    count_launch();
+    MIS2_TRY(scan_flags_list(w.acc, n, &s32[2 * kN2 + 1], nullptr, w.tent, w.aid, &s32[2 * kN2], w.scan_tmp, s));
+    LIST_DISPATCH(GL, (k_push_accepted<GLL><<<lgrid, 32 * kListWarps, 0, s>>>(w.tent, &s32[2 * kN2], &s32[2 * kN1],
+                                                                            g.rowptr, g.colinds, labels, rl, w.size,
+                                                                            &s32[2 * kErr])));
+    count_launch();
+
+    // ---- phase 3: max coupling / min size / min id over the frozen labels;
+    // choices by leftover-list position (tent), scattered at the end
+    {
+        int64_t blocks = (n + kBlock - 1) / kBlock;
+        if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
+        if (blocks < 1) blocks = 1;
+        k_leftovers<<<(unsigned)(di.sms * 4), kBlock, 0, s>>>(n, labels, w.left, (unsigned long long*)&w.scal[kLeft]);
+        count_launch();
+    }
+    const unsigned long long* nleft = (const unsigned long long*)&w.scal[kLeft];
+    LIST_DISPATCH(GL, (k_phase3_list<GLL><<<lgrid, 32 * kListWarps, 0, s>>>(
+                          w.left, nleft, g.rowptr, g.colinds, labels, w.size, w.tent, w.longq, &s32[2 * kHeavyCnt + 1],
+                          w.heavy, &s32[2 * kHeavyCnt])));
+    k_phase3_table<<<lgrid, 32 * kListWarps, 0, s>>>(w.left, w.longq, &s32[2 * kHeavyCnt + 1], g.rowptr, g.colinds,
+                                                     labels, w.size, w.tent, w.heavy, &s32[2 * kHeavyCnt]);
+    k_phase3_heavy<<<di.sms * 4, kBlock, 0, s>>>(g.rowptr, g.colinds, labels, w.size, labels, w.heavy,
+                                                &s32[2 * kHeavyCnt], &s32[2 * kErr], w.left, w.tent);
+    k_scatter_choice<<<(unsigned)(di.sms * 8), kBlock, 0, s>>>(w.left, nleft, w.tent, labels, &s32[2 * kErr]);
+    count_launch(4);
     k_finish<<<1, 1, 0, s>>>(&s32[2 * kN1], &s32[2 * kN2], (int64_t*)&w.scal[kNa]);
     count_launch();
     }  // Alg. 3

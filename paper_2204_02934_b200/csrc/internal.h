@@ -80,9 +80,17 @@ int max_coop_warps(const DeviceInfo& d);
 // Runs Alg. 1 on the device.  labels != NULL restricts to {v : labels[v] < 0}
 // (phase 2 of Alg. 3, reading Q15).  Writes in_set, *d_count, *d_iters,
 // *d_status (device).  stats_host optional (synchronises).
+// sub != NULL: g is an induced subgraph whose row v is vertex gid[v] of a
+// graph of n_full vertices (hash ids, the packing width b and the M id
+// fields use the original ids; inv maps them back to rows)
+struct SubGraph {
+    const int32_t* gid;
+    const int32_t* inv;
+    int64_t n_full;
+};
 int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uint8_t* in_set,
              int64_t* d_count, int32_t* d_iters, int32_t* d_status, int64_t* stats_host,
-             const Mis2Ws& w, cudaStream_t s);
+             const Mis2Ws& w, cudaStream_t s, const SubGraph* sub = nullptr);
 
 int choose_group(int64_t n, int64_t nnz, int requested);
 int max_iters_for(int64_t n, int requested);
@@ -152,6 +160,11 @@ void agg_phase3(int G, int64_t n, const int64_t* rowptr, const int32_t* colinds,
 
 // device-wide exclusive scan of 0/1 (uint8) flags -> int32 prefix, total to *d_total
 size_t scan_ws_bytes(int64_t n);
+// the same over the first min(n, *d_n) flags (d_n: device count or null),
+// also (list non-null) the ordered compaction list[prefix[i]] = map ? map[i]
+// : i of the set flags (prefix may be null)
+int scan_flags_list(const uint8_t* flags, int64_t n, const int32_t* d_n, int32_t* prefix, int32_t* list,
+                    const int32_t* map, int32_t* d_total, void* tmp, cudaStream_t s);
 int scan_flags(const uint8_t* flags, int64_t n, int32_t* prefix, int32_t* d_total, void* tmp,
                cudaStream_t s);
 // int64 exclusive scan of int64 counts (n entries) -> out[n+1]

@@ -261,7 +261,8 @@ int debug_read(void* ws, size_t ws_bytes, int64_t n, long long* out, int64_t cou
 }
 
 int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uint8_t* in_set, int64_t* d_count,
-             int32_t* d_iters, int32_t* d_status, int64_t* stats_host, const Mis2Ws& w, cudaStream_t s) {
+             int32_t* d_iters, int32_t* d_status, int64_t* stats_host, const Mis2Ws& w, cudaStream_t s,
+             const SubGraph* sub) {
     DeviceInfo di;
     MIS2_TRY(device_info(&di));
     if (g.n == 0) {  // empty set, 0 iterations (P5); no kernel touches rowptr (may be NULL)
@@ -278,7 +279,7 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     const int G = choose_group(g.n, g.nnz, o.group);
     const bool timeline = stats_host != nullptr && (o.flags & MIS2_FLAG_TIMELINE);
     const bool stats = stats_host != nullptr && !timeline;
-    const int max_iters = max_iters_for(g.n, o.max_iters);
+    const int max_iters = max_iters_for(sub ? sub->n_full : g.n, o.max_iters);
     if ((stats && max_iters > kStatsMaxIters) || (timeline && 2 * max_iters + 2 > kStatsMaxIters * 6)) {
         set_error("stats/timeline mode supports max_iters <= %d", kStatsMaxIters);
         return MIS2_EINVAL;
@@ -348,6 +349,7 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     if (o.flags & MIS2_FLAG_NO_KEYS) keys = 0;
     if (const char* e = getenv("MIS2_KEYS")) keys = atoi(e);  // measurement knob
     if (o.flags & MIS2_FLAG_WORD32) keys = 0;  // the keys are the words' high halves
+    if (sub) keys = 0;                          // key ties resolve to rows, M holds original ids
     p.K = keys ? w.K : nullptr;
     p.keys_mode = keys == 1 ? 1 : 0;
     for (int i = 0; i < 2; i++) {
@@ -374,11 +376,14 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     }
     p.prio.scheme = o.scheme;
     p.prio.hshift = (o.flags & MIS2_FLAG_WORD32) ? 32 : 0;
-    p.prio.b = bits_for(g.n);
+    const int64_t n_ids = sub ? sub->n_full : g.n;  // b of the whole graph (reading Q15)
+    p.prio.b = bits_for(n_ids);
     p.prio.seed = o.seed;
     p.prio.hi_mask = ~((1ull << p.prio.b) - 1ull);
     p.id_mask = (uint32_t)((1ull << p.prio.b) - 1ull);
-    p.prio.n = g.n;
+    p.prio.n = n_ids;
+    p.gid = sub ? sub->gid : nullptr;
+    p.inv = sub ? sub->inv : nullptr;
     p.l2_keep = l2_keep_for(g.nnz);
     // cyclic row ownership (mis2_kernel.cuh Rows); MIS2_CYCLIC=0: contiguous
     // ranges (measurement knob, results identical)

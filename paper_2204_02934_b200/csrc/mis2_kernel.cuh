@@ -103,6 +103,12 @@ constexpr uint32_t kPending = 1u;  // M of an active vertex before its first col
 struct MisParams {
     int64_t n;       // rows processed (all of them, or the owned rows of a partition)
     int64_t gbase;   // global id of local row 0 (0 on one GPU): hashes and ids use gbase + v
+    // an induced subgraph (the masked MIS-2 of Alg. 3 phase 2, run on the
+    // unaggregated vertices only): row v is vertex gid[v] of the whole graph,
+    // whose id the hash and the packed words use (reading Q15: original ids);
+    // inv maps those ids back to rows (push form).  Null: gbase + v.
+    const int32_t* gid;
+    const int32_t* inv;
     int64_t nnz;
     const int64_t* __restrict__ rowptr;
     const int32_t* __restrict__ colinds;
@@ -133,6 +139,13 @@ struct MisParams {
     int32_t* d_iters;
     int32_t* d_status;
 };
+
+__device__ __forceinline__ int64_t gid_of(const MisParams& p, int64_t v) {
+    return p.gid ? (int64_t)p.gid[v] : p.gbase + v;
+}
+__device__ __forceinline__ int64_t row_of_id(const MisParams& p, int64_t id) {
+    return p.inv ? (int64_t)p.inv[id] : id - p.gbase;
+}
 
 // ------------------------------------------------------------ row ownership
 // The rows of block b as "runs" of at most rpb consecutive rows (rpb = the
@@ -479,7 +492,7 @@ __device__ __forceinline__ bool decide_write(const MisParams& p, int64_t v, int 
         set_T(p, v, kIN);
         return false;
     }
-    set_T(p, v, p.prio.word(it + 1, fi_next, p.gbase + v));  // fused Refresh Row
+    set_T(p, v, p.prio.word(it + 1, fi_next, gid_of(p, v)));  // fused Refresh Row
     return true;
 }
 
@@ -547,7 +560,7 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
             uint64_t m = (act && sub == 0) ? tv : kOUT;  // closed neighbourhood (Q1)
             if (act && len > 0) {
                 if (PUSH && it == 0 && p.labels) {
-                    m = row_min_deg<GG>(p.T, x, len, sub, m, p.gbase + v, dc);
+                    m = row_min_deg<GG>(p.T, x, len, sub, m, v, dc);  // self = this row (local index)
                 } else {
                     m = row_min<GG>(p.T, x, len, sub, m);
                 }
@@ -573,7 +586,7 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
             const uint32_t key = cnt_me ? mf - 1u : (0x80000000u | (threadIdx.x & 31));
             const unsigned grp = __match_any_sync(kFull, key);
             if (cnt_me && (threadIdx.x & 31) == __ffs(grp) - 1)
-                atomicAdd(&p.cnt[(int64_t)key - p.gbase], (uint32_t)__popc(grp));
+                atomicAdd(&p.cnt[row_of_id(p, (int64_t)key)], (uint32_t)__popc(grp));
             if (it == 0 && p.labels) {
                 dc = group_sum<GG>(dc);
                 if (act && sub == 0) p.degc[v] = (uint32_t)dc + 1u;
@@ -585,7 +598,7 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
         }
     } else {
         int any_out = 0, all_eq = 1;
-        const uint32_t vid1 = (uint32_t)(p.gbase + v) + 1u;
+        const uint32_t vid1 = (uint32_t)gid_of(p, v) + 1u;
         if (act) {
             if (sub == 0) decide_acc(p.M[v], vid1, any_out, all_eq);
             if (len > 0) row_decide<GG>(p.M, x, len, sub, vid1, any_out, all_eq);
@@ -697,7 +710,7 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
                 for (int64_t j = tid; j < len; j += NT) p.oflag[x[j]] = 1;
                 if (tid == 0) p.oflag[v] = 1;
             } else if (tid == 0) {
-                atomicAdd(&p.cnt[(int64_t)(mf - 1u) - p.gbase], 1u);
+                atomicAdd(&p.cnt[row_of_id(p, (int64_t)(mf - 1u))], 1u);
             }
             if (count_deg && tid == 0) p.degc[v] = (uint32_t)dc + 1u;
         }
@@ -706,7 +719,7 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
             keep = mf != kM_OUT;
         }
     } else {
-        const uint32_t vid1 = (uint32_t)(p.gbase + v) + 1u;
+        const uint32_t vid1 = (uint32_t)gid_of(p, v) + 1u;
         int any_out = 0, all_eq = 1;
         if (tid == 0) decide_acc(p.M[v], vid1, any_out, all_eq);
         for (int64_t j = tid; j < len; j += (int64_t)NT * 8) {
@@ -1131,7 +1144,7 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, const Rows&
                 } else if (fl[u]) set_T(p, v, kOUT);
                 else if (in) set_T(p, v, kIN);
                 else {
-                    set_T(p, v, p.prio.word(it + 1, fi_next, p.gbase + v));
+                    set_T(p, v, p.prio.word(it + 1, fi_next, gid_of(p, v)));
                     keep = true;
                 }
                 if (STATS) {
@@ -1160,7 +1173,7 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, const Rows&
                 if (found) {
                     set_T(p, v, kIN);
                 } else {
-                    set_T(p, v, p.prio.word(it + 1, fi_next, p.gbase + v));
+                    set_T(p, v, p.prio.word(it + 1, fi_next, gid_of(p, v)));
                     keep = true;
                 }
             }
@@ -1225,7 +1238,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
             const int64_t v = in ? rows.row_at(base + t) : 0;
             const bool act = in && (p.labels ? (p.labels[v] < 0) : true);
             if (in) {
-                set_T(p, v, act ? p.prio.word(0, fi0, p.gbase + v) : kOUT);
+                set_T(p, v, act ? p.prio.word(0, fi0, gid_of(p, v)) : kOUT);
                 p.M[v] = act ? kPending : 0u;  // 0 = inactive sentinel (reading Q15)
                 p.oflag[v] = 0;
                 p.cnt[v] = 0u;

@@ -43,8 +43,16 @@ __device__ __forceinline__ T block_exclusive_scan(T x, T* s_warp, T* total) {
     return res;
 }
 
-__global__ void k_tile_count8(const uint8_t* __restrict__ f, int64_t n, int64_t* __restrict__ tsum) {
+__device__ __forceinline__ int64_t eff_n(int64_t n, const int32_t* d_n) {
+    if (!d_n) return n;
+    const int64_t m = *d_n;
+    return m < n ? m : n;
+}
+
+__global__ void k_tile_count8(const uint8_t* __restrict__ f, int64_t n, int64_t* __restrict__ tsum,
+                              const int32_t* __restrict__ d_n) {
     __shared__ int64_t s[33];
+    n = eff_n(n, d_n);
     const int64_t base = (int64_t)blockIdx.x * kTile8 + (int64_t)threadIdx.x * kScanItems8;
     int64_t c = 0;
 #pragma unroll
@@ -70,9 +78,13 @@ __global__ void k_scan_tiles(int64_t* __restrict__ tsum, int64_t ntiles, int64_t
     if (threadIdx.x == 0) *total = carry;
 }
 
+// prefix[i] (if non-null) = number of set flags before i; list[prefix[i]] =
+// (map ? map[i] : i) for every set flag (if non-null): the ordered compaction
 __global__ void k_tile_write8(const uint8_t* __restrict__ f, int64_t n, const int64_t* __restrict__ toff,
-                              int32_t* __restrict__ prefix) {
+                              int32_t* __restrict__ prefix, int32_t* __restrict__ list,
+                              const int32_t* __restrict__ map, const int32_t* __restrict__ d_n) {
     __shared__ int64_t s[33];
+    n = eff_n(n, d_n);
     const int64_t base = (int64_t)blockIdx.x * kTile8 + (int64_t)threadIdx.x * kScanItems8;
     uint8_t v[kScanItems8];
     int64_t c = 0;
@@ -84,7 +96,10 @@ __global__ void k_tile_write8(const uint8_t* __restrict__ f, int64_t n, const in
     int64_t run = toff[blockIdx.x] + block_exclusive_scan<int64_t>(c, s, nullptr);
 #pragma unroll
     for (int i = 0; i < kScanItems8; i++) {
-        if (base + i < n) prefix[base + i] = (int32_t)run;
+        if (base + i < n) {
+            if (prefix) prefix[base + i] = (int32_t)run;
+            if (list && v[i]) list[run] = map ? map[base + i] : (int32_t)(base + i);
+        }
         run += v[i];
     }
 }
@@ -134,17 +149,22 @@ size_t scan_ws_bytes(int64_t n) {
 }
 
 int scan_flags(const uint8_t* flags, int64_t n, int32_t* prefix, int32_t* d_total, void* tmp, cudaStream_t s) {
+    return scan_flags_list(flags, n, nullptr, prefix, nullptr, nullptr, d_total, tmp, s);
+}
+
+int scan_flags_list(const uint8_t* flags, int64_t n, const int32_t* d_n, int32_t* prefix, int32_t* list,
+                    const int32_t* map, int32_t* d_total, void* tmp, cudaStream_t s) {
     const int64_t tiles = (n + kTile8 - 1) / kTile8;
     int64_t* tsum = (int64_t*)tmp;
     int64_t* tot = tsum + tiles + 1;
     if (tiles > 0) {
-        k_tile_count8<<<(unsigned)tiles, kScanThreads, 0, s>>>(flags, n, tsum);
+        k_tile_count8<<<(unsigned)tiles, kScanThreads, 0, s>>>(flags, n, tsum, d_n);
         count_launch();
     }
     k_scan_tiles<<<1, 1024, 0, s>>>(tsum, tiles, tot);
     count_launch();
     if (tiles > 0) {
-        k_tile_write8<<<(unsigned)tiles, kScanThreads, 0, s>>>(flags, n, tsum, prefix);
+        k_tile_write8<<<(unsigned)tiles, kScanThreads, 0, s>>>(flags, n, tsum, prefix, list, map, d_n);
         count_launch();
     }
     k_total_to_i32<<<1, 1, 0, s>>>(tot, d_total);
