@@ -675,3 +675,15 @@ def test_nccl_transport_world1():
         orow, ocol = O.coarsen(g.rowptr, g.colinds, oa.labels, oa.num_aggs)
         assert np.array_equal(crow.cpu().numpy(), orow) and np.array_equal(ccol.cpu().numpy(), ocol)
         c.close()
+
+
+@pytest.mark.parametrize("sub", ["0", "1"])
+def test_aggregate_phase2_forms(sub, monkeypatch):
+    """Phase 2's MIS-2 as the masked call on G and on the induced subgraph of
+    the unaggregated vertices (row = vertex gid[row], original ids in the
+    hash and the packing): identical labels, roots and statistics."""
+    monkeypatch.setenv("MIS2_AGG_SUB", sub)
+    gs = small_graphs(30, 2700) + [G.laplace3d_7pt(20), G.kronecker(11), G.elasticity3d(6), G.config_graph(1)]
+    for g in gs:
+        check_agg(g)
+        check_agg(g, seed=3, decide="push")
