@@ -385,6 +385,32 @@ __device__ __forceinline__ uint64_t row_min(const uint64_t* __restrict__ T, cons
     return m;
 }
 
+// The same, also telling whether the row holds its own vertex (a stored
+// diagonal, Q23): |N[v]| = len + 1 - self for the push-form Decide of an
+// unmasked call (one compare per entry; counting T_w != OUT as below costs
+// more: C2 column pass 0 ~8 us)
+template <int G>
+__device__ __forceinline__ uint64_t row_min_self(const uint64_t* __restrict__ T, const int32_t* x, int len, int sub,
+                                                 uint64_t m, int32_t self, int& has) {
+    constexpr int B = gather_batch<G>();
+    const int last = len - 1;
+    for (int j = sub; j < len; j += B * G) {
+        uint64_t tt[B];
+        int32_t ww[B];
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            ww[q] = x[min(j + q * G, last)];
+            tt[q] = T[ww[q]];
+        }
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            m = tt[q] < m ? tt[q] : m;
+            has |= ww[q] == self;
+        }
+    }
+    return m;
+}
+
 // The same, also counting the entries w != self with T_w != OUT (iteration 0:
 // exactly the active neighbours) for the push-form Decide.  Clamped repeats
 // are not counted.
@@ -420,7 +446,7 @@ __device__ __forceinline__ uint64_t key_lo(uint32_t k, uint32_t w) { return ((ui
 __device__ __forceinline__ uint64_t key_hi(uint32_t k, uint32_t w) { return ((uint64_t)k << 32) | (~w); }
 template <int G>
 __device__ __forceinline__ void row_min_keys(const uint32_t* __restrict__ K, const int32_t* x, int len, int sub,
-                                             uint64_t& k1, uint64_t& k2) {
+                                             uint64_t& k1, uint64_t& k2, int32_t self = -1, int* has = nullptr) {
     constexpr int B = gather_batch<G>();
     const int last = len - 1;
     for (int j = sub; j < len; j += B * G) {
@@ -436,8 +462,9 @@ __device__ __forceinline__ void row_min_keys(const uint32_t* __restrict__ K, con
             const uint64_t a = key_lo(kk[q], (uint32_t)ww[q]), b = key_hi(kk[q], (uint32_t)ww[q]);
             k1 = a < k1 ? a : k1;
             k2 = b < k2 ? b : k2;
+            if (has) *has |= ww[q] == self;
         }
-        if ((k1 >> 32) == 0u) break;  // an IN neighbour: M is OUT
+        if (!has && (k1 >> 32) == 0u) break;  // an IN neighbour: M is OUT (no IN in iteration 0 anyway)
     }
 }
 
@@ -544,7 +571,10 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
                 k1 = key_lo(kkey(tv), (uint32_t)v);
                 k2 = key_hi(kkey(tv), (uint32_t)v);
             }
-            if (act && len > 0) row_min_keys<GG>(p.K, x, len, sub, k1, k2);
+            if (act && len > 0) {
+                if (PUSH && it == 0) row_min_keys<GG>(p.K, x, len, sub, k1, k2, (int32_t)v, &dc);  // [v in its row]
+                else row_min_keys<GG>(p.K, x, len, sub, k1, k2);
+            }
             k1 = group_min<GG>(k1);
             k2 = group_min<GG>(k2);
             const uint32_t kmin = (uint32_t)(k1 >> 32);
@@ -559,8 +589,10 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
         } else {
             uint64_t m = (act && sub == 0) ? tv : kOUT;  // closed neighbourhood (Q1)
             if (act && len > 0) {
-                if (PUSH && it == 0 && p.labels) {
+                if (PUSH && it == 0 && p.labels) {  // also |N[v] ∩ active| for the push-form Decide
                     m = row_min_deg<GG>(p.T, x, len, sub, m, v, dc);  // self = this row (local index)
+                } else if (PUSH && it == 0) {       // |N[v]| = len + 1 - [v in its own row]
+                    m = row_min_self<GG>(p.T, x, len, sub, m, (int32_t)v, dc);
                 } else {
                     m = row_min<GG>(p.T, x, len, sub, m);
                 }
@@ -587,9 +619,14 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
             const unsigned grp = __match_any_sync(kFull, key);
             if (cnt_me && (threadIdx.x & 31) == __ffs(grp) - 1)
                 atomicAdd(&p.cnt[row_of_id(p, (int64_t)key)], (uint32_t)__popc(grp));
-            if (it == 0 && p.labels) {
-                dc = group_sum<GG>(dc);
-                if (act && sub == 0) p.degc[v] = (uint32_t)dc + 1u;
+            if (it == 0) {  // |N[v] ∩ active| (closed; masked: counted, unmasked: from the row length)
+                if (p.labels) {
+                    dc = group_sum<GG>(dc);
+                    if (act && sub == 0) p.degc[v] = (uint32_t)dc + 1u;
+                } else {
+                    dc = group_or<GG>(dc);
+                    if (act && sub == 0) p.degc[v] = (uint32_t)(len + 1 - (dc ? 1 : 0));
+                }
             }
         }
         if (act && sub == 0) {
@@ -658,10 +695,11 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
     }
     if (PH == 0) {
         const uint64_t tv = p.T[v];
-        const bool count_deg = PUSH && it == 0 && p.labels;
+        const bool count_deg = PUSH && it == 0 && p.labels;  // |N[v] ∩ active| (masked)
+        const bool self_chk = PUSH && it == 0 && !p.labels;  // [v in its own row]: |N[v]| = len + 1 - it
         const bool keys = p.K && s_use_keys && !count_deg;
         uint32_t mf;
-        int dc = 0;
+        int dc = 0, has = 0;
         bool exact = !keys;
         if (keys) {
             uint64_t k1 = tid == 0 ? key_lo(kkey(tv), (uint32_t)v) : ~0ull;
@@ -678,6 +716,7 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
                     const uint64_t a = key_lo(kk[u], (uint32_t)ww[u]), b = key_hi(kk[u], (uint32_t)ww[u]);
                     k1 = a < k1 ? a : k1;
                     k2 = b < k2 ? b : k2;
+                    if (self_chk) has |= (int64_t)ww[u] == v;
                 }
             }
             k1 = nt_min<NT>(sm, k1);
@@ -699,6 +738,7 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
                 for (int u = 0; u < 8; u++) {
                     m = tt[u] < m ? tt[u] : m;
                     if (count_deg) dc += (j + (int64_t)u * NT <= last) & (tt[u] != kOUT) & ((int64_t)ww[u] != v);
+                    if (self_chk) has |= (int64_t)ww[u] == v;
                 }
             }
             m = nt_min<NT>(sm, m);
@@ -712,7 +752,9 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
             } else if (tid == 0) {
                 atomicAdd(&p.cnt[row_of_id(p, (int64_t)(mf - 1u))], 1u);
             }
+            if (self_chk) has = nt_sum<NT>(sm, has) > 0;
             if (count_deg && tid == 0) p.degc[v] = (uint32_t)dc + 1u;
+            if (self_chk && tid == 0) p.degc[v] = (uint32_t)(len + 1 - has);
         }
         if (tid == 0) {
             p.M[v] = mf;
@@ -1048,26 +1090,13 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t se
 // (cnt[v] = degc[v]); else it stays undecided and gets its word of iteration
 // it + 1 (fused Refresh Row).  No neighbour is read.  Dense: all
 // rows of the block range, membership from T_v; sparse: the worklist.
-__device__ __forceinline__ bool row_has(const int32_t* x, int64_t len, int32_t v) {
-    for (int64_t j = 0; j < len; j++)
-        if (x[j] == v) return true;
-    return false;
-}
 template <bool STATS>
 __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, const Rows& rows, const int32_t* lin,
                            int nin, bool dense, int32_t* lout, uint64_t fi_next) {
     const int t = threadIdx.x;
     const unsigned tag = 2u * (unsigned)it + 2u;
     Stat st;
-    // IN candidates whose test needs "is v in its own row": resolved after
-    // the loop, one warp per row (a serial scan inside the loop would stall
-    // its warp once per candidate)
-    int32_t* cand = sm.buf[0];
-    constexpr int kCandCap = 2 * kTileCap;
-    if (t == 0) {
-        sm.cnt = 0;
-        sm.hcount = 0;
-    }
+    if (t == 0) sm.cnt = 0;
     __syncthreads();
     const int64_t total = dense ? rows.count : (int64_t)nin;
     const bool dbg = p.timeline && it == p.dbg_it && 1 == p.dbg_ph && t == 0;
@@ -1081,38 +1110,33 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, const Rows&
         dbuf[0] = gt();
         dbuf[1] = total;
     }
-    // U rows per thread per round, loads batched by dependency level
-    constexpr int U = 4;
+    // U rows per thread per round, loads batched by dependency level.  v is
+    // IN iff every active w in N[v] counted v as its argmin: cnt[v] =
+    // |N[v] ∩ active| = degc[v], counted by the push-form column pass of
+    // iteration 0 (closed neighbourhood; Q23: a stored diagonal is not
+    // counted twice) -- no row is read here.
+    constexpr int U = 8;
     for (int64_t base = 0; base < total; base += (int64_t)kMB * U) {
-        int64_t vv[U];
+        int32_t vv[U];
         uint64_t tv[U];
-        uint32_t c[U];
+        uint32_t c[U], dg[U];
         uint8_t fl[U];
-        int64_t rs[U], re[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int64_t idx = base + u * kMB + t;
-            vv[u] = idx < total ? (dense ? rows.row_at(idx) : (int64_t)lin[rows.seg + idx]) : -1;
+            vv[u] = idx < total ? (int32_t)(dense ? rows.row_at(idx) : (int64_t)lin[rows.seg + idx]) : -1;
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
             tv[u] = kIN;
             fl[u] = 0;
             c[u] = 0;
+            dg[u] = 0;
             if (vv[u] >= 0) {
                 tv[u] = p.T[vv[u]];
                 fl[u] = p.oflag[vv[u]];
                 c[u] = p.cnt[vv[u]];
-            }
-        }
-        // IN candidates of the unmasked call need the row length
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            rs[u] = 0;
-            re[u] = 0;
-            if (vv[u] >= 0 && !p.labels && !fl[u] && c[u] > 0 && tv[u] != kIN && tv[u] != kOUT) {
-                rs[u] = p.rowptr[vv[u]];
-                re[u] = p.rowptr[vv[u] + 1];
+                dg[u] = p.degc[vv[u]];
             }
         }
 #pragma unroll
@@ -1121,28 +1145,8 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, const Rows&
             bool keep = false;
             if (v >= 0 && tv[u] != kIN && tv[u] != kOUT) {
                 if (c[u]) p.cnt[v] = 0u;
-                bool in = false, later = false;
-                if (!fl[u] && c[u] > 0) {
-                    if (p.labels) {
-                        in = c[u] == p.degc[v];  // |N[v] ∩ active| counted by the column pass of iteration 0
-                    } else {                     // all active: |N[v]| = len + 1 - [v in its own row] (Q23)
-                        const int64_t len = re[u] - rs[u];
-                        if ((int64_t)c[u] == len + 1) {
-                            in = true;
-                        } else if ((int64_t)c[u] == len) {
-                            const int h = atomicAdd(&sm.hcount, 1);
-                            if (h < kCandCap) {
-                                cand[h] = (int32_t)v;
-                                later = true;
-                            } else {
-                                in = row_has(p.colinds + rs[u], len, (int32_t)v);
-                            }
-                        }
-                    }
-                }
-                if (later) {
-                } else if (fl[u]) set_T(p, v, kOUT);
-                else if (in) set_T(p, v, kIN);
+                if (fl[u]) set_T(p, v, kOUT);
+                else if (c[u] == dg[u]) set_T(p, v, kIN);
                 else {
                     set_T(p, v, p.prio.word(it + 1, fi_next, gid_of(p, v)));
                     keep = true;
@@ -1156,31 +1160,10 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, const Rows&
             append(sm, keep, (int32_t)(v < 0 ? 0 : v), lout, rows.seg);
         }
     }
-    if (dbg) dbuf[2] = gt();
-    __syncthreads();
-    if (dbg) dbuf[5] = gt();
-    {
-        const int nh = min(sm.hcount, kCandCap), lane = t & 31;
-        if (dbg) dbuf[4] = nh;
-        for (int i = t >> 5; i < nh; i += kMW) {
-            const int32_t v = cand[i];
-            const int64_t s = p.rowptr[v], len = p.rowptr[v + 1] - s;
-            bool found = false;
-            for (int64_t j = lane; j < len; j += 32) found |= p.colinds[s + j] == v;
-            found = __any_sync(kFull, found);
-            bool keep = false;
-            if (lane == 0) {
-                if (found) {
-                    set_T(p, v, kIN);
-                } else {
-                    set_T(p, v, p.prio.word(it + 1, fi_next, gid_of(p, v)));
-                    keep = true;
-                }
-            }
-            append(sm, keep, v, lout, rows.seg);
-        }
+    if (dbg) {
+        dbuf[2] = dbuf[3] = dbuf[5] = gt();
+        dbuf[4] = 0;
     }
-    if (dbg) dbuf[3] = gt();
     stats_flush<STATS>(p, it, 0, st);
     __syncthreads();
     const int out = sm.cnt;
