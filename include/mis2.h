@@ -255,7 +255,9 @@ int mis2_dist_aggregate(mis2_comm* c, const mis2_opts* o, int32_t* labels, int64
  * on the whole graph -- is REPLICATED on every rank: c_rowptr int64
  * [num_aggs + 1] and c_colinds int32 [cap], device.  Two-call convention as
  * mis2_coarsen (MIS2_ERANGE with *c_nnz set when cap is too small; c_colinds
- * may be NULL).  Scratch is allocated internally.  Collective call. */
+ * may be NULL).  Scratch comes from the communicator's pool: allocated when
+ * a call first needs it (or more of it), kept for later calls, freed with
+ * the graph (mis2_comm_set_graph / mis2_comm_destroy).  Collective call. */
 int mis2_dist_coarsen(mis2_comm* c, const int32_t* labels, int64_t num_aggs, int64_t* c_rowptr,
                       int32_t* c_colinds, int64_t cap, int64_t* c_nnz, void* stream);
 /* rows [lo, hi) and ghost count of local part `part` (NCCL: part 0) */

@@ -213,6 +213,7 @@ struct mis2_comm {
     unsigned int epoch = 0;                // last partition-barrier epoch (advances identically on every rank)
     void* dscratch = nullptr;              // kernel parameter block + results
     int64_t* d_counts = nullptr;           // [2 * (P + 1)] allgather buffers of gather_counts
+    std::vector<std::pair<void*, size_t>> pool;  // coarsening scratch (DevBuf slots), kept across calls
 };
 
 static int dev_alloc(mis2_comm* c, void** p, size_t bytes) {
@@ -227,6 +228,9 @@ static void free_parts(mis2_comm* c) {
     c->ipc_opened.clear();
     for (void* p : c->allocs) cudaFree(p);
     c->allocs.clear();
+    for (auto& e : c->pool)
+        if (e.first) cudaFree(e.first);
+    c->pool.clear();
     c->hp.clear();
     c->dev.clear();
     c->sendT.clear();
@@ -860,29 +864,44 @@ int mis2_dist_mis2(mis2_comm* c, const mis2_opts* o, uint8_t* in_set, int64_t* c
     return dist_mis2_run(c, opt, ins, {}, count, iters, (cudaStream_t)stream);
 }
 
-// RAII device scratch for the coarsening steps
+// device scratch of the coarsening steps: slot k of the communicator's
+// pool, grown when a call needs more and kept for the next call (no
+// allocation per call once the sizes have been seen; freed with the graph)
 struct DevBuf {
     void* p = nullptr;
-    ~DevBuf() { if (p) cudaFree(p); }
+    mis2_comm* c = nullptr;
+    int slot = 0;
+    DevBuf() = default;
+    DevBuf(mis2_comm* cc, int k) : c(cc), slot(k) {}
     int alloc(size_t bytes) {
-        if (cudaMalloc(&p, bytes < 256 ? 256 : bytes) != cudaSuccess) {
-            set_error("cudaMalloc(%zu) failed", bytes);
-            return MIS2_ECUDA;
+        if (bytes < 256) bytes = 256;
+        if ((int)c->pool.size() <= slot) c->pool.resize(slot + 1, {nullptr, 0});
+        auto& e = c->pool[slot];
+        if (e.second < bytes) {
+            if (e.first) cudaFree(e.first);
+            e = {nullptr, 0};
+            if (cudaMalloc(&e.first, bytes) != cudaSuccess) {
+                set_error("cudaMalloc(%zu) failed", bytes);
+                return MIS2_ECUDA;
+            }
+            e.second = bytes;
         }
+        p = e.first;
         return MIS2_OK;
     }
 };
+enum { kSlotWsPart = 0, kSlotSrow, kSlotSlab, kSlotScol, kSlotArow, kSlotPcol, kSlotAcol, kSlotWsMerge, kSlotPart0 };
 
 // coarse rows (per-part edges) of one part: run_coarsen on its rows with the
 // labels of its ghosts filled in (the coarse rows of aggregates it does not
 // touch stay empty)
-static int part_coarse(const PartDev& d, const int32_t* lab, int64_t na, DevBuf& crow, DevBuf& ccol, int64_t& nnz,
-                       cudaStream_t s) {
+static int part_coarse(mis2_comm* c, const PartDev& d, const int32_t* lab, int64_t na, DevBuf& crow, DevBuf& ccol,
+                       int64_t& nnz, cudaStream_t s) {
     mis2_graph gl{d.n_own, d.nnz, d.rowptr, d.colinds};
     mis2_graph gs{std::max<int64_t>(d.n_own, na), d.nnz, nullptr, nullptr};
     size_t wsb = 0;
     MIS2_TRY(run_coarsen(gs, nullptr, 0, nullptr, nullptr, 0, nullptr, nullptr, 0, s, &wsb));
-    DevBuf ws;
+    DevBuf ws(c, kSlotWsPart);
     MIS2_TRY(ws.alloc(wsb));
     MIS2_TRY(crow.alloc(sizeof(int64_t) * (na + 1)));
     int rc = run_coarsen(gl, lab, na, (int64_t*)crow.p, nullptr, 0, &nnz, ws.p, wsb, s, nullptr);
@@ -910,9 +929,13 @@ static int dist_coarsen_run(mis2_comm* c, const std::vector<const int32_t*>& lab
                                           cudaMemcpyDeviceToDevice, s));
     }
     MIS2_TRY(exchange_arr(c, v_lab, 4, s));
-    std::vector<DevBuf> crow(L), ccol(L);
+    std::vector<DevBuf> crow, ccol;
+    for (int i = 0; i < L; i++) {
+        crow.emplace_back(c, kSlotPart0 + 2 * i);
+        ccol.emplace_back(c, kSlotPart0 + 2 * i + 1);
+    }
     std::vector<int64_t> nnz(L, 0);
-    for (int i = 0; i < L; i++) MIS2_TRY(part_coarse(c->dev[i], c->agg[i].lab, na, crow[i], ccol[i], nnz[i], s));
+    for (int i = 0; i < L; i++) MIS2_TRY(part_coarse(c, c->dev[i], c->agg[i].lab, na, crow[i], ccol[i], nnz[i], s));
     // stacked graph: P * na rows
     std::vector<int64_t> all_nnz;
     MIS2_TRY(gather_counts(c, nnz, all_nnz, s));
@@ -922,7 +945,8 @@ static int dist_coarsen_run(mis2_comm* c, const std::vector<const int32_t*>& lab
         mx = std::max(mx, x);
     }
     const int64_t ns = (int64_t)P * na;
-    DevBuf srow, scol, slab, arow, pcol, acol;
+    DevBuf srow(c, kSlotSrow), scol(c, kSlotScol), slab(c, kSlotSlab), arow(c, kSlotArow), pcol(c, kSlotPcol),
+        acol(c, kSlotAcol);
     MIS2_TRY(srow.alloc(sizeof(int64_t) * (ns + 1)));
     MIS2_TRY(slab.alloc(sizeof(int32_t) * (ns + 1)));
     MIS2_TRY(scol.alloc(sizeof(int32_t) * (tot + 1)));
@@ -970,7 +994,7 @@ static int dist_coarsen_run(mis2_comm* c, const std::vector<const int32_t*>& lab
     mis2_graph gm{ns, tot, sr, (const int32_t*)scol.p};
     size_t wsb = 0;
     MIS2_TRY(run_coarsen(gm, nullptr, 0, nullptr, nullptr, 0, nullptr, nullptr, 0, s, &wsb));
-    DevBuf ws;
+    DevBuf ws(c, kSlotWsMerge);
     MIS2_TRY(ws.alloc(wsb));
     return run_coarsen(gm, (const int32_t*)slab.p, na, c_rowptr, c_colinds, cap, c_nnz, ws.p, wsb, s, nullptr);
 }
