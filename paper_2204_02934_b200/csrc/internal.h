@@ -71,6 +71,7 @@ struct Mis2Ws {
     uint32_t* K;        // 32-bit column keys (mis2_core.cu kkey)
     unsigned long long* ctrl;  // [0]=barrier, [1..4]=ring of |wl1| sums, [5]=count, [6]=ticket,
                                // [7]=active, [8]=max degree
+    unsigned long long* maxdeg;  // skew test of run_mis2
     long long* dstats;         // [kStatsMaxIters * 6]
     long long* scal;           // [8] host-visible scalars of mis2()/mis2_host()
 };

@@ -1,6 +1,8 @@
 // mis2_core.cu -- host side of the persistent MIS-2 kernel (mis2_kernel.cuh):
 // launch configuration, workspace carving, the partitioned driver's phase
 // launches.  The kernel templates are instantiated per G in mis2_g<G>.cu.
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -8,6 +10,15 @@
 #include "mis2_kernel.cuh"
 
 namespace mis2k {
+
+// largest row length (skew test of run_mis2)
+__global__ void k_max_degree(int64_t n, const int64_t* __restrict__ rowptr, unsigned long long* out) {
+    int64_t m = 0;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, rowptr[v + 1] - rowptr[v]);
+    m = ~group_min<32>(~(uint64_t)m);
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, (unsigned long long)m);
+}
 
 }  // namespace mis2k
 
@@ -66,6 +77,26 @@ MIS2_DECLARE_G(16)
 MIS2_DECLARE_G(32)
 #undef MIS2_DECLARE_G
 
+// the small-tile copies (mis2_g<G>s.cu), for skewed graphs
+template <int G>
+void* persistent_kernel_small(bool stats, bool push);
+template <>
+void* persistent_kernel_small<1>(bool, bool);
+template <>
+void* persistent_kernel_small<2>(bool, bool);
+template <>
+void* persistent_kernel_small<4>(bool, bool);
+int tile_smem_small();
+int tile_cap_small();
+static void* pick_kernel_small(int G, bool stats, bool push) {
+    switch (G) {
+        case 1: return persistent_kernel_small<1>(stats, push);
+        case 2: return persistent_kernel_small<2>(stats, push);
+        case 4: return persistent_kernel_small<4>(stats, push);
+    }
+    return nullptr;
+}
+
 static void* pick_kernel(int G, bool stats, bool push) {
     switch (G) {
         case 1: return persistent_kernel<1>(stats, push);
@@ -83,6 +114,7 @@ int max_coop_warps(const DeviceInfo& d) { return d.sms * 64; }
 void carve_mis2(Carve& c, int64_t n, int64_t nnz, int max_warps, Mis2Ws* w) {
     (void)max_warps;
     w->ctrl = c.take<unsigned long long>(16);
+    w->maxdeg = c.take<unsigned long long>(1);
     w->T = c.take<uint64_t>((size_t)n + 1);
     w->M = c.take<uint32_t>((size_t)n + 1);
     for (int i = 0; i < 2; i++) {
@@ -304,10 +336,45 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
         set_error("group must be one of 1,2,4,8,16,32 (got %d)", G);
         return MIS2_EINVAL;
     }
-    const int smem = (int)sizeof(TileSmem);
+    // Skewed degree distributions (largest degree > 16x the average, on
+    // graphs with 8n > 64 MB): neighbour ids are random, the gathers hit
+    // L2 sector by sector and the hubs' words are the only reuse -- which
+    // only the L1 can serve.  One reduction over rowptr (and a 24-byte
+    // read) decides, before the launch: the 32-bit column keys (half the
+    // gather bytes) and 3 blocks per SM instead of 4, the carve-out giving
+    // the freed shared memory to L1 (C4: 72.9 -> 46.4 ms; 3 blocks on the
+    // stencils: C2 358 -> 375 us, C3 5.41 -> 5.57 ms, C5 7.71 -> 8.59 ms).
+    bool skewed = false;
+    if ((double)g.n * 8.0 > 64.0 * 1048576.0) {
+        unsigned long long md = 0;
+        MIS2_CUDA_TRY(cudaMemsetAsync(w.maxdeg, 0, sizeof(unsigned long long), s));
+        k_max_degree<<<(unsigned)(di.sms * 4), 256, 0, s>>>(g.n, g.rowptr, w.maxdeg);
+        count_launch();
+        MIS2_CUDA_TRY(cudaMemcpyAsync(&md, w.maxdeg, sizeof(md), cudaMemcpyDeviceToHost, s));
+        MIS2_CUDA_TRY(cudaStreamSynchronize(s));
+        skewed = (double)md > 16.0 * (double)g.nnz / (double)g.n;
+    }
+    // skewed: the small-tile kernels (160-row staging buffers, 35 KB per
+    // block instead of 55) when a dense step of the chosen G fits them --
+    // the shared memory saved is L1 (C4: 46.4 -> 38.0 ms)
+    int smem = (int)sizeof(TileSmem);
+    if (skewed) {
+        const double avg = (double)g.nnz / (double)g.n;
+        void* fs = (double)(kMB / G) * avg <= (double)tile_cap_small() ? pick_kernel_small(G, stats, push_iters > 0)
+                                                                       : nullptr;
+        if (const char* e = getenv("MIS2_SMALL_TILES"))
+            if (atoi(e) == 0) fs = nullptr;
+        if (fs) {
+            fn = fs;
+            smem = tile_smem_small();
+        }
+    }
     MIS2_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0;
     MIS2_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kMB, smem));
+    int skew_blocks = 3;  // MIS2_SKEW_BLOCKS: measurement knob
+    if (const char* e = getenv("MIS2_SKEW_BLOCKS")) skew_blocks = atoi(e);
+    if (skewed && per_sm > skew_blocks) per_sm = skew_blocks;
     if (per_sm < 1) {
         set_error("persistent kernel does not fit on an SM");
         return MIS2_EINTERNAL;
@@ -315,6 +382,14 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     if (const char* env = getenv("MIS2_BLOCKS_PER_SM")) {  // tuning knob (measurement only)
         const int want_per_sm = atoi(env);
         if (want_per_sm >= 1 && want_per_sm < per_sm) per_sm = want_per_sm;
+    }
+    {
+        // shared-memory carve-out: just what per_sm blocks need, the rest of
+        // the 256 KB is L1 (MIS2_CARVEOUT=percent: measurement knob)
+        int pct = (int)(((double)per_sm * (smem + 1024) * 100.0) / (228.0 * 1024.0) + 0.999);
+        if (pct > 100) pct = 100;
+        if (const char* e = getenv("MIS2_CARVEOUT")) pct = atoi(e);
+        MIS2_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     }
     const int64_t max_grid = (int64_t)per_sm * di.sms;
     // small graphs: about two steps of rows per block
@@ -340,11 +415,10 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     // 32-bit column keys: the two 64-bit minima per entry cost more ALU than
     // the halved gather bytes save on the stencil configs (C2 387 -> 451 us,
     // C3 5.6 -> 6.5 ms, C5 8.2 -> 10.1 ms); they help random-access graphs
-    // whose T does not fit L2 (C4 92 -> 77 ms).  Automatic: candidates are
-    // graphs with 8n > 64 MB; the kernel then uses the keys iff the largest
-    // degree exceeds 16x the average (skewed, random access).
+    // whose T does not fit L2 (C4 92 -> 77 ms).  Automatic: the skewed
+    // graphs (above).
     // MIS2_FLAG_KEYS / MIS2_FLAG_NO_KEYS force (results identical).
-    int keys = (double)g.n * 8.0 > 64.0 * 1048576.0 ? 2 : 0;  // 2 = decide on the device
+    int keys = skewed ? 1 : 0;
     if (o.flags & MIS2_FLAG_KEYS) keys = 1;
     if (o.flags & MIS2_FLAG_NO_KEYS) keys = 0;
     if (const char* e = getenv("MIS2_KEYS")) keys = atoi(e);  // measurement knob
