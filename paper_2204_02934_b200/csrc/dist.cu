@@ -145,11 +145,6 @@ void finish_sends(HostPart& owner, const std::vector<std::vector<int64_t>>& want
     }
 }
 
-__global__ void k_pack_u64(const uint64_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t cnt,
-                           uint64_t* __restrict__ dst) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
-        dst[i] = src[idx[i]];
-}
 __global__ void k_pack_u32(const uint32_t* __restrict__ src, const int32_t* __restrict__ idx, int64_t cnt,
                            uint32_t* __restrict__ dst) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)

@@ -344,9 +344,10 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     // gather bytes) and 3 blocks per SM instead of 4, the carve-out giving
     // the freed shared memory to L1 (C4: 72.9 -> 46.4 ms; 3 blocks on the
     // stencils: C2 358 -> 375 us, C3 5.41 -> 5.57 ms, C5 7.71 -> 8.59 ms).
-    bool skewed = false;
+    bool skewed = false, tested = false;
+    unsigned long long md = 0;
     if ((double)g.n * 8.0 > 64.0 * 1048576.0) {
-        unsigned long long md = 0;
+        tested = true;
         MIS2_CUDA_TRY(cudaMemsetAsync(w.maxdeg, 0, sizeof(unsigned long long), s));
         k_max_degree<<<(unsigned)(di.sms * 4), 256, 0, s>>>(g.n, g.rowptr, w.maxdeg);
         count_launch();
@@ -354,16 +355,23 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
         MIS2_CUDA_TRY(cudaStreamSynchronize(s));
         skewed = (double)md > 16.0 * (double)g.nnz / (double)g.n;
     }
-    // skewed: the small-tile kernels (160-row staging buffers, 35 KB per
-    // block instead of 55) when a dense step of the chosen G fits them --
-    // the shared memory saved is L1 (C4: 46.4 -> 38.0 ms)
+    // The small-tile kernels (160-row staging buffers, 35 KB per block
+    // instead of 55) whenever a dense step of the chosen G fits them: every
+    // step of a tested graph (G rows at the largest degree: C3), or the
+    // average step of a skewed one (its hub rows are deferred anyway: C4)
+    // -- the shared memory saved is L1 (C4 46.4 -> 37.9 ms, C3 5.29 -> 4.83
+    // ms).  MIS2_SMALL_TILES=0/2: never / whenever the average step fits
+    // (measurement knob).
     int smem = (int)sizeof(TileSmem);
-    if (skewed) {
-        const double avg = (double)g.nnz / (double)g.n;
-        void* fs = (double)(kMB / G) * avg <= (double)tile_cap_small() ? pick_kernel_small(G, stats, push_iters > 0)
-                                                                       : nullptr;
-        if (const char* e = getenv("MIS2_SMALL_TILES"))
-            if (atoi(e) == 0) fs = nullptr;
+    {
+        int mode = 1;
+        if (const char* e = getenv("MIS2_SMALL_TILES")) mode = atoi(e);
+        const double step_avg = g.n > 0 ? (double)(kMB / G) * (double)g.nnz / (double)g.n : 0.0;
+        const double step_max = (double)(kMB / G) * (double)md;
+        const double cap = (double)tile_cap_small();
+        const bool small = mode == 2 ? step_avg <= cap
+                                     : mode == 1 && tested && (skewed ? step_avg <= cap : step_max + 8.0 <= cap);
+        void* fs = small ? pick_kernel_small(G, stats, push_iters > 0) : nullptr;
         if (fs) {
             fn = fs;
             smem = tile_smem_small();
