@@ -184,6 +184,7 @@ class Mis2Result:
     rc: int = OK
     stats: np.ndarray | None = None
     launches: int = 0
+    extra: dict | None = None  # timeline: init_us / final_us
 
 
 def mis2(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int = 0, group: int = 0,
@@ -211,11 +212,14 @@ def mis2(rowptr, colinds, seed: int = 0, scheme: str = "xorstar", max_iters: int
                     st.ctypes.data if st is not None else None, ws.data_ptr(), wsb, _stream())
     launches = int(lib().mis2_last_launch_count())
     _check(rc, "mis2", allow=(ENOTCONVERGED,) if allow_partial else ())
+    extra = None
     if timeline:
+        # kernel entry -> first phase (init), last phase -> kernel end (output)
+        extra = {"init_us": float(st[0] - st[2 * mi]) / 1e3, "final_us": float(st[2 * mi + 1] - st[2 * its.value]) / 1e3}
         st = np.diff(st[: 2 * its.value + 1]) / 1e3  # microseconds per phase
     elif st is not None:
         st = st[: its.value].copy()
-    return Mis2Result(in_set[:n], int(cnt.value), int(its.value), rc, st, launches)
+    return Mis2Result(in_set[:n], int(cnt.value), int(its.value), rc, st, launches, extra)
 
 
 def mis2_async(rowptr, colinds, in_set, d_scalars, seed: int = 0, scheme: str = "xorstar", group: int = 0,

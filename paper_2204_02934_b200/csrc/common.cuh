@@ -129,6 +129,64 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, int mode = 0) {
     __syncthreads();
 }
 
+// Grid barrier that also sums one value per block (the loop condition
+// |worklist_1|, and the active count), so no extra L2 round trip
+// follows the barrier.  One 64-bit counter per barrier parity (ctr[0] and
+// ctr[kSumStride], separate lines): bits [0, 40) accumulate the values, bits
+// [40, 63) count arrivals, bit 63 flips when the last block arrives (block 0
+// adds 2^63 - (B-1) 2^40, every other block 2^40).  A block reaches barrier
+// k + 2 -- the same counter -- only after every block has left barrier k + 1,
+// hence after every block has read barrier k's final value, so that value
+// minus the one seen at barrier k - 2 is barrier k's sum.  Thread 0 keeps
+// the previous totals; every thread gets the sum.
+constexpr int kSumStride = 16;  // 128 bytes
+struct SumBarrier {
+    unsigned long long last[2];
+    unsigned int k;
+};
+// Split phase: grid_arrive_sum (after the block's writes; thread 0's atomic
+// returns the pre-arrival value `old`), independent work (the next phase's
+// prologue: it only reads static data and the block's own rows), then
+// grid_wait_sum.
+// sb lives in shared memory (only thread 0 touches it; fewer registers)
+__device__ __forceinline__ unsigned long long grid_arrive_sum(unsigned long long* ctr, const SumBarrier& sb,
+                                                              unsigned long long val) {
+    __syncthreads();
+    unsigned long long old = 0;
+    if (threadIdx.x == 0) {
+        unsigned long long* c = ctr + (sb.k & 1u) * kSumStride;
+        const unsigned long long add =
+            (blockIdx.x == 0 ? (1ull << 63) - ((unsigned long long)(gridDim.x - 1) << 40) : (1ull << 40)) + val;
+        asm volatile("atom.add.release.gpu.u64 %0,[%1],%2;" : "=l"(old) : "l"(c), "l"(add) : "memory");
+    }
+    return old;
+}
+__device__ __forceinline__ unsigned long long grid_wait_sum(unsigned long long* ctr, SumBarrier& sb,
+                                                            unsigned long long old, unsigned long long* s_out) {
+    constexpr unsigned long long kSumMask = (1ull << 40) - 1ull;
+    if (threadIdx.x == 0) {
+        unsigned long long* c = ctr + (sb.k & 1u) * kSumStride;
+        unsigned long long cur;
+        for (;;) {
+            asm volatile("ld.relaxed.gpu.u64 %0,[%1];" : "=l"(cur) : "l"(c) : "memory");
+            if ((old ^ cur) >> 63) break;
+            __nanosleep(32);
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        const unsigned long long tot = cur & kSumMask;
+        *s_out = (tot - sb.last[sb.k & 1u]) & kSumMask;
+        sb.last[sb.k & 1u] = tot;
+        sb.k++;
+    }
+    __syncthreads();
+    return *(volatile unsigned long long*)s_out;
+}
+__device__ __forceinline__ unsigned long long grid_sync_sum(unsigned long long* ctr, SumBarrier& sb,
+                                                            unsigned long long val, unsigned long long* s_out) {
+    const unsigned long long old = grid_arrive_sum(ctr, sb, val);
+    return grid_wait_sum(ctr, sb, old, s_out);
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.u64 %0,[%1];" : "=l"(v) : "l"(p) : "memory");

@@ -69,8 +69,8 @@ struct Mis2Ws {
     uint32_t* cnt;
     uint32_t* degc;
     uint32_t* K;        // 32-bit column keys (mis2_core.cu kkey)
-    unsigned long long* ctrl;  // [0]=barrier, [1..4]=ring of |wl1| sums, [5]=count, [6]=ticket,
-                               // [7]=active, [8]=max degree
+    unsigned long long* ctrl;  // [48]: [0]=barrier, [5]=count, [6]=ticket, [8]=max degree,
+                               // [16], [32] = the two counters of grid_sync_sum
     unsigned long long* maxdeg;  // skew test of run_mis2
     long long* dstats;         // [kStatsMaxIters * 6]
     long long* scal;           // [8] host-visible scalars of mis2()/mis2_host()

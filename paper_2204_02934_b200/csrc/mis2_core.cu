@@ -113,7 +113,7 @@ int max_coop_warps(const DeviceInfo& d) { return d.sms * 64; }
 
 void carve_mis2(Carve& c, int64_t n, int64_t nnz, int max_warps, Mis2Ws* w) {
     (void)max_warps;
-    w->ctrl = c.take<unsigned long long>(16);
+    w->ctrl = c.take<unsigned long long>(48);
     w->maxdeg = c.take<unsigned long long>(1);
     w->T = c.take<uint64_t>((size_t)n + 1);
     w->M = c.take<uint32_t>((size_t)n + 1);
@@ -316,18 +316,17 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
         set_error("stats/timeline mode supports max_iters <= %d", kStatsMaxIters);
         return MIS2_EINVAL;
     }
-    // Decide form per iteration: push (its per-row push / count overhead
-    // amortised over long rows) for every iteration of a dense graph; for a
-    // medium one in iterations 0 and 1: in iteration 0 no M is OUT yet
-    // (nothing to push) and the pull form's full second sweep over all rows
-    // is replaced by one count per row; in iteration 1 ~99% of the rows are
-    // still undecided, so the pull Decide is again a full sweep (C2 push
-    // iterations 1 / 2 / 3: 376.8 / 374.8 / 374.9 us).  Pull otherwise.
-    // Measured on C5 (avg degree 80), C2 (26.5), C3 (7).
-    // MIS2_FLAG_PUSH_DECIDE / PULL_DECIDE force a form (MIS2_PUSH_ITERS:
-    // measurement knob).
+    // Decide form per iteration: push for the first iterations, where
+    // nearly every row of worklist_2 is still undecided and the pull form's
+    // second sweep would re-read almost every row the column pass read; pull
+    // once worklist_1 is a small part of worklist_2 (the push form's OUT
+    // pushes then cost more than the pull form's early-exit reads).  Short
+    // rows (average degree < 16): iteration 0 only (there is no OUT to push
+    // yet).  Measured (us / ms per call, push iterations 1 / 2 / 3 / 4 / all):
+    // C2 (avg 26.5) - / 348 / 342 / - / 395; C3 (7) 4.68 / 4.84 (0: 4.84) ms;
+    // C4 (31) 40.9 / 38.2 / 37.5 ms; C5 (80) 8.03 / 7.52 / 7.26 / 7.24 / 7.67 ms.
     const double avg_deg = g.n > 0 ? (double)g.nnz / (double)g.n : 0.0;
-    int push_iters = avg_deg >= 32.0 ? max_iters : (avg_deg >= 16.0 ? 2 : 0);
+    int push_iters = avg_deg >= 16.0 ? 3 : 1;
     if (o.flags & MIS2_FLAG_PUSH_DECIDE) push_iters = max_iters;
     if (o.flags & MIS2_FLAG_PULL_DECIDE) push_iters = 0;
     if (const char* e = getenv("MIS2_PUSH_ITERS")) push_iters = atoi(e);
@@ -405,7 +404,7 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     const int64_t want = (g.n + 2 * rpb - 1) / (2 * rpb);
     const int grid = (int)(want < 1 ? 1 : (want > max_grid ? max_grid : want));
 
-    MIS2_CUDA_TRY(cudaMemsetAsync(w.ctrl, 0, 16 * sizeof(unsigned long long), s));
+    MIS2_CUDA_TRY(cudaMemsetAsync(w.ctrl, 0, 48 * sizeof(unsigned long long), s));
     if (stats) {
         MIS2_CUDA_TRY(cudaMemsetAsync(w.mark, 0, sizeof(unsigned int) * ((size_t)g.n + 1), s));
         MIS2_CUDA_TRY(cudaMemsetAsync(w.dstats, 0, sizeof(long long) * kStatsMaxIters * 6, s));

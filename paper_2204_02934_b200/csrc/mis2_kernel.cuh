@@ -61,6 +61,11 @@ constexpr int kTileCap = (MIS2_TILE_ROWS) * 27;
 // rows longer than 8 gather batches of their lane group are deferred and
 // reduced by the whole block (flattened over all deferred rows of the block)
 // independent gathers per lane per batch of the row loops
+// issue each phase's prologue between the barrier arrival and wait (1) or
+// after the wait (0, measurement knob)
+#ifndef MIS2_HOIST
+#define MIS2_HOIST 1
+#endif
 #ifndef MIS2_B1
 #define MIS2_B1 9  // measured: 9 is best on C2 (27 entries = 3 batches, 373 us vs 388 at 16) and near-best on C3
 #endif
@@ -213,6 +218,8 @@ struct __align__(16) TileSmem {
     int hcount;
     int hnext;       // deferred rows: next row for a warp
     int nhuge;       // deferred rows too long for a warp
+    int64_t nx_s, nx_e;  // dense phase, thread 0: colinds span of the step after the next
+    int pending;         // a phase prologue was issued and not yet run (PhaseState)
     uint64_t red64[kMW];
     int wred[kMW];
 };
@@ -850,24 +857,84 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t se
 // colinds span is bulk-copied into shared memory one step ahead.
 // PH = 0: Refresh Column over worklist_2 (M_v != OUT, active)
 // PH = 1: Decide over worklist_1 (T_v undecided)
-template <int G, bool STATS, int PH, bool PUSH = false>
-__device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, const Rows& rows, int32_t* lout,
-                           uint32_t& ph, uint64_t fi_next) {
-    const int t = threadIdx.x, g = t / G, sub = t % G;
-    const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
-    Stat st;
+//
+// Every phase is split into a prologue (*_begin: the first tile's bulk copy,
+// the first rows' bounds and own status words) and the steps (*_run).  The
+// prologue reads only static CSR data and words of the block's OWN rows,
+// which only this block writes, so the persistent kernel issues it between
+// its arrival at the grid barrier that precedes the phase and its wait
+// (grid_arrive_sum / grid_wait_sum): the copy and the loads land while the
+// block waits for the others, and the phase's first step starts with its
+// data in shared memory instead of after three dependent memory round trips
+// (C2 356 -> 348 us).
+// The state is parked in the idle second staging buffer (buf[1], written
+// by the copy of step 1 only after the run's first __syncthreads), so no
+// register stays live across the barrier; thread 0's bounds of the dense
+// step after next live in TileSmem.
+struct PhaseState {
+    int64_t s;    // rowptr of the row: dense, this thread's row of step 0; sparse, the leader's row of tile 1
+    uint64_t tv;  // its T_v
+    int32_t len;  // its length
+    int32_t x;    // dense: its M_v (id field); sparse: the row of tile 1 (-1: none)
+    int32_t y;    // sparse: the leader's row of tile 2 (-1: none)
+    int32_t pending;  // 0 none, 1 dense tile 0 issued, 2 sparse tile 0 issued
+};
+
+__device__ __forceinline__ PhaseState* park(TileSmem& sm) {
+    return reinterpret_cast<PhaseState*>(sm.buf[1]) + threadIdx.x;
+}
+static_assert(sizeof(PhaseState) * kMB <= sizeof(int32_t) * kTileCap, "PhaseState park");
+
+template <int G, int PH>
+__device__ __forceinline__ void dense_begin(TileSmem& sm, const MisParams& p, const Rows& rows) {
+    PhaseState ps;
+    const int t = threadIdx.x, g = t / G;
     if (t == 0) {
+        if (sm.nhuge) fence_proxy_async();  // buf[0] held the huge-row list (generic writes)
+        sm.nhuge = 0;
         sm.cnt = 0;
         sm.hcount = 0;
     }
-    const int64_t nsteps = rows.nruns;  // step k = run k of the block's rows (<= kMB / G rows)
-    int64_t nx_s = 0, nx_e = 0;  // bounds of the next tile (thread 0), prefetched a step ahead
+    const int64_t nsteps = rows.nruns;
     if (t == 0 && nsteps > 0) {
+        int64_t nx_s = 0, nx_e = 0;
         if (nsteps > 1) {
             nx_s = p.rowptr[rows.run_lo(1)];
             nx_e = p.rowptr[rows.run_hi(1)];
         }
+        sm.nx_s = nx_s;
+        sm.nx_e = nx_e;
         stage_tile(sm, p, 0, p.rowptr[rows.run_lo(0)], p.rowptr[rows.run_hi(0)]);
+    }
+    ps.s = 0;
+    ps.len = 0;
+    ps.tv = kOUT;
+    ps.x = (int32_t)kM_OUT;
+    ps.y = -1;
+    if (nsteps > 0 && rows.run_lo(0) + g < rows.run_hi(0)) {
+        const int64_t v0 = rows.run_lo(0) + g;
+        ps.s = p.rowptr[v0];
+        ps.len = (int32_t)(p.rowptr[v0 + 1] - ps.s);
+        ps.tv = p.T[v0];
+        if (PH == 0) ps.x = (int32_t)p.M[v0];
+    }
+    ps.pending = nsteps > 0 ? 1 : 0;
+    if (t == 0) sm.pending = ps.pending;
+    *park(sm) = ps;
+}
+
+template <int G, bool STATS, int PH, bool PUSH = false>
+__device__ int dense_run(TileSmem& sm, const MisParams& p, int it, const Rows& rows, int32_t* lout, uint32_t& ph,
+                         uint64_t fi_next) {
+    const PhaseState ps = *park(sm);  // before the first __syncthreads (step 1's copy refills buf[1])
+    const int t = threadIdx.x, g = t / G, sub = t % G;
+    const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
+    Stat st;
+    const int64_t nsteps = rows.nruns;  // step k = run k of the block's rows (<= kMB / G rows)
+    int64_t nx_s = 0, nx_e = 0;  // bounds of the next tile (thread 0), prefetched a step ahead
+    if (t == 0) {
+        nx_s = sm.nx_s;
+        nx_e = sm.nx_e;
     }
     const bool dbg = p.timeline && it == p.dbg_it && PH == p.dbg_ph && threadIdx.x == 0;
     long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
@@ -885,16 +952,9 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, const Rows&
         dbuf[59] = smid;
     }
     // prefetched row bounds / status of the next tile (this thread's row)
-    int64_t ns0 = 0, ne0 = 0;
-    uint64_t ntv = kOUT;
-    uint32_t nmv = kM_OUT;
-    if (nsteps > 0 && rows.run_lo(0) + g < rows.run_hi(0)) {
-        const int64_t v0 = rows.run_lo(0) + g;
-        ns0 = p.rowptr[v0];
-        ne0 = p.rowptr[v0 + 1];
-        ntv = p.T[v0];
-        if (PH == 0) nmv = p.M[v0];
-    }
+    int64_t ns0 = ps.s, ne0 = ps.s + ps.len;
+    uint64_t ntv = ps.tv;
+    uint32_t nmv = (uint32_t)ps.x;
     for (int64_t k = 0; k < nsteps; k++) {
         const int slot = (int)(k & 1);
         if (dbg && k < 12) dbuf[4 + 5 * k] = gt();
@@ -945,6 +1005,13 @@ __device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, const Rows&
     return finish_phase<STATS, PH, PUSH>(sm, p, it, rows.seg, lout, fi_next, st);
 }
 
+template <int G, bool STATS, int PH, bool PUSH = false>
+__device__ int dense_phase(TileSmem& sm, const MisParams& p, int it, const Rows& rows, int32_t* lout,
+                           uint32_t& ph, uint64_t fi_next) {
+    dense_begin<G, PH>(sm, p, rows);
+    return dense_run<G, STATS, PH, PUSH>(sm, p, it, rows, lout, ph, fi_next);
+}
+
 // ------------------------------------------------------------ sparse phase
 // Rows of the block's compacted worklist, RPBS = kMB/GS per step with
 // GS = 2G lanes per row.  Each group leader bulk-copies its own row into a
@@ -961,9 +1028,92 @@ constexpr int kTvOff = kTileCap - 2 * kMaxRowsS;      // uint64 T_v per row
 constexpr int kSlotRegion = kTvOff - 4 * kMaxRowsS;   // entries used for row slots; SMeta after
 static_assert(kSlotRegion > 0 && (kSlotRegion % 4) == 0, "sparse layout");
 
+// the leader of row group gs of a sparse step: its SMeta, T_v and (when the
+// row fits the group's slot) the bulk copy of its colinds hull into `slot`
+template <int G>
+__device__ __forceinline__ void sparse_issue(TileSmem& sm, const MisParams& p, int slot, int gs, int64_t v,
+                                             int64_t s, int64_t e, uint64_t tv) {
+    constexpr int GS = sparse_group<G>();
+    constexpr int RPBS = kMB / GS;
+    constexpr int SLOT = (kSlotRegion / RPBS) & ~3;
+    constexpr int kStaged = 1 << 30;
+    const int64_t nnz4 = p.nnz & ~(int64_t)3;
+    SMeta* meta = reinterpret_cast<SMeta*>(sm.buf[slot] + kSlotRegion);
+    SMeta m;
+    m.v = -1;
+    m.s = 0;
+    m.len = 0;
+    uint32_t bytes = 0;
+    int64_t sal = 0;
+    if (v >= 0) {
+        sal = s & ~(int64_t)3;
+        const int64_t ecp = (e + 3) & ~(int64_t)3;
+        const bool fits = (ecp - sal) <= SLOT && ecp <= nnz4;
+        m.v = (int32_t)v;
+        m.s = s;
+        m.len = (int32_t)(e - s) | (fits ? kStaged : 0);
+        if (fits && ecp > sal) bytes = (uint32_t)((ecp - sal) * 4);
+    }
+    meta[gs] = m;
+    reinterpret_cast<uint64_t*>(sm.buf[slot] + kTvOff)[gs] = tv;
+    mbar_expect_tx(&sm.mbarS[slot], bytes);
+    if (bytes) bulk_g2s(sm.buf[slot] + gs * SLOT, p.colinds + sal, bytes, &sm.mbarS[slot], sm.pol);
+}
+
+// Leaders pipeline the row metadata: worklist entry of tile j+3, row bounds
+// of tile j+2 and T_v of tile j+1 are loaded while tile j is processed, so
+// the copy of tile j+1 is issued without waiting on loads.  The prologue
+// (tile 0 issued, tiles 1 / 2 loaded) is sparse_begin.
+template <int G>
+__device__ __forceinline__ void sparse_begin(TileSmem& sm, const MisParams& p, int64_t seg, const int32_t* lin,
+                                             int nin) {
+    PhaseState ps;
+    constexpr int GS = sparse_group<G>();
+    constexpr int RPBS = kMB / GS;
+    const int t = threadIdx.x, gs = t / GS, sub = t % GS;
+    if (t == 0) {
+        if (sm.nhuge) fence_proxy_async();  // buf[0] held the huge-row list (generic writes)
+        sm.nhuge = 0;
+        sm.cnt = 0;
+        sm.hcount = 0;
+    }
+    const int nsteps = (nin + RPBS - 1) / RPBS;
+    auto row_of = [&](int j) -> int64_t {
+        const int idx = j * RPBS + gs;
+        return (sub == 0 && j < nsteps && idx < nin) ? (int64_t)lin[seg + idx] : -1;
+    };
+    ps.x = ps.y = -1;
+    ps.s = 0;
+    ps.len = 0;
+    ps.tv = kOUT;
+    ps.pending = 0;
+    if (nsteps > 0) {
+        const int64_t v0 = row_of(0);
+        const int64_t v1 = row_of(1);
+        ps.x = (int32_t)v1;
+        ps.y = (int32_t)row_of(2);
+        int64_t s0 = 0, e0 = 0;
+        if (v0 >= 0) {
+            s0 = p.rowptr[v0];
+            e0 = p.rowptr[v0 + 1];
+        }
+        if (v1 >= 0) {
+            ps.s = p.rowptr[v1];
+            ps.len = (int32_t)(p.rowptr[v1 + 1] - ps.s);
+        }
+        const uint64_t tv0 = v0 >= 0 ? p.T[v0] : kOUT;
+        ps.tv = v1 >= 0 ? p.T[v1] : kOUT;
+        if (sub == 0) sparse_issue<G>(sm, p, 0, gs, v0, s0, e0, tv0);
+        ps.pending = 2;
+    }
+    if (t == 0) sm.pending = ps.pending;
+    *park(sm) = ps;
+}
+
 template <int G, bool STATS, int PH, bool PUSH = false>
-__device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t seg, const int32_t* lin, int nin,
-                            int32_t* lout, uint32_t& ph, uint64_t fi_next) {
+__device__ int sparse_run(TileSmem& sm, const MisParams& p, int it, int64_t seg, const int32_t* lin, int nin,
+                          int32_t* lout, uint32_t& ph, uint64_t fi_next) {
+    const PhaseState ps = *park(sm);  // before the first __syncthreads (tile 1's copy refills buf[1])
     constexpr int GS = sparse_group<G>();
     constexpr int RPBS = kMB / GS;
     constexpr int SLOT = (kSlotRegion / RPBS) & ~3;
@@ -972,42 +1122,10 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t se
     const int t = threadIdx.x, gs = t / GS, sub = t % GS;
     const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
     Stat st;
-    if (t == 0) {
-        sm.cnt = 0;
-        sm.hcount = 0;
-    }
     const int nsteps = (nin + RPBS - 1) / RPBS;
-    const int64_t nnz4 = p.nnz & ~(int64_t)3;
-
-    // Leaders pipeline the row metadata: worklist entry of tile j+3, row
-    // bounds of tile j+2 and T_v of tile j+1 are loaded while tile j is
-    // processed, so the copy of tile j+1 is issued without waiting on loads.
     auto row_of = [&](int j) -> int64_t {
         const int idx = j * RPBS + gs;
         return (sub == 0 && j < nsteps && idx < nin) ? (int64_t)lin[seg + idx] : -1;
-    };
-    auto issue = [&](int slot, int64_t v, int64_t s, int64_t e, uint64_t tv) {
-        if (sub != 0) return;
-        SMeta* meta = reinterpret_cast<SMeta*>(sm.buf[slot] + kSlotRegion);
-        SMeta m;
-        m.v = -1;
-        m.s = 0;
-        m.len = 0;
-        uint32_t bytes = 0;
-        int64_t sal = 0;
-        if (v >= 0) {
-            sal = s & ~(int64_t)3;
-            const int64_t ecp = (e + 3) & ~(int64_t)3;
-            const bool fits = (ecp - sal) <= SLOT && ecp <= nnz4;
-            m.v = (int32_t)v;
-            m.s = s;
-            m.len = (int32_t)(e - s) | (fits ? kStaged : 0);
-            if (fits && ecp > sal) bytes = (uint32_t)((ecp - sal) * 4);
-        }
-        meta[gs] = m;
-        reinterpret_cast<uint64_t*>(sm.buf[slot] + kTvOff)[gs] = tv;
-        mbar_expect_tx(&sm.mbarS[slot], bytes);
-        if (bytes) bulk_g2s(sm.buf[slot] + gs * SLOT, p.colinds + sal, bytes, &sm.mbarS[slot], sm.pol);
     };
     auto bounds = [&](int64_t v, int64_t& s, int64_t& e) {
         s = 0;
@@ -1018,20 +1136,8 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t se
         }
     };
 
-    // prologue
-    int64_t v1 = -1, s1 = 0, e1 = 0, v2 = -1, s2 = 0, e2 = 0, v3 = -1;
-    uint64_t tv1 = kOUT, tv2 = kOUT;
-    if (nsteps > 0) {
-        const int64_t v0 = row_of(0);
-        v1 = row_of(1);
-        v2 = row_of(2);
-        int64_t s0, e0;
-        bounds(v0, s0, e0);
-        bounds(v1, s1, e1);
-        const uint64_t tv0 = v0 >= 0 ? p.T[v0] : kOUT;
-        tv1 = v1 >= 0 ? p.T[v1] : kOUT;
-        issue(0, v0, s0, e0, tv0);
-    }
+    int64_t v1 = ps.x, s1 = ps.s, e1 = ps.s + ps.len, v2 = ps.y, s2 = 0, e2 = 0, v3 = -1;
+    uint64_t tv1 = ps.tv, tv2 = kOUT;
     const bool dbg = p.timeline && it == p.dbg_it && PH == p.dbg_ph && threadIdx.x == 0;
     long long* dbuf = reinterpret_cast<long long*>(p.mark) + (int64_t)blockIdx.x * 64;
     auto gt = []() {
@@ -1049,7 +1155,7 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t se
         if (dbg && k < 12) dbuf[4 + 5 * k] = gt();
         __syncthreads();  // metadata of tile k visible; buffer of tile k-1 free
         if (dbg && k < 12) dbuf[4 + 5 * k + 1] = gt();
-        if (k + 1 < nsteps) issue(slot ^ 1, v1, s1, e1, tv1);  // no proxy fence needed (see stage_tile)
+        if (k + 1 < nsteps && sub == 0) sparse_issue<G>(sm, p, slot ^ 1, gs, v1, s1, e1, tv1);  // no proxy fence needed (see stage_tile)
         bounds(v2, s2, e2);     // prefetch for tile k+2
         tv2 = v2 >= 0 ? p.T[v2] : kOUT;
         v3 = row_of(k + 3);     // prefetch for tile k+3
@@ -1081,6 +1187,26 @@ __device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t se
     }
     if (dbg) dbuf[3] = gt();
     return finish_phase<STATS, PH, PUSH>(sm, p, it, seg, lout, fi_next, st);
+}
+
+template <int G, bool STATS, int PH, bool PUSH = false>
+__device__ int sparse_phase(TileSmem& sm, const MisParams& p, int it, int64_t seg, const int32_t* lin, int nin,
+                            int32_t* lout, uint32_t& ph, uint64_t fi_next) {
+    sparse_begin<G>(sm, p, seg, lin, nin);
+    return sparse_run<G, STATS, PH, PUSH>(sm, p, it, seg, lin, nin, lout, ph, fi_next);
+}
+
+// A prologue issued ahead of a phase that does not run (the loop ended):
+// its bulk copy must land before the block exits.
+__device__ __forceinline__ void drain_pending(TileSmem& sm, uint32_t& ph) {
+    const int pending = sm.pending;
+    if (pending == 1) {
+        mbar_wait(&sm.mbar[0], ph & 1u);
+        ph ^= 1u;
+    } else if (pending == 2) {
+        mbar_wait(&sm.mbarS[0], (ph >> 2) & 1u);
+        ph ^= 1u << 2;
+    }
 }
 
 // ------------------------------------------------------------ push-form Decide
@@ -1192,10 +1318,11 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
     const int t = threadIdx.x;
     const int64_t B = gridDim.x;
     const Rows rows = make_rows(p.n, B, blockIdx.x, kMB / G, p.cyclic != 0);
-    unsigned int* bar = (unsigned int*)&p.ctrl[0];
-    unsigned long long* ring = &p.ctrl[1];
+    stamp(p, 2 * p.max_iters);  // timeline: kernel entry
 
     if (t == 0) {
+        sm.nhuge = 0;
+        sm.pending = 0;
         mbar_init(&sm.mbar[0], 1);
         mbar_init(&sm.mbar[1], 1);
         constexpr int kRowGroups = kMB / sparse_group<G>();
@@ -1245,15 +1372,34 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         }
         const long long s = block_sum_int(sm, act_cnt);
         act_block = (int)s;
-        if (t == 0 && s) atomicAdd(&p.ctrl[7], (unsigned long long)s);
         if (p.K && !p.keys_mode) {
             const uint64_t bm = ~block_min_u64(sm, ~(uint64_t)maxdeg);  // block max
             if (t == 0 && bm) atomicMax(&p.ctrl[8], (unsigned long long)bm);
         }
     }
-    grid_barrier(bar);
+    const int64_t range = rows.count;
+    // this block's worklist segment sizes (a masked call starts from its lists)
+    int cnt1 = p.labels ? act_block : (int)range, cnt2 = cnt1;
+    __shared__ SumBarrier sb;
+    if (t == 0) {
+        sb.last[0] = sb.last[1] = 0ull;
+        sb.k = 0u;
+    }
+    __shared__ unsigned long long s_sum;
+    unsigned long long* sumc = &p.ctrl[16];
+    // Every phase's prologue (PhaseState: its first tile's bulk copy, its
+    // first rows' bounds and own status words) is issued between this
+    // block's barrier arrival and its wait, so it lands while the other
+    // blocks finish the previous phase.
+    auto col_begin = [&](int i, int c2, const int32_t* l2) {
+        if ((i == 0 && !p.labels) || (int64_t)c2 * kDenseDen >= range * kDenseNum) dense_begin<G, 0>(sm, p, rows);
+        else sparse_begin<G>(sm, p, rows.seg, l2, c2);
+    };
+    unsigned long long bold = grid_arrive_sum(sumc, sb, (unsigned long long)act_block);
+    if (MIS2_HOIST) col_begin(0, cnt2, p.L2[0]);  // own rows: written above by this block
+    const unsigned long long n_active = grid_wait_sum(sumc, sb, bold, &s_sum);
+    if (!MIS2_HOIST) col_begin(0, cnt2, p.L2[0]);
     stamp(p, 0);
-    const unsigned long long n_active = ld_acquire_u64(&p.ctrl[7]);
     // 32-bit column keys for skewed degree distributions: random neighbour
     // ids gather from all of T, which does not stay in L2 (C4); on meshes the
     // extra key arithmetic costs more than the halved bytes save
@@ -1266,43 +1412,54 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
 
     int it = 0;
     int status = MIS2_OK;
-    const int64_t range = rows.count;
-    // this block's worklist segment sizes (a masked call starts from its lists)
-    int cnt1 = p.labels ? act_block : (int)range, cnt2 = cnt1;
-    while (n_active > 0) {  // while worklist_1 != {}
+    const bool skip_loop = n_active == 0;
+    while (!skip_loop) {  // while worklist_1 != {}
         const int cur = it & 1;
-        // ---- Refresh Column over worklist_2
+        // ---- Refresh Column over worklist_2; its prologue was issued
         const bool push = PUSH && it < p.push_iters;
         const bool dense2 = (it == 0 && !p.labels) || (int64_t)cnt2 * kDenseDen >= range * kDenseNum;
         if (push) {
-            cnt2 = dense2 ? dense_phase<G, STATS, 0, PUSH>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0)
-                          : sparse_phase<G, STATS, 0, PUSH>(sm, p, it, rows.seg, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
+            cnt2 = dense2 ? dense_run<G, STATS, 0, PUSH>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0)
+                          : sparse_run<G, STATS, 0, PUSH>(sm, p, it, rows.seg, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
         } else {
-            cnt2 = dense2 ? dense_phase<G, STATS, 0, false>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0)
-                          : sparse_phase<G, STATS, 0, false>(sm, p, it, rows.seg, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
+            cnt2 = dense2 ? dense_run<G, STATS, 0, false>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0)
+                          : sparse_run<G, STATS, 0, false>(sm, p, it, rows.seg, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
         }
-        grid_barrier(bar);
+        if (t == 0) sm.pending = 0;
+        // prologue of Decide (pull form: its rows' colinds and own T_v)
+        const bool dense1 = (it == 0 && !p.labels) || (int64_t)cnt1 * kDenseDen >= range * kDenseNum;
+        auto dec_begin = [&]() {
+            if (push) return;
+            if (dense1) dense_begin<G, 1>(sm, p, rows);
+            else sparse_begin<G>(sm, p, rows.seg, p.L1[cur], cnt1);
+        };
+        bold = grid_arrive_sum(sumc, sb, 0ull);
+        if (MIS2_HOIST) dec_begin();
+        grid_wait_sum(sumc, sb, bold, &s_sum);
+        if (!MIS2_HOIST) dec_begin();
         stamp(p, 1 + 2 * it);
         // ---- Decide over worklist_1 + fused refresh of iteration it+1
         const uint64_t fi_next = p.prio.iter_term(it + 1);
-        const bool dense1 = (it == 0 && !p.labels) || (int64_t)cnt1 * kDenseDen >= range * kDenseNum;
         if (push) cnt1 = decide_push<STATS>(sm, p, it, rows, p.L1[cur], cnt1, dense1, p.L1[cur ^ 1], fi_next);
-        else if (dense1) cnt1 = dense_phase<G, STATS, 1>(sm, p, it, rows, p.L1[cur ^ 1], ph, fi_next);
-        else cnt1 = sparse_phase<G, STATS, 1>(sm, p, it, rows.seg, p.L1[cur], cnt1, p.L1[cur ^ 1], ph, fi_next);
-        if (t == 0) {
-            if (cnt1) atomicAdd(&ring[it & 3], (unsigned long long)cnt1);
-            if (blockIdx.x == 0) ring[(it + 2) & 3] = 0;  // slot last read two barriers ago
-        }
-        grid_barrier(bar);
+        else if (dense1) cnt1 = dense_run<G, STATS, 1>(sm, p, it, rows, p.L1[cur ^ 1], ph, fi_next);
+        else cnt1 = sparse_run<G, STATS, 1>(sm, p, it, rows.seg, p.L1[cur], cnt1, p.L1[cur ^ 1], ph, fi_next);
+        if (t == 0) sm.pending = 0;
+        // the loop condition rides on the barrier; the next Refresh Column's
+        // prologue is issued even if the loop ends (drained below)
+        bold = grid_arrive_sum(sumc, sb, (unsigned long long)cnt1);
+        if (MIS2_HOIST) col_begin(it + 1, cnt2, p.L2[cur ^ 1]);
+        const unsigned long long remaining = grid_wait_sum(sumc, sb, bold, &s_sum);
         stamp(p, 2 + 2 * it);
-        const unsigned long long remaining = ld_acquire_u64(&ring[it & 3]);
         it++;
         if (remaining == 0) break;
         if (it >= p.max_iters) {  // reading Q12
             status = MIS2_ENOTCONVERGED;
             break;
         }
+        if (!MIS2_HOIST) col_begin(it, cnt2, p.L2[cur ^ 1]);  // it already advanced
     }
+    __syncthreads();
+    drain_pending(sm, ph);
 
     // return {v : T_v = IN}
     l2_release(p, rows);
@@ -1323,6 +1480,11 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
             *p.d_count = (int64_t)ld_acquire_u64(&p.ctrl[5]);
             *p.d_iters = it;
             *p.d_status = status;
+            if (p.timeline) {  // timeline: kernel end
+                unsigned long long ns;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+                p.timeline[2 * p.max_iters + 1] = (long long)ns;
+            }
         }
     }
 }
@@ -1523,6 +1685,8 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_dist_persistent(con
     const Rows rows = make_rows(p.n, pk.nblk, lb, kMB / G, true);
     unsigned int e = epoch0;
     if (t == 0) {
+        sm.nhuge = 0;
+        sm.pending = 0;
         mbar_init(&sm.mbar[0], 1);
         mbar_init(&sm.mbar[1], 1);
         mbar_init(&sm.mbarS[0], kMB / sparse_group<G>());
