@@ -515,6 +515,14 @@ __device__ __forceinline__ void set_T(const MisParams& p, int64_t v, uint64_t t)
     p.T[v] = t;
     if (p.K) p.K[v] = kkey(t);
 }
+// v decided IN: the output mask is written at the decision
+// (init cleared it) and counted per block, so no pass over T follows the loop
+__shared__ int s_nin;
+__device__ __forceinline__ void set_IN(const MisParams& p, int64_t v) {
+    set_T(p, v, kIN);
+    p.in_set[v] = 1;
+    atomicAdd(&s_nin, 1);
+}
 
 __device__ __forceinline__ bool decide_write(const MisParams& p, int64_t v, int any_out, int all_eq, int it,
                                              uint64_t fi_next) {
@@ -523,7 +531,7 @@ __device__ __forceinline__ bool decide_write(const MisParams& p, int64_t v, int 
         return false;
     }
     if (all_eq) {
-        set_T(p, v, kIN);
+        set_IN(p, v);
         return false;
     }
     set_T(p, v, p.prio.word(it + 1, fi_next, gid_of(p, v)));  // fused Refresh Row
@@ -885,8 +893,10 @@ __device__ __forceinline__ PhaseState* park(TileSmem& sm) {
 }
 static_assert(sizeof(PhaseState) * kMB <= sizeof(int32_t) * kTileCap, "PhaseState park");
 
+// fresh: the first Refresh Column of an unmasked call (M not initialised,
+// every row active)
 template <int G, int PH>
-__device__ __forceinline__ void dense_begin(TileSmem& sm, const MisParams& p, const Rows& rows) {
+__device__ __forceinline__ void dense_begin(TileSmem& sm, const MisParams& p, const Rows& rows, bool fresh = false) {
     PhaseState ps;
     const int t = threadIdx.x, g = t / G;
     if (t == 0) {
@@ -916,7 +926,7 @@ __device__ __forceinline__ void dense_begin(TileSmem& sm, const MisParams& p, co
         ps.s = p.rowptr[v0];
         ps.len = (int32_t)(p.rowptr[v0 + 1] - ps.s);
         ps.tv = p.T[v0];
-        if (PH == 0) ps.x = (int32_t)p.M[v0];
+        if (PH == 0) ps.x = fresh ? (int32_t)kPending : (int32_t)p.M[v0];
     }
     ps.pending = nsteps > 0 ? 1 : 0;
     if (t == 0) sm.pending = ps.pending;
@@ -925,7 +935,7 @@ __device__ __forceinline__ void dense_begin(TileSmem& sm, const MisParams& p, co
 
 template <int G, bool STATS, int PH, bool PUSH = false>
 __device__ int dense_run(TileSmem& sm, const MisParams& p, int it, const Rows& rows, int32_t* lout, uint32_t& ph,
-                         uint64_t fi_next) {
+                         uint64_t fi_next, bool fresh = false) {
     const PhaseState ps = *park(sm);  // before the first __syncthreads (step 1's copy refills buf[1])
     const int t = threadIdx.x, g = t / G, sub = t % G;
     const unsigned tag = 2u * (unsigned)it + 1u + (unsigned)PH;
@@ -983,7 +993,7 @@ __device__ int dense_run(TileSmem& sm, const MisParams& p, int it, const Rows& r
                 ns0 = p.rowptr[vn];
                 ne0 = p.rowptr[vn + 1];
                 ntv = p.T[vn];
-                if (PH == 0) nmv = p.M[vn];
+                if (PH == 0) nmv = fresh ? kPending : p.M[vn];
             }
         }
         const int64_t len = e - s;
@@ -1272,7 +1282,7 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, const Rows&
             if (v >= 0 && tv[u] != kIN && tv[u] != kOUT) {
                 if (c[u]) p.cnt[v] = 0u;
                 if (fl[u]) set_T(p, v, kOUT);
-                else if (c[u] == dg[u]) set_T(p, v, kIN);
+                else if (c[u] == dg[u]) set_IN(p, v);
                 else {
                     set_T(p, v, p.prio.word(it + 1, fi_next, gid_of(p, v)));
                     keep = true;
@@ -1323,6 +1333,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
     if (t == 0) {
         sm.nhuge = 0;
         sm.pending = 0;
+        s_nin = 0;
         mbar_init(&sm.mbar[0], 1);
         mbar_init(&sm.mbar[1], 1);
         constexpr int kRowGroups = kMB / sparse_group<G>();
@@ -1349,9 +1360,13 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
             const bool act = in && (p.labels ? (p.labels[v] < 0) : true);
             if (in) {
                 set_T(p, v, act ? p.prio.word(0, fi0, gid_of(p, v)) : kOUT);
-                p.M[v] = act ? kPending : 0u;  // 0 = inactive sentinel (reading Q15)
+                // M: the first column pass of an unmasked call takes every
+                // row without reading M (`fresh`); a masked one marks the
+                // inactive rows (0 = inactive sentinel, reading Q15)
+                if (p.labels) p.M[v] = act ? kPending : 0u;
                 p.oflag[v] = 0;
                 p.cnt[v] = 0u;
+                p.in_set[v] = 0;
                 if (p.K && !p.keys_mode) maxdeg = max(maxdeg, p.rowptr[v + 1] - p.rowptr[v]);
             }
             act_cnt += act;
@@ -1392,7 +1407,8 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
     // block's barrier arrival and its wait, so it lands while the other
     // blocks finish the previous phase.
     auto col_begin = [&](int i, int c2, const int32_t* l2) {
-        if ((i == 0 && !p.labels) || (int64_t)c2 * kDenseDen >= range * kDenseNum) dense_begin<G, 0>(sm, p, rows);
+        if ((i == 0 && !p.labels) || (int64_t)c2 * kDenseDen >= range * kDenseNum)
+            dense_begin<G, 0>(sm, p, rows, i == 0 && !p.labels);
         else sparse_begin<G>(sm, p, rows.seg, l2, c2);
     };
     unsigned long long bold = grid_arrive_sum(sumc, sb, (unsigned long long)act_block);
@@ -1418,11 +1434,12 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         // ---- Refresh Column over worklist_2; its prologue was issued
         const bool push = PUSH && it < p.push_iters;
         const bool dense2 = (it == 0 && !p.labels) || (int64_t)cnt2 * kDenseDen >= range * kDenseNum;
+        const bool fresh = it == 0 && !p.labels;
         if (push) {
-            cnt2 = dense2 ? dense_run<G, STATS, 0, PUSH>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0)
+            cnt2 = dense2 ? dense_run<G, STATS, 0, PUSH>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0, fresh)
                           : sparse_run<G, STATS, 0, PUSH>(sm, p, it, rows.seg, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
         } else {
-            cnt2 = dense2 ? dense_run<G, STATS, 0, false>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0)
+            cnt2 = dense2 ? dense_run<G, STATS, 0, false>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0, fresh)
                           : sparse_run<G, STATS, 0, false>(sm, p, it, rows.seg, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
         }
         if (t == 0) sm.pending = 0;
@@ -1461,16 +1478,10 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
     __syncthreads();
     drain_pending(sm, ph);
 
-    // return {v : T_v = IN}
+    // return {v : T_v = IN}: written at the decisions (set_IN)
     l2_release(p, rows);
-    int cnt = 0;
-    for (int64_t i = t; i < rows.count; i += kMB) {
-        const int64_t v = rows.row_at(i);
-        const uint8_t in = (p.T[v] == kIN);
-        p.in_set[v] = in;
-        cnt += in;
-    }
-    const long long bc = block_sum_int(sm, cnt);
+    __syncthreads();
+    const long long bc = s_nin;
     if (t == 0) {
         atomicAdd(&p.ctrl[5], (unsigned long long)bc);
         __threadfence();
