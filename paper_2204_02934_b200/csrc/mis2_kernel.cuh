@@ -1251,7 +1251,10 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, const Rows&
     // |N[v] ∩ active| = degc[v], counted by the push-form column pass of
     // iteration 0 (closed neighbourhood; Q23: a stored diagonal is not
     // counted twice) -- no row is read here.
-    constexpr int U = 8;
+#ifndef MIS2_DPU
+#define MIS2_DPU 2  // rows per thread per round: measured 2 / 4 / 8 / 16 -> C2 334 / 336 / 340 / 365 us (the unrolled code is fetched cold every phase)
+#endif
+    constexpr int U = MIS2_DPU;
     for (int64_t base = 0; base < total; base += (int64_t)kMB * U) {
         int32_t vv[U];
         uint64_t tv[U];
@@ -1284,7 +1287,11 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, const Rows&
                 if (fl[u]) set_T(p, v, kOUT);
                 else if (c[u] == dg[u]) set_IN(p, v);
                 else {
+#ifdef MIS2_DP_NOHASH
+                    set_T(p, v, ((uint64_t)(it + 5) << 40) | (uint64_t)(v + 1));
+#else
                     set_T(p, v, p.prio.word(it + 1, fi_next, gid_of(p, v)));
+#endif
                     keep = true;
                 }
                 if (STATS) {
