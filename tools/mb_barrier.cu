@@ -36,6 +36,20 @@ __global__ void bar_kernel(unsigned int* ctr, int iters, int stores, unsigned in
                     if (cur >= (unsigned)gridDim.x * (unsigned)(i / 4 + 1)) break;
                 }
                 asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            } else if (MODE == 6 || MODE == 7) {
+                // one arrival counter; the last arriver publishes the epoch to 8
+                // release lines (256 B apart); block b polls line b & 7
+                unsigned int old, cur;
+                asm volatile("atom.add.acq_rel.gpu.u32 %0,[%1],1;" : "=r"(old) : "l"(ctr) : "memory");
+                if (old == (unsigned)gridDim.x * (unsigned)(i + 1) - 1)
+                    for (int q = 0; q < 8; q++) asm volatile("st.relaxed.gpu.u32 [%0], %1;" ::"l"(ctr + 64 * (q + 1)), "r"(i + 1) : "memory");
+                unsigned int* rl = ctr + 64 * ((blockIdx.x & 7) + 1);
+                for (;;) {
+                    asm volatile("ld.relaxed.gpu.u32 %0,[%1];" : "=r"(cur) : "l"(rl) : "memory");
+                    if (cur >= (unsigned)(i + 1)) break;
+                    if (MODE == 6) __nanosleep(32);
+                }
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
             } else if (MODE == 4 || MODE == 5) {
                 // arrivals spread over 32 counters 256 B apart (different L2 slices);
                 // the poll sums them (warp 0 polls, lane j reads counter j)
@@ -106,6 +120,8 @@ int main() {
             run(bar_kernel<3>, "two-level 16", sms * per, blk, stores);
             run(bar_kernel<4>, "spread32 red, warp poll", sms * per, blk, stores);
             run(bar_kernel<5>, "spread32 + sleep", sms * per, blk, stores);
+            run(bar_kernel<6>, "last->8 lines +sleep", sms * per, blk, stores);
+            run(bar_kernel<7>, "last->8 lines", sms * per, blk, stores);
         }
     }
     return 0;
