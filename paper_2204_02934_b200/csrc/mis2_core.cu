@@ -471,6 +471,14 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     p.cyclic = 1;
     if (const char* e = getenv("MIS2_CYCLIC")) p.cyclic = atoi(e) != 0;
     p.push_iters = push_iters;
+    // Skewed graphs defer rows beyond one gather batch of their lane group
+    // (G = 2 on C4: 32 entries) to the block's warps, whose coalesced row
+    // loops beat the lane groups' on long rows (C4, batches 1 / 2 / 3 / 4 /
+    // 8 / 16 / 32: 30.9-31.2 / 31.1-31.4 / 32.1 / 31.6 / 37.5 / 37.9 / 55.4
+    // ms); the others keep 8 (C2's 27-entry rows at G = 1 need > 3; C5
+    // unchanged).
+    p.heavy_batches = skewed ? 1 : 0;
+    if (const char* e = getenv("MIS2_HEAVY_BATCHES_RT")) p.heavy_batches = atoi(e);  // measurement knob
     p.prio.override_ = o.prio_override;
     p.prio.override_iters = o.prio_override ? o.prio_iters : 0;
     p.max_iters = max_iters;

@@ -135,6 +135,8 @@ struct MisParams {
     long long* timeline;  // MIS2_FLAG_TIMELINE only
     float l2_keep;        // fraction of each block's colinds span kept in L2 (evict_last)
     int cyclic;           // row ownership: 0 = one contiguous range per block, 1 = cyclic chunks (Rows)
+    int heavy_batches;    // > 0: rows longer than heavy_batches gather batches of their lane group are
+                          // deferred to warps (0: MIS2_HEAVY_BATCHES)
     int push_iters;       // PUSH kernels: iterations it < push_iters use the push-form Decide
     int dbg_it, dbg_ph;   // MIS2_FLAG_TIMELINE: sparse phase instrumented into `mark`
     Prio prio;
@@ -667,7 +669,7 @@ template <int GG>
 __device__ __forceinline__ bool defer_long(TileSmem& sm, const MisParams& p, int64_t seg, bool act, int sub,
                                            int64_t v, int64_t len) {
     bool defer = false;
-    if (act && sub == 0 && len > heavy_len<GG>()) {
+    if (act && sub == 0 && len > (p.heavy_batches > 0 ? p.heavy_batches * GG * gather_batch<GG>() : heavy_len<GG>())) {
         const int h = atomicAdd(&sm.hcount, 1);
         p.heavy[seg + h] = (int32_t)v;  // at most one entry per row of the block's segment
         defer = true;
