@@ -478,6 +478,8 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     // ms); the others keep 8 (C2's 27-entry rows at G = 1 need > 3; C5
     // unchanged).
     p.heavy_batches = skewed ? 1 : 0;
+    p.gather_keep = skewed ? 1 : 0;
+    if (const char* e = getenv("MIS2_GATHER_KEEP")) p.gather_keep = atoi(e);  // measurement knob
     if (const char* e = getenv("MIS2_HEAVY_BATCHES_RT")) p.heavy_batches = atoi(e);  // measurement knob
     p.prio.override_ = o.prio_override;
     p.prio.override_iters = o.prio_override ? o.prio_iters : 0;

@@ -135,6 +135,7 @@ struct MisParams {
     long long* timeline;  // MIS2_FLAG_TIMELINE only
     float l2_keep;        // fraction of each block's colinds span kept in L2 (evict_last)
     int cyclic;           // row ownership: 0 = one contiguous range per block, 1 = cyclic chunks (Rows)
+    int gather_keep;      // 1: key / M gathers carry an L2 evict_last hint (skewed graphs)
     int heavy_batches;    // > 0: rows longer than heavy_batches gather batches of their lane group are
                           // deferred to warps (0: MIS2_HEAVY_BATCHES)
     int push_iters;       // PUSH kernels: iterations it < push_iters use the push-form Decide
@@ -299,6 +300,14 @@ __device__ __forceinline__ void l2_release(const MisParams& p, const Rows& r) {
     for (int64_t l = l0 + threadIdx.x; l < l1; l += blockDim.x)
         asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(base + l * 128) : "memory");
 }
+// gather of a 32-bit status word with an L2 eviction-priority hint (skewed
+// graphs: the keys / M ids are the reuse targets; the CSR stream goes by)
+__device__ __forceinline__ uint32_t ld_keep(const uint32_t* a, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__shared__ uint64_t s_keep_pol;  // evict_last when p.gather_keep, else evict_normal
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ------------------------------------------------------------ block helpers
@@ -464,7 +473,7 @@ __device__ __forceinline__ void row_min_keys(const uint32_t* __restrict__ K, con
 #pragma unroll
         for (int q = 0; q < B; q++) {
             ww[q] = x[min(j + q * G, last)];
-            kk[q] = K[ww[q]];
+            kk[q] = ld_keep(K + ww[q], s_keep_pol);
         }
 #pragma unroll
         for (int q = 0; q < B; q++) {
@@ -491,7 +500,7 @@ __device__ __forceinline__ void row_decide(const uint32_t* __restrict__ M, const
     for (int j = sub; j < len; j += B * G) {
         uint32_t mm[B];
 #pragma unroll
-        for (int q = 0; q < B; q++) mm[q] = M[x[min(j + q * G, last)]];
+        for (int q = 0; q < B; q++) mm[q] = ld_keep(M + x[min(j + q * G, last)], s_keep_pol);
 #pragma unroll
         for (int q = 0; q < B; q++) decide_acc(mm[q], vid1, any_out, all_eq);
         if (any_out) break;  // the row is OUT whatever follows
@@ -727,7 +736,7 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
 #pragma unroll
                 for (int u = 0; u < 8; u++) ww[u] = x[min(j + (int64_t)u * NT, last)];
 #pragma unroll
-                for (int u = 0; u < 8; u++) kk[u] = p.K[ww[u]];
+                for (int u = 0; u < 8; u++) kk[u] = ld_keep(p.K + ww[u], s_keep_pol);
 #pragma unroll
                 for (int u = 0; u < 8; u++) {
                     const uint64_t a = key_lo(kk[u], (uint32_t)ww[u]), b = key_hi(kk[u], (uint32_t)ww[u]);
@@ -784,7 +793,7 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
         for (int64_t j = tid; j < len; j += (int64_t)NT * 8) {
             uint32_t mm[8];
 #pragma unroll
-            for (int u = 0; u < 8; u++) mm[u] = p.M[x[min(j + (int64_t)u * NT, last)]];
+            for (int u = 0; u < 8; u++) mm[u] = ld_keep(p.M + x[min(j + (int64_t)u * NT, last)], s_keep_pol);
 #pragma unroll
             for (int u = 0; u < 8; u++) decide_acc(mm[u], vid1, any_out, all_eq);
             if (any_out) break;  // the row is OUT whatever follows
@@ -1343,6 +1352,12 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         sm.nhuge = 0;
         sm.pending = 0;
         s_nin = 0;
+        {
+            uint64_t pol;
+            if (p.gather_keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+            else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+            s_keep_pol = pol;
+        }
         mbar_init(&sm.mbar[0], 1);
         mbar_init(&sm.mbar[1], 1);
         constexpr int kRowGroups = kMB / sparse_group<G>();
@@ -1707,6 +1722,12 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_dist_persistent(con
     if (t == 0) {
         sm.nhuge = 0;
         sm.pending = 0;
+        {
+            uint64_t pol;
+            if (p.gather_keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+            else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+            s_keep_pol = pol;
+        }
         mbar_init(&sm.mbar[0], 1);
         mbar_init(&sm.mbar[1], 1);
         mbar_init(&sm.mbarS[0], kMB / sparse_group<G>());
