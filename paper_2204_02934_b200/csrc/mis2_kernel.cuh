@@ -66,6 +66,11 @@ constexpr int kTileCap = (MIS2_TILE_ROWS) * 27;
 #ifndef MIS2_HOIST
 #define MIS2_HOIST 1
 #endif
+// 32-bit column keys with one minimum and a tie flag (1) or two 64-bit
+// minima (0)
+#ifndef MIS2_K32
+#define MIS2_K32 1  // C4 31.0 -> 30.7 ms; the stencils keep 64-bit words (keys there: C2 342 -> 381 us)
+#endif
 #ifndef MIS2_B1
 #define MIS2_B1 9  // measured: 9 is best on C2 (27 entries = 3 batches, 373 us vs 388 at 16) and near-best on C3
 #endif
@@ -486,6 +491,54 @@ __device__ __forceinline__ void row_min_keys(const uint32_t* __restrict__ K, con
     }
 }
 
+// Refresh Column on 32-bit keys, one minimum: (km, am) = the least key and
+// the entry holding it; tie = another vertex holds the same key (resolved by
+// the caller on the full words).  Cheaper than the two 64-bit minima of
+// row_min_keys.
+template <int G>
+__device__ __forceinline__ void row_min_k32(const uint32_t* __restrict__ K, const int32_t* x, int len, int sub,
+                                            uint32_t& km, int32_t& am, int& tie, int32_t self = -1,
+                                            int* has = nullptr) {
+    constexpr int B = gather_batch<G>();
+    const int last = len - 1;
+    for (int j = sub; j < len; j += B * G) {
+        uint32_t kk[B];
+        int32_t ww[B];
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            ww[q] = x[min(j + q * G, last)];
+            kk[q] = ld_keep(K + ww[q], s_keep_pol);
+        }
+#pragma unroll
+        for (int q = 0; q < B; q++) {
+            const bool lt = kk[q] < km;
+            const int eq = (kk[q] == km) & (ww[q] != am);
+            tie = lt ? 0 : (tie | eq);
+            am = lt ? ww[q] : am;
+            km = lt ? kk[q] : km;
+            if (has) *has |= ww[q] == self;
+        }
+        if (!has && km == 0u) break;  // an IN neighbour: M is OUT
+    }
+}
+template <int G>
+__device__ __forceinline__ void group_min_k32(uint32_t& km, int32_t& am, int& tie) {
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+        const uint32_t k2 = __shfl_xor_sync(kFull, km, off);
+        const int32_t a2 = __shfl_xor_sync(kFull, am, off);
+        const int t2 = __shfl_xor_sync(kFull, tie, off);
+        if (k2 < km) {
+            km = k2;
+            am = a2;
+            tie = t2;
+        } else if (k2 == km) {
+            tie = tie | t2 | (a2 != am);
+            am = a2 < am ? a2 : am;
+        }
+    }
+}
+
 // Decide of one row on id fields: exists M_w = OUT / forall
 // M_w = T_v (id v+1); M_w = 0 (inactive, reading Q15) is ignored.
 __device__ __forceinline__ void decide_acc(uint32_t m, uint32_t vid1, int& any_out, int& all_eq) {
@@ -590,6 +643,32 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
     if (PH == 0) {
         uint32_t mf;
         int dc = 0;
+#if MIS2_K32
+        if (p.K && s_use_keys && !(PUSH && it == 0 && p.labels)) {
+            // keys (single GPU: local ids are global ids)
+            uint32_t km = 0xffffffffu;
+            int32_t am = -1;
+            int tie = 0;
+            if (act && sub == 0) {  // closed neighbourhood (Q1)
+                km = kkey(tv);
+                am = (int32_t)v;
+            }
+            if (act && len > 0) {
+                if (PUSH && it == 0) row_min_k32<GG>(p.K, x, len, sub, km, am, tie, (int32_t)v, &dc);
+                else row_min_k32<GG>(p.K, x, len, sub, km, am, tie);
+            }
+            group_min_k32<GG>(km, am, tie);
+            const bool decided = km == 0u || km == 0xffffffffu;
+            const bool tie_real = act && tie && !decided;
+            mf = decided ? kM_OUT : (uint32_t)am + 1u;
+            if (__any_sync(kFull, tie_real)) {  // equal keys: the full words decide
+                uint64_t m = (tie_real && sub == 0) ? tv : kOUT;
+                if (tie_real && len > 0) m = row_min<GG>(p.T, x, len, sub, m);
+                m = group_min<GG>(m);
+                if (tie_real) mf = m_field(m, p.id_mask);
+            }
+        } else
+#endif
         if (p.K && s_use_keys && !(PUSH && it == 0 && p.labels)) {
             // keys (single GPU: local ids are global ids)
             uint64_t k1 = ~0ull, k2 = ~0ull;
