@@ -116,6 +116,26 @@ def test_column_keys(decide, keys):
         check_mis2(G.kronecker(11), group=grp, decide=decide, keys=keys)
 
 
+@pytest.mark.parametrize("decide", ["pull", "push", "auto"])
+def test_skewed_graph_paths_forced(decide, monkeypatch):
+    """The launch choices run_mis2 makes for skewed graphs (C4), forced on small
+    graphs through the library's measurement knobs: rows longer than ONE
+    gather batch of their lane group deferred to the block's warps
+    (MIS2_HEAVY_BATCHES_RT=1), 32-bit column keys with the one-minimum tie
+    path, and the L2 evict_last hint on the key / M-id gathers; MIS-2 and
+    Alg. 3 (masked phase-2 call) bit-exact with the oracle."""
+    monkeypatch.setenv("MIS2_HEAVY_BATCHES_RT", "1")
+    monkeypatch.setenv("MIS2_GATHER_KEEP", "1")
+    gs = small_graphs(25, 777, nmax=300) + [G.kronecker(12), G.random_powerlaw_graph(4000, 40, 3),
+                                          G.laplace3d_27pt(10), G.elasticity3d(6)]
+    for g in gs:
+        check_mis2(g, decide=decide, keys="on")
+        check_mis2(g, decide=decide, keys="on", seed=7, scheme="fixed")
+        check_agg(g, decide=decide, keys="on")
+    for grp in (1, 2, 8):
+        check_mis2(G.kronecker(11), group=grp, decide=decide, keys="on")
+
+
 @pytest.mark.parametrize("decide", ["pull", "push"])
 def test_decide_forms_long_rows(decide):
     """Both Decide forms on graphs with rows beyond the deferred-row threshold
