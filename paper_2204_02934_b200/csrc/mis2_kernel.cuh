@@ -52,7 +52,7 @@ namespace mis2k {
 #endif
 constexpr int kMW = MIS2_WARPS;
 constexpr int kMB = 32 * kMW;
-constexpr int kMinBlocksPerSM = kMW >= 16 ? 1 : 4;
+constexpr int kMinBlocksPerSM = kMW >= 16 ? 1 : 32 / kMW;  // 32 warps per SM at 64 registers
 // int32 colinds per staging buffer: a dense step of 27-entry rows
 #ifndef MIS2_TILE_ROWS
 #define MIS2_TILE_ROWS (kMB >= 512 ? kMB / 2 : kMB)
