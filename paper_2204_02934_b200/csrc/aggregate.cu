@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "common.cuh"
 #include "internal.h"
@@ -934,26 +935,25 @@ void agg_phase3(int G, int64_t n, const int64_t* rowptr, const int32_t* colinds,
 }
 #undef AGG_DISPATCH
 
-int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int64_t* num_aggs, int32_t* roots,
-                  int64_t* stats, void* ws, size_t ws_bytes, cudaStream_t s, size_t* bytes_needed) {
-    DeviceInfo di;
-    MIS2_TRY(device_info(&di));
-    Carve c(ws, ws_bytes);
-    AggWs w;
-    carve_agg(c, g.n, g.nnz, max_coop_warps(di), &w);
-    if (bytes_needed) { *bytes_needed = c.off; return MIS2_OK; }
-    if (!c.ok()) { set_error("workspace too small: need %zu bytes", c.off); return MIS2_ENOMEM; }
+// Large graphs run the phase-2 MIS-2 on the induced subgraph of the
+// unaggregated vertices (below); small ones the masked call on G (the
+// build's two host reads of the subgraph's size cost more than the smaller
+// passes save: C2 0.88 ms masked, 0.97 ms on the subgraph; C3 11.1 -> 10.0
+// ms, C5 14.8 -> 14.0 ms).  MIS2_AGG_SUB=0/1 forces (measurement knob).
+static bool agg_use_sub(const mis2_graph& g) {
+    bool use_sub = g.nnz >= (int64_t)1 << 26;
+    if (const char* e = getenv("MIS2_AGG_SUB")) use_sub = atoi(e) != 0;
+    return use_sub;
+}
+
+// All device work of Alg. 3 on stream s; the host reads the
+// scalars afterwards (run_aggregate).
+static int agg_enqueue(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int32_t* roots, AggWs& w,
+                       int64_t* ist1, int64_t* ist2, const DeviceInfo& di, cudaStream_t s) {
     const int64_t n = g.n;
     const int G = choose_group(g.n, g.nnz, o.group);
     int32_t* s32 = (int32_t*)w.scal;
     MIS2_CUDA_TRY(cudaMemsetAsync(w.scal, 0, 32 * sizeof(long long), s));
-
-    // per-iteration worklist statistics of both MIS-2 calls (MIS2_FLAG_ITER_STATS)
-    const bool iter_stats = stats && (o.flags & MIS2_FLAG_ITER_STATS) && !(o.flags & MIS2_FLAG_TIMELINE);
-    const int64_t mi = max_iters_for(n, o.max_iters);
-    int64_t* ist1 = iter_stats ? stats + 8 : nullptr;
-    int64_t* ist2 = iter_stats ? stats + 8 + 6 * mi : nullptr;
-    if (iter_stats) memset(stats + 8, 0, sizeof(int64_t) * 12 * (size_t)mi);
 
     // ---- phase 1: M1 = MIS2(G)
     MIS2_TRY(run_mis2(g, o, nullptr, w.in1, (int64_t*)&w.scal[kCount1], &s32[2 * kIters1],
@@ -999,14 +999,7 @@ int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int6
     } else {
 
     // ---- phase 2: M2 = MIS2(G \ aggregated) on the same ids / seed (Q15)
-    // Large graphs: on the induced subgraph of the unaggregated vertices
-    // (below); small ones: the masked call on G (the build's two host reads
-    // of the subgraph's size cost more than the smaller passes save: C2
-    // 0.88 ms masked, 0.97 ms on the subgraph; C3 11.1 -> 10.0 ms, C5 14.8
-    // -> 14.0 ms).  MIS2_AGG_SUB=0/1 forces (measurement knob).
-    bool use_sub = g.nnz >= (int64_t)1 << 26;
-    if (const char* e = getenv("MIS2_AGG_SUB")) use_sub = atoi(e) != 0;
-    if (!use_sub) {
+    if (!agg_use_sub(g)) {
         MIS2_TRY(run_mis2(g, o, labels, w.in2, (int64_t*)&w.scal[kCount2], &s32[2 * kIters2], &s32[2 * kStatus2],
                           ist2, w.mis, s));
     } else {
@@ -1090,6 +1083,135 @@ int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int6
     count_launch();
     }  // Alg. 3
     MIS2_CUDA_TRY(cudaGetLastError());
+    return MIS2_OK;
+}
+
+// ---- CUDA-graph replay of repeated aggregate() calls
+// Alg. 3 is ~20 launches whose sizes depend only on (n, nnz, options), so a
+// call on the same graph, outputs and workspace as an earlier one replays
+// the captured launch sequence (one graph launch instead of ~20 kernel
+// launches and their gaps) on a private stream joined to the caller's by
+// events -- from the second call with the same key on (a one-off call, e.g.
+// a level of the multilevel loop, pays no capture).  Only sequences without
+// host reads are captured: the masked
+// phase-2 call (not the induced subgraph, whose size the host reads), no
+// skew test (8n <= 64 MB), no per-iteration statistics.  MIS2_AGG_GRAPH=0:
+// never (measurement knob).
+struct AggGraphKey {
+    int64_t n, nnz;
+    const void *rowptr, *colinds, *labels, *roots, *ws;
+    size_t ws_bytes;
+    uint64_t seed;
+    int32_t scheme, max_iters, group;
+    uint32_t flags;
+    bool operator==(const AggGraphKey& k) const { return memcmp(this, &k, sizeof(k)) == 0; }
+};
+struct AggGraph {
+    AggGraphKey key;
+    cudaGraphExec_t exec;
+    int64_t launches;
+    int dev;
+};
+static std::mutex g_agg_mu;
+static AggGraph g_agg_cache[4];
+static int g_agg_n = 0, g_agg_next = 0;
+static cudaStream_t g_agg_stream[64];
+static cudaEvent_t g_agg_ev[64][2];
+
+static int agg_graph_run(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int32_t* roots, AggWs& w,
+                         void* ws, size_t ws_bytes, const DeviceInfo& di, cudaStream_t s, bool* done) {
+    *done = false;
+    if (const char* e = getenv("MIS2_AGG_GRAPH"))
+        if (atoi(e) == 0) return MIS2_OK;
+    int dev = 0;
+    MIS2_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return MIS2_OK;
+    AggGraphKey key;
+    memset(&key, 0, sizeof(key));
+    key.n = g.n;
+    key.nnz = g.nnz;
+    key.rowptr = g.rowptr;
+    key.colinds = g.colinds;
+    key.labels = labels;
+    key.roots = roots;
+    key.ws = ws;
+    key.ws_bytes = ws_bytes;
+    key.seed = o.seed;
+    key.scheme = o.scheme;
+    key.max_iters = o.max_iters;
+    key.group = o.group;
+    key.flags = o.flags;
+    std::lock_guard<std::mutex> lock(g_agg_mu);
+    if (!g_agg_stream[dev]) {
+        MIS2_CUDA_TRY(cudaStreamCreateWithFlags(&g_agg_stream[dev], cudaStreamNonBlocking));
+        MIS2_CUDA_TRY(cudaEventCreateWithFlags(&g_agg_ev[dev][0], cudaEventDisableTiming));
+        MIS2_CUDA_TRY(cudaEventCreateWithFlags(&g_agg_ev[dev][1], cudaEventDisableTiming));
+    }
+    cudaStream_t cs = g_agg_stream[dev];
+    AggGraph* hit = nullptr;
+    for (int i = 0; i < g_agg_n; i++)
+        if (g_agg_cache[i].dev == dev && g_agg_cache[i].key == key) hit = &g_agg_cache[i];
+    if (!hit) {  // first call with this key: run directly, capture on the next one
+        AggGraph& slot = g_agg_cache[g_agg_n < 4 ? g_agg_n++ : (g_agg_next++ & 3)];
+        if (slot.exec) cudaGraphExecDestroy(slot.exec);
+        slot.key = key;
+        slot.exec = nullptr;
+        slot.launches = 0;
+        slot.dev = dev;
+        return MIS2_OK;
+    }
+    MIS2_CUDA_TRY(cudaEventRecord(g_agg_ev[dev][0], s));
+    MIS2_CUDA_TRY(cudaStreamWaitEvent(cs, g_agg_ev[dev][0], 0));
+    if (!hit->exec) {
+        reset_launches();
+        MIS2_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+        const int rc = agg_enqueue(g, o, labels, roots, w, nullptr, nullptr, di, cs);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t ie = (rc == MIS2_OK && ce == cudaSuccess) ? cudaGraphInstantiate(&exec, graph, 0)
+                                                                    : cudaErrorUnknown;
+        if (graph) cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) {  // not capturable here: the caller runs the sequence directly
+            (void)cudaGetLastError();
+            MIS2_CUDA_TRY(cudaStreamWaitEvent(s, g_agg_ev[dev][0], 0));
+            return MIS2_OK;
+        }
+        hit->exec = exec;
+        hit->launches = mis2_last_launch_count();
+    }
+    MIS2_CUDA_TRY(cudaGraphLaunch(hit->exec, cs));
+    MIS2_CUDA_TRY(cudaEventRecord(g_agg_ev[dev][1], cs));
+    MIS2_CUDA_TRY(cudaStreamWaitEvent(s, g_agg_ev[dev][1], 0));
+    reset_launches();
+    count_launch((int)hit->launches);
+    *done = true;
+    return MIS2_OK;
+}
+
+int run_aggregate(const mis2_graph& g, const mis2_opts& o, int32_t* labels, int64_t* num_aggs, int32_t* roots,
+                  int64_t* stats, void* ws, size_t ws_bytes, cudaStream_t s, size_t* bytes_needed) {
+    DeviceInfo di;
+    MIS2_TRY(device_info(&di));
+    Carve c(ws, ws_bytes);
+    AggWs w;
+    carve_agg(c, g.n, g.nnz, max_coop_warps(di), &w);
+    if (bytes_needed) { *bytes_needed = c.off; return MIS2_OK; }
+    if (!c.ok()) { set_error("workspace too small: need %zu bytes", c.off); return MIS2_ENOMEM; }
+    const int64_t n = g.n;
+
+    // per-iteration worklist statistics of both MIS-2 calls (MIS2_FLAG_ITER_STATS)
+    const bool iter_stats = stats && (o.flags & MIS2_FLAG_ITER_STATS) && !(o.flags & MIS2_FLAG_TIMELINE);
+    const int64_t mi = max_iters_for(n, o.max_iters);
+    int64_t* ist1 = iter_stats ? stats + 8 : nullptr;
+    int64_t* ist2 = iter_stats ? stats + 8 + 6 * mi : nullptr;
+    if (iter_stats) memset(stats + 8, 0, sizeof(int64_t) * 12 * (size_t)mi);
+
+    bool done = false;
+    const bool graphable = !iter_stats && !(o.flags & MIS2_FLAG_TIMELINE) && !agg_use_sub(g) &&
+                           (double)g.n * 8.0 <= 64.0 * 1048576.0 && g.n > 0;
+    if (graphable) MIS2_TRY(agg_graph_run(g, o, labels, roots, w, ws, ws_bytes, di, s, &done));
+    if (!done) MIS2_TRY(agg_enqueue(g, o, labels, roots, w, ist1, ist2, di, s));
 
     long long h[32];
     MIS2_CUDA_TRY(cudaMemcpyAsync(h, w.scal, sizeof(h), cudaMemcpyDeviceToHost, s));

@@ -707,3 +707,45 @@ def test_aggregate_phase2_forms(sub, monkeypatch):
     for g in gs:
         check_agg(g)
         check_agg(g, seed=3, decide="push")
+
+
+def test_aggregate_graph_replay():
+    """Repeated mis2_aggregate() calls on the same buffers: the first runs
+    directly, the second captures the launch sequence into a CUDA graph, the
+    later ones replay it -- every result equals the oracle's, also after the
+    buffers are refilled with another graph of the same size (a replay reads
+    the current contents)."""
+    import ctypes
+    m = M()
+    g1 = G.laplace3d_27pt(14)
+    # a second graph with exactly g1's n and nnz: g1 with its ids permuted
+    perm = np.random.RandomState(3).permutation(g1.n)
+    inv = np.argsort(perm)
+    rows = [np.sort(perm[g1.colinds[g1.rowptr[inv[v]]:g1.rowptr[inv[v] + 1]]]) for v in range(g1.n)]
+    rp2 = np.zeros(g1.n + 1, dtype=np.int64)
+    rp2[1:] = np.cumsum([len(r) for r in rows])
+    ci2 = np.concatenate(rows).astype(np.int32)
+    rp, ci = dev(g1)
+    gg, n, nnz = m._graph(rp, ci)
+    o = m._opts(0, "xorstar", 0, 0)
+    ws, wsb = m.workspace(m.OP_AGGREGATE, n, nnz)
+    labels = torch.empty(n, dtype=torch.int32, device="cuda")
+    roots = torch.empty(n, dtype=torch.int32, device="cuda")
+    na = ctypes.c_int64(0)
+    st = np.zeros(8, dtype=np.int64)
+
+    def call_and_check(rowptr, colinds):
+        rc = m.lib().mis2_aggregate(ctypes.byref(gg), ctypes.byref(o), labels.data_ptr(), ctypes.byref(na),
+                                    roots.data_ptr(), st.ctypes.data, ws.data_ptr(), wsb, m._stream())
+        assert rc == 0
+        ref = O.aggregate(rowptr, colinds)
+        assert na.value == ref.num_aggs
+        assert np.array_equal(labels.cpu().numpy(), ref.labels)
+        assert np.array_equal(roots.cpu().numpy()[:ref.num_aggs], ref.roots[:ref.num_aggs])
+
+    for _ in range(3):
+        call_and_check(g1.rowptr, g1.colinds)
+    rp.copy_(torch.from_numpy(rp2))
+    ci.copy_(torch.from_numpy(ci2))
+    for _ in range(2):
+        call_and_check(rp2, ci2)
