@@ -192,6 +192,14 @@ def sub_records(m, torch, flush, stream, peak, steps: int, c2=None):
         out.append({"config": name, "configs_index": cfg, "n": g.n, "nnz": g.nnz, "ms": med, "ms_min": mn,
                     "gteps": g.nnz / (med / 1e3) / 1e9, "iterations": ref.iterations, "mis2_size": ref.count,
                     "alg_bytes": b, "achieved_gbs": b / (med / 1e3) / 1e9, "frac": b / (med / 1e3) / 1e9 / peak})
+        if cfg == 4:  # configs[4]'s workload: repeated aggregation + coarsening down to < 1000 vertices
+            levels, _, _ = m.multilevel(rp, ci, threshold=1000)
+            med, mn = time_calls(lambda: m.multilevel(rp, ci, threshold=1000), min(steps, 5), flush, stream, torch)
+            out.append({"config": "C5 multilevel aggregation + coarsening to < 1000 vertices", "configs_index": 4,
+                        "n": g.n, "nnz": g.nnz, "ms": med, "ms_min": mn,
+                        "levels": [{"n": int(a), "nnz": int(b_), "num_aggs": int(c)} for a, b_, c in levels],
+                        "note": "levels x (aggregate + coarsen) through the Python API (host reads of each level's "
+                                "aggregate count and coarse size between levels)"})
         del rp, ci, res
         torch.cuda.empty_cache()
     if c2 is not None:
