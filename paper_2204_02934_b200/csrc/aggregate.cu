@@ -1126,6 +1126,11 @@ static int agg_graph_run(const mis2_graph& g, const mis2_opts& o, int32_t* label
     int dev = 0;
     MIS2_CUDA_TRY(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64) return MIS2_OK;
+    {  // the caller is capturing its own graph: stay a plain sequence inside it
+        cudaStreamCaptureStatus cs_status = cudaStreamCaptureStatusNone;
+        MIS2_CUDA_TRY(cudaStreamIsCapturing(s, &cs_status));
+        if (cs_status != cudaStreamCaptureStatusNone) return MIS2_OK;
+    }
     AggGraphKey key;
     memset(&key, 0, sizeof(key));
     key.n = g.n;
