@@ -228,6 +228,7 @@ struct __align__(16) TileSmem {
     int nhuge;       // deferred rows too long for a warp
     int64_t nx_s, nx_e;  // dense phase, thread 0: colinds span of the step after the next
     int pending;         // a phase prologue was issued and not yet run (PhaseState)
+    int gen0;            // buf[0] written by the generic proxy (push_halo's scan)
     uint64_t red64[kMW];
     int wred[kMW];
 };
@@ -945,8 +946,9 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t se
         dbuf[63] = e;
     }
     __syncthreads();
+    // no trailing barrier: every caller's next step is a barrier (grid or
+    // partition sync, halo push) before sm.cnt is written again
     const int out = sm.cnt;
-    __syncthreads();
     return out;
 }
 
@@ -990,8 +992,11 @@ __device__ __forceinline__ void dense_begin(TileSmem& sm, const MisParams& p, co
     PhaseState ps;
     const int t = threadIdx.x, g = t / G;
     if (t == 0) {
-        if (sm.nhuge) fence_proxy_async();  // buf[0] held the huge-row list (generic writes)
+        // buf[0] held the huge-row list or the halo scan (generic writes)
+        // before the bulk copy refills it
+        if (sm.nhuge || sm.gen0) fence_proxy_async();
         sm.nhuge = 0;
+        sm.gen0 = 0;
         sm.cnt = 0;
         sm.hcount = 0;
     }
@@ -1172,8 +1177,11 @@ __device__ __forceinline__ void sparse_begin(TileSmem& sm, const MisParams& p, i
     constexpr int RPBS = kMB / GS;
     const int t = threadIdx.x, gs = t / GS, sub = t % GS;
     if (t == 0) {
-        if (sm.nhuge) fence_proxy_async();  // buf[0] held the huge-row list (generic writes)
+        // buf[0] held the huge-row list or the halo scan (generic writes)
+        // before the bulk copy refills it
+        if (sm.nhuge || sm.gen0) fence_proxy_async();
         sm.nhuge = 0;
+        sm.gen0 = 0;
         sm.cnt = 0;
         sm.hcount = 0;
     }
@@ -1399,8 +1407,9 @@ __device__ int decide_push(TileSmem& sm, const MisParams& p, int it, const Rows&
     }
     stats_flush<STATS>(p, it, 0, st);
     __syncthreads();
+    // no trailing barrier: every caller's next step is a barrier (grid or
+    // partition sync, halo push) before sm.cnt is written again
     const int out = sm.cnt;
-    __syncthreads();
     return out;
 }
 
@@ -1429,6 +1438,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
 
     if (t == 0) {
         sm.nhuge = 0;
+        sm.gen0 = 0;
         sm.pending = 0;
         s_nin = 0;
         {
@@ -1740,6 +1750,7 @@ __device__ __forceinline__ void push_halo(TileSmem& sm, const PartK& pk, const R
     const int t = threadIdx.x;
     const int64_t per = (rows.nruns + kMB - 1) / kMB;  // runs of this thread: [t * per, t * per + per)
     int64_t* pre = reinterpret_cast<int64_t*>(sm.buf[0]);  // [kMB + 1] exclusive prefix of the groups' counts
+    if (t == 0) sm.gen0 = 1;
     int64_t cnt = 0;
     for (int64_t k = t * per; k < rows.nruns && k < (t + 1) * per; k++)
         cnt += pk.send_csp[(rows.run_hi(k) + 7) >> 3] - pk.send_csp[rows.run_lo(k) >> 3];
@@ -1800,6 +1811,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_dist_persistent(con
     unsigned int e = epoch0;
     if (t == 0) {
         sm.nhuge = 0;
+        sm.gen0 = 0;
         sm.pending = 0;
         {
             uint64_t pol;
