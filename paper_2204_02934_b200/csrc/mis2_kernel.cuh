@@ -888,7 +888,10 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
 // Deferred long rows, stats flush, survivor count.  Warps take deferred rows
 // from a shared counter and reduce one row each; rows longer than
 // kHugeRow are reduced afterwards by the whole block, one at a time.
-constexpr int kHugeRow = 32768;
+#ifndef MIS2_HUGE_ROW
+#define MIS2_HUGE_ROW 32768
+#endif
+constexpr int kHugeRow = MIS2_HUGE_ROW;
 template <bool STATS, int PH, bool PUSH>
 __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t seg, int32_t* lout, uint64_t fi_next,
                             Stat& st) {
