@@ -48,5 +48,36 @@ for g in [G.config_graph(0), G.laplace3d_7pt(30)]:
     cg = m.ClusterSGS(rpv, civ, torch.from_numpy(vals).cuda(), labels=av.labels, num_aggs=av.num_aggs)
     cg.apply(torch.ones(gv.n, dtype=torch.float64, device="cuda"), sweeps=1)
     cg.close()
+# round 2 session c paths: repeated aggregate() on fixed buffers (the third
+# call replays the captured CUDA graph), and the skewed-graph launch choices
+# forced on a power-law graph (deferral beyond one gather batch, one-minimum
+# 32-bit keys, evict_last gathers)
+import ctypes
+g = G.laplace3d_7pt(20)
+rp, ci = torch.from_numpy(g.rowptr).cuda(), torch.from_numpy(g.colinds).cuda()
+oa = O.aggregate(g.rowptr, g.colinds)
+gg, n, nnz = m._graph(rp, ci)
+opt = m._opts(0, "xorstar", 0, 0)
+ws, wsb = m.workspace(m.OP_AGGREGATE, n, nnz)
+lab = torch.empty(n, dtype=torch.int32, device="cuda")
+roots = torch.empty(n, dtype=torch.int32, device="cuda")
+na = ctypes.c_int64(0)
+st = np.zeros(8, dtype=np.int64)
+for _ in range(3):
+    rc = m.lib().mis2_aggregate(ctypes.byref(gg), ctypes.byref(opt), lab.data_ptr(), ctypes.byref(na), roots.data_ptr(),
+                                st.ctypes.data, ws.data_ptr(), wsb, m._stream())
+    assert rc == 0 and na.value == oa.num_aggs and np.array_equal(lab.cpu().numpy(), oa.labels)
+os.environ["MIS2_HEAVY_BATCHES_RT"] = "1"
+os.environ["MIS2_GATHER_KEEP"] = "1"
+g = G.random_powerlaw_graph(3000, 30, 3)
+rp, ci = torch.from_numpy(g.rowptr).cuda(), torch.from_numpy(g.colinds).cuda()
+o = O.mis2(g.rowptr, g.colinds)
+for decide in ("pull", "push"):
+    r = m.mis2(rp, ci, decide=decide, keys="on")
+    assert r.count == o.count and np.array_equal(r.in_set.cpu().numpy().astype(bool), o.in_set)
+oa = O.aggregate(g.rowptr, g.colinds)
+a = m.aggregate(rp, ci, keys="on")
+assert a.num_aggs == oa.num_aggs and np.array_equal(a.labels.cpu().numpy(), oa.labels)
+del os.environ["MIS2_HEAVY_BATCHES_RT"], os.environ["MIS2_GATHER_KEEP"]
 torch.cuda.synchronize()
 print("sanitize workload ok")
