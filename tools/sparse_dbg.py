@@ -32,3 +32,11 @@ if (d[:, 59] > 0).any():
     per_sm_first = np.array([ends[sm == s].min() for s in np.unique(sm)])
     print(f"SMs {len(per_sm_last)}: last block end median {np.median(per_sm_last):.2f} max {per_sm_last.max():.2f}; "
           f"first block end median {np.median(per_sm_first):.2f}")
+# deferred (long) rows of the phase, per block (finish_phase: dbuf[60] start, [61] rows, [62] end, [63] entries)
+hv = d[:, 60] > 0
+if hv.any():
+    dur = (d[hv, 62] - d[hv, 60]) / 1e3
+    endh = (d[hv, 62] - t0) / 1e3
+    print(f"deferred rows: blocks {hv.sum()}  rows/block median {np.median(d[hv,61]):.0f} max {d[hv,61].max()}  "
+          f"entries/block median {np.median(d[hv,63]):.0f} max {d[hv,63].max()}  "
+          f"time median {np.median(dur):.1f} max {dur.max():.1f} us  end median {np.median(endh):.1f} max {endh.max():.1f} us")
