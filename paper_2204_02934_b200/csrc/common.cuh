@@ -150,10 +150,15 @@ struct SumBarrier {
 // grid_wait_sum.
 // sb lives in shared memory (only thread 0 touches it; fewer registers)
 __device__ __forceinline__ unsigned long long grid_arrive_sum(unsigned long long* ctr, const SumBarrier& sb,
-                                                              unsigned long long val) {
+                                                              unsigned long long val,
+                                                              unsigned long long* side = nullptr,
+                                                              unsigned long long side_val = 0ull) {
     __syncthreads();
     unsigned long long old = 0;
     if (threadIdx.x == 0) {
+        // an extra per-block value accumulated beside the barrier (visible to
+        // every block once the barrier completes: the arrival is a release)
+        if (side && side_val) asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(side), "l"(side_val) : "memory");
         unsigned long long* c = ctr + (sb.k & 1u) * kSumStride;
         const unsigned long long add =
             (blockIdx.x == 0 ? (1ull << 63) - ((unsigned long long)(gridDim.x - 1) << 40) : (1ull << 40)) + val;

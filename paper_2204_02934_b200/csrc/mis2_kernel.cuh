@@ -1579,7 +1579,12 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         if (t == 0) sm.pending = 0;
         // the loop condition rides on the barrier; the next Refresh Column's
         // prologue is issued even if the loop ends (drained below)
-        bold = grid_arrive_sum(sumc, sb, (unsigned long long)cnt1);
+        // the IN decisions of this Decide go to the count beside the barrier
+        __shared__ int s_nin_rep;
+        if (it == 0 && t == 0) s_nin_rep = 0;
+        bold = grid_arrive_sum(sumc, sb, (unsigned long long)cnt1, &p.ctrl[5],
+                               t == 0 ? (unsigned long long)(s_nin - s_nin_rep) : 0ull);
+        if (t == 0) s_nin_rep = s_nin;
         if (MIS2_HOIST) col_begin(it + 1, cnt2, p.L2[cur ^ 1]);
         const unsigned long long remaining = grid_wait_sum(sumc, sb, bold, &s_sum);
         stamp(p, 2 + 2 * it);
@@ -1594,26 +1599,20 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
     __syncthreads();
     drain_pending(sm, ph);
 
-    // return {v : T_v = IN}: written at the decisions (set_IN)
-    l2_release(p, rows);
-    __syncthreads();
-    const long long bc = s_nin;
-    if (t == 0) {
-        atomicAdd(&p.ctrl[5], (unsigned long long)bc);
-        __threadfence();
-        const unsigned long long ticket = atomicAdd(&p.ctrl[6], 1ull);
-        if (ticket == gridDim.x - 1) {  // last block publishes the scalars
-            __threadfence();
-            *p.d_count = (int64_t)ld_acquire_u64(&p.ctrl[5]);
-            *p.d_iters = it;
-            *p.d_status = status;
-            if (p.timeline) {  // timeline: kernel end
-                unsigned long long ns;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
-                p.timeline[2 * p.max_iters + 1] = (long long)ns;
-            }
+    // return {v : T_v = IN}: the mask was written at the decisions
+    // (set_IN) and every Decide's IN count was added beside its barrier, so
+    // after the last barrier the count is complete: block 0 publishes
+    if (blockIdx.x == 0 && t == 0) {
+        *p.d_count = (int64_t)ld_acquire_u64(&p.ctrl[5]);
+        *p.d_iters = it;
+        *p.d_status = status;
+        if (p.timeline) {  // timeline: kernel end (of block 0)
+            unsigned long long ns;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+            p.timeline[2 * p.max_iters + 1] = (long long)ns;
         }
     }
+    l2_release(p, rows);
 }
 
 // ------------------------------------------------------------ partitioned kernel
