@@ -184,6 +184,12 @@ int mis2_host(int64_t n, int64_t nnz, const int64_t* rowptr_h, const int32_t* co
  *   roots    : device int32[n] or NULL; roots[a] = root vertex of aggregate a
  *   stats    : host int64[8] or NULL: |M1|, iters1, |M2|, iters2, accepted
  *              phase-2 roots, phase-3 leftovers, n1, num_aggs
+ * Repeated calls with the same graph pointers, sizes, outputs, workspace and
+ * options (graphs with 8n <= 64 MB and no per-iteration statistics) replay
+ * the call's launch sequence as one CUDA graph captured on the second such
+ * call; it runs on a library-owned stream per device, ordered after and
+ * before the caller's stream by events (calls from several threads then
+ * serialise on that stream).  MIS2_AGG_GRAPH=0 in the environment disables it.
  */
 int mis2_aggregate(const mis2_graph* g, const mis2_opts* o, int32_t* labels, int64_t* num_aggs,
                    int32_t* roots, int64_t* stats, void* ws, size_t ws_bytes, void* stream);
