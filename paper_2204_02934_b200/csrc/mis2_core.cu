@@ -264,6 +264,7 @@ int dist_mis2_launch(const std::vector<PartDev>& parts, const std::vector<uint64
         last_dst = (void*)dk;
     }
     unsigned int e0 = *epoch;
+    MIS2_CUDA_TRY(cudaMemsetAsync(dout + 3, 0, sizeof(unsigned long long), s));  // peer-wait timeout flag
     void* args[] = {&dk, (void*)&nl, &peers, &e0, &max_iters, &dout};
     int nlv = nl;
     args[1] = &nlv;
@@ -276,7 +277,8 @@ int dist_mis2_launch(const std::vector<PartDev>& parts, const std::vector<uint64
     *iters = (int32_t)(h[1] & 0xffffffffull);
     *epoch = (unsigned int)h[2];
     const int st = (int)(int32_t)(h[1] >> 32);
-    if (st != MIS2_OK) set_error("MIS-2 did not converge within max_iters");
+    if (st == MIS2_EINTERNAL) set_error("partition barrier: a peer GPU did not post within 10 s");
+    else if (st != MIS2_OK) set_error("MIS-2 did not converge within max_iters");
     return st;
 }
 

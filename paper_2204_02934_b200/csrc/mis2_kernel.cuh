@@ -1679,8 +1679,12 @@ __device__ __forceinline__ void part_barrier(unsigned int* bar, int lb, int nblk
 // that global sum to every block.  Mailboxes are double buffered by epoch
 // parity: a partition can post e + 2 only after every partition has posted
 // e + 1, i.e. after every leader has read the posts of e.
+// A leader that waits more than kPeerWaitNs for a peer partition's post (a
+// GPU of the job gone or hung) sets *tflag, treats the missing posts as 0 --
+// so the loop ends -- and the call returns MIS2_EINTERNAL instead of hanging.
+constexpr unsigned long long kPeerWaitNs = 10000000000ull;  // 10 s
 static __device__ unsigned long long part_sync(const PartK& pk, const PeerTab& peers, int lb, unsigned int e,
-                                        unsigned long long value) {
+                                        unsigned long long value, unsigned long long* tflag) {
     __syncthreads();
     if (threadIdx.x == 0) {
         if (value) atomicAdd(&pk.acc[e & 1], value);
@@ -1708,6 +1712,9 @@ static __device__ unsigned long long part_sync(const PartK& pk, const PeerTab& p
                 else asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(dst), "l"(post) : "memory");
             }
             unsigned long long sum = 0;
+            unsigned long long t0;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            bool dead = *(volatile unsigned long long*)tflag != 0ull;
             for (int q = 0; q < peers.P; q++) {
                 unsigned long long v;
                 const unsigned long long* src = pk.box + (e & 1) * peers.P + q;
@@ -1715,10 +1722,19 @@ static __device__ unsigned long long part_sync(const PartK& pk, const PeerTab& p
                     if (peers.sys) asm volatile("ld.acquire.sys.u64 %0,[%1];" : "=l"(v) : "l"(src) : "memory");
                     else asm volatile("ld.acquire.gpu.u64 %0,[%1];" : "=l"(v) : "l"(src) : "memory");
                     if ((unsigned int)(v >> 32) == e) break;
+                    unsigned long long now;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                    if (dead || now - t0 > kPeerWaitNs) {
+                        dead = true;
+                        *(volatile unsigned long long*)tflag = 1ull;
+                        v = 0ull;
+                        break;
+                    }
                     __nanosleep(64);
                 }
                 sum += v & 0xffffffffull;
             }
+            if (dead) sum = 0ull;
             asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(pk.rel), "l"(((unsigned long long)e << 32) | sum)
                          : "memory");
             s_sum = sum;
@@ -1864,7 +1880,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_dist_persistent(con
     // ghost T / M of iteration 0 (inactive ghosts: T = OUT, M = 0)
     push_halo<uint64_t>(sm, pk, rows, p.T, peers.T);
     push_halo<uint32_t>(sm, pk, rows, p.M, peers.M);
-    const unsigned long long n_active = part_sync(pk, peers, lb, ++e, (unsigned long long)act_block);
+    const unsigned long long n_active = part_sync(pk, peers, lb, ++e, (unsigned long long)act_block, out + 3);
 
     int it = 0, status = MIS2_OK;
     const int64_t range = rows.count;
@@ -1876,14 +1892,14 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_dist_persistent(con
         cnt2 = dense2 ? dense_phase<G, false, 0>(sm, p, it, rows, p.L2[cur ^ 1], ph, 0)
                       : sparse_phase<G, false, 0>(sm, p, it, rows.seg, p.L2[cur], cnt2, p.L2[cur ^ 1], ph, 0);
         push_halo<uint32_t>(sm, pk, rows, p.M, peers.M);
-        part_sync(pk, peers, lb, ++e, 0ull);
+        part_sync(pk, peers, lb, ++e, 0ull, out + 3);
         // ---- Decide over worklist_1 + fused refresh; ghost T pushed
         const uint64_t fi_next = p.prio.iter_term(it + 1);
         const bool dense1 = (int64_t)cnt1 * kDenseDen >= range * kDenseNum;
         cnt1 = dense1 ? dense_phase<G, false, 1>(sm, p, it, rows, p.L1[cur ^ 1], ph, fi_next)
                       : sparse_phase<G, false, 1>(sm, p, it, rows.seg, p.L1[cur], cnt1, p.L1[cur ^ 1], ph, fi_next);
         push_halo<uint64_t>(sm, pk, rows, p.T, peers.T);
-        const unsigned long long remaining = part_sync(pk, peers, lb, ++e, (unsigned long long)cnt1);
+        const unsigned long long remaining = part_sync(pk, peers, lb, ++e, (unsigned long long)cnt1, out + 3);
         it++;
         if (remaining == 0) break;
         if (it >= max_iters) {  // reading Q12
@@ -1901,9 +1917,10 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_dist_persistent(con
         cnt += in;
     }
     const long long bc = block_sum_int(sm, cnt);
-    const unsigned long long total = part_sync(pk, peers, lb, ++e, (unsigned long long)bc);
+    const unsigned long long total = part_sync(pk, peers, lb, ++e, (unsigned long long)bc, out + 3);
     if (blockIdx.x == 0 && t == 0) {
         out[0] = total;
+        if (*(volatile unsigned long long*)(out + 3)) status = MIS2_EINTERNAL;  // a peer never arrived
         out[1] = (unsigned long long)(unsigned)it | ((unsigned long long)(unsigned)status << 32);
         out[2] = e;  // the last epoch used
     }
