@@ -24,12 +24,17 @@
 //    status words (M_v != OUT for worklist_2, T_v undecided for worklist_1).
 //  * Sparse phases read the block's compacted worklist; each row group
 //    leader bulk-copies its row into a shared-memory slot one step ahead.
-//    Rows longer than heavy_len<G>() are deferred to warps, rows longer than
-//    kHugeRow to the whole block.
+//    Rows longer than heavy_len<G>() (skewed graphs: one gather batch of
+//    the lane group) are deferred to warps, rows longer than kHugeRow to the
+//    whole block.
 //  * Neighbour loops issue batches of independent gathers (indices clamped
 //    to the row's last entry: min / exists / forall are idempotent).
-//  * Phases are separated by a grid-wide barrier; |worklist_1| == 0
-//    is tested on the device, so one call is 1 memset + 1 kernel launch.
+//  * Phases are separated by a split-phase grid barrier that also sums the
+//    loop condition |worklist_1|, so one call is 1 memset + 1 kernel
+//    launch; each phase's prologue (first tile's bulk copy, first rows'
+//    bounds and own status) is issued between the block's arrival and its
+//    wait (PhaseState).  The IN decisions write the output mask directly and
+//    their count rides beside the barrier.
 //  * Refresh Row of iteration i+1 is fused into Decide of
 //    iteration i; iteration 0's refresh is the init phase.
 //  * 64-bit status words (Eq. 1, reading Q6): a min is one compare.
