@@ -637,8 +637,12 @@ __global__ void __launch_bounds__(32 * kListWarps) k_phase3_list(const int32_t* 
 // candidate aggregates counted in the warp's shared-memory table (match
 // groups of each 32-entry chunk add at once); a table overflow -> heavy.
 constexpr int kP3Slots = 128;
+// longq == nullptr: every listed leftover (rows mostly longer than the list
+// kernel's groups: no listing pass, whose one append per row serialises on
+// its counter -- C5 1.1 ms)
 __global__ void __launch_bounds__(32 * kListWarps) k_phase3_table(const int32_t* __restrict__ left,
                                                                   const int32_t* __restrict__ longq, const int* longq_cnt,
+                                                                  const unsigned long long* nleft,
                                                                   const int64_t* __restrict__ rowptr,
                                                                   const int32_t* __restrict__ colinds,
                                                                   const int32_t* __restrict__ labels,
@@ -650,9 +654,9 @@ __global__ void __launch_bounds__(32 * kListWarps) k_phase3_table(const int32_t*
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int32_t* key = tkey[wib];
     int32_t* cnt = tcnt[wib];
-    const int64_t m = *longq_cnt;
+    const int64_t m = longq ? (int64_t)*longq_cnt : (int64_t)*nleft;
     for (int64_t q = (int64_t)blockIdx.x * kListWarps + wib; q < m; q += (int64_t)gridDim.x * kListWarps) {
-        const int32_t i = longq[q];
+        const int32_t i = longq ? longq[q] : (int32_t)q;
         const int32_t v = left[i];
         const int64_t s = rowptr[v], e = rowptr[v + 1];
 #pragma unroll
@@ -1070,15 +1074,20 @@ static int agg_enqueue(const mis2_graph& g, const mis2_opts& o, int32_t* labels,
         count_launch();
     }
     const unsigned long long* nleft = (const unsigned long long*)&w.scal[kLeft];
-    LIST_DISPATCH(GL, (k_phase3_list<GLL><<<lgrid, 32 * kListWarps, 0, s>>>(
-                          w.left, nleft, g.rowptr, g.colinds, labels, w.size, w.tent, w.longq, &s32[2 * kHeavyCnt + 1],
-                          w.heavy, &s32[2 * kHeavyCnt])));
-    k_phase3_table<<<lgrid, 32 * kListWarps, 0, s>>>(w.left, w.longq, &s32[2 * kHeavyCnt + 1], g.rowptr, g.colinds,
-                                                     labels, w.size, w.tent, w.heavy, &s32[2 * kHeavyCnt]);
+    // rows mostly longer than 32 entries (C5: 81): every leftover goes
+    // straight to the table kernel (a warp per row)
+    const bool all_long = avg > 32.0;
+    if (!all_long)
+        LIST_DISPATCH(GL, (k_phase3_list<GLL><<<lgrid, 32 * kListWarps, 0, s>>>(
+                              w.left, nleft, g.rowptr, g.colinds, labels, w.size, w.tent, w.longq,
+                              &s32[2 * kHeavyCnt + 1], w.heavy, &s32[2 * kHeavyCnt])));
+    k_phase3_table<<<lgrid, 32 * kListWarps, 0, s>>>(w.left, all_long ? nullptr : w.longq, &s32[2 * kHeavyCnt + 1],
+                                                     nleft, g.rowptr, g.colinds, labels, w.size, w.tent, w.heavy,
+                                                     &s32[2 * kHeavyCnt]);
     k_phase3_heavy<<<di.sms * 4, kBlock, 0, s>>>(g.rowptr, g.colinds, labels, w.size, labels, w.heavy,
                                                 &s32[2 * kHeavyCnt], &s32[2 * kErr], w.left, w.tent);
     k_scatter_choice<<<(unsigned)(di.sms * 8), kBlock, 0, s>>>(w.left, nleft, w.tent, labels, &s32[2 * kErr]);
-    count_launch(4);
+    count_launch(all_long ? 3 : 4);
     k_finish<<<1, 1, 0, s>>>(&s32[2 * kN1], &s32[2 * kN2], (int64_t*)&w.scal[kNa]);
     count_launch();
     }  // Alg. 3
