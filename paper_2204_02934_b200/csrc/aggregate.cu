@@ -732,7 +732,17 @@ __global__ void __launch_bounds__(32 * kListWarps) k_sub_len(const int32_t* __re
         if (i < cnt) {
             const int32_t v = gid[i];
             const int64_t s = rowptr[v], e = rowptr[v + 1];
-            for (int64_t j = s + li.sub; j < e; j += GL) c += act[colinds[j]];
+            constexpr int U = 4;  // steps of the row in flight (the walk is latency bound)
+            for (int64_t j0 = s + li.sub; j0 < e; j0 += (int64_t)GL * U) {
+                int32_t w[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int64_t j = j0 + (int64_t)u * GL;
+                    w[u] = j < e ? colinds[j] : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) c += w[u] >= 0 ? act[w[u]] : 0;
+            }
         }
         c = group_sum<GL>(c);
         if (i < cnt && li.sub == 0) len[i] = c;
@@ -770,14 +780,25 @@ __global__ void __launch_bounds__(32 * kListWarps) k_sub_fill(const int32_t* __r
             const int64_t y = __shfl_xor_sync(kFull, maxsteps, off);
             maxsteps = y > maxsteps ? y : maxsteps;
         }
-        for (int64_t k = 0; k < maxsteps; k++) {
-            const int64_t j = s + k * GL + li.sub;
-            int32_t w = -1;
-            if (j < e) w = colinds[j];
-            const bool a = w >= 0 && act[w];
-            const unsigned ball = __ballot_sync(kFull, a) & gmask;
-            if (a) scol[o + __popc(ball & lanemask_lt())] = inv[w];
-            o += __popc(ball);
+        constexpr int U = 4;  // steps in flight: colinds, then act, then inv of U steps
+        for (int64_t k0 = 0; k0 < maxsteps; k0 += U) {
+            int32_t w[U], x[U];
+            bool a[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int64_t j = s + (k0 + u) * GL + li.sub;
+                w[u] = j < e ? colinds[j] : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) a[u] = w[u] >= 0 && act[w[u]];
+#pragma unroll
+            for (int u = 0; u < U; u++) x[u] = a[u] ? inv[w[u]] : 0;
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const unsigned ball = __ballot_sync(kFull, a[u]) & gmask;
+                if (a[u]) scol[o + __popc(ball & lanemask_lt())] = x[u];
+                o += __popc(ball);
+            }
         }
     }
 }
