@@ -13,6 +13,8 @@
 //      distinct; else a block per segment up to 2047 distinct); segments with
 //      more distinct labels use an na-bit bitmap (ordered compaction = sorted unique)
 //   5. c_rowptr = exclusive scan(unique counts); copy out.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -324,7 +326,13 @@ int run_coarsen(const mis2_graph& g, const int32_t* labels, int64_t na, int64_t*
     if (!c.ok()) { set_error("workspace too small: need %zu bytes", c.off); return MIS2_ENOMEM; }
     if (na < 0 || na > nab || (n > 0 && na == 0)) { set_error("num_aggs out of range"); return MIS2_EINVAL; }
 
-    const int G = choose_group(g.n, g.nnz, 0);
+    // lanes per row of the fill: a quarter of the MIS-2 kernels' group for
+    // long rows -- each lane's distinct-label list then sees more of its
+    // row (C5, G = 1 / 2 / 4 / 8 / 32: 2.17 / 2.37 / 2.79 / 3.49 / 6.21 ms;
+    // C3 at 1 / 2 / 4: 4.23 / 4.56 / 5.15 ms; C2 0.273 / 0.288 ms)
+    int G = choose_group(g.n, g.nnz, 0);
+    if (G >= 4) G /= 4;
+    if (const char* e = getenv("MIS2_COARSEN_G")) G = atoi(e);  // measurement knob (1..32, power of 2)
     int64_t blocks = (n + kBlock - 1) / kBlock;
     if (blocks > (int64_t)di.sms * 16) blocks = (int64_t)di.sms * 16;
     if (blocks < 1) blocks = 1;
