@@ -1045,7 +1045,10 @@ static int agg_enqueue(const mis2_graph& g, const mis2_opts& o, int32_t* labels,
     int32_t* d_m = &s32[2 * kN2 + 1];
     MIS2_TRY(scan_flags_list(w.acc, n, nullptr, inv, gid, nullptr, d_m, w.scan_tmp, s));
     // the subgraph build is latency bound: several rows per warp (GL <= 8)
-    const int GS = GL < 8 ? GL : 8;
+    // (C3, 7-entry rows, GS = 2 / 4 / 8: 12.5 / 8.8 / 9.4 ms; C5, 81-entry
+    // rows, 4 / 8 / 16: 12.4 / 12.0 / 12.5 ms)
+    int GS = GL <= 8 ? 4 : 8;
+    if (const char* e = getenv("MIS2_SUB_G")) GS = atoi(e);  // measurement knob: 4 / 8 / 16 / 32
     LIST_DISPATCH(GS, (k_sub_len<GLL><<<lgrid, 32 * kListWarps, 0, s>>>(gid, d_m, g.rowptr, g.colinds, w.acc,
                                                                       w.slen)));
     count_launch();
