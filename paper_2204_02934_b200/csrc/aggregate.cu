@@ -988,7 +988,8 @@ static int agg_enqueue(const mis2_graph& g, const mis2_opts& o, int32_t* labels,
     // lanes per list entry: the average row length rounded up to a power of
     // two in [4, 32] (short rows: several entries per warp)
     const double avg = n > 0 ? (double)g.nnz / (double)n : 0.0;
-    const int GL = avg <= 4.0 ? 4 : (avg <= 8.0 ? 8 : (avg <= 16.0 ? 16 : 32));
+    int GL = avg <= 4.0 ? 4 : (avg <= 8.0 ? 8 : (avg <= 16.0 ? 16 : 32));
+    if (const char* e = getenv("MIS2_AGG_GL")) GL = atoi(e);  // measurement knob: 4 / 8 / 16 / 32
 #define LIST_DISPATCH(gl, CALL)                             \
     switch (gl) {                                           \
         case 4: { constexpr int GLL = 4; CALL; } break;     \
