@@ -241,6 +241,12 @@ int mis2_comm_init_nccl(const uint8_t* id128, int nranks, int rank, mis2_comm** 
 int mis2_comm_init_local(int nparts, mis2_comm** out);
 int mis2_comm_set_graph(mis2_comm* c, int64_t n_global, const int64_t* rowptr_h, const int32_t* colinds_h,
                         void* stream);
+/* One launch of the partitioned persistent kernel per call (halo words
+ * stored straight into the peers' ghost slots, partitions meeting at a
+ * device-side mailbox barrier).  If a peer partition does not post at a
+ * barrier within 10 s (a GPU of the job gone or hung) the call gives up and
+ * returns MIS2_EINTERNAL instead of hanging; the communicator is then
+ * unusable. */
 int mis2_dist_mis2(mis2_comm* c, const mis2_opts* o, uint8_t* in_set, int64_t* count, int32_t* iters,
                    void* stream);
 /* Alg. 3 over the partition, bit-identical to mis2_aggregate():
