@@ -636,7 +636,10 @@ __global__ void __launch_bounds__(32 * kListWarps) k_phase3_list(const int32_t* 
 // Phase 3 for the longer listed rows: a warp per row, the couplings of its
 // candidate aggregates counted in the warp's shared-memory table (match
 // groups of each 32-entry chunk add at once); a table overflow -> heavy.
-constexpr int kP3Slots = 128;
+#ifndef MIS2_P3_SLOTS
+#define MIS2_P3_SLOTS 128
+#endif
+constexpr int kP3Slots = MIS2_P3_SLOTS;
 // longq == nullptr: every listed leftover (rows mostly longer than the list
 // kernel's groups: no listing pass, whose one append per row serialises on
 // its counter -- C5 1.1 ms)
