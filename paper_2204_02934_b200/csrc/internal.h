@@ -65,12 +65,13 @@ struct Mis2Ws {
     int32_t* L2[2];
     int32_t* heavy;
     unsigned int* mark;
+    int32_t* gq;        // global queue of deferred rows (skewed graphs, mis2_kernel.cuh MIS2_GQ)
     uint8_t* oflag;     // push-form Decide state (mis2_core.cu)
     uint32_t* cnt;
     uint32_t* degc;
     uint32_t* K;        // 32-bit column keys (mis2_core.cu kkey)
-    unsigned long long* ctrl;  // [48]: [0]=barrier, [5]=count, [6]=ticket, [8]=max degree,
-                               // [16], [32] = the two counters of grid_sync_sum
+    unsigned long long* ctrl;  // [80]: [0]=barrier, [5]=IN count, [8]=max degree,
+                               // [16], [32] = the two counters of grid_sync_sum, [64..67] deferred-row queue
     unsigned long long* maxdeg;  // skew test of run_mis2
     long long* dstats;         // [kStatsMaxIters * 6]
     long long* scal;           // [8] host-visible scalars of mis2()/mis2_host()

@@ -113,7 +113,7 @@ int max_coop_warps(const DeviceInfo& d) { return d.sms * 64; }
 
 void carve_mis2(Carve& c, int64_t n, int64_t nnz, int max_warps, Mis2Ws* w) {
     (void)max_warps;
-    w->ctrl = c.take<unsigned long long>(48);
+    w->ctrl = c.take<unsigned long long>(80);
     w->maxdeg = c.take<unsigned long long>(1);
     w->T = c.take<uint64_t>((size_t)n + 1);
     w->M = c.take<uint32_t>((size_t)n + 1);
@@ -123,6 +123,7 @@ void carve_mis2(Carve& c, int64_t n, int64_t nnz, int max_warps, Mis2Ws* w) {
     }
     w->heavy = c.take<int32_t>((size_t)n + 1);
     w->mark = c.take<unsigned int>((size_t)n + 1);
+    w->gq = c.take<int32_t>((size_t)n + 1);
     w->oflag = c.take<uint8_t>((size_t)n + 1);
     w->cnt = c.take<uint32_t>((size_t)n + 1);
     w->degc = c.take<uint32_t>((size_t)n + 1);
@@ -406,7 +407,7 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     const int64_t want = (g.n + 2 * rpb - 1) / (2 * rpb);
     const int grid = (int)(want < 1 ? 1 : (want > max_grid ? max_grid : want));
 
-    MIS2_CUDA_TRY(cudaMemsetAsync(w.ctrl, 0, 48 * sizeof(unsigned long long), s));
+    MIS2_CUDA_TRY(cudaMemsetAsync(w.ctrl, 0, 80 * sizeof(unsigned long long), s));
     if (stats) {
         MIS2_CUDA_TRY(cudaMemsetAsync(w.mark, 0, sizeof(unsigned int) * ((size_t)g.n + 1), s));
         MIS2_CUDA_TRY(cudaMemsetAsync(w.dstats, 0, sizeof(long long) * kStatsMaxIters * 6, s));
@@ -481,6 +482,10 @@ int run_mis2(const mis2_graph& g, const mis2_opts& o, const int32_t* labels, uin
     // unchanged).
     p.heavy_batches = skewed ? 1 : 0;
     p.gather_keep = skewed ? 1 : 0;
+    // global queue of deferred rows (compiled into the G = 2 small-tile
+    // kernels only: mis2_g2s.cu); MIS2_GQ_RT=0: off (measurement knob)
+    p.gq = skewed ? w.gq : nullptr;
+    if (const char* e = getenv("MIS2_GQ_RT")) p.gq = atoi(e) ? w.gq : nullptr;
     if (const char* e = getenv("MIS2_GATHER_KEEP")) p.gather_keep = atoi(e);  // measurement knob
     if (const char* e = getenv("MIS2_HEAVY_BATCHES_RT")) p.heavy_batches = atoi(e);  // measurement knob
     p.prio.override_ = o.prio_override;

@@ -3,6 +3,7 @@
 // skewed graph the shared memory they leave is L1, where the hubs' words stay
 // (run_mis2).  Its own namespace (mis2k_s); MisParams has the same layout.
 #define MIS2_TILE_ROWS 160
+#define MIS2_GQ 1  // the skewed graphs' kernel: global queue of deferred rows
 #define mis2k mis2k_s
 #include "mis2_kernel.cuh"
 #undef mis2k

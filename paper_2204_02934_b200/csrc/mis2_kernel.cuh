@@ -146,6 +146,7 @@ struct MisParams {
     float l2_keep;        // fraction of each block's colinds span kept in L2 (evict_last)
     int cyclic;           // row ownership: 0 = one contiguous range per block, 1 = cyclic chunks (Rows)
     int gather_keep;      // 1: key / M gathers carry an L2 evict_last hint (skewed graphs)
+    int32_t* gq;          // MIS2_GQ kernels: global queue of deferred rows (int32[n]), null = off
     int heavy_batches;    // > 0: rows longer than heavy_batches gather batches of their lane group are
                           // deferred to warps (0: MIS2_HEAVY_BATCHES)
     int push_iters;       // PUSH kernels: iterations it < push_iters use the push-form Decide
@@ -219,6 +220,9 @@ __device__ __forceinline__ Rows make_rows(int64_t n, int64_t B, int64_t b, int64
 // per block: the column passes use the 32-bit keys (decided once per call,
 // after the init phase; see the kernel)
 __shared__ int s_use_keys;
+// per block: this iteration's phases use the global deferred-row queue
+// (decided from the global |worklist_1|, so every block agrees)
+__shared__ int s_gq_on;
 
 struct __align__(16) TileSmem {
     int32_t buf[2][kTileCap + 8];
@@ -759,13 +763,29 @@ __device__ __forceinline__ bool process_row(const MisParams& p, bool act, int su
 }
 
 // defer a long row to whole-block processing (group leader decides, group agrees)
+#ifndef MIS2_HUGE_ROW
+#define MIS2_HUGE_ROW 32768
+#endif
+constexpr int kHugeRow = MIS2_HUGE_ROW;
+// Global queue of deferred rows (MIS2_GQ, skewed graphs, p.gq): the rows a
+// block defers are published to one queue after its steps and drained by
+// every warp (rows for a whole block by whole blocks, first), so the long
+// rows of a power-law graph no longer pile up on the blocks that own them
+// (C4: deferred entries per block 1.03 M median, 1.53 M max).  Two extra
+// grid barriers per phase; the owner appends its survivors afterwards.
+#ifndef MIS2_GQ
+#define MIS2_GQ 0
+#endif
+constexpr int kGqChunk = 16;  // rows per warp grab
 template <int GG>
 __device__ __forceinline__ bool defer_long(TileSmem& sm, const MisParams& p, int64_t seg, bool act, int sub,
-                                           int64_t v, int64_t len) {
+                                           int64_t v, int64_t len, bool gq_phase = false) {
     bool defer = false;
     if (act && sub == 0 && len > (p.heavy_batches > 0 ? p.heavy_batches * GG * gather_batch<GG>() : heavy_len<GG>())) {
         const int h = atomicAdd(&sm.hcount, 1);
-        p.heavy[seg + h] = (int32_t)v;  // at most one entry per row of the block's segment
+        // at most one entry per row of the block's segment; with the global
+        // queue (MIS2_GQ) rows for a whole block are marked ~v
+        p.heavy[seg + h] = (MIS2_GQ && gq_phase && p.gq && s_gq_on && len > kHugeRow) ? ~(int32_t)v : (int32_t)v;
         defer = true;
     }
     return __shfl_sync(kFull, defer, (threadIdx.x & 31) & ~(GG - 1));
@@ -893,10 +913,7 @@ __device__ bool heavy_row(TileSmem& sm, const MisParams& p, int it, uint64_t fi_
 // Deferred long rows, stats flush, survivor count.  Warps take deferred rows
 // from a shared counter and reduce one row each; rows longer than
 // kHugeRow are reduced afterwards by the whole block, one at a time.
-#ifndef MIS2_HUGE_ROW
-#define MIS2_HUGE_ROW 32768
-#endif
-constexpr int kHugeRow = MIS2_HUGE_ROW;
+
 template <bool STATS, int PH, bool PUSH>
 __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t seg, int32_t* lout, uint64_t fi_next,
                             Stat& st) {
@@ -913,6 +930,75 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t se
         dbuf[61] = nh;
     }
     int32_t* huge = sm.buf[0];  // rows for the whole block (<= nh <= the buffer)
+#if MIS2_GQ
+    // column passes only: a Decide's deferred rows mostly stop at their first
+    // OUT neighbour, and their grabs cost more than the balance saves (C4
+    // Decide 3: 1.09 -> 1.12 ms with the queue)
+    if (!STATS && PH == 0 && p.gq && s_gq_on) {
+        unsigned long long* qc = p.ctrl + 64;  // [0] rows, [1] warp head, [2] whole-block rows, [3] block head
+        unsigned int* gbar = (unsigned int*)&p.ctrl[0];
+        // publish: counts of the two kinds, one reservation each
+        int nhb = 0;
+        for (int i = t; i < nh; i += kMB) nhb += p.heavy[seg + i] < 0;
+        const int nhuge_blk = (int)block_sum_int(sm, nhb);
+        __shared__ unsigned long long s_base[2];
+        if (t == 0) {
+            s_base[0] = nh - nhuge_blk ? atomicAdd(&qc[0], (unsigned long long)(nh - nhuge_blk)) : 0ull;
+            s_base[1] = nhuge_blk ? atomicAdd(&qc[2], (unsigned long long)nhuge_blk) : 0ull;
+            sm.hnext = 0;
+            sm.nhuge = 0;
+        }
+        __syncthreads();
+        for (int i = t; i < nh; i += kMB) {
+            const int32_t x = p.heavy[seg + i];
+            if (x >= 0) p.gq[s_base[0] + atomicAdd(&sm.hnext, 1)] = x;
+            else p.gq[p.n - 1 - (int64_t)(s_base[1] + atomicAdd(&sm.nhuge, 1))] = ~x;  // from the end
+        }
+        grid_barrier(gbar);  // every block's deferred rows are in the queue
+        const int64_t nq = (int64_t)*(volatile unsigned long long*)&qc[0];
+        const int64_t nqh = (int64_t)*(volatile unsigned long long*)&qc[2];
+        // whole-block rows first, a block at a time
+        __shared__ long long s_k;
+        for (;;) {
+            if (t == 0) s_k = (long long)atomicAdd(&qc[3], 1ull);
+            __syncthreads();
+            const int64_t k = s_k;
+            __syncthreads();
+            if (k >= nqh) break;
+            const int64_t v = p.gq[p.n - 1 - k];
+            heavy_row<kMB, STATS, PH, PUSH>(sm, p, it, fi_next, v, st, tag);
+        }
+        // the rest, a warp per row, kGqChunk rows per grab
+        for (;;) {
+            long long k0 = 0;
+            if (lane == 0) k0 = (long long)atomicAdd(&qc[1], (unsigned long long)kGqChunk);
+            k0 = __shfl_sync(kFull, k0, 0);
+            if (k0 >= nq) break;
+            const int64_t k1 = k0 + kGqChunk < nq ? k0 + kGqChunk : nq;
+            for (int64_t k = k0; k < k1; k++) heavy_row<32, STATS, PH, PUSH>(sm, p, it, fi_next, p.gq[k], st, tag);
+        }
+        grid_barrier(gbar);  // every deferred row has its result
+        // the owner keeps its survivors: M_v != OUT (column) / T_v undecided (Decide)
+        for (int base = 0; base < nh; base += kMB) {
+            const int i = base + t;
+            bool keep = false;
+            int32_t v = 0;
+            if (i < nh) {
+                const int32_t x = p.heavy[seg + i];
+                v = x < 0 ? ~x : x;
+                if (PH == 0) keep = p.M[v] != kM_OUT;
+                else {
+                    const uint64_t tv = p.T[v];
+                    keep = tv != kIN && tv != kOUT;
+                }
+            }
+            append(sm, keep, v, lout, seg);
+        }
+        if (blockIdx.x == 0 && t == 0) {  // the queue is empty for the next phase (after its barrier)
+            qc[0] = qc[1] = qc[2] = qc[3] = 0ull;
+        }
+    } else
+#endif
     if (nh > 0) {
         if (t == 0) {
             sm.hnext = 0;
@@ -1100,7 +1186,7 @@ __device__ int dense_run(TileSmem& sm, const MisParams& p, int it, const Rows& r
             }
         }
         const int64_t len = e - s;
-        if (defer_long<G>(sm, p, rows.seg, act, sub, v, len)) act = false;
+        if (defer_long<G>(sm, p, rows.seg, act, sub, v, len, PH == 0)) act = false;
         if (dbg && k < 12) dbuf[4 + 5 * k + 2] = gt();
         mbar_wait(&sm.mbar[slot], (ph >> slot) & 1u);
         ph ^= 1u << slot;
@@ -1281,7 +1367,7 @@ __device__ int sparse_run(TileSmem& sm, const MisParams& p, int it, int64_t seg,
         const int len = m.len & ~kStaged;
         const uint64_t tv = reinterpret_cast<const uint64_t*>(sm.buf[slot] + kTvOff)[gs];
         bool act = valid;
-        if (defer_long<GS>(sm, p, seg, act, sub, v, len)) act = false;
+        if (defer_long<GS>(sm, p, seg, act, sub, v, len, PH == 0)) act = false;
         if (dbg && k < 12) dbuf[4 + 5 * k + 2] = gt();
         mbar_wait(&sm.mbarS[slot], (ph >> (2 + slot)) & 1u);
         ph ^= 1u << (2 + slot);
@@ -1544,6 +1630,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         int use = 0;
         if (p.K) use = p.keys_mode ? 1 : (double)ld_acquire_u64(&p.ctrl[8]) > 16.0 * (double)p.nnz / (double)p.n;
         s_use_keys = use;
+        s_gq_on = p.gq != nullptr && n_active * 64ull > (unsigned long long)p.n;
     }
     __syncthreads();
 
@@ -1592,6 +1679,8 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         if (t == 0) s_nin_rep = s_nin;
         if (MIS2_HOIST) col_begin(it + 1, cnt2, p.L2[cur ^ 1]);
         const unsigned long long remaining = grid_wait_sum(sumc, sb, bold, &s_sum);
+        // the queue's two extra barriers pay only while many rows remain
+        if (t == 0) s_gq_on = p.gq != nullptr && remaining * 64ull > (unsigned long long)p.n;
         stamp(p, 2 + 2 * it);
         it++;
         if (remaining == 0) break;

@@ -134,6 +134,12 @@ def test_skewed_graph_paths_forced(decide, monkeypatch):
         check_agg(g, decide=decide, keys="on")
     for grp in (1, 2, 8):
         check_mis2(G.kronecker(11), group=grp, decide=decide, keys="on")
+    # the G = 2 small-tile kernel with the global queue of deferred rows
+    monkeypatch.setenv("MIS2_SMALL_TILES", "2")
+    monkeypatch.setenv("MIS2_GQ_RT", "1")
+    for g in [G.kronecker(12), G.kronecker(13), G.random_powerlaw_graph(4000, 40, 3)] + small_graphs(10, 778, 300):
+        check_mis2(g, group=2, decide=decide, keys="on")
+        check_mis2(g, group=2, decide=decide, keys="off", seed=3)
 
 
 @pytest.mark.parametrize("decide", ["pull", "push"])
