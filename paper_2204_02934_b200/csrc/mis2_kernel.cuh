@@ -776,7 +776,10 @@ constexpr int kHugeRow = MIS2_HUGE_ROW;
 #ifndef MIS2_GQ
 #define MIS2_GQ 0
 #endif
-constexpr int kGqChunk = 16;  // rows per warp grab
+#ifndef MIS2_GQ_CHUNK
+#define MIS2_GQ_CHUNK 4  // C4, rows per grab 1 / 2 / 4 / 8 / 16 / 64: 29.8 / 28.4 / 28.3 / 28.4 / 28.5 / 29.3 ms
+#endif
+constexpr int kGqChunk = MIS2_GQ_CHUNK;  // rows per warp grab
 template <int GG>
 __device__ __forceinline__ bool defer_long(TileSmem& sm, const MisParams& p, int64_t seg, bool act, int sub,
                                            int64_t v, int64_t len, bool gq_phase = false) {
