@@ -937,7 +937,7 @@ __device__ int finish_phase(TileSmem& sm, const MisParams& p, int it, int64_t se
     // column passes only: a Decide's deferred rows mostly stop at their first
     // OUT neighbour, and their grabs cost more than the balance saves (C4
     // Decide 3: 1.09 -> 1.12 ms with the queue)
-    if (!STATS && PH == 0 && p.gq && s_gq_on) {
+    if (!STATS && PH == 0 && p.gq && s_gq_on) {  // (s_gq_on is 0 in STATS kernels: defer_long marks no row)
         unsigned long long* qc = p.ctrl + 64;  // [0] rows, [1] warp head, [2] whole-block rows, [3] block head
         unsigned int* gbar = (unsigned int*)&p.ctrl[0];
         // publish: counts of the two kinds, one reservation each
@@ -1633,7 +1633,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         int use = 0;
         if (p.K) use = p.keys_mode ? 1 : (double)ld_acquire_u64(&p.ctrl[8]) > 16.0 * (double)p.nnz / (double)p.n;
         s_use_keys = use;
-        s_gq_on = p.gq != nullptr && n_active * 64ull > (unsigned long long)p.n;
+        s_gq_on = !STATS && p.gq != nullptr && n_active * 64ull > (unsigned long long)p.n;
     }
     __syncthreads();
 
@@ -1683,7 +1683,7 @@ __global__ void __launch_bounds__(kMB, kMinBlocksPerSM) mis2_persistent(MisParam
         if (MIS2_HOIST) col_begin(it + 1, cnt2, p.L2[cur ^ 1]);
         const unsigned long long remaining = grid_wait_sum(sumc, sb, bold, &s_sum);
         // the queue's two extra barriers pay only while many rows remain
-        if (t == 0) s_gq_on = p.gq != nullptr && remaining * 64ull > (unsigned long long)p.n;
+        if (t == 0) s_gq_on = !STATS && p.gq != nullptr && remaining * 64ull > (unsigned long long)p.n;
         stamp(p, 2 + 2 * it);
         it++;
         if (remaining == 0) break;
