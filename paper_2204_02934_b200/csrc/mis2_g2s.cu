@@ -4,6 +4,9 @@
 // (run_mis2).  Its own namespace (mis2k_s); MisParams has the same layout.
 #define MIS2_TILE_ROWS 160
 #define MIS2_GQ 1  // the skewed graphs' kernel: global queue of deferred rows
+// rows for a whole block from 4K entries (balanced by the queue): C4, 1K /
+// 2K / 4K / 8K / 32K: 28.8 / 28.8 / 27.4 / 27.5 / 28.3 ms
+#define MIS2_HUGE_ROW 4096
 #define mis2k mis2k_s
 #include "mis2_kernel.cuh"
 #undef mis2k
